@@ -1,0 +1,353 @@
+"""CPU oracle for the EntQuant hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2601_22787_b200`` never imports it and shares no code with it.
+
+The arithmetic lives in ``eq_oracle.c`` (plain C, fp64, one function per paper step,
+each citing PAPER.md / SPEC.md lines).  This module only marshals numpy arrays into it
+and composes the steps in Alg. 1 / Alg. 2 order.
+
+Parity status per function: every function here is pinned by a
+``-m "not gpu"`` test in tests/test_oracle_*.py except ``search`` at λ's absolute scale,
+which is "parity unpinned" for the paper's L-BFGS trajectory (only the exhaustive
+reading is pinned, by brute force on tiny tensors and by the special cases).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "eq_oracle.c")
+_SO = os.path.join(_HERE, "liboracle.so")
+
+PROB_BITS = 12
+CHUNK_SYMBOLS = 4096
+
+
+def build(force: bool = False) -> str:
+    """Compile eq_oracle.c with gcc (plain -O2, no fast-math)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
+             "-ffp-contract=off", "-o", _SO, _SRC, "-lm", "-lpthread"])
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        i64, i32, u16, u32, dbl = (ctypes.c_int64, ctypes.c_int32, ctypes.c_uint16,
+                                   ctypes.c_uint32, ctypes.c_double)
+        sig = {
+            "eqo_e4m3_value": (dbl, [u32]),
+            "eqo_bf16_to_double": (dbl, [u16]),
+            "eqo_bf16_from_double": (u16, [dbl]),
+            "eqo_quantize_value": (ctypes.c_uint8, [dbl]),
+            "eqo_quantize_value_scan": (ctypes.c_uint8, [dbl]),
+            "eqo_quantize_one": (ctypes.c_uint8, [u16, u16]),
+            "eqo_absmax_scale": (u16, [P, i64]),
+            "eqo_quantize": (None, [P, i64, i64, P, P]),
+            "eqo_dequant": (None, [P, i64, i64, P, P]),
+            "eqo_row_terms": (None, [P, i64, u16, P, P]),
+            "eqo_l1": (dbl, [P, i64]),
+            "eqo_objective": (dbl, [P, i64, i64, P, dbl]),
+            "eqo_candidates": (i64, [u16, i32, i32, P]),
+            "eqo_search_rows": (None, [P, i64, i64, dbl, i32, i32, i64, i64, P, P]),
+            "eqo_row_objectives": (i64, [P, i64, i64, i64, dbl, i32, i32, P, P, i64]),
+            "eqo_histogram": (None, [P, i64, P]),
+            "eqo_normalize": (ctypes.c_int, [P, P]),
+            "eqo_entropy": (dbl, [P]),
+            "eqo_encode_chunk": (i64, [P, i64, P, P, i64]),
+            "eqo_decode_chunk": (ctypes.c_int, [P, i64, P, P, i64]),
+            "eqo_block_chunks": (i64, [P, i32, i64]),
+            "eqo_encode_block": (i64, [P, P, i32, i64, P, P, i64, P]),
+            "eqo_decode_block": (ctypes.c_int, [P, P, P, i32, i64, P, P]),
+            "eqo_decode_chunks_mt": (ctypes.c_int, [P, P, P, P, i64, P, P, ctypes.c_int]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _u16(a) -> np.ndarray:
+    """bf16 bit patterns as uint16 (accepts torch bf16 tensors or uint16 arrays)."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            return np.ascontiguousarray(a.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16))
+    except ImportError:  # pragma: no cover
+        pass
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint16))
+
+
+# ---------------------------------------------------------------- scalar steps
+def e4m3_value(code: int) -> float:
+    return lib().eqo_e4m3_value(code)
+
+
+def bf16_to_float(b: int) -> float:
+    return lib().eqo_bf16_to_double(b)
+
+
+def bf16_from_float(x: float) -> int:
+    return lib().eqo_bf16_from_double(x)
+
+
+def quantize_value(r: float) -> int:
+    return lib().eqo_quantize_value(r)
+
+
+def quantize_value_scan(r: float) -> int:
+    return lib().eqo_quantize_value_scan(r)
+
+
+def quantize_one(w_bf16: int, s_bf16: int) -> int:
+    return lib().eqo_quantize_one(w_bf16, s_bf16)
+
+
+# ---------------------------------------------------------------- matrix steps
+def absmax_scales(W) -> np.ndarray:
+    """Eq. (1), Alg. 1 l.1: per-row AbsMax scale as bf16 bits."""
+    W = _u16(W)
+    M, N = W.shape
+    return np.array([lib().eqo_absmax_scale(_p(W[i]), N) for i in range(M)], dtype=np.uint16)
+
+
+def quantize(W, S) -> np.ndarray:
+    """Alg. 1 l.3: codes = Q_γ(W, S)."""
+    W, S = _u16(W), _u16(S)
+    M, N = W.shape
+    out = np.empty((M, N), dtype=np.uint8)
+    lib().eqo_quantize(_p(W), M, N, _p(S), _p(out))
+    return out
+
+
+def dequant(codes: np.ndarray, S) -> np.ndarray:
+    """Q†: bf16 bits of RNE(s·value(code))."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    S = _u16(S)
+    M, N = codes.shape
+    out = np.empty((M, N), dtype=np.uint16)
+    lib().eqo_dequant(_p(codes), M, N, _p(S), _p(out))
+    return out
+
+
+def row_terms(w_row, s_bf16: int):
+    w_row = _u16(w_row)
+    D, R = ctypes.c_double(), ctypes.c_double()
+    lib().eqo_row_terms(_p(w_row), w_row.size, s_bf16, ctypes.byref(D), ctypes.byref(R))
+    return D.value, R.value
+
+
+def l1(W) -> float:
+    W = _u16(W)
+    return lib().eqo_l1(_p(W), W.size)
+
+
+def objective(W, S, lam: float) -> float:
+    W, S = _u16(W), _u16(S)
+    M, N = W.shape
+    return lib().eqo_objective(_p(W), M, N, _p(S), lam)
+
+
+def candidates(s0: int, oct_lo: int = -1, oct_hi: int = 20):
+    first = ctypes.c_uint16()
+    n = lib().eqo_candidates(s0, oct_lo, oct_hi, ctypes.byref(first))
+    return first.value, n
+
+
+def search(W, lam: float, oct_lo: int = -1, oct_hi: int = 20, rows=None):
+    """Alg. 1 l.2 (exhaustive per-row reading): returns (S bf16 bits, per-row objective).
+
+    ``rows`` optionally restricts the search to a list of row indices (others are 0)."""
+    W = _u16(W)
+    M, N = W.shape
+    S = np.zeros(M, dtype=np.uint16)
+    f = np.zeros(M, dtype=np.float64)
+    if rows is None:
+        lib().eqo_search_rows(_p(W), M, N, lam, oct_lo, oct_hi, 0, M, _p(S), _p(f))
+    else:
+        for r in rows:
+            lib().eqo_search_rows(_p(W), M, N, lam, oct_lo, oct_hi, int(r), int(r) + 1, _p(S), _p(f))
+    return S, f
+
+
+def row_objectives(W, row: int, lam: float, oct_lo: int = -1, oct_hi: int = 20):
+    """All candidate objectives f_i(s) of one row: (first pattern, array)."""
+    W = _u16(W)
+    M, N = W.shape
+    cap = 128 * (oct_hi - oct_lo) + 8
+    f = np.zeros(cap, dtype=np.float64)
+    first = ctypes.c_uint16()
+    n = lib().eqo_row_objectives(_p(W), M, N, row, lam, oct_lo, oct_hi, ctypes.byref(first), _p(f), cap)
+    return first.value, f[:n].copy()
+
+
+def histogram(sym: np.ndarray) -> np.ndarray:
+    sym = np.ascontiguousarray(sym, dtype=np.uint8).reshape(-1)
+    h = np.zeros(256, dtype=np.uint64)
+    lib().eqo_histogram(_p(sym), sym.size, _p(h))
+    return h
+
+
+def normalize(hist: np.ndarray) -> np.ndarray:
+    hist = np.ascontiguousarray(hist, dtype=np.uint64)
+    f = np.zeros(256, dtype=np.uint16)
+    if lib().eqo_normalize(_p(hist), _p(f)) != 0:
+        raise ValueError("empty")
+    return f
+
+
+def entropy(hist: np.ndarray) -> float:
+    hist = np.ascontiguousarray(hist, dtype=np.uint64)
+    return lib().eqo_entropy(_p(hist))
+
+
+def encode_chunk(sym: np.ndarray, freq: np.ndarray) -> bytes:
+    sym = np.ascontiguousarray(sym, dtype=np.uint8).reshape(-1)
+    freq = np.ascontiguousarray(freq, dtype=np.uint16)
+    cap = 4 + 2 * sym.size + 8
+    out = np.zeros(cap, dtype=np.uint8)
+    n = lib().eqo_encode_chunk(_p(sym), sym.size, _p(freq), _p(out), cap)
+    if n == -2:
+        raise ValueError("unknown-symbol")
+    if n < 0:
+        raise ValueError("buffer")
+    return out[:n].tobytes()
+
+
+def decode_chunk(data: bytes, freq: np.ndarray, n: int) -> np.ndarray:
+    buf = np.frombuffer(data, dtype=np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
+    freq = np.ascontiguousarray(freq, dtype=np.uint16)
+    out = np.zeros(max(n, 1), dtype=np.uint8)
+    st = lib().eqo_decode_chunk(_p(buf), len(data), _p(freq), _p(out), n)
+    if st == 1:
+        raise ValueError("corrupt")
+    if st == 2:
+        raise ValueError("truncated")
+    return out[:n]
+
+
+# ---------------------------------------------------------------- block (Alg. 1 / Alg. 2)
+@dataclass
+class OracleBlock:
+    layer_shapes: list
+    scales: list                     # per layer, uint16 bf16 bits
+    freq: np.ndarray                 # uint16[256]
+    hist: np.ndarray                 # uint64[256]
+    payload: bytes
+    chunk_off: np.ndarray            # uint32[n_chunks+1]
+    chunk_symbols: int = CHUNK_SYMBOLS
+    codes: np.ndarray = field(default=None, repr=False)   # concatenated symbol stream
+
+    @property
+    def n_params(self) -> int:
+        return int(sum(r * c for r, c in self.layer_shapes))
+
+    @property
+    def n_chunks(self) -> int:
+        return int(self.chunk_off.size - 1)
+
+    def effective_bits(self) -> float:
+        """S:413-417 / SURVEY §8c.12: 8·(payload + offsets + scales + table)/params."""
+        rows = sum(r for r, _ in self.layer_shapes)
+        b = len(self.payload) + 4 * (self.n_chunks + 1) + 2 * rows + 2 * 256
+        return 8.0 * b / self.n_params
+
+
+def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS) -> OracleBlock:
+    """Alg. 1 l.4-5 + App. A.1: concatenate vec(W_q) of the block's layers, one table,
+    chunked rANS."""
+    stream = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1) for c in codes_list])
+    hist = histogram(stream)
+    freq = normalize(hist)
+    sizes = np.array([r * c for r, c in layer_shapes], dtype=np.int64)
+    n_chunks = lib().eqo_block_chunks(_p(sizes), len(layer_shapes), cs)
+    cap = 4 * n_chunks + 2 * stream.size + 64
+    payload = np.zeros(cap, dtype=np.uint8)
+    off = np.zeros(n_chunks + 1, dtype=np.uint32)
+    n = lib().eqo_encode_block(_p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(payload), cap, _p(off))
+    if n < 0:
+        raise ValueError("encode failed %d" % n)
+    return OracleBlock(list(layer_shapes), [np.asarray(s, dtype=np.uint16) for s in scales], freq, hist,
+                       payload[:n].tobytes(), off, cs, stream)
+
+
+def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int = -1, oct_hi: int = 20,
+                    cs: int = CHUNK_SYMBOLS) -> OracleBlock:
+    """Alg. 1 for one block.  ``layers``: list of bf16 [M,N] arrays (uint16 bits or torch).
+    Either ``scales`` (per layer) is given, or ``lam`` selects the exhaustive search
+    (lam=None -> AbsMax scales, i.e. the λ=0 lossless-FP8 baseline of P:257)."""
+    Ws = [_u16(W) for W in layers]
+    shapes = [tuple(W.shape) for W in Ws]
+    if scales is None:
+        if lam is None:
+            scales = [absmax_scales(W) for W in Ws]
+        else:
+            scales = [search(W, lam, oct_lo, oct_hi)[0] for W in Ws]
+    codes = [quantize(W, S) for W, S in zip(Ws, scales)]
+    return encode_codes(codes, shapes, scales, cs)
+
+
+def decode_block(blk: OracleBlock) -> np.ndarray:
+    """Alg. 2 l.1: concatenated symbol stream."""
+    sizes = np.array([r * c for r, c in blk.layer_shapes], dtype=np.int64)
+    out = np.zeros(int(sizes.sum()), dtype=np.uint8)
+    payload = np.frombuffer(blk.payload, dtype=np.uint8).copy()
+    off = np.ascontiguousarray(blk.chunk_off, dtype=np.uint32)
+    st = lib().eqo_decode_block(_p(payload), _p(off), _p(sizes), len(blk.layer_shapes), blk.chunk_symbols,
+                                _p(blk.freq), _p(out))
+    if st:
+        raise ValueError({1: "corrupt", 2: "truncated"}[st])
+    return out
+
+
+def decode_dequant(blk: OracleBlock) -> list:
+    """Alg. 2 l.1-2: per-layer bf16 bits of the dequantised weights."""
+    stream = decode_block(blk)
+    outs, a = [], 0
+    for (r, c), S in zip(blk.layer_shapes, blk.scales):
+        outs.append(dequant(stream[a:a + r * c].reshape(r, c), S))
+        a += r * c
+    return outs
+
+
+def chunk_table(layer_shapes, cs: int = CHUNK_SYMBOLS):
+    """(sym0, n) per chunk of a block stream (layer-restart chunking)."""
+    sym0, ns, base = [], [], 0
+    for r, c in layer_shapes:
+        n = r * c
+        for a in range(0, n, cs):
+            sym0.append(base + a)
+            ns.append(min(cs, n - a))
+        base += n
+    return np.array(sym0, dtype=np.uint64), np.array(ns, dtype=np.uint32)
+
+
+def decode_chunks_mt(payload: np.ndarray, chunk_off: np.ndarray, sym0: np.ndarray, ns: np.ndarray,
+                     freq: np.ndarray, out: np.ndarray, threads: int) -> None:
+    """Multi-threaded oracle decode of selected chunks (CPU baseline timing only)."""
+    st = lib().eqo_decode_chunks_mt(_p(payload), _p(chunk_off), _p(sym0), _p(ns), ns.size,
+                                    _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(out), threads)
+    if st:
+        raise ValueError({1: "corrupt", 2: "truncated"}[st])

@@ -1,0 +1,540 @@
+/*
+ * eq_oracle.c — plain, slow, obviously-correct CPU ORACLE for the EntQuant hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2601_22787_b200/) never links, imports or calls it, and this file shares no
+ * code, headers, tables or constants with the CUDA path.
+ *
+ * Paper: "Float8@2bits: Entropy Coding Enables Data-Free Model Compression"
+ * (arXiv 2601.22787), cited as P:<line> of PAPER.md; SPEC.md lines as S:<line>;
+ * readings of ambiguous passages follow SURVEY.md §8(c) and are listed in DESIGN.md §3.
+ *
+ * Arithmetic: fp64 throughout; integers are exact.  No blocking, fusion or
+ * reordering beyond the definitions.  Every function names the passage it follows.
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"): E4M3 grid vs the bit-layout closed form
+ * and vs ml_dtypes/torch float8_e4m3fn; quantiser exhaustively vs ml_dtypes RNE of the
+ * exact quotient; dequant vs ml_dtypes bf16 RNE of the exact f64 product; objective
+ * special cases (λ=0, λ→∞, on-grid W) and brute-force scan on tiny tensors;
+ * normalisation worked examples; rANS lossless round trip, Shannon
+ * lower bound, cross-entropy upper bound, hand-derived stream (tests/golden/).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+#define EQO_L        (1u << 23)   /* rANS lower bound L = 2^23 */
+#define EQO_PROB_BITS 12          /* M = 2^12                                 */
+#define EQO_M        (1u << EQO_PROB_BITS)
+
+/* ------------------------------------------------------------------------------------
+ * §2.1 Float8-E4M3 grid, torch.float8_e4m3fn flavour:
+ * sign | 4 exponent bits (bias 7) | 3 mantissa bits; e=0 subnormal m/8·2^-6;
+ * normal (1+m/8)·2^(e-7); 0x7F / 0xFF are NaN (no infinities).
+ * ---------------------------------------------------------------------------------- */
+double eqo_e4m3_value(uint32_t code)
+{
+    code &= 0xFF;
+    uint32_t sign = code >> 7, e = (code >> 3) & 0xF, m = code & 7;
+    if ((code & 0x7F) == 0x7F) return NAN;
+    double mag = (e == 0) ? ldexp((double)m / 8.0, -6) : ldexp(1.0 + (double)m / 8.0, (int)e - 7);
+    return sign ? -mag : mag;
+}
+
+/* bf16 <-> f64.  bf16 = top 16 bits of an IEEE binary32; rounding f64 -> bf16 is
+ * round-to-nearest-even on the exact value (scales are stored BF16). */
+double eqo_bf16_to_double(uint16_t b)
+{
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+/* Exact RNE of a double to bf16 by enumerating the two bf16 neighbours: plain and
+ * slow on purpose.  IEEE overflow rule: beyond the last midpoint the result is inf. */
+uint16_t eqo_bf16_from_double(double x)
+{
+    if (x != x) return 0x7FC0;
+    uint16_t sign = (x < 0) ? 0x8000 : 0;
+    double a = fabs(x);
+    /* find largest non-negative bf16 pattern p with value(p) <= a by bisection over
+     * the ordered positive patterns 0x0000..0x7F80 (values increase with the pattern). */
+    uint32_t lo = 0, hi = 0x7F80; /* value(0x7F80) = +inf */
+    if (a >= ldexp(1.0, 128)) return sign | 0x7F80;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) / 2;
+        if (eqo_bf16_to_double((uint16_t)mid) <= a) lo = mid; else hi = mid;
+    }
+    double vlo = eqo_bf16_to_double((uint16_t)lo), vhi = eqo_bf16_to_double((uint16_t)hi);
+    if (hi == 0x7F80) vhi = ldexp(1.0, 128);  /* IEEE overflow: the value 2^128 stands for inf */
+    uint32_t p;
+    if (a - vlo < vhi - a) p = lo;
+    else if (a - vlo > vhi - a) p = hi;
+    else p = (lo & 1) ? hi : lo;          /* tie -> even pattern */
+    return (uint16_t)(sign | p);
+}
+
+/* ------------------------------------------------------------------------------------
+ * §2.1 quantiser Q_γ: W_q = clamp(⌊W/s⌉, -Q_max, Q_max), ⌊·⌉ = nearest value
+ * representable in γ = E4M3, Q_max = 448.
+ * Readings: clamp before rounding; ties to the even code;
+ * signed zero resolved to +0 (App. A.1).
+ * The quotient is formed in f64.  For bf16 W and bf16 s an exact E4M3 midpoint quotient
+ * is representable in f64 and the f64 division returns it exactly; any other quotient is
+ * ≥ 2^-13 (relative) from every midpoint, far above f64 rounding, so the
+ * nearest-value choice below equals the choice for the exact quotient.
+ * Nearest value: textbook RNE to a 3-bit mantissa (cross-checked against a brute-force
+ * scan of all 253 finite codes, eqo_quantize_value_scan, in the pins).
+ * ---------------------------------------------------------------------------------- */
+/* Code of a grid value (inverse of eqo_e4m3_value on the finite grid; -0 -> 0x00). */
+static uint8_t eqo_e4m3_code(double v)
+{
+    uint8_t sign = (v < 0) ? 0x80 : 0;
+    double a = fabs(v);
+    if (a == 0.0) return 0x00;
+    if (a < ldexp(1.0, -6))                       /* subnormal: m/8 * 2^-6 */
+        return (uint8_t)(sign | (uint8_t)(a * 512.0));
+    int k;
+    double m = frexp(a, &k);                      /* a = m * 2^k, m in [0.5, 1) */
+    int e = k - 1 + 7;                            /* a = (1+f) 2^(k-1)          */
+    int mant = (int)((m * 2.0 - 1.0) * 8.0);
+    return (uint8_t)(sign | (uint8_t)(e << 3) | (uint8_t)mant);
+}
+
+/* Nearest E4M3 value to r after clamping, the textbook way: 4 significant bits in the
+ * normal range (|r| >= 2^-6), fixed spacing 2^-9 in the subnormal range; rint() is
+ * round-half-even in the default rounding mode, so a tie goes to the even mantissa. */
+uint8_t eqo_quantize_value(double r)
+{
+    if (r > 448.0) r = 448.0;
+    if (r < -448.0) r = -448.0;
+    double a = fabs(r), q;
+    if (a < ldexp(1.0, -6)) {
+        q = ldexp(rint(ldexp(a, 9)), -9);
+    } else {
+        int k;
+        double m = frexp(a, &k);                  /* m in [0.5,1): 4 bits = m*16 */
+        q = ldexp(rint(m * 16.0), k - 4);
+    }
+    if (q == 0.0) return 0x00;                    /* signed zero resolved */
+    return eqo_e4m3_code(r < 0 ? -q : q);
+}
+
+/* Independent brute-force definition (pins only): scan all 253 finite codes for the
+ * nearest value, ties to the even code. */
+uint8_t eqo_quantize_value_scan(double r)
+{
+    if (r > 448.0) r = 448.0;
+    if (r < -448.0) r = -448.0;
+    int best = -1;
+    double bestd = 0.0;
+    for (int c = 0; c < 256; c++) {
+        if ((c & 0x7F) == 0x7F || c == 0x80) continue;   /* NaN codes; -0 resolved */
+        double d = fabs(r - eqo_e4m3_value((uint32_t)c));
+        if (best < 0 || d < bestd || (d == bestd && (c & 1) == 0 && (best & 1) == 1)) {
+            best = c;
+            bestd = d;
+        }
+    }
+    return (uint8_t)best;
+}
+
+uint8_t eqo_quantize_one(uint16_t w_bf16, uint16_t s_bf16)
+{
+    double w = eqo_bf16_to_double(w_bf16), s = eqo_bf16_to_double(s_bf16);
+    return eqo_quantize_value(w / s);
+}
+
+/* Eq. (1), Alg. 1 l.1: s = max|W_row| / Q_max, per output channel
+ * (P:148).  Stored as bf16 (RNE) since scales are BF16.  All-zero row -> 1. */
+uint16_t eqo_absmax_scale(const uint16_t* w_row, int64_t n)
+{
+    double m = 0.0;
+    for (int64_t j = 0; j < n; j++) {
+        double a = fabs(eqo_bf16_to_double(w_row[j]));
+        if (a > m) m = a;
+    }
+    if (m == 0.0) return eqo_bf16_from_double(1.0);
+    return eqo_bf16_from_double(m / 448.0);
+}
+
+/* Alg. 1 l.3: W_q = Q_γ(W, S*) with one scale per row. */
+void eqo_quantize(const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, uint8_t* codes)
+{
+    for (int64_t i = 0; i < M; i++)
+        for (int64_t j = 0; j < N; j++)
+            codes[i * N + j] = eqo_quantize_one(W[i * N + j], S[i]);
+}
+
+/* §2.1 dequantiser Q†: Ŵ = s·W_q, returned as bf16 (RNE of the exact f64
+ * product; the product of a bf16 and an E4M3 value has ≤ 12 significant bits). */
+void eqo_dequant(const uint8_t* codes, int64_t M, int64_t N, const uint16_t* S, uint16_t* out)
+{
+    for (int64_t i = 0; i < M; i++) {
+        double s = eqo_bf16_to_double(S[i]);
+        for (int64_t j = 0; j < N; j++)
+            out[i * N + j] = eqo_bf16_from_double(s * eqo_e4m3_value(codes[i * N + j]));
+    }
+}
+
+/* ------------------------------------------------------------------------------------
+ * Eq. (4): objective d(W,Ŵ) + λ R(W_q), d = ‖W-Ŵ‖₁/‖W‖₁, R = ‖W_q‖₁.
+ * Reading: R in the code domain (grid values, pre-scale), normalised by
+ * M·N.  The objective is separable over rows, so row i contributes
+ *   f_i(s) = D_i(s)/‖W‖₁ + λ·R_i(s)/(M·N),
+ *   D_i(s) = Σ_j |W_ij − s·v_ij|,  R_i(s) = Σ_j |v_ij|,  v_ij = value(Q_γ(W_ij, s)).
+ * Each term is exact in f64; sums are sequential in j (f64).
+ * ---------------------------------------------------------------------------------- */
+void eqo_row_terms(const uint16_t* w_row, int64_t n, uint16_t s_bf16, double* D, double* R)
+{
+    double s = eqo_bf16_to_double(s_bf16), d = 0.0, r = 0.0;
+    for (int64_t j = 0; j < n; j++) {
+        double w = eqo_bf16_to_double(w_row[j]);
+        double v = eqo_e4m3_value(eqo_quantize_value(w / s));
+        d += fabs(w - s * v);
+        r += fabs(v);
+    }
+    *D = d;
+    *R = r;
+}
+
+double eqo_l1(const uint16_t* W, int64_t n)
+{
+    double a = 0.0;
+    for (int64_t j = 0; j < n; j++) a += fabs(eqo_bf16_to_double(W[j]));
+    return a;
+}
+
+/* Full-matrix objective (Eq. 4) for given per-row scales. */
+double eqo_objective(const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, double lambda)
+{
+    double l1 = eqo_l1(W, M * N), Dt = 0.0, Rt = 0.0;
+    for (int64_t i = 0; i < M; i++) {
+        double D, R;
+        eqo_row_terms(W + i * N, N, S[i], &D, &R);
+        Dt += D;
+        Rt += R;
+    }
+    double d = (l1 > 0.0) ? Dt / l1 : 0.0;
+    return d + lambda * Rt / ((double)M * (double)N);
+}
+
+/* Candidate set for row search (reading, DESIGN.md §3 / SURVEY §8c.5): the contiguous
+ * positive bf16 patterns from bf16(s0·2^oct_lo) to bf16(s0·2^oct_hi) (positive bf16 values
+ * are ordered by their bit patterns).  Returns the count, writes first pattern. */
+int64_t eqo_candidates(uint16_t s0, int32_t oct_lo, int32_t oct_hi, uint16_t* first)
+{
+    double v0 = eqo_bf16_to_double(s0);
+    uint16_t lo = eqo_bf16_from_double(ldexp(v0, oct_lo));
+    uint16_t hi = eqo_bf16_from_double(ldexp(v0, oct_hi));
+    if (lo < 0x0001) lo = 0x0001;
+    if (hi > 0x7F7F) hi = 0x7F7F;
+    if (hi < lo) hi = lo;
+    *first = lo;
+    return (int64_t)hi - (int64_t)lo + 1;
+}
+
+/* Alg. 1 l.1-2, solved per row by exhaustive minimisation over the
+ * candidate set (reading replacing L-BFGS+STE).  Tie rule: the
+ * smallest candidate attaining the minimum.  All-zero rows keep s = 1.
+ * obj_rows (nullable) receives f_i(s*_i). */
+void eqo_search_rows(const uint16_t* W, int64_t M, int64_t N, double lambda,
+                     int32_t oct_lo, int32_t oct_hi, int64_t row_begin, int64_t row_end,
+                     uint16_t* S, double* obj_rows)
+{
+    double l1 = eqo_l1(W, M * N);
+    double mn = (double)M * (double)N;
+    for (int64_t i = row_begin; i < row_end; i++) {
+        const uint16_t* row = W + i * N;
+        uint16_t s0 = eqo_absmax_scale(row, N);
+        int zero_row = 1;
+        for (int64_t j = 0; j < N; j++)
+            if ((row[j] & 0x7FFF) != 0) { zero_row = 0; break; }
+        if (zero_row) {
+            S[i] = s0;
+            if (obj_rows) obj_rows[i] = 0.0;
+            continue;
+        }
+        uint16_t first;
+        int64_t nc = eqo_candidates(s0, oct_lo, oct_hi, &first);
+        double best = INFINITY;
+        uint16_t bests = first;
+        for (int64_t k = 0; k < nc; k++) {
+            uint16_t s = (uint16_t)(first + k);
+            double D, R;
+            eqo_row_terms(row, N, s, &D, &R);
+            double f = (l1 > 0.0 ? D / l1 : 0.0) + lambda * R / mn;
+            if (f < best) { best = f; bests = s; }
+        }
+        S[i] = bests;
+        if (obj_rows) obj_rows[i] = best;
+    }
+}
+
+/* Per-candidate objective table of one row (used by tests to check GPU choices
+ * against every candidate).  f[k] for candidate first+k.  Returns the count. */
+int64_t eqo_row_objectives(const uint16_t* W, int64_t M, int64_t N, int64_t row, double lambda,
+                           int32_t oct_lo, int32_t oct_hi, uint16_t* first_out, double* f,
+                           int64_t cap)
+{
+    double l1 = eqo_l1(W, M * N);
+    double mn = (double)M * (double)N;
+    const uint16_t* r = W + row * N;
+    uint16_t s0 = eqo_absmax_scale(r, N), first;
+    int64_t nc = eqo_candidates(s0, oct_lo, oct_hi, &first);
+    *first_out = first;
+    for (int64_t k = 0; k < nc && k < cap; k++) {
+        double D, R;
+        eqo_row_terms(r, N, (uint16_t)(first + k), &D, &R);
+        f[k] = (l1 > 0.0 ? D / l1 : 0.0) + lambda * R / mn;
+    }
+    return nc;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Metadata ℳ: symbol histogram of the block stream and the
+ * frequency table normalised to 2^12.  Reading:
+ * integer-only largest-remainder rule, because SPEC's literal rule can go negative.
+ *   1. f_s = c_s>0 ? max(1, ⌊4096 c_s / T⌋) : 0 ;  r_s = (4096 c_s) mod T
+ *   2. D = 4096 − Σ f
+ *   3. D > 0: +1 to the D present symbols with largest r_s (ties: larger c_s, lower code)
+ *   4. while D < 0: −1 from the current largest f_s with f_s > 1 (ties: lower code)
+ * Returns 0, or -1 when T = 0 ("empty").
+ * ---------------------------------------------------------------------------------- */
+void eqo_histogram(const uint8_t* sym, int64_t n, uint64_t hist[256])
+{
+    for (int c = 0; c < 256; c++) hist[c] = 0;
+    for (int64_t i = 0; i < n; i++) hist[sym[i]]++;
+}
+
+int eqo_normalize(const uint64_t hist[256], uint16_t freq[256])
+{
+    uint64_t T = 0;
+    for (int c = 0; c < 256; c++) T += hist[c];
+    if (T == 0) return -1;
+    int64_t f[256], sum = 0;
+    uint64_t r[256];
+    for (int c = 0; c < 256; c++) {
+        if (hist[c] == 0) { f[c] = 0; r[c] = 0; continue; }
+        unsigned __int128 num = (unsigned __int128)EQO_M * hist[c];
+        uint64_t q = (uint64_t)(num / T);
+        r[c] = (uint64_t)(num % T);
+        f[c] = q < 1 ? 1 : (int64_t)q;
+        sum += f[c];
+    }
+    int64_t D = (int64_t)EQO_M - sum;
+    if (D > 0) {
+        /* pick D present symbols with largest (r, c, -code) by repeated selection */
+        int taken[256] = {0};
+        for (int64_t k = 0; k < D; k++) {
+            int b = -1;
+            for (int c = 0; c < 256; c++) {
+                if (hist[c] == 0 || taken[c]) continue;
+                if (b < 0 || r[c] > r[b] || (r[c] == r[b] && hist[c] > hist[b])) b = c;
+            }
+            taken[b] = 1;
+            f[b] += 1;
+        }
+    }
+    while (D < 0) {
+        int b = -1;
+        for (int c = 0; c < 256; c++)
+            if (f[c] > 1 && (b < 0 || f[c] > f[b])) b = c;
+        f[b] -= 1;
+        D += 1;
+    }
+    for (int c = 0; c < 256; c++) freq[c] = (uint16_t)f[c];
+    return 0;
+}
+
+/* Shannon empirical entropy Ĥ, Eq. (2), bits per symbol. */
+double eqo_entropy(const uint64_t hist[256])
+{
+    uint64_t T = 0;
+    for (int c = 0; c < 256; c++) T += hist[c];
+    if (T == 0) return 0.0;
+    double h = 0.0;
+    for (int c = 0; c < 256; c++)
+        if (hist[c]) {
+            double p = (double)hist[c] / (double)T;
+            h -= p * log2(p);
+        }
+    return h;
+}
+
+/* ------------------------------------------------------------------------------------
+ * ANS (§2.1; Alg. 1 l.5 P:213; Alg. 2 l.1 P:229): byte-wise rANS, 32-bit state,
+ * L = 2^23, M = 2^12, cumulative frequencies in code order.
+ * Encoder: reverse symbol order from x = L; before coding s, emit low bytes while
+ * x ≥ ((L>>12)<<8)·f_s; then x = ⌊x/f_s⌋·M + (x mod f_s) + c_s; finally the 4-byte state,
+ * little-endian, precedes the renormalisation bytes in decode order.
+ * ---------------------------------------------------------------------------------- */
+static void eqo_cum(const uint16_t freq[256], uint32_t cum[257])
+{
+    cum[0] = 0;
+    for (int c = 0; c < 256; c++) cum[c + 1] = cum[c] + freq[c];
+}
+
+/* Encodes n symbols; writes into out[0..cap).  Returns the byte count, -1 if cap is too
+ * small, -2 if a symbol has zero frequency ("unknown-symbol"). */
+int64_t eqo_encode_chunk(const uint8_t* sym, int64_t n, const uint16_t freq[256],
+                         uint8_t* out, int64_t cap)
+{
+    uint32_t cum[257];
+    eqo_cum(freq, cum);
+    /* bytes are produced back-to-front into a temporary of worst-case size */
+    int64_t tcap = 4 + 2 * n + 8;
+    uint8_t* tmp = (uint8_t*)malloc((size_t)tcap);
+    int64_t pos = tcap;
+    uint64_t x = EQO_L;
+    for (int64_t i = n - 1; i >= 0; i--) {
+        uint32_t f = freq[sym[i]], c = cum[sym[i]];
+        if (f == 0) { free(tmp); return -2; }
+        uint64_t x_max = (uint64_t)((EQO_L >> EQO_PROB_BITS) << 8) * f;
+        while (x >= x_max) {
+            tmp[--pos] = (uint8_t)(x & 0xFF);
+            x >>= 8;
+        }
+        x = (x / f) * EQO_M + (x % f) + c;
+    }
+    pos -= 4;
+    tmp[pos + 0] = (uint8_t)(x & 0xFF);
+    tmp[pos + 1] = (uint8_t)((x >> 8) & 0xFF);
+    tmp[pos + 2] = (uint8_t)((x >> 16) & 0xFF);
+    tmp[pos + 3] = (uint8_t)((x >> 24) & 0xFF);
+    int64_t len = tcap - pos;
+    if (len > cap) { free(tmp); return -1; }
+    memcpy(out, tmp + pos, (size_t)len);
+    free(tmp);
+    return len;
+}
+
+/* Decoder (Alg. 2 l.1): x = LE32; per symbol: slot = x mod M; s = the symbol with
+ * cum[s] ≤ slot < cum[s+1] (linear scan); x = f_s·⌊x/M⌋ + slot − c_s; while x < L read
+ * a byte.  Integrity: at the end x must equal L and every byte must have
+ * been consumed.  Returns 0 ok, 1 corrupt, 2 truncated. */
+int eqo_decode_chunk(const uint8_t* in, int64_t nbytes, const uint16_t freq[256],
+                     uint8_t* sym, int64_t n)
+{
+    uint32_t cum[257];
+    eqo_cum(freq, cum);
+    if (nbytes < 4) return 2;
+    uint64_t x = (uint64_t)in[0] | ((uint64_t)in[1] << 8) | ((uint64_t)in[2] << 16) |
+                 ((uint64_t)in[3] << 24);
+    int64_t p = 4;
+    for (int64_t i = 0; i < n; i++) {
+        uint32_t slot = (uint32_t)(x % EQO_M);
+        int s = 0;
+        while (!(cum[s] <= slot && slot < cum[s + 1])) s++;   /* cum[256] = M > slot */
+        sym[i] = (uint8_t)s;
+        x = (uint64_t)freq[s] * (x / EQO_M) + slot - cum[s];
+        while (x < EQO_L) {
+            if (p >= nbytes) return 2;
+            x = (x << 8) | in[p++];
+        }
+    }
+    if (x != EQO_L || p != nbytes) return 1;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Block stream (App. A.1): the vec'd code matrices of a block's
+ * layers are concatenated in order; one table over the whole stream; the stream is
+ * split into chunks of `cs` symbols that restart at each layer start;
+ * payload = chunk streams back to back; chunk_off[k] = byte offset of chunk k,
+ * chunk_off[n_chunks] = payload bytes.
+ * ---------------------------------------------------------------------------------- */
+int64_t eqo_block_chunks(const int64_t* layer_sizes, int32_t n_layers, int64_t cs)
+{
+    int64_t n = 0;
+    for (int32_t l = 0; l < n_layers; l++) n += (layer_sizes[l] + cs - 1) / cs;
+    return n;
+}
+
+/* Returns payload bytes, or a negative error. */
+int64_t eqo_encode_block(const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers,
+                         int64_t cs, const uint16_t freq[256], uint8_t* payload, int64_t cap,
+                         uint32_t* chunk_off)
+{
+    int64_t pos = 0, k = 0, sbase = 0;
+    for (int32_t l = 0; l < n_layers; l++) {
+        for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
+            int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
+            chunk_off[k++] = (uint32_t)pos;
+            int64_t len = eqo_encode_chunk(codes + sbase + a, n, freq, payload + pos, cap - pos);
+            if (len < 0) return len;
+            pos += len;
+        }
+        sbase += layer_sizes[l];
+    }
+    chunk_off[k] = (uint32_t)pos;
+    return pos;
+}
+
+/* Decodes a whole block stream into codes; returns 0 / first failing status. */
+int eqo_decode_block(const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
+                     int32_t n_layers, int64_t cs, const uint16_t freq[256], uint8_t* codes)
+{
+    int64_t k = 0, sbase = 0;
+    for (int32_t l = 0; l < n_layers; l++) {
+        for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
+            int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
+            int st = eqo_decode_chunk(payload + chunk_off[k], (int64_t)chunk_off[k + 1] - chunk_off[k],
+                                      freq, codes + sbase + a, n);
+            if (st) return st;
+            k++;
+        }
+        sbase += layer_sizes[l];
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------
+ * CPU baseline timing helper (bench.py cpu_baseline only): the same decoder as above,
+ * chunks statically partitioned over `threads` POSIX threads.  No change to the
+ * arithmetic; it only runs eqo_decode_chunk on disjoint chunks concurrently.
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+    const uint8_t* payload; const uint32_t* chunk_off; const uint64_t* chunk_sym0;
+    const uint32_t* chunk_n; const uint16_t* freq; uint8_t* codes;
+    int64_t k0, k1; int status;
+} eqo_job;
+
+static void* eqo_worker(void* p)
+{
+    eqo_job* j = (eqo_job*)p;
+    j->status = 0;
+    for (int64_t k = j->k0; k < j->k1; k++) {
+        int st = eqo_decode_chunk(j->payload + j->chunk_off[k],
+                                  (int64_t)j->chunk_off[k + 1] - j->chunk_off[k], j->freq,
+                                  j->codes + j->chunk_sym0[k], j->chunk_n[k]);
+        if (st && !j->status) j->status = st;
+    }
+    return NULL;
+}
+
+int eqo_decode_chunks_mt(const uint8_t* payload, const uint32_t* chunk_off,
+                         const uint64_t* chunk_sym0, const uint32_t* chunk_n, int64_t n_chunks,
+                         const uint16_t freq[256], uint8_t* codes, int threads)
+{
+    if (threads < 1) threads = 1;
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    eqo_job* jobs = (eqo_job*)malloc(sizeof(eqo_job) * (size_t)threads);
+    for (int t = 0; t < threads; t++) {
+        jobs[t] = (eqo_job){payload, chunk_off, chunk_sym0, chunk_n, freq, codes,
+                            n_chunks * t / threads, n_chunks * (t + 1) / threads, 0};
+        pthread_create(&th[t], NULL, eqo_worker, &jobs[t]);
+    }
+    int st = 0;
+    for (int t = 0; t < threads; t++) {
+        pthread_join(th[t], NULL);
+        if (jobs[t].status && !st) st = jobs[t].status;
+    }
+    free(th);
+    free(jobs);
+    return st;
+}
