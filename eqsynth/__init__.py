@@ -133,6 +133,20 @@ def weights(rows: int, cols: int, seed: int = 0, layer: int = 0, matrix: int = 0
     return out
 
 
+def weights_rows(row_ids, rows: int, cols: int, seed: int = 0, layer: int = 0, matrix: int = 0,
+                 dist: str = "t4", device="cpu") -> torch.Tensor:
+    """The listed rows of ``weights(rows, cols, ...)`` (same bits; no planted outliers)."""
+    device = torch.device(device)
+    k1, k2 = _key(seed, layer, matrix, dist, "a"), _key(seed, layer, matrix, dist, "b")
+    tab = _table(dist, device)
+    gains = torch.from_numpy(row_gains(rows, seed, layer, matrix)).to(device)
+    rid = torch.as_tensor(list(row_ids), dtype=torch.int64, device=device)
+    idx = (rid[:, None] * cols + torch.arange(cols, dtype=torch.int64, device=device)[None, :]).reshape(-1)
+    u = lowbias32((lowbias32(idx ^ k1) + k2) & _MASK32)
+    t = tab[u >> (32 - TABLE_BITS)].view(rid.numel(), cols)
+    return (t * gains[rid][:, None]).to(torch.bfloat16)
+
+
 def block_weights(model: str, layer: int, seed: int = 0, dist: str = "t4", device="cpu",
                   outliers: bool = False):
     """The 7 bf16 matrices of decoder block ``layer`` of a Llama-shaped model."""

@@ -1,0 +1,209 @@
+/*
+ * entquant.h — C ABI of the B200-native EntQuant hot path (libentquant.so).
+ *
+ * Paper: "Float8@2bits: Entropy Coding Enables Data-Free Model Compression",
+ * arXiv 2601.22787.  P:<n> = line n of PAPER.md, S:<n> = line n of SPEC.md; the
+ * readings of ambiguous passages are listed in DESIGN.md §3 and numbered R1..R12.
+ *
+ * Conventions (all entry points):
+ *  - Tensor / array pointers are CUDA DEVICE pointers unless the parameter name ends in
+ *    `_host`.  The caller allocates and owns every buffer (PyTorch does, in the binding).
+ *    The library is stateless, holds no persistent allocation, is reentrant, and orders
+ *    all device work on the given stream.  Structs are read on the host at call time.
+ *  - bf16 values are passed as their 16-bit patterns (uint16_t); row-major storage.
+ *  - Synchronous errors (bad arguments, shapes, undersized buffers, CUDA launch failures)
+ *    are returned before any kernel is queued.  Data-dependent errors found on the device
+ *    (corrupt / truncated streams, empty histograms) are OR-ed as EQ_EF_* bits into a
+ *    caller-provided device word `d_err` (zero it first); eq_check() maps it to a status.
+ *  - Only the entry points documented "synchronous" block the host.
+ *  - Errors never write outside the caller's buffers.
+ */
+#ifndef ENTQUANT_H
+#define ENTQUANT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* eq_stream_t;   /* a cudaStream_t; NULL = legacy default */
+
+typedef enum {
+    EQ_OK = 0,
+    EQ_ERR_ARG = 1,                 /* null pointer, bad enum / parameter value           */
+    EQ_ERR_SHAPE = 2,               /* rows/cols invalid or mismatched              */
+    EQ_ERR_EMPTY = 3,               /* empty stream / histogram                    */
+    EQ_ERR_BUFFER = 4,              /* arena, payload or scratch too small         */
+    EQ_ERR_CORRUPT = 5,             /* rANS end-state / length check failed        */
+    EQ_ERR_TRUNCATED = 6,           /* chunk offsets outside the payload           */
+    EQ_ERR_UNKNOWN_SYMBOL = 7,      /* symbol with zero table frequency            */
+    EQ_ERR_UNREACHABLE_TARGET = 8,  /* λ calibration cannot reach the target rate  */
+    EQ_ERR_CUDA = 9                 /* a CUDA runtime error                                */
+} eq_status;
+
+/* device error-word bits (d_err) */
+#define EQ_EF_CORRUPT        0x1u
+#define EQ_EF_TRUNCATED      0x2u
+#define EQ_EF_EMPTY          0x4u
+#define EQ_EF_UNKNOWN_SYMBOL 0x8u
+#define EQ_EF_BUFFER         0x10u
+
+#define EQ_FMT_E4M3   0u            /* Float8 E4M3 (torch float8_e4m3fn)            */
+#define EQ_OUT_FP8    0u            /* decode to raw E4M3 codes (scale left to the GEMM)   */
+#define EQ_OUT_BF16   1u            /* decode + fused per-row dequant to bf16      */
+
+#define EQ_SCALES_SEARCH 0u         /* exhaustive per-row Eq. 4 minimisation (R5)          */
+#define EQ_SCALES_ABSMAX 1u         /* AbsMax scales, Eq. 1 (the λ = 0 lossless-FP8 rate)  */
+#define EQ_SCALES_GIVEN  2u         /* caller supplies eq_block.scales                     */
+
+#define EQ_MAX_LAYERS 8             /* layers per block (a Llama block has 7)              */
+#define EQ_DEFAULT_CHUNK 4096u      /* symbols per chunk (R9)               */
+#define EQ_PROB_BITS 12u            /* table precision M = 2^12                    */
+#define EQ_PAYLOAD_SLACK 16u        /* bytes of readable slack required after a payload    */
+#define EQ_ARENA_ALIGN 256u         /* each decoded layer starts at a multiple of this     */
+
+/* One weight matrix W [rows, cols], bf16 row-major, row = output channel. */
+typedef struct {
+    const void* w;                  /* device, rows*cols bf16                              */
+    int64_t rows, cols;
+} eq_tensor;
+
+typedef struct {
+    uint32_t format;                /* EQ_FMT_E4M3                                         */
+    uint32_t chunk_symbols;         /* 1 .. 262144; default EQ_DEFAULT_CHUNK       */
+    uint32_t prob_bits;             /* must be 12                                          */
+    uint32_t scale_mode;            /* EQ_SCALES_*                                         */
+    double   lambda;                /* Eq. 4 λ ≥ 0, SPEC normalisation (R4)                */
+    int32_t  oct_lo, oct_hi;        /* search bracket, octaves around AbsMax (R5): -1, 20  */
+} eq_params;
+
+/* One compressed transformer block: all its layers in one bitstream with one table
+ * (App. A.1).  Device arrays are caller-allocated; sizes from
+ * eq_encode_bounds().  Host fields describe the layers in block order. */
+typedef struct {
+    uint8_t*  payload;              /* device: chunk streams back to back                 */
+    uint64_t  payload_cap;          /* bytes allocated (must include EQ_PAYLOAD_SLACK)    */
+    uint64_t  payload_bytes;        /* bytes used (set by eq_quantize_encode)             */
+    uint32_t* chunk_off;            /* device: n_chunks+1 byte offsets into payload       */
+    uint32_t  n_chunks;
+    uint32_t  chunk_symbols;        /* chunk length used when encoding                     */
+    uint16_t* freq;                 /* device: 256 normalised frequencies, Σ = 4096       */
+    uint16_t* scales;               /* device: bf16 per-row scales, layers concatenated   */
+    uint32_t  n_layers;
+    int64_t   layer_rows[EQ_MAX_LAYERS];
+    int64_t   layer_cols[EQ_MAX_LAYERS];
+} eq_block;
+
+/* ---------------------------------------------------------------- library info */
+const char* eq_status_string(eq_status s);
+const char* eq_version(void);
+
+/* ---------------------------------------------------------------- sizing (host only)
+ * Sizes for encoding `n_layers` tensors as one block: payload capacity (worst case
+ * 4 + 2 bytes per symbol per chunk, plus slack), chunk count, and the scratch bytes
+ * eq_quantize_encode needs (codes stream + tables + chunk sizes).  EQ_ERR_SHAPE for
+ * rows/cols < 1 or > 2^31, EQ_ERR_ARG for n_layers outside 1..EQ_MAX_LAYERS. */
+eq_status eq_encode_bounds(const eq_tensor* layers, uint32_t n_layers, const eq_params* p,
+                           uint64_t* payload_cap, uint32_t* n_chunks, uint64_t* scratch_bytes);
+
+/* Byte offset of each decoded layer inside an arena holding `n_blocks` blocks, in block
+ * then layer order, each start aligned to EQ_ARENA_ALIGN; elements are 1 (FP8) or 2
+ * (bf16) bytes.  layer_offsets[b*EQ_MAX_LAYERS + l]; *total_bytes = arena size needed. */
+eq_status eq_arena_layout(const eq_block* blocks, uint32_t n_blocks, uint32_t out_dtype,
+                          uint64_t* layer_offsets, uint64_t* total_bytes);
+
+/* ---------------------------------------------------------------- encode-side steps
+ * §8(a) rows a1-a6; each is also used by eq_quantize_encode.  Asynchronous. */
+
+/* a1, Eq. (1), Alg. 1 l.1: s0_i = bf16_rne(max_j |W_ij| / 448); all-zero row -> 1
+ * (S:67).  s0: device [rows] bf16. */
+eq_status eq_absmax(const eq_tensor* w, uint16_t* s0, eq_stream_t stream);
+
+/* Scratch bytes eq_search_scales needs for `w`. */
+uint64_t eq_search_scratch_bytes(const eq_tensor* w);
+
+/* a2, Eq. (4) P:175-188 with R4/R5: for each row i (all rows, or the `n_rows` row indices
+ * in device array `rows`) and each of the `n_lambda` host values lambdas_host[k], the bf16
+ * scale minimising f_i(s) = Σ_j|W_ij − s·v_ij| / ‖W‖₁ + λ_k·Σ_j|v_ij| / (rows·cols) over the
+ * contiguous bf16 patterns in [bf16(s0·2^oct_lo), bf16(s0·2^oct_hi)], smallest s on ties;
+ * all-zero rows keep s = 1.  Outputs (device): scales[k*rows + i] and, if obj != NULL,
+ * obj[k*rows + i] = f_i(s*).  Terms |W − s·v| are exact f32, sums f64 (deterministic
+ * order).  n_lambda ≤ 32. */
+eq_status eq_search_scales(const eq_tensor* w, const double* lambdas_host, uint32_t n_lambda,
+                           int32_t oct_lo, int32_t oct_hi, const uint32_t* rows, uint32_t n_rows,
+                           uint16_t* scales, double* obj, void* scratch, uint64_t scratch_bytes,
+                           eq_stream_t stream);
+
+/* a3 + a4, Alg. 1 l.3: codes = RNE_E4M3(clamp(W/s, ±448)) with
+ * −0 → +0 for all rows (rows == NULL) or the listed rows, written row-major into `codes`
+ * (device, rows*cols bytes; may be NULL to only count), and the 256-bin histogram
+ * ACCUMULATED into hist (device uint64[256]). */
+eq_status eq_quantize_hist(const eq_tensor* w, const uint16_t* scales, const uint32_t* rows,
+                           uint32_t n_rows, uint8_t* codes, uint64_t* hist, eq_stream_t stream);
+
+/* a5 (R8): normalise hist (device uint64[256]) to freq (device uint16[256],
+ * Σ = 4096, every present symbol ≥ 1) by the integer largest-remainder rule.  An empty
+ * histogram sets EQ_EF_EMPTY in d_err. */
+eq_status eq_build_table(const uint64_t* hist, uint16_t* freq, uint32_t* d_err, eq_stream_t stream);
+
+/* a6 (Alg. 1 l.4-5, R9/R10): rANS-encode the concatenated symbol stream `codes`
+ * of the block's layers (sizes rows*cols in block order, from `blk`), chunks of
+ * blk->chunk_symbols restarting at each layer, into blk->payload / blk->chunk_off with
+ * table blk->freq.  chunk_sizes: device scratch uint32[n_chunks].  *payload_bytes_dev
+ * (device uint64) receives the total.  A zero-frequency symbol sets EQ_EF_UNKNOWN_SYMBOL. */
+eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, uint32_t* chunk_sizes,
+                         uint64_t* payload_bytes_dev, uint32_t* d_err, eq_stream_t stream);
+
+/* ---------------------------------------------------------------- north-star calls */
+
+/* Alg. 1 for one block: scales (per p->scale_mode), FP8 quantisation, one
+ * histogram + table over the concatenated stream, chunked rANS.  Fills out->payload,
+ * chunk_off, n_chunks, chunk_symbols, freq, scales (device, caller-allocated per
+ * eq_encode_bounds) and out->payload_bytes.  SYNCHRONOUS: waits for the stream to read
+ * payload_bytes and the device error word.  scratch: device, ≥ *scratch_bytes of
+ * eq_encode_bounds.  EQ_ERR_BUFFER if a capacity is too small. */
+eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_layers, const eq_params* p,
+                             eq_block* out, void* scratch, uint64_t scratch_bytes,
+                             eq_stream_t stream);
+
+/* Alg. 2 l.1-2 + App. A.1 arena: decode every chunk of `n_blocks`
+ * blocks in ONE launch (chunk-parallel, lane per chunk) and write each layer, row-major,
+ * into `arena` at the offsets of eq_arena_layout (views, no copies).  EQ_OUT_BF16 fuses
+ * the dequantiser out = RNE_bf16(s_row · value(code)); EQ_OUT_FP8 writes the codes.
+ * Per-chunk integrity (final state == 2^23, every byte consumed) and offset bounds are
+ * checked on the device and reported in d_err (EQ_EF_CORRUPT / EQ_EF_TRUNCATED).
+ * Asynchronous; EQ_ERR_BUFFER if arena_bytes is below the layout's total. */
+eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks, uint32_t out_dtype,
+                            void* arena, uint64_t arena_bytes, uint32_t* d_err,
+                            eq_stream_t stream);
+
+/* End-to-end variant with HOST buffers: blocks_host[b].payload / chunk_off / freq / scales
+ * are host pointers (pinned for full speed).  Copies them into `workspace` (device,
+ * ≥ eq_decode_host_workspace_bytes), decodes, and copies the decoded arena to arena_host.
+ * All on `stream`; SYNCHRONOUS (returns after the device→host copy, with eq_check). */
+uint64_t eq_decode_host_workspace_bytes(const eq_block* blocks_host, uint32_t n_blocks,
+                                        uint32_t out_dtype);
+eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks, uint32_t out_dtype,
+                                 void* arena_host, uint64_t arena_bytes, void* workspace,
+                                 uint64_t workspace_bytes, eq_stream_t stream);
+
+/* SYNCHRONOUS: waits for `stream`, reads the device error word and maps its first set
+ * bit to a status (EQ_OK when zero). */
+eq_status eq_check(const uint32_t* d_err, eq_stream_t stream);
+
+/* λ for a target rate (one global λ per target entropy; R11).  Estimates
+ * the rate on every `row_stride`-th row of the given layers (all treated as one layer
+ * set) as histogram entropy + per-parameter side information, over a log-spaced λ grid
+ * refined twice.  SYNCHRONOUS.  scratch ≥ eq_calibrate_scratch_bytes.  Returns
+ * EQ_ERR_UNREACHABLE_TARGET if the target lies outside the rates of λ ∈ [0, 1e6]. */
+uint64_t eq_calibrate_scratch_bytes(const eq_tensor* layers, uint32_t n_layers, uint32_t row_stride);
+eq_status eq_calibrate_lambda(const eq_tensor* layers, uint32_t n_layers, const eq_params* p,
+                              double target_bits, uint32_t row_stride, double* lambda_out,
+                              double* est_bits_out, void* scratch, uint64_t scratch_bytes,
+                              eq_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENTQUANT_H */

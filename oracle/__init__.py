@@ -75,6 +75,7 @@ def lib():
             "eqo_encode_block": (i64, [P, P, i32, i64, P, P, i64, P]),
             "eqo_decode_block": (ctypes.c_int, [P, P, P, i32, i64, P, P]),
             "eqo_decode_chunks_mt": (ctypes.c_int, [P, P, P, P, i64, P, P, ctypes.c_int]),
+            "eqo_decode_dequant_layer_mt": (ctypes.c_int, [P, P, i64, i64, i64, i64, P, P, P, ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -351,3 +352,17 @@ def decode_chunks_mt(payload: np.ndarray, chunk_off: np.ndarray, sym0: np.ndarra
                                     _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(out), threads)
     if st:
         raise ValueError({1: "corrupt", 2: "truncated"}[st])
+
+
+def decode_dequant_layer_mt(payload: np.ndarray, chunk_off: np.ndarray, cs: int, rows: int, cols: int,
+                            scales: np.ndarray, freq: np.ndarray, threads: int) -> np.ndarray:
+    """Alg. 2 l.1-2 for one layer's chunks on ``threads`` host threads (CPU baseline)."""
+    payload = np.ascontiguousarray(payload, dtype=np.uint8)
+    off = np.ascontiguousarray(chunk_off, dtype=np.uint32)
+    out = np.zeros(rows * cols, dtype=np.uint16)
+    st = lib().eqo_decode_dequant_layer_mt(_p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
+                                           _p(np.ascontiguousarray(scales, dtype=np.uint16)),
+                                           _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(out), threads)
+    if st:
+        raise ValueError({1: "corrupt", 2: "truncated"}[st])
+    return out.reshape(rows, cols)

@@ -1,0 +1,60 @@
+// common.cuh — shared device helpers of libentquant (sm_100a).  No code here is shared
+// with the oracle (oracle/ is a separate CPU program).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp8.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/entquant.h"
+
+namespace eq {
+
+constexpr uint32_t kL = 1u << 23;            // rANS lower bound (R9)
+constexpr uint32_t kProbBits = 12;
+constexpr uint32_t kM = 1u << kProbBits;
+constexpr float kQmax = 448.0f;              // E4M3 Q_max
+
+#define EQ_CUDA_TRY(expr)                                   \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) return EQ_ERR_CUDA;          \
+    } while (0)
+
+#define EQ_TRY(expr)                                        \
+    do {                                                    \
+        eq_status _s = (expr);                              \
+        if (_s != EQ_OK) return _s;                         \
+    } while (0)
+
+__device__ __forceinline__ float bf16_bits_to_float(uint32_t b) {
+    return __uint_as_float(b << 16);
+}
+
+// round-to-nearest-even f32 -> bf16 bits (hardware cvt.rn.bf16.f32; subnormals kept)
+__device__ __forceinline__ uint16_t float_to_bf16_bits(float f) {
+    __nv_bfloat16 h = __float2bfloat16_rn(f);
+    return *reinterpret_cast<uint16_t*>(&h);
+}
+
+// Two E4M3 codes (lo byte = first) from two floats: cvt.rn.satfinite.e4m3x2.f32, which
+// clamps to ±448 before rounding (R2) and rounds to nearest even; then −0 (0x80) -> +0.
+__device__ __forceinline__ uint32_t e4m3x2_from_float2(float a, float b) {
+    __nv_fp8x2_storage_t p = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+    uint32_t u = (uint32_t)p;
+    if ((u & 0xFFu) == 0x80u) u &= 0xFF00u;
+    if ((u & 0xFF00u) == 0x8000u) u &= 0x00FFu;
+    return u;
+}
+
+// Two E4M3 codes (packed lo/hi byte) to two exact floats via the f16 path (exact).
+__device__ __forceinline__ float2 e4m3x2_to_float2(uint32_t pair) {
+    __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(pair & 0xFFFFu), __NV_E4M3);
+    __half2 hh = *reinterpret_cast<__half2*>(&h);
+    return __half22float2(hh);
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+}  // namespace eq

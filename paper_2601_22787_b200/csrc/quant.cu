@@ -1,0 +1,315 @@
+// quant.cu — §8(a) rows a1-a4 on sm_100a:
+//   a1 AbsMax init (Eq. 1; Alg. 1 l.1)
+//   a2 per-row scale search minimising Eq. 4 over bf16 candidates (R4, R5)
+//   a3 FP8-E4M3 quantisation (clamp before RNE, −0 → +0 per P:509)
+//   a4 256-bin symbol histogram (metadata ℳ) fused into a3
+#include "common.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+namespace eq {
+
+constexpr int kRedThreads = 256;
+constexpr int kSearchThreads = 256;
+constexpr int kMaxLambda = 32;
+
+// ---------------------------------------------------------------- a1: AbsMax
+// |max| of a bf16 row is exact in f32; s0 = bf16(max/448): the f32 quotient is within
+// 2^-24 of the exact one and m/448 (m with 8 significant bits) is never within 2^-12
+// (relative) of a bf16 rounding midpoint unless exact, so bf16(fl32(max/448)) is the
+// exact RNE.  All-zero row -> 1.0.
+__device__ __forceinline__ uint16_t absmax_from_max(float m) {
+    return m == 0.f ? (uint16_t)0x3F80u : float_to_bf16_bits(__fdiv_rn(m, kQmax));
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+k_absmax(const uint16_t* __restrict__ W, int64_t rows, int64_t cols, uint16_t* __restrict__ s0) {
+    const int64_t r = blockIdx.x;
+    if (r >= rows) return;
+    const uint16_t* row = W + r * cols;
+    uint32_t m = 0;                      // max of |w| bit patterns (monotone for |bf16|)
+    for (int64_t j = threadIdx.x; j < cols; j += kRedThreads) m = max(m, (uint32_t)(row[j] & 0x7FFFu));
+    #pragma unroll
+    for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, d));
+    __shared__ uint32_t wm[kRedThreads / 32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kRedThreads / 32; ++w) m = max(m, wm[w]);
+        s0[r] = absmax_from_max(bf16_bits_to_float(m));
+    }
+}
+
+// ---------------------------------------------------------------- ‖W‖₁ (deterministic)
+// Stage 1: each CTA sums a fixed range in a fixed tree order (f64); stage 2 sums the
+// partials in index order.  Bitwise reproducible run to run.
+__global__ void __launch_bounds__(kRedThreads)
+k_l1_partial(const uint16_t* __restrict__ W, int64_t n, int64_t per_cta, double* __restrict__ part) {
+    const int64_t a = (int64_t)blockIdx.x * per_cta, b = min(n, a + per_cta);
+    double s = 0.0;
+    for (int64_t j = a + threadIdx.x; j < b; j += kRedThreads) s += (double)fabsf(bf16_bits_to_float(W[j]));
+    #pragma unroll
+    for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, d);
+    __shared__ double ws[kRedThreads / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) t += ws[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_l1_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += part[i];
+        *out = t;
+    }
+}
+
+// ---------------------------------------------------------------- a2: scale search
+struct SearchParams {
+    const uint16_t* W;
+    int64_t rows, cols;
+    const uint32_t* row_list;   // nullable
+    uint32_t n_rows;
+    int32_t oct_lo, oct_hi;
+    uint32_t n_lambda;
+    double lambda[kMaxLambda];
+    const double* l1;           // device ‖W‖₁
+    uint16_t* scales;           // [n_lambda][rows]
+    double* obj;                // [n_lambda][rows] or null
+};
+
+// one exact term pair: |w − s·v| in f32 (exact: see DESIGN.md §6 K-SRCH), |v|·512 integer
+__device__ __forceinline__ void term2(float w0, float w1, float s, double& D, uint32_t& R) {
+    const uint32_t q = e4m3x2_from_float2(__fdiv_rn(w0, s), __fdiv_rn(w1, s));
+    const float2 v = e4m3x2_to_float2(q);
+    D += (double)fabsf(__fsub_rn(w0, __fmul_rn(s, v.x)));
+    D += (double)fabsf(__fsub_rn(w1, __fmul_rn(s, v.y)));
+    R += (uint32_t)__fmul_rn(fabsf(v.x), 512.f) + (uint32_t)__fmul_rn(fabsf(v.y), 512.f);
+}
+
+__device__ __forceinline__ bool better(double f, uint32_t k, double bf, uint32_t bk) {
+    return f < bf || (f == bf && k < bk);
+}
+
+// One CTA per searched row.  The row is staged in shared memory as f32 (exact bf16
+// values); warps take candidates k = warp, warp+8, ...; lanes stride over the row; warp
+// reduction in fixed order; per-λ best kept by lane 0, merged over warps at the end.
+__global__ void __launch_bounds__(kSearchThreads)
+k_search(const __grid_constant__ SearchParams P) {
+    extern __shared__ float srow[];
+    __shared__ double bestf[kSearchThreads / 32][kMaxLambda];
+    __shared__ uint32_t bestk[kSearchThreads / 32][kMaxLambda];
+    __shared__ uint32_t s_max;
+
+    const uint32_t ri = blockIdx.x;
+    if (ri >= P.n_rows) return;
+    const int64_t r = P.row_list ? (int64_t)P.row_list[ri] : (int64_t)ri;
+    const int64_t N = P.cols;
+    const uint16_t* row = P.W + r * N;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+    if (t == 0) s_max = 0;
+    __syncthreads();
+    uint32_t m = 0;
+    for (int64_t j = t; j < N; j += kSearchThreads) {
+        uint16_t b = row[j];
+        srow[j] = bf16_bits_to_float(b);
+        m = max(m, (uint32_t)(b & 0x7FFFu));
+    }
+    if (N & 1) if (t == 0) srow[N] = 0.f;          // pad for pairwise processing
+    #pragma unroll
+    for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, d));
+    if (lane == 0) atomicMax(&s_max, m);
+    __syncthreads();
+    m = s_max;
+    const uint16_t s0 = absmax_from_max(bf16_bits_to_float(m));
+    if (m == 0) {                                   // all-zero row keeps s = 1
+        if (t < (int)P.n_lambda) {
+            P.scales[(int64_t)t * P.rows + r] = 0x3F80u;
+            if (P.obj) P.obj[(int64_t)t * P.rows + r] = 0.0;
+        }
+        return;
+    }
+    // candidate bracket: bf16(s0·2^oct_lo) .. bf16(s0·2^oct_hi), clamped to finite > 0
+    const float s0f = bf16_bits_to_float(s0);
+    int lo = float_to_bf16_bits(ldexpf(s0f, P.oct_lo)), hi = float_to_bf16_bits(ldexpf(s0f, P.oct_hi));
+    lo = max(lo, 1);
+    hi = min(hi, 0x7F7F);
+    if (hi < lo) hi = lo;
+    const uint32_t nc = (uint32_t)(hi - lo + 1);
+
+    const double l1 = *P.l1;
+    const double mn = (double)P.rows * (double)N;
+    double my_bf[kMaxLambda];
+    uint32_t my_bk[kMaxLambda];
+    for (uint32_t q = 0; q < P.n_lambda; ++q) { my_bf[q] = INFINITY; my_bk[q] = 0xFFFFFFFFu; }
+
+    const int64_t npair = (N + 1) >> 1;
+    for (uint32_t k = warp; k < nc; k += kSearchThreads / 32) {
+        const float s = bf16_bits_to_float((uint32_t)(lo + (int)k));
+        double D = 0.0;
+        uint32_t R = 0;
+        for (int64_t p = lane; p < npair; p += 32) {
+            const float2 w = reinterpret_cast<const float2*>(srow)[p];
+            term2(w.x, w.y, s, D, R);
+        }
+        unsigned long long R64 = R;                 // a 28672-wide row overflows u32
+        #pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            D += __shfl_xor_sync(0xFFFFFFFFu, D, d);
+            R64 += __shfl_xor_sync(0xFFFFFFFFu, R64, d);
+        }
+        // exact pad term: a zero pad quantises to 0 with zero error, adds nothing
+        if (lane == 0) {
+            // same operation order as Eq. 4 in the oracle: D/‖W‖₁ + (λ·R)/(M·N)
+            const double Dd = l1 > 0.0 ? D / l1 : 0.0, Rd = (double)R64 * (1.0 / 512.0);
+            for (uint32_t q = 0; q < P.n_lambda; ++q) {
+                const double f = Dd + P.lambda[q] * Rd / mn;
+                if (better(f, k, my_bf[q], my_bk[q])) { my_bf[q] = f; my_bk[q] = k; }
+            }
+        }
+    }
+    if (lane == 0)
+        for (uint32_t q = 0; q < P.n_lambda; ++q) { bestf[warp][q] = my_bf[q]; bestk[warp][q] = my_bk[q]; }
+    __syncthreads();
+    if (t < (int)P.n_lambda) {
+        double bf = bestf[0][t];
+        uint32_t bk = bestk[0][t];
+        for (int w = 1; w < kSearchThreads / 32; ++w)
+            if (better(bestf[w][t], bestk[w][t], bf, bk)) { bf = bestf[w][t]; bk = bestk[w][t]; }
+        P.scales[(int64_t)t * P.rows + r] = (uint16_t)(lo + (int)bk);
+        if (P.obj) P.obj[(int64_t)t * P.rows + r] = bf;
+    }
+}
+
+// ---------------------------------------------------------------- a3 + a4
+// Quantise (exact-rounded f32 quotient -> cvt.rn.satfinite.e4m3) and histogram with
+// per-warp shared sub-histograms; the dominant zero symbol is counted in a register.
+constexpr int kQhThreads = 256;
+
+__global__ void __launch_bounds__(kQhThreads)
+k_quant_hist(const uint16_t* __restrict__ W, int64_t rows, int64_t cols, const uint16_t* __restrict__ S,
+             const uint32_t* __restrict__ row_list, uint32_t n_rows, uint8_t* __restrict__ codes,
+             unsigned long long* __restrict__ hist) {
+    __shared__ uint32_t h[kQhThreads / 32][256];
+    const int t = threadIdx.x, warp = t >> 5;
+    for (int i = t; i < (kQhThreads / 32) * 256; i += kQhThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t zeros = 0;
+    // CTAs stride over rows (in row-list order); threads stride over column pairs
+    const int64_t npair = (cols + 1) >> 1;
+    for (int64_t ri = blockIdx.x; ri < (int64_t)n_rows; ri += gridDim.x) {
+        const int64_t r = row_list ? (int64_t)row_list[ri] : ri;
+        const float s = bf16_bits_to_float(S[r]);
+        const uint16_t* wr = W + r * cols;
+        uint8_t* cr = codes ? codes + r * cols : nullptr;
+        for (int64_t p = t; p < npair; p += kQhThreads) {
+            const int64_t j = 2 * p;
+            const float w0 = bf16_bits_to_float(wr[j]);
+            const bool two = (j + 1 < cols);
+            const float w1 = two ? bf16_bits_to_float(wr[j + 1]) : 0.f;
+            const uint32_t q = e4m3x2_from_float2(__fdiv_rn(w0, s), __fdiv_rn(w1, s));
+            const uint32_t c0 = q & 0xFFu, c1 = q >> 8;
+            if (cr) {
+                cr[j] = (uint8_t)c0;
+                if (two) cr[j + 1] = (uint8_t)c1;
+            }
+            if (c0 == 0) ++zeros; else atomicAdd(&h[warp][c0], 1u);
+            if (two) { if (c1 == 0) ++zeros; else atomicAdd(&h[warp][c1], 1u); }
+        }
+    }
+    #pragma unroll
+    for (int d = 16; d > 0; d >>= 1) zeros += __shfl_xor_sync(0xFFFFFFFFu, zeros, d);
+    if ((t & 31) == 0) atomicAdd(&h[warp][0], zeros);
+    __syncthreads();
+    for (int c = t; c < 256; c += kQhThreads) {
+        unsigned long long v = 0;
+        for (int w = 0; w < kQhThreads / 32; ++w) v += h[w][c];
+        if (v) atomicAdd(hist + c, v);
+    }
+}
+
+}  // namespace eq
+
+using namespace eq;
+
+static eq_status check_tensor(const eq_tensor* w) {
+    if (!w || !w->w) return EQ_ERR_ARG;
+    if (w->rows < 1 || w->cols < 1 || w->rows > (1ll << 31) || w->cols > (1ll << 31)) return EQ_ERR_SHAPE;
+    return EQ_OK;
+}
+
+extern "C" eq_status eq_absmax(const eq_tensor* w, uint16_t* s0, eq_stream_t stream) {
+    EQ_TRY(check_tensor(w));
+    if (!s0) return EQ_ERR_ARG;
+    k_absmax<<<(unsigned)w->rows, kRedThreads, 0, (cudaStream_t)stream>>>(
+        (const uint16_t*)w->w, w->rows, w->cols, s0);
+    EQ_CUDA_TRY(cudaGetLastError());
+    return EQ_OK;
+}
+
+static int l1_ctas(int64_t n) { return (int)std::min<int64_t>(1184, (n + 4095) / 4096); }
+
+extern "C" uint64_t eq_search_scratch_bytes(const eq_tensor* w) {
+    if (!w) return 0;
+    return 256 + 8ull * (uint64_t)l1_ctas(w->rows * w->cols);
+}
+
+extern "C" eq_status eq_search_scales(const eq_tensor* w, const double* lambdas_host, uint32_t n_lambda,
+                                      int32_t oct_lo, int32_t oct_hi, const uint32_t* rows, uint32_t n_rows,
+                                      uint16_t* scales, double* obj, void* scratch, uint64_t scratch_bytes,
+                                      eq_stream_t stream) {
+    EQ_TRY(check_tensor(w));
+    if (!lambdas_host || n_lambda == 0 || n_lambda > (uint32_t)kMaxLambda || !scales || !scratch) return EQ_ERR_ARG;
+    if (oct_hi < oct_lo || oct_lo < -40 || oct_hi > 40) return EQ_ERR_ARG;
+    for (uint32_t q = 0; q < n_lambda; ++q)
+        if (!(lambdas_host[q] >= 0.0)) return EQ_ERR_ARG;
+    if (scratch_bytes < eq_search_scratch_bytes(w)) return EQ_ERR_BUFFER;
+    const int64_t n = w->rows * w->cols;
+    const uint64_t smem = (uint64_t)((w->cols + 2) & ~1ll) * 4;
+    if (smem > 200 * 1024) return EQ_ERR_SHAPE;            // rows up to 51200 columns
+    cudaStream_t st = (cudaStream_t)stream;
+    double* l1 = (double*)scratch;
+    double* part = (double*)((char*)scratch + 256);
+    const int nct = l1_ctas(n);
+    const int64_t per = (n + nct - 1) / nct;
+    k_l1_partial<<<nct, kRedThreads, 0, st>>>((const uint16_t*)w->w, n, per, part);
+    k_l1_final<<<1, 32, 0, st>>>(part, nct, l1);
+    SearchParams P;
+    P.W = (const uint16_t*)w->w;
+    P.rows = w->rows;
+    P.cols = w->cols;
+    P.row_list = rows;
+    P.n_rows = rows ? n_rows : (uint32_t)w->rows;
+    P.oct_lo = oct_lo;
+    P.oct_hi = oct_hi;
+    P.n_lambda = n_lambda;
+    for (int q = 0; q < kMaxLambda; ++q) P.lambda[q] = q < (int)n_lambda ? lambdas_host[q] : 0.0;
+    P.l1 = l1;
+    P.scales = scales;
+    P.obj = obj;
+    if (P.n_rows == 0) return EQ_OK;
+    EQ_CUDA_TRY(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_search<<<P.n_rows, kSearchThreads, smem, st>>>(P);
+    EQ_CUDA_TRY(cudaGetLastError());
+    return EQ_OK;
+}
+
+extern "C" eq_status eq_quantize_hist(const eq_tensor* w, const uint16_t* scales, const uint32_t* rows,
+                                      uint32_t n_rows, uint8_t* codes, uint64_t* hist, eq_stream_t stream) {
+    EQ_TRY(check_tensor(w));
+    if (!scales || !hist) return EQ_ERR_ARG;
+    const uint32_t nr = rows ? n_rows : (uint32_t)w->rows;
+    if (nr == 0) return EQ_OK;
+    const int ctas = (int)std::min<int64_t>(148 * 8, nr);
+    k_quant_hist<<<ctas, kQhThreads, 0, (cudaStream_t)stream>>>((const uint16_t*)w->w, w->rows, w->cols, scales,
+                                                                 rows, nr, codes, (unsigned long long*)hist);
+    EQ_CUDA_TRY(cudaGetLastError());
+    return EQ_OK;
+}

@@ -1,0 +1,189 @@
+// rans_enc.cu — §8(a) row a6: per-chunk byte-wise rANS encoding (Alg. 1 l.4-5, P:212-213;
+// S:316-324) of the block's concatenated E4M3 symbol stream (App. A.1).
+// Wire format (R9): 32-bit state, L = 2^23, M = 2^12, cum in code order; per chunk the
+// symbols are coded in reverse from x = L, bytes emitted while x ≥ ((L>>12)<<8)·f; the
+// final state is stored first (little-endian), followed by the renormalisation bytes in
+// decode order.  Chunks of cs symbols restart at each layer start (R10).
+//
+// Two passes, one thread per chunk: (1) exact byte count per chunk, (2) exclusive scan
+// into chunk offsets, (3) encode again writing back-to-front straight into the final
+// payload position — no worst-case scratch, no compaction copy.
+#include "common.cuh"
+
+#include <algorithm>
+
+namespace eq {
+
+constexpr int kEncThreads = 128;
+
+struct EncParams {
+    const uint8_t* codes;
+    uint8_t* payload;
+    uint32_t* chunk_off;
+    uint32_t* sizes;
+    const uint16_t* freq;
+    uint32_t* err;
+    unsigned long long* total;
+    uint64_t payload_cap;
+    uint32_t n_chunks;
+    uint32_t cs;
+    uint32_t n_layers;
+    uint32_t chunk0[EQ_MAX_LAYERS + 1];
+    uint64_t sym_base[EQ_MAX_LAYERS];
+    uint64_t size[EQ_MAX_LAYERS];
+};
+
+__device__ __forceinline__ void chunk_range(const EncParams& P, uint32_t c, uint64_t& base, uint32_t& n) {
+    uint32_t l = 0;
+    while (l + 1 < P.n_layers && c >= P.chunk0[l + 1]) ++l;
+    const uint64_t a = (uint64_t)(c - P.chunk0[l]) * P.cs;
+    base = P.sym_base[l] + a;
+    n = (uint32_t)min((uint64_t)P.cs, P.size[l] - a);
+}
+
+__device__ __forceinline__ void load_table(const EncParams& P, uint32_t* sf, uint32_t* scum) {
+    // sf[s] = freq, scum[s] = cumulative (code order); one warp scans, others wait
+    if (threadIdx.x < 32) {
+        uint32_t run = 0;
+        for (int b = 0; b < 256; b += 32) {
+            uint32_t f = P.freq[b + threadIdx.x], v = f;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+                if ((int)threadIdx.x >= d) v += o;
+            }
+            sf[b + threadIdx.x] = f;
+            scum[b + threadIdx.x] = run + v - f;
+            run += __shfl_sync(0xFFFFFFFFu, v, 31);
+        }
+    }
+    __syncthreads();
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ EncParams P) {
+    __shared__ uint32_t sf[256], scum[256];
+    load_table(P, sf, scum);
+    const uint32_t c = blockIdx.x * kEncThreads + threadIdx.x;
+    if (c >= P.n_chunks) return;
+    uint64_t base;
+    uint32_t n;
+    chunk_range(P, c, base, n);
+    const uint8_t* sym = P.codes + base;
+    uint8_t* dst = nullptr;
+    uint64_t end = 0, beg = 0;
+    if (WRITE) {
+        beg = P.chunk_off[c];
+        end = P.chunk_off[c + 1];
+        if (end + EQ_PAYLOAD_SLACK > P.payload_cap) {
+            atomicOr(P.err, EQ_EF_BUFFER);
+            return;
+        }
+        dst = P.payload + end;
+    }
+    uint32_t x = kL, bytes = 0;
+    for (int64_t i = (int64_t)n - 1; i >= 0; --i) {
+        const uint32_t s = sym[i];
+        const uint32_t f = sf[s];
+        if (f == 0) {
+            atomicOr(P.err, EQ_EF_UNKNOWN_SYMBOL);
+            break;
+        }
+        const uint32_t x_max = ((kL >> kProbBits) << 8) * f;
+        while (x >= x_max) {
+            if (WRITE) *--dst = (uint8_t)(x & 0xFFu);
+            ++bytes;
+            x >>= 8;
+        }
+        x = (x / f) * kM + (x % f) + scum[s];
+    }
+    if (WRITE) {
+        if (end - beg != (uint64_t)bytes + 4) {
+            atomicOr(P.err, EQ_EF_BUFFER);
+            return;
+        }
+        dst -= 4;
+        dst[0] = (uint8_t)x;
+        dst[1] = (uint8_t)(x >> 8);
+        dst[2] = (uint8_t)(x >> 16);
+        dst[3] = (uint8_t)(x >> 24);
+    } else {
+        P.sizes[c] = bytes + 4;
+    }
+}
+
+// exclusive scan of sizes -> chunk_off[0..n], total; one CTA, fixed segments (deterministic)
+__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ sizes, uint32_t n,
+                                               uint32_t* __restrict__ off, unsigned long long* total,
+                                               uint32_t* err) {
+    __shared__ unsigned long long part[1024];
+    const uint32_t t = threadIdx.x;
+    const uint32_t per = (n + 1023) / 1024;
+    const uint32_t a = min(n, t * per), b = min(n, a + per);
+    unsigned long long s = 0;
+    for (uint32_t i = a; i < b; ++i) s += sizes[i];
+    part[t] = s;
+    __syncthreads();
+    for (uint32_t d = 1; d < 1024; d <<= 1) {       // Hillis-Steele inclusive scan
+        unsigned long long v = t >= d ? part[t - d] : 0ull;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    unsigned long long run = t ? part[t - 1] : 0ull;
+    for (uint32_t i = a; i < b; ++i) {
+        if (run > 0xFFFFFFFFull) atomicOr(err, EQ_EF_BUFFER);
+        off[i] = (uint32_t)run;
+        run += sizes[i];
+    }
+    if (t == 1023) {
+        off[n] = (uint32_t)part[1023];
+        *total = part[1023];
+        if (part[1023] > 0xFFFFFFFFull) atomicOr(err, EQ_EF_BUFFER);
+    }
+}
+
+}  // namespace eq
+
+using namespace eq;
+
+extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, uint32_t* chunk_sizes,
+                                    uint64_t* payload_bytes_dev, uint32_t* d_err, eq_stream_t stream) {
+    if (!codes || !blk || !chunk_sizes || !payload_bytes_dev || !d_err) return EQ_ERR_ARG;
+    if (!blk->payload || !blk->chunk_off || !blk->freq) return EQ_ERR_ARG;
+    if (blk->n_layers == 0 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
+    if (blk->chunk_symbols == 0 || blk->chunk_symbols > 262144u) return EQ_ERR_ARG;
+    EncParams P;
+    memset(&P, 0, sizeof(P));
+    P.codes = codes;
+    P.payload = blk->payload;
+    P.chunk_off = blk->chunk_off;
+    P.sizes = chunk_sizes;
+    P.freq = blk->freq;
+    P.err = d_err;
+    P.total = (unsigned long long*)payload_bytes_dev;
+    P.payload_cap = blk->payload_cap;
+    P.cs = blk->chunk_symbols;
+    P.n_layers = blk->n_layers;
+    uint64_t base = 0;
+    uint32_t chunk = 0;
+    for (uint32_t l = 0; l < blk->n_layers; ++l) {
+        if (blk->layer_rows[l] < 1 || blk->layer_cols[l] < 1) return EQ_ERR_SHAPE;
+        const uint64_t sz = (uint64_t)blk->layer_rows[l] * (uint64_t)blk->layer_cols[l];
+        P.chunk0[l] = chunk;
+        P.sym_base[l] = base;
+        P.size[l] = sz;
+        chunk += (uint32_t)((sz + P.cs - 1) / P.cs);
+        base += sz;
+    }
+    P.chunk0[blk->n_layers] = chunk;
+    if (chunk != blk->n_chunks) return EQ_ERR_SHAPE;
+    P.n_chunks = chunk;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = (chunk + kEncThreads - 1) / kEncThreads;
+    k_encode<false><<<g, kEncThreads, 0, st>>>(P);
+    k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
+    k_encode<true><<<g, kEncThreads, 0, st>>>(P);
+    EQ_CUDA_TRY(cudaGetLastError());
+    return EQ_OK;
+}
