@@ -60,7 +60,7 @@ typedef enum {
 #define EQ_MAX_LAYERS 8             /* layers per block (a Llama block has 7)              */
 #define EQ_DEFAULT_CHUNK 4096u      /* symbols per chunk (R9)               */
 #define EQ_PROB_BITS 12u            /* table precision M = 2^12                    */
-#define EQ_PAYLOAD_SLACK 16u        /* bytes of readable slack required after a payload    */
+#define EQ_PAYLOAD_SLACK 256u       /* bytes of readable slack required after a payload    */
 #define EQ_ARENA_ALIGN 256u         /* each decoded layer starts at a multiple of this     */
 
 /* One weight matrix W [rows, cols], bf16 row-major, row = output channel. */

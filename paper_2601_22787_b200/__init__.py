@@ -18,7 +18,8 @@ from dataclasses import dataclass, field
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libentquant.so")
+# EQ_LIB selects an alternative in-tree build (used only for A/B kernel experiments)
+LIB_PATH = os.environ.get("EQ_LIB") or os.path.join(_HERE, "libentquant.so")
 
 EQ_OK, EQ_ERR_ARG, EQ_ERR_SHAPE, EQ_ERR_EMPTY, EQ_ERR_BUFFER = 0, 1, 2, 3, 4
 EQ_ERR_CORRUPT, EQ_ERR_TRUNCATED, EQ_ERR_UNKNOWN_SYMBOL, EQ_ERR_UNREACHABLE_TARGET, EQ_ERR_CUDA = 5, 6, 7, 8, 9
@@ -28,7 +29,7 @@ EQ_SCALES_SEARCH, EQ_SCALES_ABSMAX, EQ_SCALES_GIVEN = 0, 1, 2
 EQ_MAX_LAYERS = 8
 EQ_DEFAULT_CHUNK = 4096
 EQ_PROB_BITS = 12
-EQ_PAYLOAD_SLACK = 16
+EQ_PAYLOAD_SLACK = 256
 EQ_ARENA_ALIGN = 256
 
 EXPORTS = (

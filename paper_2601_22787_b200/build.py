@@ -29,24 +29,28 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), so: str | None = None) -> str:
+    """Compile and link.  ``defines``/``so`` produce alternative builds for A/B experiments."""
+    target = so or SO
+    if not force and not defines and not stale():
         return SO
     objs = []
     for s in SOURCES:
         o = os.path.join(CSRC, s.replace(".cu", ".o"))
-        cmd = [_nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
+        cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
         objs.append(o)
-    subprocess.check_call([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", SO + ".tmp",
+    subprocess.check_call([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", target + ".tmp",
                            *objs, "-cudart", "static"])
-    os.replace(SO + ".tmp", SO)
+    os.replace(target + ".tmp", target)
     for o in objs:
         os.remove(o)
-    return SO
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[len("--so="):] for a in sys.argv[1:] if a.startswith("--so=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, so=outs[0] if outs else None))

@@ -54,39 +54,75 @@ struct DecParams {
 };
 
 // ---------------------------------------------------------------- per-lane bit reader
+// Upcoming payload bits, most significant first, in a 64-bit window (hi:lo) holding nb
+// valid bits.  A symbol consumes k ∈ {0,8,16} bits with funnel shifts (branch-free);
+// refill() runs after every PAIR of symbols and restores nb ≥ 32.
+// The lane's compressed bytes are staged in a 64-byte shared-memory ring by cp.async
+// (16-byte segments issued warp-uniformly every 8 symbols, ≥ 8 symbols before use), so
+// no register ever waits on a global load (the warp-level scoreboard would otherwise
+// serialise the lanes' independent refills).
+constexpr int kRingWords = 16;
 struct BitReader {
-    uint64_t bb;           // upcoming bits, next byte in bits 63..56
-    int nb;                // valid bits in bb
-    uint32_t used;         // payload bits consumed after the 4-byte state
-    const uint32_t* wp;    // next aligned word
-    const uint32_t* wend;  // first word that must not be read
+    uint32_t hi, lo;
+    int nb;
+    uint32_t wi4;          // 4 × (absolute index of the next payload word to insert)
+    uint32_t gs;           // next 16-byte payload segment to stage
+    uint32_t ring;         // shared address of this lane's ring (64-byte aligned)
 
-    __device__ __forceinline__ uint32_t load_word() {
-        uint32_t w = (wp < wend) ? __ldg(wp) : 0u;
-        ++wp;
-        return bswap32(w);
-    }
     __device__ __forceinline__ void refill() {
-        if (nb <= 32) {
-            bb |= (uint64_t)load_word() << (32 - nb);
+        if (nb < 32) {                              // predicated, not a divergent branch
+            uint32_t w;
+            asm("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(ring | (wi4 & 0x3Cu)));
+            w = bswap32(w);
+            hi |= w >> nb;                          // lo is empty when nb < 32
+            lo = __funnelshift_r(0u, w, nb);        // = w << (32 − nb)
             nb += 32;
+            wi4 += 4;
         }
     }
 };
 
-__device__ __forceinline__ uint32_t decode_one(uint32_t& x, BitReader& br, const uint32_t* lut) {
-    uint32_t e = lut[x & (kM - 1)];
-    uint32_t xs = x >> kProbBits;
-    x = ((e >> 8) & 0xFFFu) * xs + xs + (e >> 20);
-    if (x < kL) {
-        uint32_t k = (x < (1u << 15)) ? 16u : 8u;
-        x = (x << k) | (uint32_t)(br.bb >> (64 - k));
-        br.bb <<= k;
-        br.nb -= (int)k;
-        br.used += k;
-        br.refill();
+__device__ __forceinline__ void stage_segment(uint32_t ring, const uint8_t* payload, uint32_t seg) {
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(ring | ((seg & 3u) << 4)),
+                 "l"(payload + (uint64_t)seg * 16));
+}
+__device__ __forceinline__ void stage_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void stage_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Every 8 symbols: the copies of the previous boundary have landed (wait_all); stage one
+// more segment if fewer than 13 words lie ahead of the reader (≤ 4 words are consumed per
+// 8 symbols, so the words needed before the next boundary are always already landed and
+// the ring never overwrites an unread word).
+__device__ __forceinline__ void ring_boundary(BitReader& br, const uint8_t* payload) {
+    stage_wait_all();
+    if (br.gs * 16u <= br.wi4 + 48u) {
+        stage_segment(br.ring, payload, br.gs);
+        ++br.gs;
     }
-    return e & 0xFFu;
+    stage_commit();
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// One rANS decode step (Alg. 2 l.1): slot lookup, state update, byte renormalisation.
+// LUT entry e: sym | (f−1) << 8 | (slot − c_sym) << 20; returns e (sym in the low byte).
+// Field extraction and x>>12 use IMAD.HI (FMA pipe) to balance the integer ALU pipe.
+__device__ __forceinline__ uint32_t decode_one(uint32_t& x, BitReader& br, uint32_t lut_s) {
+    const uint32_t e = lds_u32(lut_s + (x & (kM - 1)) * 4u);
+    const uint32_t xs = __umulhi(x, 1u << 20);             // x >> 12
+    const uint32_t fm1 = __umulhi(e << 12, 1u << 12);      // (e >> 8) & 0xFFF
+    x = fm1 * xs + (xs + (e >> 20));                       // f·⌊x/M⌋ + slot − c
+    // bytes to read: 0 if x ≥ 2^23, 1 if x ≥ 2^15, else 2 (after a step x ≥ 2^11)
+    const uint32_t k = (uint32_t)(__clz(x) - 1) & 0x18u;
+    x = __funnelshift_lc(br.hi, x, k);
+    br.hi = __funnelshift_lc(br.lo, br.hi, k);
+    br.lo = br.lo << k;
+    br.nb -= (int)k;
+    return e;
 }
 
 template <bool BF16>
@@ -98,6 +134,37 @@ __device__ __forceinline__ void store_one(uint8_t* out, uint64_t i, uint32_t sym
     } else {
         out[i] = (uint8_t)sym;
     }
+}
+
+// decoded output is written once and never re-read by this kernel: evict-first in L2 so
+// it does not push the (re-read) compressed input out of the cache
+#ifndef EQ_CS_STORES
+#define EQ_CS_STORES 1
+#endif
+__device__ __forceinline__ void st_out(uint4* p, uint4 v) {
+#if EQ_CS_STORES
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
+// 4 symbols -> one word of codes (first symbol in the low byte), two refills
+__device__ __forceinline__ uint32_t decode4(uint32_t& x, BitReader& br, uint32_t lut_s) {
+    const uint32_t a = decode_one(x, br, lut_s);
+    const uint32_t b = decode_one(x, br, lut_s);
+    br.refill();
+    const uint32_t c = decode_one(x, br, lut_s);
+    const uint32_t d = decode_one(x, br, lut_s);
+    br.refill();
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// Q† on two codes: exact e4m3 -> f32, one exact f32 product each, one RNE to bf16 each
+__device__ __forceinline__ uint32_t dequant2(uint32_t pair, float s) {
+    const float2 v = e4m3x2_to_float2(pair);
+    __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(s, v.x), __fmul_rn(s, v.y));
+    return *reinterpret_cast<uint32_t*>(&b);
 }
 
 template <bool BF16>
@@ -112,9 +179,8 @@ k_decode(const __grid_constant__ DecParams P) {
 
     // ---- table: exclusive prefix of the 256 frequencies, then the slot LUT
     const int t = threadIdx.x;
-    uint32_t f = B.freq[t];
     {
-        uint32_t v = f;
+        uint32_t v = B.freq[t];
         #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
@@ -143,6 +209,7 @@ k_decode(const __grid_constant__ DecParams P) {
         lut[slot] = (uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20);
     }
     __syncthreads();
+    const uint32_t lut_s = (uint32_t)__cvta_generic_to_shared(lut);
 
     // ---- this lane's chunk
     const uint32_t c = (blockIdx.x - B.cta0) * kDecThreads + t;
@@ -158,20 +225,34 @@ k_decode(const __grid_constant__ DecParams P) {
         atomicOr(P.err, EQ_EF_TRUNCATED);
         return;
     }
+    // ---- stage the first 64 bytes of the chunk and read the state
     BitReader br;
-    br.wp = reinterpret_cast<const uint32_t*>(B.payload) + (a >> 2);
-    br.wend = reinterpret_cast<const uint32_t*>(B.payload) + B.word_end;
+    uint32_t x;
     {
+        __shared__ __align__(64) uint32_t rings[kDecThreads * kRingWords];
+        br.ring = (uint32_t)__cvta_generic_to_shared(rings + t * kRingWords);
+        const uint32_t s0 = (uint32_t)(a >> 4);
+        #pragma unroll
+        for (int q = 0; q < 4; ++q) stage_segment(br.ring, B.payload, s0 + q);
+        stage_commit();
+        stage_wait_all();
+        br.gs = s0 + 4;
+        const uint32_t wa = (uint32_t)(a >> 2);
+        uint32_t h, m;
+        asm("ld.shared.u32 %0, [%1];" : "=r"(h) : "r"(br.ring | ((wa * 4u) & 0x3Cu)));
+        asm("ld.shared.u32 %0, [%1];" : "=r"(m) : "r"(br.ring | (((wa + 1) * 4u) & 0x3Cu)));
+        h = bswap32(h);
+        m = bswap32(m);
         const uint32_t sh = (uint32_t)(a & 3) * 8;
-        uint64_t hi = br.load_word(), lo = br.load_word();
-        br.bb = ((hi << 32) | lo) << sh;
-        br.nb = 64 - (int)sh;
+        x = bswap32(__funnelshift_lc(m, h, sh));   // 4-byte little-endian initial state
+        br.hi = m << sh;                            // remaining bytes of word 1
+        br.lo = 0;
+        br.nb = 32 - (int)sh;
+        br.wi4 = (wa + 2) * 4u;
+        br.refill();                                // nb ≥ 32 from here on, at pair starts
     }
-    uint32_t x = bswap32((uint32_t)(br.bb >> 32));   // 4-byte little-endian state
-    br.bb <<= 32;
-    br.nb -= 32;
-    br.used = 0;
-    br.refill();
+    // a corrupt chunk may read past its end: stop (and flag) once 64 bytes beyond it
+    const uint32_t wlimit4 = (uint32_t)((e >> 2) + 16) * 4u;
 
     const uint32_t esz = BF16 ? 2 : 1;
     uint8_t* out = P.arena + Ly.out_off + sym0 * esz;
@@ -180,51 +261,62 @@ k_decode(const __grid_constant__ DecParams P) {
     float s = BF16 ? bf16_bits_to_float(sc[row]) : 0.f;
 
     uint32_t i = 0;
-    if ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) {
-        for (; i + 16 <= n; i += 16) {
-            uint32_t w[4];
-            #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t acc = 0;
-                #pragma unroll
-                for (int r = 0; r < 4; ++r) acc |= decode_one(x, br, lut) << (8 * r);
-                w[q] = acc;
-            }
-            if (BF16) {
-                uint32_t o[8];
-                #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    float2 v0 = e4m3x2_to_float2(w[q] & 0xFFFFu);
-                    float2 v1 = e4m3x2_to_float2(w[q] >> 16);
-                    __nv_bfloat162 b0 = __floats2bfloat162_rn(__fmul_rn(s, v0.x), __fmul_rn(s, v0.y));
-                    __nv_bfloat162 b1 = __floats2bfloat162_rn(__fmul_rn(s, v1.x), __fmul_rn(s, v1.y));
-                    o[2 * q] = *reinterpret_cast<uint32_t*>(&b0);
-                    o[2 * q + 1] = *reinterpret_cast<uint32_t*>(&b1);
-                }
+    bool runaway = false;
+    if (BF16) {
+        if ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) {
+            for (; i + 16 <= n; i += 16) {
+                const uint32_t q0 = decode4(x, br, lut_s), q1 = decode4(x, br, lut_s);
+                ring_boundary(br, B.payload);
+                const uint32_t q2 = decode4(x, br, lut_s), q3 = decode4(x, br, lut_s);
+                ring_boundary(br, B.payload);
                 uint4* dst = reinterpret_cast<uint4*>(out + (uint64_t)i * 2);
-                dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-                dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+                st_out(dst, make_uint4(dequant2(q0, s), dequant2(q0 >> 16, s), dequant2(q1, s), dequant2(q1 >> 16, s)));
+                st_out(dst + 1, make_uint4(dequant2(q2, s), dequant2(q2 >> 16, s), dequant2(q3, s), dequant2(q3 >> 16, s)));
                 col += 16;
                 if (col >= Ly.cols) {
                     col -= Ly.cols;
                     ++row;
                     if (i + 16 < n) s = bf16_bits_to_float(sc[row]);
                 }
-            } else {
-                *reinterpret_cast<uint4*>(out + i) = make_uint4(w[0], w[1], w[2], w[3]);
+                if (br.wi4 > wlimit4) { runaway = true; break; }
+            }
+        }
+    } else {
+        if ((B.cs & 31) == 0) {
+            for (; i + 32 <= n; i += 32) {
+                uint32_t q[8];
+                #pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    q[k] = decode4(x, br, lut_s);
+                    if (k & 1) ring_boundary(br, B.payload);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(out + i);
+                st_out(dst, make_uint4(q[0], q[1], q[2], q[3]));
+                st_out(dst + 1, make_uint4(q[4], q[5], q[6], q[7]));
+                if (br.wi4 > wlimit4) { runaway = true; break; }
             }
         }
     }
-    for (; i < n; ++i) {                       // generic / ragged tail: one symbol at a time
-        uint32_t sym = decode_one(x, br, lut);
-        store_one<BF16>(out, i, sym, s);
-        if (BF16 && ++col == Ly.cols) {
-            col = 0;
-            ++row;
-            if (i + 1 < n) s = bf16_bits_to_float(sc[row]);
+    if (!runaway) {
+        for (; i < n; ++i) {                   // generic / ragged tail: one symbol at a time
+            const uint32_t sym = decode_one(x, br, lut_s) & 0xFFu;
+            br.refill();
+            if ((i & 7) == 7) ring_boundary(br, B.payload);
+            store_one<BF16>(out, i, sym, s);
+            if (BF16 && ++col == Ly.cols) {
+                col = 0;
+                ++row;
+                if (i + 1 < n) s = bf16_bits_to_float(sc[row]);
+            }
+            if (br.wi4 > wlimit4) { runaway = true; break; }
         }
     }
-    if (x != kL || 4ull + (br.used >> 3) != e - a) atomicOr(P.err, EQ_EF_CORRUPT);
+    // integrity: final state L and every payload byte of the chunk consumed exactly
+    // (bits inserted into the window = 32·(words inserted) − 8·misalignment)
+    stage_wait_all();
+    const int64_t inserted = 8ll * (int64_t)(br.wi4 - (uint32_t)(a >> 2) * 4u) - 8ll * (int64_t)(a & 3);
+    const int64_t consumed = inserted - br.nb;            // includes the 32-bit state
+    if (runaway || x != kL || consumed != 8ll * (int64_t)(e - a)) atomicOr(P.err, EQ_EF_CORRUPT);
 }
 
 }  // namespace eq
@@ -261,7 +353,7 @@ extern "C" eq_status eq_arena_layout(const eq_block* blocks, uint32_t n_blocks, 
 static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& d, uint32_t cta0) {
     if (!blk.payload || !blk.chunk_off || !blk.freq || !blk.scales) return EQ_ERR_ARG;
     if (blk.chunk_symbols == 0 || blk.chunk_symbols > 262144u) return EQ_ERR_ARG;
-    if ((reinterpret_cast<uintptr_t>(blk.payload) & 3) != 0) return EQ_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(blk.payload) & 15) != 0) return EQ_ERR_ARG;   // cp.async 16-byte segments
     if (blk.payload_cap < blk.payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;
     d.payload = blk.payload;
     d.off = blk.chunk_off;
