@@ -19,8 +19,17 @@
 
 namespace eq {
 
-constexpr int kDecThreads = 256;
+#ifndef EQ_DEC_CHAINS
+#define EQ_DEC_CHAINS 2
+#endif
+#ifndef EQ_K_FLO
+#define EQ_K_FLO 0
+#endif
+constexpr int kChunksPerCta = 256;
+constexpr int kChains = EQ_DEC_CHAINS;            // independent chunks per thread (ILP)
+constexpr int kDecThreads = kChunksPerCta / kChains;
 constexpr int kMaxDecBlocks = 48;
+constexpr int kRingWords = 16;
 
 struct DecLayer {
     uint64_t out_off;      // byte offset of the layer in the arena
@@ -37,7 +46,7 @@ struct DecBlock {
     const uint16_t* freq;
     const uint16_t* scales;
     uint64_t payload_bytes;
-    uint64_t word_end;     // index of the first 32-bit word that must not be read
+    uint64_t word_end;     // unused by the kernel (kept for the layout)
     uint32_t n_chunks;
     uint32_t cs;           // chunk symbols
     uint32_t n_layers;
@@ -53,21 +62,20 @@ struct DecParams {
     DecBlock b[kMaxDecBlocks];
 };
 
-// ---------------------------------------------------------------- per-lane bit reader
+// ---------------------------------------------------------------- per-chunk bit reader
 // Upcoming payload bits, most significant first, in a 64-bit window (hi:lo) holding nb
 // valid bits.  A symbol consumes k ∈ {0,8,16} bits with funnel shifts (branch-free);
 // refill() runs after every PAIR of symbols and restores nb ≥ 32.
-// The lane's compressed bytes are staged in a 64-byte shared-memory ring by cp.async
-// (16-byte segments issued warp-uniformly every 8 symbols, ≥ 8 symbols before use), so
+// The chunk's compressed bytes are staged in a 64-byte shared-memory ring by cp.async
+// (16-byte segments issued thread-uniformly every 8 symbols, ≥ 8 symbols before use), so
 // no register ever waits on a global load (the warp-level scoreboard would otherwise
 // serialise the lanes' independent refills).
-constexpr int kRingWords = 16;
 struct BitReader {
     uint32_t hi, lo;
     int nb;
     uint32_t wi4;          // 4 × (absolute index of the next payload word to insert)
     uint32_t gs;           // next 16-byte payload segment to stage
-    uint32_t ring;         // shared address of this lane's ring (64-byte aligned)
+    uint32_t ring;         // shared address of this chunk's ring (64-byte aligned)
 
     __device__ __forceinline__ void refill() {
         if (nb < 32) {                              // predicated, not a divergent branch
@@ -89,17 +97,14 @@ __device__ __forceinline__ void stage_segment(uint32_t ring, const uint8_t* payl
 __device__ __forceinline__ void stage_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void stage_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Every 8 symbols: the copies of the previous boundary have landed (wait_all); stage one
-// more segment if fewer than 13 words lie ahead of the reader (≤ 4 words are consumed per
-// 8 symbols, so the words needed before the next boundary are always already landed and
-// the ring never overwrites an unread word).
-__device__ __forceinline__ void ring_boundary(BitReader& br, const uint8_t* payload) {
-    stage_wait_all();
+// Every 8 symbols (after stage_wait_all): stage one more segment if fewer than 13 words
+// lie ahead of the reader.  ≤ 4 words are consumed per 8 symbols, so the words needed
+// before the next boundary have always landed and the ring never overwrites an unread word.
+__device__ __forceinline__ void ring_issue(BitReader& br, const uint8_t* payload) {
     if (br.gs * 16u <= br.wi4 + 48u) {
         stage_segment(br.ring, payload, br.gs);
         ++br.gs;
     }
-    stage_commit();
 }
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
@@ -108,21 +113,82 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     return v;
 }
 
+// LUT address: one LOP3 + one IMAD (slot·4 + base) — written in PTX so ptxas keeps the
+// mad instead of re-deriving it as shl / and / add
+__device__ __forceinline__ uint32_t lut_addr(uint32_t x, uint32_t lut_s) {
+    uint32_t a;
+    asm("{ .reg .u32 t; and.b32 t, %1, 4095; mad.lo.u32 %0, t, 4, %2; }" : "=r"(a) : "r"(x), "r"(lut_s));
+    return a;
+}
+
+// bytes to read after a step, ×8: 0 if x ≥ 2^23, 8 if x ≥ 2^15, else 16 (x ≥ 2^11)
+__device__ __forceinline__ uint32_t renorm_bits(uint32_t x) {
+#if EQ_K_FLO
+    return (uint32_t)(__clz(x) - 1) & 0x18u;
+#else
+    return (x < (1u << 23) ? 8u : 0u) + (x < (1u << 15) ? 8u : 0u);
+#endif
+}
+
+#ifndef EQ_ZFAST
+#define EQ_ZFAST 0
+#endif
+// Per-block constants of the decode step.  ez = the LUT entry of code 0x00 with slot 0:
+// code 0x00 is first in code order, so its slots are [0, f0) and its entry for slot s is
+// ez | s << 20 — computed in registers instead of loaded, which removes the most frequent
+// symbol's lanes from the shared-memory LUT access (fewer bank conflicts).
+struct DecTable {
+    uint32_t lut_s;        // shared address of the LUT
+    uint32_t f0;           // frequency of code 0x00
+    uint32_t ez;           // (f0 − 1) << 8
+};
+
 // One rANS decode step (Alg. 2 l.1): slot lookup, state update, byte renormalisation.
 // LUT entry e: sym | (f−1) << 8 | (slot − c_sym) << 20; returns e (sym in the low byte).
 // Field extraction and x>>12 use IMAD.HI (FMA pipe) to balance the integer ALU pipe.
-__device__ __forceinline__ uint32_t decode_one(uint32_t& x, BitReader& br, uint32_t lut_s) {
-    const uint32_t e = lds_u32(lut_s + (x & (kM - 1)) * 4u);
+__device__ __forceinline__ uint32_t decode_one(uint32_t& x, BitReader& br, const DecTable& T) {
+#if EQ_ZFAST
+    const uint32_t slot = x & (kM - 1);
+    uint32_t e = T.ez | (slot << 20);
+    if (slot >= T.f0) e = lds_u32(T.lut_s + slot * 4u);
+#else
+    const uint32_t e = lds_u32(lut_addr(x, T.lut_s));
+#endif
     const uint32_t xs = __umulhi(x, 1u << 20);             // x >> 12
     const uint32_t fm1 = __umulhi(e << 12, 1u << 12);      // (e >> 8) & 0xFFF
     x = fm1 * xs + (xs + (e >> 20));                       // f·⌊x/M⌋ + slot − c
-    // bytes to read: 0 if x ≥ 2^23, 1 if x ≥ 2^15, else 2 (after a step x ≥ 2^11)
-    const uint32_t k = (uint32_t)(__clz(x) - 1) & 0x18u;
+    const uint32_t k = renorm_bits(x);
     x = __funnelshift_lc(br.hi, x, k);
     br.hi = __funnelshift_lc(br.lo, br.hi, k);
     br.lo = br.lo << k;
     br.nb -= (int)k;
     return e;
+}
+
+// Q† on two codes: exact e4m3 -> f32, one exact f32 product each, one RNE to bf16 each
+__device__ __forceinline__ uint32_t dequant2(uint32_t pair, float s) {
+    const float2 v = e4m3x2_to_float2(pair);
+    __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(s, v.x), __fmul_rn(s, v.y));
+    return *reinterpret_cast<uint32_t*>(&b);
+}
+
+// decoded output is written once and never re-read by this kernel: evict-first in L2
+__device__ __forceinline__ void st_out(uint4* p, uint4 v) { __stcs(p, v); }
+
+#ifndef EQ_ST256
+#define EQ_ST256 1
+#endif
+// 32 bytes per lane in one STG.256 (sm_100): half the store instructions and L1 wavefronts
+// of two STG.128 to the same per-lane line
+__device__ __forceinline__ void st_out32(void* p, uint4 a, uint4 b) {
+#if EQ_ST256
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
+                 "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+#else
+    st_out(reinterpret_cast<uint4*>(p), a);
+    st_out(reinterpret_cast<uint4*>(p) + 1, b);
+#endif
 }
 
 template <bool BF16>
@@ -136,67 +202,193 @@ __device__ __forceinline__ void store_one(uint8_t* out, uint64_t i, uint32_t sym
     }
 }
 
-// decoded output is written once and never re-read by this kernel: evict-first in L2 so
-// it does not push the (re-read) compressed input out of the cache
-#ifndef EQ_CS_STORES
-#define EQ_CS_STORES 1
-#endif
-__device__ __forceinline__ void st_out(uint4* p, uint4 v) {
-#if EQ_CS_STORES
-    __stcs(p, v);
-#else
-    *p = v;
-#endif
+// ---------------------------------------------------------------- one chunk's decode state
+struct Chain {
+    uint32_t x;
+    BitReader br;
+    uint8_t* out;
+    const uint16_t* sc;
+    uint32_t row, col, cols;
+    float s;
+    uint32_t n, i;
+    uint32_t a;            // chunk payload byte range [a, e)
+    uint32_t e;
+    uint32_t wlimit4;      // runaway guard: 64 bytes past the chunk end
+    bool active, runaway, fast;
+};
+
+// 4 symbols -> one word of codes (first symbol in the low byte), two pair refills
+__device__ __forceinline__ uint32_t decode4(Chain& c, const DecTable& T) {
+    const uint32_t a = decode_one(c.x, c.br, T);
+    const uint32_t b = decode_one(c.x, c.br, T);
+    c.br.refill();
+    const uint32_t d = decode_one(c.x, c.br, T);
+    const uint32_t f = decode_one(c.x, c.br, T);
+    c.br.refill();
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(d, f, 0x0040), 0x5410);
 }
 
-// 4 symbols -> one word of codes (first symbol in the low byte), two refills
-__device__ __forceinline__ uint32_t decode4(uint32_t& x, BitReader& br, uint32_t lut_s) {
-    const uint32_t a = decode_one(x, br, lut_s);
-    const uint32_t b = decode_one(x, br, lut_s);
-    br.refill();
-    const uint32_t c = decode_one(x, br, lut_s);
-    const uint32_t d = decode_one(x, br, lut_s);
-    br.refill();
-    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
-}
-
-// Q† on two codes: exact e4m3 -> f32, one exact f32 product each, one RNE to bf16 each
-__device__ __forceinline__ uint32_t dequant2(uint32_t pair, float s) {
-    const float2 v = e4m3x2_to_float2(pair);
-    __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(s, v.x), __fmul_rn(s, v.y));
-    return *reinterpret_cast<uint32_t*>(&b);
+// 16 symbols -> bf16 with one row scale (cols % 16 == 0), 32-byte store
+__device__ __forceinline__ void store16_bf16(Chain& c, const uint32_t q[4]) {
+    st_out32(c.out + (uint64_t)c.i * 2,
+             make_uint4(dequant2(q[0], c.s), dequant2(q[0] >> 16, c.s), dequant2(q[1], c.s), dequant2(q[1] >> 16, c.s)),
+             make_uint4(dequant2(q[2], c.s), dequant2(q[2] >> 16, c.s), dequant2(q[3], c.s), dequant2(q[3] >> 16, c.s)));
+    c.col += 16;
+    if (c.col >= c.cols) {
+        c.col -= c.cols;
+        ++c.row;
+        if (c.i + 16 < c.n) c.s = bf16_bits_to_float(c.sc[c.row]);
+    }
 }
 
 template <bool BF16>
-__global__ void __launch_bounds__(kDecThreads)
+__device__ __forceinline__ void chain_setup(Chain& c, const DecBlock& B, uint32_t chunk, uint32_t ring,
+                                            uint8_t* arena, uint32_t* err) {
+    c.active = chunk < B.n_chunks;
+    c.runaway = false;
+    c.i = 0;
+    c.n = 0;
+    if (!c.active) return;
+    uint32_t l = 0;
+    while (l + 1 < B.n_layers && chunk >= B.layer[l + 1].chunk0) ++l;
+    const DecLayer& Ly = B.layer[l];
+    const uint64_t sym0 = (uint64_t)(chunk - Ly.chunk0) * B.cs;
+    c.n = (uint32_t)min((uint64_t)B.cs, Ly.size - sym0);
+    const uint32_t a = __ldg(B.off + chunk), e = __ldg(B.off + chunk + 1);
+    if (e < a || (uint64_t)e > B.payload_bytes || e - a < 4) {
+        atomicOr(err, EQ_EF_TRUNCATED);
+        c.active = false;
+        return;
+    }
+    c.a = a;
+    c.e = e;
+    c.wlimit4 = ((e >> 2) + 16) * 4u;
+    c.br.ring = ring;
+    const uint32_t s0 = a >> 4;
+    #pragma unroll
+    for (int q = 0; q < 4; ++q) stage_segment(ring, B.payload, s0 + q);
+    c.br.gs = s0 + 4;
+    c.out = arena + Ly.out_off + sym0 * (BF16 ? 2 : 1);
+    c.sc = B.scales + Ly.scale_off;
+    c.cols = Ly.cols;
+    c.row = (uint32_t)(sym0 / Ly.cols);
+    c.col = (uint32_t)(sym0 % Ly.cols);
+    c.s = BF16 ? bf16_bits_to_float(c.sc[c.row]) : 0.f;
+    c.fast = BF16 ? ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) : ((B.cs & 31) == 0);
+}
+
+// after the initial segments landed: read the 4-byte state and fill the window
+__device__ __forceinline__ void chain_start(Chain& c) {
+    if (!c.active) return;
+    const uint32_t wa = c.a >> 2;
+    uint32_t h = bswap32(lds_u32(c.br.ring | ((wa * 4u) & 0x3Cu)));
+    uint32_t m = bswap32(lds_u32(c.br.ring | (((wa + 1) * 4u) & 0x3Cu)));
+    const uint32_t sh = (c.a & 3) * 8;
+    c.x = bswap32(__funnelshift_lc(m, h, sh));  // 4-byte little-endian initial state
+    c.br.hi = m << sh;                           // remaining bytes of word 1
+    c.br.lo = 0;
+    c.br.nb = 32 - (int)sh;
+    c.br.wi4 = (wa + 2) * 4u;
+    c.br.refill();                               // nb ≥ 32 from here on, at pair starts
+}
+
+// one chunk alone from its current position to its end (16/32-symbol groups while the
+// layout allows, then one symbol at a time)
+template <bool BF16>
+__device__ __forceinline__ void chain_finish(Chain& c, const uint8_t* payload, const DecTable& T) {
+    if (!c.active || c.runaway) return;
+    if (c.fast) {
+        const uint32_t G = BF16 ? 16 : 32;
+        while (c.i + G <= c.n) {
+            if (BF16) {
+                uint32_t q[4];
+                q[0] = decode4(c, T);
+                q[1] = decode4(c, T);
+                stage_wait_all(); ring_issue(c.br, payload); stage_commit();
+                q[2] = decode4(c, T);
+                q[3] = decode4(c, T);
+                stage_wait_all(); ring_issue(c.br, payload); stage_commit();
+                store16_bf16(c, q);
+            } else {
+                uint32_t q[8];
+                #pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    q[k] = decode4(c, T);
+                    if (k & 1) { stage_wait_all(); ring_issue(c.br, payload); stage_commit(); }
+                }
+                st_out32(c.out + c.i, make_uint4(q[0], q[1], q[2], q[3]), make_uint4(q[4], q[5], q[6], q[7]));
+            }
+            c.i += G;
+            if (c.br.wi4 > c.wlimit4) { c.runaway = true; return; }
+        }
+    }
+    for (; c.i < c.n; ++c.i) {                  // generic / ragged tail: one symbol at a time
+        const uint32_t sym = decode_one(c.x, c.br, T) & 0xFFu;
+        c.br.refill();
+        if ((c.i & 7) == 7) { stage_wait_all(); ring_issue(c.br, payload); stage_commit(); }
+        store_one<BF16>(c.out, c.i, sym, c.s);
+        if (BF16 && ++c.col == c.cols) {
+            c.col = 0;
+            ++c.row;
+            if (c.i + 1 < c.n) c.s = bf16_bits_to_float(c.sc[c.row]);
+        }
+        if (c.br.wi4 > c.wlimit4) { c.runaway = true; return; }
+    }
+}
+
+#ifndef EQ_DEC_MIN_CTAS
+#define EQ_DEC_MIN_CTAS 1
+#endif
+
+template <bool BF16>
+__global__ void __launch_bounds__(kDecThreads, EQ_DEC_MIN_CTAS)
 k_decode(const __grid_constant__ DecParams P) {
     __shared__ uint32_t lut[kM];
     __shared__ uint32_t cum[257];
+    __shared__ __align__(64) uint32_t rings[kChunksPerCta * kRingWords];
 
     uint32_t bi = 0;
     while (bi + 1 < P.n_blocks && blockIdx.x >= P.b[bi + 1].cta0) ++bi;
     const DecBlock& B = P.b[bi];
+    const int t = threadIdx.x;
+
+    // ---- chunk setup first: the initial cp.async copies overlap the table build
+    Chain ch[kChains];
+    #pragma unroll
+    for (int j = 0; j < kChains; ++j) {
+        const uint32_t slot = (uint32_t)(j * kDecThreads + t);
+        chain_setup<BF16>(ch[j], B, (blockIdx.x - B.cta0) * kChunksPerCta + slot,
+                          (uint32_t)__cvta_generic_to_shared(rings + slot * kRingWords), P.arena, P.err);
+    }
+    stage_commit();
 
     // ---- table: exclusive prefix of the 256 frequencies, then the slot LUT
-    const int t = threadIdx.x;
     {
-        uint32_t v = B.freq[t];
-        #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
-            if ((t & 31) >= d) v += o;
+        __shared__ uint32_t wsum[8];
+        const int lane = t & 31, w = t >> 5;
+        for (int base = 0; base < 256; base += kDecThreads) {
+            uint32_t v = B.freq[base + t];
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+                if (lane >= d) v += o;
+            }
+            if (lane == 31) wsum[(base >> 5) + w] = v;
+            cum[base + t + 1] = v;                  // warp-local inclusive prefix for now
         }
-        __shared__ uint32_t wsum[kDecThreads / 32];
-        if ((t & 31) == 31) wsum[t >> 5] = v;
         __syncthreads();
-        uint32_t add = 0;
-        for (int w = 0; w < (t >> 5); ++w) add += wsum[w];
-        cum[t + 1] = v + add;
+        for (int base = 0; base < 256; base += kDecThreads) {
+            const int idx = base + t;
+            uint32_t add = 0;
+            for (int q = 0; q < (idx >> 5); ++q) add += wsum[q];
+            cum[idx + 1] += add;
+        }
         if (t == 0) cum[0] = 0;
     }
     __syncthreads();
     if (cum[256] != kM) {                     // corrupt table: nothing decodable
         if (t == 0) atomicOr(P.err, EQ_EF_CORRUPT);
+        stage_wait_all();
         return;
     }
     for (int slot = t; slot < (int)kM; slot += kDecThreads) {
@@ -208,115 +400,88 @@ k_decode(const __grid_constant__ DecParams P) {
         uint32_t fs = cum[lo + 1] - cum[lo];
         lut[slot] = (uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20);
     }
+    stage_wait_all();
     __syncthreads();
-    const uint32_t lut_s = (uint32_t)__cvta_generic_to_shared(lut);
+    DecTable T;
+    T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
+    T.f0 = cum[1];
+    T.ez = (T.f0 - 1) << 8;
 
-    // ---- this lane's chunk
-    const uint32_t c = (blockIdx.x - B.cta0) * kDecThreads + t;
-    if (c >= B.n_chunks) return;
-    uint32_t l = 0;
-    while (l + 1 < B.n_layers && c >= B.layer[l + 1].chunk0) ++l;
-    const DecLayer& Ly = B.layer[l];
-    const uint64_t sym0 = (uint64_t)(c - Ly.chunk0) * B.cs;
-    const uint32_t n = (uint32_t)min((uint64_t)B.cs, Ly.size - sym0);
+    #pragma unroll
+    for (int j = 0; j < kChains; ++j) chain_start(ch[j]);
 
-    const uint64_t a = __ldg(B.off + c), e = __ldg(B.off + c + 1);
-    if (e < a || e > B.payload_bytes || e - a < 4) {
-        atomicOr(P.err, EQ_EF_TRUNCATED);
-        return;
+    // ---- joint loop: the chains' independent dependency chains interleave (ILP)
+    bool joint = true;
+    uint32_t ng = 0xFFFFFFFFu;
+    #pragma unroll
+    for (int j = 0; j < kChains; ++j) {
+        joint = joint && ch[j].active && ch[j].fast;
+        ng = min(ng, ch[j].n / (BF16 ? 16u : 32u));
     }
-    // ---- stage the first 64 bytes of the chunk and read the state
-    BitReader br;
-    uint32_t x;
-    {
-        __shared__ __align__(64) uint32_t rings[kDecThreads * kRingWords];
-        br.ring = (uint32_t)__cvta_generic_to_shared(rings + t * kRingWords);
-        const uint32_t s0 = (uint32_t)(a >> 4);
-        #pragma unroll
-        for (int q = 0; q < 4; ++q) stage_segment(br.ring, B.payload, s0 + q);
-        stage_commit();
-        stage_wait_all();
-        br.gs = s0 + 4;
-        const uint32_t wa = (uint32_t)(a >> 2);
-        uint32_t h, m;
-        asm("ld.shared.u32 %0, [%1];" : "=r"(h) : "r"(br.ring | ((wa * 4u) & 0x3Cu)));
-        asm("ld.shared.u32 %0, [%1];" : "=r"(m) : "r"(br.ring | (((wa + 1) * 4u) & 0x3Cu)));
-        h = bswap32(h);
-        m = bswap32(m);
-        const uint32_t sh = (uint32_t)(a & 3) * 8;
-        x = bswap32(__funnelshift_lc(m, h, sh));   // 4-byte little-endian initial state
-        br.hi = m << sh;                            // remaining bytes of word 1
-        br.lo = 0;
-        br.nb = 32 - (int)sh;
-        br.wi4 = (wa + 2) * 4u;
-        br.refill();                                // nb ≥ 32 from here on, at pair starts
-    }
-    // a corrupt chunk may read past its end: stop (and flag) once 64 bytes beyond it
-    const uint32_t wlimit4 = (uint32_t)((e >> 2) + 16) * 4u;
-
-    const uint32_t esz = BF16 ? 2 : 1;
-    uint8_t* out = P.arena + Ly.out_off + sym0 * esz;
-    const uint16_t* sc = B.scales + Ly.scale_off;
-    uint32_t row = (uint32_t)(sym0 / Ly.cols), col = (uint32_t)(sym0 % Ly.cols);
-    float s = BF16 ? bf16_bits_to_float(sc[row]) : 0.f;
-
-    uint32_t i = 0;
-    bool runaway = false;
-    if (BF16) {
-        if ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) {
-            for (; i + 16 <= n; i += 16) {
-                const uint32_t q0 = decode4(x, br, lut_s), q1 = decode4(x, br, lut_s);
-                ring_boundary(br, B.payload);
-                const uint32_t q2 = decode4(x, br, lut_s), q3 = decode4(x, br, lut_s);
-                ring_boundary(br, B.payload);
-                uint4* dst = reinterpret_cast<uint4*>(out + (uint64_t)i * 2);
-                st_out(dst, make_uint4(dequant2(q0, s), dequant2(q0 >> 16, s), dequant2(q1, s), dequant2(q1 >> 16, s)));
-                st_out(dst + 1, make_uint4(dequant2(q2, s), dequant2(q2 >> 16, s), dequant2(q3, s), dequant2(q3 >> 16, s)));
-                col += 16;
-                if (col >= Ly.cols) {
-                    col -= Ly.cols;
-                    ++row;
-                    if (i + 16 < n) s = bf16_bits_to_float(sc[row]);
+    if (joint && kChains > 1) {
+        for (uint32_t g = 0; g < ng; ++g) {
+            if (BF16) {
+                uint32_t q[kChains][4];
+                #pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    #pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        #pragma unroll
+                        for (int j = 0; j < kChains; ++j) q[j][2 * h + r] = decode4(ch[j], T);
+                    }
+                    stage_wait_all();
+                    #pragma unroll
+                    for (int j = 0; j < kChains; ++j) ring_issue(ch[j].br, B.payload);
+                    stage_commit();
                 }
-                if (br.wi4 > wlimit4) { runaway = true; break; }
-            }
-        }
-    } else {
-        if ((B.cs & 31) == 0) {
-            for (; i + 32 <= n; i += 32) {
-                uint32_t q[8];
+                #pragma unroll
+                for (int j = 0; j < kChains; ++j) {
+                    store16_bf16(ch[j], q[j]);
+                    ch[j].i += 16;
+                }
+            } else {
+                uint32_t q[kChains][8];
                 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    q[k] = decode4(x, br, lut_s);
-                    if (k & 1) ring_boundary(br, B.payload);
+                    #pragma unroll
+                    for (int j = 0; j < kChains; ++j) q[j][k] = decode4(ch[j], T);
+                    if (k & 1) {
+                        stage_wait_all();
+                        #pragma unroll
+                        for (int j = 0; j < kChains; ++j) ring_issue(ch[j].br, B.payload);
+                        stage_commit();
+                    }
                 }
-                uint4* dst = reinterpret_cast<uint4*>(out + i);
-                st_out(dst, make_uint4(q[0], q[1], q[2], q[3]));
-                st_out(dst + 1, make_uint4(q[4], q[5], q[6], q[7]));
-                if (br.wi4 > wlimit4) { runaway = true; break; }
+                #pragma unroll
+                for (int j = 0; j < kChains; ++j) {
+                    st_out32(ch[j].out + ch[j].i, make_uint4(q[j][0], q[j][1], q[j][2], q[j][3]),
+                             make_uint4(q[j][4], q[j][5], q[j][6], q[j][7]));
+                    ch[j].i += 32;
+                }
             }
+            bool bad = false;
+            #pragma unroll
+            for (int j = 0; j < kChains; ++j) bad = bad || (ch[j].br.wi4 > ch[j].wlimit4);
+            if (bad) break;
         }
     }
-    if (!runaway) {
-        for (; i < n; ++i) {                   // generic / ragged tail: one symbol at a time
-            const uint32_t sym = decode_one(x, br, lut_s) & 0xFFu;
-            br.refill();
-            if ((i & 7) == 7) ring_boundary(br, B.payload);
-            store_one<BF16>(out, i, sym, s);
-            if (BF16 && ++col == Ly.cols) {
-                col = 0;
-                ++row;
-                if (i + 1 < n) s = bf16_bits_to_float(sc[row]);
-            }
-            if (br.wi4 > wlimit4) { runaway = true; break; }
-        }
+    // ---- remainders (ragged tails, unequal lengths, non-fast layouts), one chain at a time
+    #pragma unroll
+    for (int j = 0; j < kChains; ++j) {
+        if (ch[j].active && ch[j].br.wi4 > ch[j].wlimit4) ch[j].runaway = true;
+        chain_finish<BF16>(ch[j], B.payload, T);
     }
+    stage_wait_all();
     // integrity: final state L and every payload byte of the chunk consumed exactly
     // (bits inserted into the window = 32·(words inserted) − 8·misalignment)
-    stage_wait_all();
-    const int64_t inserted = 8ll * (int64_t)(br.wi4 - (uint32_t)(a >> 2) * 4u) - 8ll * (int64_t)(a & 3);
-    const int64_t consumed = inserted - br.nb;            // includes the 32-bit state
-    if (runaway || x != kL || consumed != 8ll * (int64_t)(e - a)) atomicOr(P.err, EQ_EF_CORRUPT);
+    #pragma unroll
+    for (int j = 0; j < kChains; ++j) {
+        const Chain& c = ch[j];
+        if (!c.active) continue;
+        const int64_t inserted = 8ll * (int64_t)(c.br.wi4 - (c.a >> 2) * 4u) - 8ll * (int64_t)(c.a & 3);
+        const int64_t consumed = inserted - c.br.nb;            // includes the 32-bit state
+        if (c.runaway || c.x != kL || consumed != 8ll * (int64_t)(c.e - c.a)) atomicOr(P.err, EQ_EF_CORRUPT);
+    }
 }
 
 }  // namespace eq
@@ -406,7 +571,7 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
         uint32_t ctas = 0;
         for (uint32_t k = 0; k < nb; ++k) {
             EQ_TRY(fill_desc(blocks[b0 + k], all.get() + (size_t)(b0 + k) * EQ_MAX_LAYERS, P.b[k], ctas));
-            ctas += (P.b[k].n_chunks + kDecThreads - 1) / kDecThreads;
+            ctas += (P.b[k].n_chunks + kChunksPerCta - 1) / kChunksPerCta;
         }
         // blocks with zero chunks cannot exist (layers are non-empty); ctas > 0
         if (out_dtype == EQ_OUT_BF16)
