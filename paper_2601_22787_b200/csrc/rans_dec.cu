@@ -20,10 +20,10 @@
 namespace eq {
 
 #ifndef EQ_DEC_CHAINS
-#define EQ_DEC_CHAINS 2
+#define EQ_DEC_CHAINS 1
 #endif
 #ifndef EQ_K_FLO
-#define EQ_K_FLO 0
+#define EQ_K_FLO 1
 #endif
 constexpr int kChunksPerCta = 256;
 constexpr int kChains = EQ_DEC_CHAINS;            // independent chunks per thread (ILP)
@@ -59,6 +59,9 @@ struct DecParams {
     uint32_t* err;
     uint32_t n_blocks;
     uint32_t pad;
+    // multipliers passed at run time so ptxas keeps IMAD / IMAD.HI (FMA pipe) instead of
+    // strength-reducing them to LEA / SHF on the (binding) integer ALU pipe
+    uint32_t k2p20, k2p12, kneg2p14, k4;
     DecBlock b[kMaxDecBlocks];
 };
 
@@ -82,7 +85,7 @@ struct BitReader {
             uint32_t w;
             asm("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(ring | (wi4 & 0x3Cu)));
             w = bswap32(w);
-            hi |= w >> nb;                          // lo is empty when nb < 32
+            hi += w >> nb;                          // = |: the low 32−nb bits of hi are 0
             lo = __funnelshift_r(0u, w, nb);        // = w << (32 − nb)
             nb += 32;
             wi4 += 4;
@@ -124,7 +127,7 @@ __device__ __forceinline__ uint32_t lut_addr(uint32_t x, uint32_t lut_s) {
 // bytes to read after a step, ×8: 0 if x ≥ 2^23, 8 if x ≥ 2^15, else 16 (x ≥ 2^11)
 __device__ __forceinline__ uint32_t renorm_bits(uint32_t x) {
 #if EQ_K_FLO
-    return (uint32_t)(__clz(x) - 1) & 0x18u;
+    return (30u - (31u - (uint32_t)__clz(x))) & 0x18u;    // FLO (XU pipe) + IADD + LOP3
 #else
     return (x < (1u << 23) ? 8u : 0u) + (x < (1u << 15) ? 8u : 0u);
 #endif
@@ -138,6 +141,7 @@ __device__ __forceinline__ uint32_t renorm_bits(uint32_t x) {
 // ez | s << 20 — computed in registers instead of loaded, which removes the most frequent
 // symbol's lanes from the shared-memory LUT access (fewer bank conflicts).
 struct DecTable {
+    uint32_t k2p20, k2p12, kneg2p14, k4;   // 2^20, 2^12, −2^14, 4 (see DecParams)
     uint32_t lut_s;        // shared address of the LUT
     uint32_t f0;           // frequency of code 0x00
     uint32_t ez;           // (f0 − 1) << 8
@@ -146,17 +150,35 @@ struct DecTable {
 // One rANS decode step (Alg. 2 l.1): slot lookup, state update, byte renormalisation.
 // LUT entry e: sym | (f−1) << 8 | (slot − c_sym) << 20; returns e (sym in the low byte).
 // Field extraction and x>>12 use IMAD.HI (FMA pipe) to balance the integer ALU pipe.
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// One rANS decode step (Alg. 2 l.1): slot lookup, state update, byte renormalisation.
+// LUT entry e: sym | (f−1) << 8 | (slot − c_sym) << 20; returns e (sym in the low byte).
+// Everything that has an exact integer-multiply form runs as IMAD / IMAD.HI on the FMA
+// pipe, leaving the (binding) ALU pipe the funnel shifts, masks and byte permutes:
+//   xs = x >> 12 = hi(x · 2^20);  slot·4 + base = 4x − 2^14·xs + base
+//   xs + (slot − c) = hi(e · 2^12) + xs;  f − 1 = hi((e << 12) · 2^12)
 __device__ __forceinline__ uint32_t decode_one(uint32_t& x, BitReader& br, const DecTable& T) {
 #if EQ_ZFAST
     const uint32_t slot = x & (kM - 1);
     uint32_t e = T.ez | (slot << 20);
     if (slot >= T.f0) e = lds_u32(T.lut_s + slot * 4u);
+    const uint32_t xs = mad_hi(x, 1u << 20, 0u);
 #else
-    const uint32_t e = lds_u32(lut_addr(x, T.lut_s));
+    const uint32_t xs = mad_hi(x, T.k2p20, 0u);                         // x >> 12
+    const uint32_t e = lds_u32(mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s)));
 #endif
-    const uint32_t xs = __umulhi(x, 1u << 20);             // x >> 12
-    const uint32_t fm1 = __umulhi(e << 12, 1u << 12);      // (e >> 8) & 0xFFF
-    x = fm1 * xs + (xs + (e >> 20));                       // f·⌊x/M⌋ + slot − c
+    const uint32_t fm1 = mad_hi(mad_lo(e, T.k2p12, 0u), T.k2p12, 0u);   // (e >> 8) & 0xFFF
+    x = mad_lo(fm1, xs, mad_hi(e, T.k2p12, xs));                        // f·⌊x/M⌋ + slot − c
     const uint32_t k = renorm_bits(x);
     x = __funnelshift_lc(br.hi, x, k);
     br.hi = __funnelshift_lc(br.lo, br.hi, k);
@@ -403,6 +425,10 @@ k_decode(const __grid_constant__ DecParams P) {
     stage_wait_all();
     __syncthreads();
     DecTable T;
+    T.k2p20 = P.k2p20;
+    T.k2p12 = P.k2p12;
+    T.kneg2p14 = P.kneg2p14;
+    T.k4 = P.k4;
     T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
     T.f0 = cum[1];
     T.ez = (T.f0 - 1) << 8;
@@ -568,6 +594,10 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
         P.arena = static_cast<uint8_t*>(arena);
         P.err = d_err;
         P.n_blocks = nb;
+        P.k2p20 = 1u << 20;
+        P.k2p12 = 1u << 12;
+        P.kneg2p14 = 0u - (1u << 14);
+        P.k4 = 4u;
         uint32_t ctas = 0;
         for (uint32_t k = 0; k < nb; ++k) {
             EQ_TRY(fill_desc(blocks[b0 + k], all.get() + (size_t)(b0 + k) * EQ_MAX_LAYERS, P.b[k], ctas));
