@@ -32,13 +32,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FP8 weight entropy-decode GB/s (frac of HBM peak) at 1/2/4/8 B200; bits/param"
 FALLBACK_HBM_GBS = 6650.0            # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
-DEFAULT_LAMBDA = 180.0               # reference arm only (no GPU calibration there); see DESIGN.md §7
+DEFAULT_LAMBDA = 230.2               # reference arm only: the GPU calibration of λ for 2.0 bits
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="llama-3-8b")
@@ -78,7 +78,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -141,7 +141,7 @@ def run_reference(args, rank, world):
     lam = args.lam if args.lam is not None else DEFAULT_LAMBDA
     threads = os.cpu_count() or 1
     shapes = eqsynth.block_shapes(args.model)
-    rows_per = 8
+    rows_per = 16
     layers, full_shapes = [], []
     for m, (r, c) in enumerate(shapes):
         ids = list(range(0, r, max(1, r // rows_per)))[:rows_per]
@@ -226,10 +226,8 @@ def main():
     L = eqsynth.LLAMA[args.model]["layers"]
     if args.blocks <= 0:
         args.blocks = L
-    if args.scaling == "weak":
-        layer_ids = [rank * args.blocks + i for i in range(args.blocks)]
-    else:
-        layer_ids = [i for i in range(args.blocks) if i % world == rank]
+    from paper_2601_22787_b200 import shard
+    layer_ids = shard.layer_ids(rank, world, args.blocks, args.scaling)
 
     # ---- encode side (once): λ calibration (global) then Alg. 1 per block
     t0 = time.time()
@@ -286,17 +284,14 @@ def main():
         per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
         total = ev[0].elapsed_time(ev[steps])
         dec.check(stream)
-        if world > 1:
-            t = torch.tensor([total], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total = float(t.item())
+        total = shard.max_over_ranks(total, dist if world > 1 else None, dev)
         return total, per
 
     # ---- main metric: bf16-out decode of the whole layer set
     dec = eq.Decoder(blocks, eq.EQ_OUT_BF16)
     clocks = ClockSampler(local) if not args.profile else None
     total_ms, per = time_decoder(dec, args.steps, args.warmup, clocks)
-    value = bytes_bf16 * world * args.steps / (total_ms / 1e3) / 1e9
+    value = shard.aggregate_gbs(bytes_bf16, world, args.steps, total_ms)
     launch_ms = statistics.mean(per)
     achieved = bytes_bf16 / (launch_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
@@ -308,7 +303,7 @@ def main():
         dec8 = eq.Decoder(blocks, eq.EQ_OUT_FP8)
         t8, per8 = time_decoder(dec8, args.steps, args.warmup)
         l8 = statistics.mean(per8)
-        fp8 = {"value": bytes_fp8 * world * args.steps / (t8 / 1e3) / 1e9, "unit": "GB/s",
+        fp8 = {"value": shard.aggregate_gbs(bytes_fp8, world, args.steps, t8), "unit": "GB/s",
                "ms_per_step": t8 / args.steps, "frac": bytes_fp8 / (l8 / 1e3) / 1e9 / peak,
                "traffic": traffic_from_profiles("fp8")}
         del dec8
@@ -334,11 +329,8 @@ def main():
         barrier()
         ms = s_ev.elapsed_time(e_ev)
         ms = max(ms, 1e3 * wall)
-        if world > 1:
-            tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
-        e2e = {"value": bytes_bf16 * world * k_e2e / (ms / 1e3) / 1e9, "unit": "GB/s",
+        ms = shard.max_over_ranks(ms, dist if world > 1 else None, dev)
+        e2e = {"value": shard.aggregate_gbs(bytes_bf16, world, k_e2e, ms), "unit": "GB/s",
                "h2d_bytes_per_step": hb.h2d_bytes(), "d2h_bytes_per_step": hb.total, "steps": k_e2e,
                "ms_per_step": ms / k_e2e}
         del hb
@@ -346,7 +338,7 @@ def main():
     # ---- CPU baseline: the oracle on the host cores, rank 0, N=1, bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cpu = cpu_baseline(blocks[0], args.cpu_seconds)
+        cpu = cpu_baseline(blocks, args.cpu_seconds)
 
     if rank == 0:
         cs = clocks.summary() if clocks is not None else None
@@ -379,37 +371,42 @@ class _Null:
         return False
 
 
-def cpu_baseline(blk, seconds: float):
-    """The oracle, as it stands, decoding+dequantising a bounded sample (leading chunks of
-    the first layer of block 0) on all host cores.  Timing only — not a parity check."""
+def cpu_baseline(blocks, seconds: float):
+    """The oracle, as it stands, decoding+dequantising a bounded sample of the same
+    workload (whole layers of the leading blocks, until ~``seconds`` of host work) on all
+    host cores.  Timing only — not a parity check."""
     import numpy as np
     import torch
 
     import oracle as o
     threads = os.cpu_count() or 1
-    r, c = blk.shapes[0]
-    cs = blk.chunk_symbols
-    off_all = blk.chunk_off.cpu().numpy().astype(np.uint32)
-    nk_layer = (r * c + cs - 1) // cs
-    payload = blk.payload.cpu().numpy()
-    freq = blk.freq.cpu().numpy().view(np.uint16)
-    scales = blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)
-
-    def run(nk):
-        rows = (nk * cs + c - 1) // c
-        off = off_all[:nk + 1]
-        t = time.perf_counter()
-        o.decode_dequant_layer_mt(payload, off, cs, rows, c, scales[:rows], freq, threads)
-        return time.perf_counter() - t, int(off[-1]) + 4 * (nk + 1) + 2 * rows + 512 + 2 * rows * c
-
-    nk = min(nk_layer, max(threads, 64))
-    dt, _ = run(nk)
-    nk = int(min(nk_layer, max(nk, nk * seconds / max(dt, 1e-3))))
-    nk = max(1, (nk * cs // c) * c // cs)      # whole rows
-    dt, nbytes = run(nk)
-    return {"value": nbytes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {nk} chunks ({nk * cs} symbols) of block 0 layer 0 ({r}x{c}), decode+dequant to bf16, "
-                      f"{dt:.1f} s wall"}
+    done_bytes, done_syms, wall, layers = 0, 0, 0.0, 0
+    for blk in blocks:
+        cs = blk.chunk_symbols
+        off_all = blk.chunk_off.cpu().numpy().astype(np.uint32)
+        payload = blk.payload.cpu().numpy()
+        freq = blk.freq.cpu().numpy().view(np.uint16)
+        scales = blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)
+        k0, r0 = 0, 0
+        for (r, c) in blk.shapes:
+            nk = (r * c + cs - 1) // cs
+            off = off_all[k0:k0 + nk + 1]
+            t = time.perf_counter()
+            o.decode_dequant_layer_mt(payload, off, cs, r, c, scales[r0:r0 + r], freq, threads)
+            wall += time.perf_counter() - t
+            done_bytes += int(off[-1] - off[0]) + 4 * (nk + 1) + 2 * r + 2 * r * c
+            done_syms += r * c
+            layers += 1
+            k0 += nk
+            r0 += r
+            if wall >= seconds:
+                break
+        done_bytes += 512
+        if wall >= seconds:
+            break
+    return {"value": done_bytes / wall / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"{layers} whole layers ({done_syms} symbols) of the leading blocks, decode+dequant to bf16 "
+                      f"with eqo_decode_chunk on {threads} threads, {wall:.1f} s wall"}
 
 
 if __name__ == "__main__":

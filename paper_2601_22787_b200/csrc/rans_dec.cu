@@ -93,9 +93,30 @@ struct BitReader {
     }
 };
 
+#ifndef EQ_L2HINT
+#define EQ_L2HINT 0
+#endif
+// L2 policies: the compressed input is re-read segment by segment while ~14 GB of output
+// streams through L2, so input lines are kept (evict_last) and output lines go first
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void stage_segment(uint32_t ring, const uint8_t* payload, uint32_t seg) {
+#if EQ_L2HINT
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint.L2::128B [%0], [%1], 16, %2;" ::"r"(ring | ((seg & 3u) << 4)),
+                 "l"(payload + (uint64_t)seg * 16), "l"(policy_evict_last()));
+#else
     asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(ring | ((seg & 3u) << 4)),
                  "l"(payload + (uint64_t)seg * 16));
+#endif
 }
 __device__ __forceinline__ void stage_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void stage_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
@@ -203,7 +224,11 @@ __device__ __forceinline__ void st_out(uint4* p, uint4 v) { __stcs(p, v); }
 // 32 bytes per lane in one STG.256 (sm_100): half the store instructions and L1 wavefronts
 // of two STG.128 to the same per-lane line
 __device__ __forceinline__ void st_out32(void* p, uint4 a, uint4 b) {
-#if EQ_ST256
+#if EQ_ST256 && EQ_L2HINT
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+                 "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+#elif EQ_ST256
     asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
                  "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                  : "memory");
