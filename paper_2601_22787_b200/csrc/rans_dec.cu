@@ -148,7 +148,10 @@ __device__ __forceinline__ uint32_t lut_addr(uint32_t x, uint32_t lut_s) {
 // bytes to read after a step, ×8: 0 if x ≥ 2^23, 8 if x ≥ 2^15, else 16 (x ≥ 2^11)
 __device__ __forceinline__ uint32_t renorm_bits(uint32_t x) {
 #if EQ_K_FLO
-    return (30u - (31u - (uint32_t)__clz(x))) & 0x18u;    // FLO (XU pipe) + IADD + LOP3
+    // clz(2x) = clz(x) − 1: one IMAD (FMA pipe), FLO.SH (XU pipe), LOP3
+    uint32_t z;
+    asm("bfind.shiftamt.u32 %0, %1;" : "=r"(z) : "r"(x + x));
+    return z & 0x18u;
 #else
     return (x < (1u << 23) ? 8u : 0u) + (x < (1u << 15) ? 8u : 0u);
 #endif
@@ -199,7 +202,7 @@ __device__ __forceinline__ uint32_t decode_one(uint32_t& x, BitReader& br, const
     const uint32_t e = lds_u32(mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s)));
 #endif
     const uint32_t fm1 = mad_hi(mad_lo(e, T.k2p12, 0u), T.k2p12, 0u);   // (e >> 8) & 0xFFF
-    x = mad_lo(fm1, xs, mad_hi(e, T.k2p12, xs));                        // f·⌊x/M⌋ + slot − c
+    x = mad_lo(fm1, xs, xs + (e >> 20));                                // f·⌊x/M⌋ + slot − c
     const uint32_t k = renorm_bits(x);
     x = __funnelshift_lc(br.hi, x, k);
     br.hi = __funnelshift_lc(br.lo, br.hi, k);
@@ -213,6 +216,28 @@ __device__ __forceinline__ uint32_t dequant2(uint32_t pair, float s) {
     const float2 v = e4m3x2_to_float2(pair);
     __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(s, v.x), __fmul_rn(s, v.y));
     return *reinterpret_cast<uint32_t*>(&b);
+}
+
+// Same result when the row scale is exactly representable in f16 (bf16's 8-bit mantissa
+// fits f16's 11 bits; only the range is checked): the e4m3 pair unpacks to f16x2 and the
+// mixed-precision FHFMA multiplies each f16 half by the f16 scale straight into f32 —
+// the product of a 4- and an 8-bit significand is exact in f32 — then one RNE to bf16.
+__device__ __forceinline__ uint32_t dequant2_h(uint32_t pair, uint16_t s16) {
+    __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(pair & 0xFFFFu), __NV_E4M3);
+    const uint32_t hv = *reinterpret_cast<uint32_t*>(&h);
+    float a, b;
+    asm("{ .reg .b16 l, u; mov.b32 {l, u}, %2; fma.rn.f32.f16 %0, l, %3, 0f00000000; fma.rn.f32.f16 %1, u, %3, 0f00000000; }"
+        : "=f"(a), "=f"(b) : "r"(hv), "h"(s16));
+    __nv_bfloat162 r = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// f16 bits of a bf16 scale if exactly representable (normal f16 range), else 0
+__device__ __forceinline__ uint16_t scale_f16(float s) {
+    const float a = fabsf(s);
+    if (!(a >= 6.103515625e-05f && a <= 65504.f)) return 0;
+    __half h = __float2half_rn(s);
+    return *reinterpret_cast<uint16_t*>(&h);
 }
 
 // decoded output is written once and never re-read by this kernel: evict-first in L2
@@ -257,6 +282,7 @@ struct Chain {
     const uint16_t* sc;
     uint32_t row, col, cols;
     float s;
+    uint16_t s16;          // f16 bits of s when exact, else 0 (FMUL path)
     uint32_t n, i;
     uint32_t a;            // chunk payload byte range [a, e)
     uint32_t e;
@@ -277,14 +303,25 @@ __device__ __forceinline__ uint32_t decode4(Chain& c, const DecTable& T) {
 
 // 16 symbols -> bf16 with one row scale (cols % 16 == 0), 32-byte store
 __device__ __forceinline__ void store16_bf16(Chain& c, const uint32_t q[4]) {
-    st_out32(c.out + (uint64_t)c.i * 2,
-             make_uint4(dequant2(q[0], c.s), dequant2(q[0] >> 16, c.s), dequant2(q[1], c.s), dequant2(q[1] >> 16, c.s)),
-             make_uint4(dequant2(q[2], c.s), dequant2(q[2] >> 16, c.s), dequant2(q[3], c.s), dequant2(q[3] >> 16, c.s)));
+    uint4 lo, hi;
+    if (c.s16) {
+        lo = make_uint4(dequant2_h(q[0], c.s16), dequant2_h(q[0] >> 16, c.s16), dequant2_h(q[1], c.s16),
+                        dequant2_h(q[1] >> 16, c.s16));
+        hi = make_uint4(dequant2_h(q[2], c.s16), dequant2_h(q[2] >> 16, c.s16), dequant2_h(q[3], c.s16),
+                        dequant2_h(q[3] >> 16, c.s16));
+    } else {
+        lo = make_uint4(dequant2(q[0], c.s), dequant2(q[0] >> 16, c.s), dequant2(q[1], c.s), dequant2(q[1] >> 16, c.s));
+        hi = make_uint4(dequant2(q[2], c.s), dequant2(q[2] >> 16, c.s), dequant2(q[3], c.s), dequant2(q[3] >> 16, c.s));
+    }
+    st_out32(c.out + (uint64_t)c.i * 2, lo, hi);
     c.col += 16;
     if (c.col >= c.cols) {
         c.col -= c.cols;
         ++c.row;
-        if (c.i + 16 < c.n) c.s = bf16_bits_to_float(c.sc[c.row]);
+        if (c.i + 16 < c.n) {
+            c.s = bf16_bits_to_float(c.sc[c.row]);
+            c.s16 = scale_f16(c.s);
+        }
     }
 }
 
@@ -321,6 +358,7 @@ __device__ __forceinline__ void chain_setup(Chain& c, const DecBlock& B, uint32_
     c.row = (uint32_t)(sym0 / Ly.cols);
     c.col = (uint32_t)(sym0 % Ly.cols);
     c.s = BF16 ? bf16_bits_to_float(c.sc[c.row]) : 0.f;
+    c.s16 = BF16 ? scale_f16(c.s) : 0;
     c.fast = BF16 ? ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) : ((B.cs & 31) == 0);
 }
 

@@ -264,3 +264,23 @@ def test_calibrate_lambda_reaches_target():
     with pytest.raises(eq.EqError) as ei:
         eq.calibrate_lambda(dl, 9.5, row_stride=4)
     assert ei.value.status == eq.EQ_ERR_UNREACHABLE_TARGET
+
+
+def test_dequant_all_codes_all_scale_ranges():
+    """Every finite E4M3 code × row scales across the bf16 range (f16-exact scales take the
+    FHFMA path, the rest the FMUL path; subnormal bf16 products included), decoded through
+    the C-ABI and compared with the oracle's exact dequantiser."""
+    codes = np.array([c for c in range(256) if (c & 0x7F) != 0x7F and c != 0x80], dtype=np.uint8)   # 253
+    row = np.concatenate([codes, codes[:3]])                                                       # 256 cols
+    rng = np.random.default_rng(11)
+    s_bits = np.concatenate([
+        rng.integers(0x0080, 0x3800, 40),     # below the f16 normal range (FMUL path), incl. tiny
+        rng.integers(0x3880, 0x4780, 40),     # f16-exact range (FHFMA path)
+        rng.integers(0x4780, 0x7B00, 40),     # above f16 max (FMUL path)
+        [0x0001, 0x0005, 0x3880, 0x387F, 0x477F, 0x4780, 0x3F80],
+    ]).astype(np.uint16)
+    M = s_bits.size
+    C = np.tile(row, (M, 1))
+    blk = o.encode_codes([C], [(M, 256)], [s_bits], cs=512)
+    v = eq.decode_dequant([oracle_block_to_gpu(blk)], eq.EQ_OUT_BF16)[0][0]
+    assert (u16(v) == o.dequant(C, s_bits)).all()
