@@ -422,7 +422,7 @@ __device__ __forceinline__ void chain_finish(Chain& c, const uint8_t* payload, c
 }
 
 #ifndef EQ_DEC_MIN_CTAS
-#define EQ_DEC_MIN_CTAS 1
+#define EQ_DEC_MIN_CTAS 5
 #endif
 
 template <bool BF16>
