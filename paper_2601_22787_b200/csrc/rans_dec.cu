@@ -301,8 +301,17 @@ __device__ __forceinline__ uint32_t decode4(Chain& c, const DecTable& T) {
     return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(d, f, 0x0040), 0x5410);
 }
 
+#ifndef EQ_UNROLL2
+#define EQ_UNROLL2 0
+#endif
+__device__ __forceinline__ void store16_bf16_at(Chain& c, const uint32_t q[4], uint8_t* dst);
+
 // 16 symbols -> bf16 with one row scale (cols % 16 == 0), 32-byte store
 __device__ __forceinline__ void store16_bf16(Chain& c, const uint32_t q[4]) {
+    store16_bf16_at(c, q, c.out + (uint64_t)c.i * 2);
+}
+
+__device__ __forceinline__ void store16_bf16_at(Chain& c, const uint32_t q[4], uint8_t* dst) {
     uint4 lo, hi;
     if (c.s16) {
         lo = make_uint4(dequant2_h(q[0], c.s16), dequant2_h(q[0] >> 16, c.s16), dequant2_h(q[1], c.s16),
@@ -313,7 +322,7 @@ __device__ __forceinline__ void store16_bf16(Chain& c, const uint32_t q[4]) {
         lo = make_uint4(dequant2(q[0], c.s), dequant2(q[0] >> 16, c.s), dequant2(q[1], c.s), dequant2(q[1] >> 16, c.s));
         hi = make_uint4(dequant2(q[2], c.s), dequant2(q[2] >> 16, c.s), dequant2(q[3], c.s), dequant2(q[3] >> 16, c.s));
     }
-    st_out32(c.out + (uint64_t)c.i * 2, lo, hi);
+    st_out32(dst, lo, hi);
     c.col += 16;
     if (c.col >= c.cols) {
         c.col -= c.cols;
@@ -384,6 +393,29 @@ __device__ __forceinline__ void chain_finish(Chain& c, const uint8_t* payload, c
     if (!c.active || c.runaway) return;
     if (c.fast) {
         const uint32_t G = BF16 ? 16 : 32;
+#if EQ_UNROLL2
+        if (BF16) {
+            // two 16-symbol groups per iteration with a running output pointer (fewer
+            // loop-control and address instructions per symbol)
+            uint8_t* o = c.out + (uint64_t)c.i * 2;
+            while (c.i + 32 <= c.n) {
+                #pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    uint32_t q[4];
+                    q[0] = decode4(c, T);
+                    q[1] = decode4(c, T);
+                    stage_wait_all(); ring_issue(c.br, payload); stage_commit();
+                    q[2] = decode4(c, T);
+                    q[3] = decode4(c, T);
+                    stage_wait_all(); ring_issue(c.br, payload); stage_commit();
+                    store16_bf16_at(c, q, o + 32 * g);
+                    c.i += 16;
+                }
+                o += 64;
+                if (c.br.wi4 > c.wlimit4) { c.runaway = true; return; }
+            }
+        }
+#endif
         while (c.i + G <= c.n) {
             if (BF16) {
                 uint32_t q[4];
