@@ -28,6 +28,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 
 PROB_BITS = 12
 CHUNK_SYMBOLS = 4096
+FMT_E4M3, FMT_INT8 = 0, 1
 
 
 def build(force: bool = False) -> str:
@@ -66,6 +67,16 @@ def lib():
             "eqo_candidates": (i64, [u16, i32, i32, P]),
             "eqo_search_rows": (None, [P, i64, i64, dbl, i32, i32, i64, i64, P, P]),
             "eqo_row_objectives": (i64, [P, i64, i64, i64, dbl, i32, i32, P, P, i64]),
+            "eqo_qmax": (dbl, [ctypes.c_int]),
+            "eqo_grid_value": (dbl, [ctypes.c_int, u32]),
+            "eqo_grid_quantize": (ctypes.c_uint8, [ctypes.c_int, dbl]),
+            "eqo_absmax_scale_fmt": (u16, [ctypes.c_int, P, i64]),
+            "eqo_quantize_fmt": (None, [ctypes.c_int, P, i64, i64, P, P]),
+            "eqo_dequant_fmt": (None, [ctypes.c_int, P, i64, i64, P, P]),
+            "eqo_row_terms_fmt": (None, [ctypes.c_int, P, i64, u16, P, P]),
+            "eqo_objective_fmt": (dbl, [ctypes.c_int, P, i64, i64, P, dbl]),
+            "eqo_search_rows_fmt": (None, [ctypes.c_int, P, i64, i64, dbl, i32, i32, i64, i64, P, P]),
+            "eqo_row_objectives_fmt": (i64, [ctypes.c_int, P, i64, i64, i64, dbl, i32, i32, P, P, i64]),
             "eqo_histogram": (None, [P, i64, P]),
             "eqo_normalize": (ctypes.c_int, [P, P]),
             "eqo_entropy": (dbl, [P]),
@@ -127,36 +138,44 @@ def quantize_one(w_bf16: int, s_bf16: int) -> int:
 
 
 # ---------------------------------------------------------------- matrix steps
-def absmax_scales(W) -> np.ndarray:
+def grid_value(code: int, fmt: int = FMT_E4M3) -> float:
+    return lib().eqo_grid_value(fmt, code)
+
+
+def grid_quantize(r: float, fmt: int = FMT_E4M3) -> int:
+    return lib().eqo_grid_quantize(fmt, r)
+
+
+def absmax_scales(W, fmt: int = FMT_E4M3) -> np.ndarray:
     """Eq. (1), Alg. 1 l.1: per-row AbsMax scale as bf16 bits."""
     W = _u16(W)
     M, N = W.shape
-    return np.array([lib().eqo_absmax_scale(_p(W[i]), N) for i in range(M)], dtype=np.uint16)
+    return np.array([lib().eqo_absmax_scale_fmt(fmt, _p(W[i]), N) for i in range(M)], dtype=np.uint16)
 
 
-def quantize(W, S) -> np.ndarray:
+def quantize(W, S, fmt: int = FMT_E4M3) -> np.ndarray:
     """Alg. 1 l.3: codes = Q_γ(W, S)."""
     W, S = _u16(W), _u16(S)
     M, N = W.shape
     out = np.empty((M, N), dtype=np.uint8)
-    lib().eqo_quantize(_p(W), M, N, _p(S), _p(out))
+    lib().eqo_quantize_fmt(fmt, _p(W), M, N, _p(S), _p(out))
     return out
 
 
-def dequant(codes: np.ndarray, S) -> np.ndarray:
+def dequant(codes: np.ndarray, S, fmt: int = FMT_E4M3) -> np.ndarray:
     """Q†: bf16 bits of RNE(s·value(code))."""
     codes = np.ascontiguousarray(codes, dtype=np.uint8)
     S = _u16(S)
     M, N = codes.shape
     out = np.empty((M, N), dtype=np.uint16)
-    lib().eqo_dequant(_p(codes), M, N, _p(S), _p(out))
+    lib().eqo_dequant_fmt(fmt, _p(codes), M, N, _p(S), _p(out))
     return out
 
 
-def row_terms(w_row, s_bf16: int):
+def row_terms(w_row, s_bf16: int, fmt: int = FMT_E4M3):
     w_row = _u16(w_row)
     D, R = ctypes.c_double(), ctypes.c_double()
-    lib().eqo_row_terms(_p(w_row), w_row.size, s_bf16, ctypes.byref(D), ctypes.byref(R))
+    lib().eqo_row_terms_fmt(fmt, _p(w_row), w_row.size, s_bf16, ctypes.byref(D), ctypes.byref(R))
     return D.value, R.value
 
 
@@ -165,10 +184,10 @@ def l1(W) -> float:
     return lib().eqo_l1(_p(W), W.size)
 
 
-def objective(W, S, lam: float) -> float:
+def objective(W, S, lam: float, fmt: int = FMT_E4M3) -> float:
     W, S = _u16(W), _u16(S)
     M, N = W.shape
-    return lib().eqo_objective(_p(W), M, N, _p(S), lam)
+    return lib().eqo_objective_fmt(fmt, _p(W), M, N, _p(S), lam)
 
 
 def candidates(s0: int, oct_lo: int = -1, oct_hi: int = 20):
@@ -177,7 +196,7 @@ def candidates(s0: int, oct_lo: int = -1, oct_hi: int = 20):
     return first.value, n
 
 
-def search(W, lam: float, oct_lo: int = -1, oct_hi: int = 20, rows=None):
+def search(W, lam: float, oct_lo: int = -1, oct_hi: int = 20, rows=None, fmt: int = FMT_E4M3):
     """Alg. 1 l.2 (exhaustive per-row reading): returns (S bf16 bits, per-row objective).
 
     ``rows`` optionally restricts the search to a list of row indices (others are 0)."""
@@ -186,21 +205,21 @@ def search(W, lam: float, oct_lo: int = -1, oct_hi: int = 20, rows=None):
     S = np.zeros(M, dtype=np.uint16)
     f = np.zeros(M, dtype=np.float64)
     if rows is None:
-        lib().eqo_search_rows(_p(W), M, N, lam, oct_lo, oct_hi, 0, M, _p(S), _p(f))
+        lib().eqo_search_rows_fmt(fmt, _p(W), M, N, lam, oct_lo, oct_hi, 0, M, _p(S), _p(f))
     else:
         for r in rows:
-            lib().eqo_search_rows(_p(W), M, N, lam, oct_lo, oct_hi, int(r), int(r) + 1, _p(S), _p(f))
+            lib().eqo_search_rows_fmt(fmt, _p(W), M, N, lam, oct_lo, oct_hi, int(r), int(r) + 1, _p(S), _p(f))
     return S, f
 
 
-def row_objectives(W, row: int, lam: float, oct_lo: int = -1, oct_hi: int = 20):
+def row_objectives(W, row: int, lam: float, oct_lo: int = -1, oct_hi: int = 20, fmt: int = FMT_E4M3):
     """All candidate objectives f_i(s) of one row: (first pattern, array)."""
     W = _u16(W)
     M, N = W.shape
     cap = 128 * (oct_hi - oct_lo) + 8
     f = np.zeros(cap, dtype=np.float64)
     first = ctypes.c_uint16()
-    n = lib().eqo_row_objectives(_p(W), M, N, row, lam, oct_lo, oct_hi, ctypes.byref(first), _p(f), cap)
+    n = lib().eqo_row_objectives_fmt(fmt, _p(W), M, N, row, lam, oct_lo, oct_hi, ctypes.byref(first), _p(f), cap)
     return first.value, f[:n].copy()
 
 
@@ -260,6 +279,7 @@ class OracleBlock:
     chunk_off: np.ndarray            # uint32[n_chunks+1]
     chunk_symbols: int = CHUNK_SYMBOLS
     codes: np.ndarray = field(default=None, repr=False)   # concatenated symbol stream
+    fmt: int = FMT_E4M3
 
     @property
     def n_params(self) -> int:
@@ -276,7 +296,7 @@ class OracleBlock:
         return 8.0 * b / self.n_params
 
 
-def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS) -> OracleBlock:
+def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3) -> OracleBlock:
     """Alg. 1 l.4-5 + App. A.1: concatenate vec(W_q) of the block's layers, one table,
     chunked rANS."""
     stream = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1) for c in codes_list])
@@ -291,23 +311,26 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS) -> O
     if n < 0:
         raise ValueError("encode failed %d" % n)
     return OracleBlock(list(layer_shapes), [np.asarray(s, dtype=np.uint16) for s in scales], freq, hist,
-                       payload[:n].tobytes(), off, cs, stream)
+                       payload[:n].tobytes(), off, cs, stream, fmt)
 
 
 def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int = -1, oct_hi: int = 20,
-                    cs: int = CHUNK_SYMBOLS) -> OracleBlock:
+                    cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3, exclude=()) -> OracleBlock:
     """Alg. 1 for one block.  ``layers``: list of bf16 [M,N] arrays (uint16 bits or torch).
     Either ``scales`` (per layer) is given, or ``lam`` selects the exhaustive search
-    (lam=None -> AbsMax scales, i.e. the λ=0 lossless-FP8 baseline of P:257)."""
+    (lam=None -> AbsMax scales, i.e. the λ=0 lossless-FP8 baseline of P:257).  Layers whose
+    index is in ``exclude`` keep AbsMax scales (super-weight exclusion)."""
     Ws = [_u16(W) for W in layers]
     shapes = [tuple(W.shape) for W in Ws]
     if scales is None:
-        if lam is None:
-            scales = [absmax_scales(W) for W in Ws]
-        else:
-            scales = [search(W, lam, oct_lo, oct_hi)[0] for W in Ws]
-    codes = [quantize(W, S) for W, S in zip(Ws, scales)]
-    return encode_codes(codes, shapes, scales, cs)
+        scales = []
+        for i, W in enumerate(Ws):
+            if lam is None or i in exclude:
+                scales.append(absmax_scales(W, fmt))
+            else:
+                scales.append(search(W, lam, oct_lo, oct_hi, fmt=fmt)[0])
+    codes = [quantize(W, S, fmt) for W, S in zip(Ws, scales)]
+    return encode_codes(codes, shapes, scales, cs, fmt)
 
 
 def decode_block(blk: OracleBlock) -> np.ndarray:
@@ -328,7 +351,7 @@ def decode_dequant(blk: OracleBlock) -> list:
     stream = decode_block(blk)
     outs, a = [], 0
     for (r, c), S in zip(blk.layer_shapes, blk.scales):
-        outs.append(dequant(stream[a:a + r * c].reshape(r, c), S))
+        outs.append(dequant(stream[a:a + r * c].reshape(r, c), S, blk.fmt))
         a += r * c
     return outs
 

@@ -149,9 +149,36 @@ uint8_t eqo_quantize_one(uint16_t w_bf16, uint16_t s_bf16)
     return eqo_quantize_value(w / s);
 }
 
+/* ------------------------------------------------------------------------------------
+ * Base formats γ (§2.1; P:392 Int8 vs Float8; SPEC quantgrid S:26-118):
+ *   fmt 0 = Float8 E4M3 (above), Q_max 448;
+ *   fmt 1 = symmetric Int8, codes −127..127 stored as the two's-complement byte, value =
+ *           the integer ("value(c)=c"), Q_max 127; −128 (0x80) never produced.
+ * Quantiser for Int8: clamp the quotient to ±127, then round half to even.
+ * The f64 quotient is exact enough: for bf16 W and s a non-tie quotient is ≥ 2^-9
+ * (relative) away from every half-integer.
+ * ---------------------------------------------------------------------------------- */
+double eqo_qmax(int fmt) { return fmt == 1 ? 127.0 : 448.0; }
+
+double eqo_grid_value(int fmt, uint32_t code)
+{
+    if (fmt == 1) return (double)(int8_t)(uint8_t)code;
+    return eqo_e4m3_value(code);
+}
+
+uint8_t eqo_grid_quantize(int fmt, double r)
+{
+    if (fmt != 1) return eqo_quantize_value(r);
+    if (r > 127.0) r = 127.0;
+    if (r < -127.0) r = -127.0;
+    double q = rint(r);                           /* round half to even */
+    if (q == 0.0) return 0x00;
+    return (uint8_t)(int8_t)q;
+}
+
 /* Eq. (1), Alg. 1 l.1: s = max|W_row| / Q_max, per output channel
  * (P:148).  Stored as bf16 (RNE) since scales are BF16.  All-zero row -> 1. */
-uint16_t eqo_absmax_scale(const uint16_t* w_row, int64_t n)
+uint16_t eqo_absmax_scale_fmt(int fmt, const uint16_t* w_row, int64_t n)
 {
     double m = 0.0;
     for (int64_t j = 0; j < n; j++) {
@@ -159,26 +186,40 @@ uint16_t eqo_absmax_scale(const uint16_t* w_row, int64_t n)
         if (a > m) m = a;
     }
     if (m == 0.0) return eqo_bf16_from_double(1.0);
-    return eqo_bf16_from_double(m / 448.0);
+    return eqo_bf16_from_double(m / eqo_qmax(fmt));
 }
+
+uint16_t eqo_absmax_scale(const uint16_t* w_row, int64_t n) { return eqo_absmax_scale_fmt(0, w_row, n); }
 
 /* Alg. 1 l.3: W_q = Q_γ(W, S*) with one scale per row. */
-void eqo_quantize(const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, uint8_t* codes)
-{
-    for (int64_t i = 0; i < M; i++)
-        for (int64_t j = 0; j < N; j++)
-            codes[i * N + j] = eqo_quantize_one(W[i * N + j], S[i]);
-}
-
-/* §2.1 dequantiser Q† (P:142): Ŵ = s·W_q, returned as bf16 (RNE of the exact f64
- * product; the product of a bf16 and an E4M3 value has ≤ 12 significant bits). */
-void eqo_dequant(const uint8_t* codes, int64_t M, int64_t N, const uint16_t* S, uint16_t* out)
+void eqo_quantize_fmt(int fmt, const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, uint8_t* codes)
 {
     for (int64_t i = 0; i < M; i++) {
         double s = eqo_bf16_to_double(S[i]);
         for (int64_t j = 0; j < N; j++)
-            out[i * N + j] = eqo_bf16_from_double(s * eqo_e4m3_value(codes[i * N + j]));
+            codes[i * N + j] = eqo_grid_quantize(fmt, eqo_bf16_to_double(W[i * N + j]) / s);
     }
+}
+
+void eqo_quantize(const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, uint8_t* codes)
+{
+    eqo_quantize_fmt(0, W, M, N, S, codes);
+}
+
+/* §2.1 dequantiser Q† (P:142): Ŵ = s·W_q, returned as bf16 (RNE of the exact f64
+ * product; the product of a bf16 and an E4M3 value has ≤ 12 significant bits). */
+void eqo_dequant_fmt(int fmt, const uint8_t* codes, int64_t M, int64_t N, const uint16_t* S, uint16_t* out)
+{
+    for (int64_t i = 0; i < M; i++) {
+        double s = eqo_bf16_to_double(S[i]);
+        for (int64_t j = 0; j < N; j++)
+            out[i * N + j] = eqo_bf16_from_double(s * eqo_grid_value(fmt, codes[i * N + j]));
+    }
+}
+
+void eqo_dequant(const uint8_t* codes, int64_t M, int64_t N, const uint16_t* S, uint16_t* out)
+{
+    eqo_dequant_fmt(0, codes, M, N, S, out);
 }
 
 /* ------------------------------------------------------------------------------------
@@ -189,17 +230,22 @@ void eqo_dequant(const uint8_t* codes, int64_t M, int64_t N, const uint16_t* S, 
  *   D_i(s) = Σ_j |W_ij − s·v_ij|,  R_i(s) = Σ_j |v_ij|,  v_ij = value(Q_γ(W_ij, s)).
  * Each term is exact in f64; sums are sequential in j (f64).
  * ---------------------------------------------------------------------------------- */
-void eqo_row_terms(const uint16_t* w_row, int64_t n, uint16_t s_bf16, double* D, double* R)
+void eqo_row_terms_fmt(int fmt, const uint16_t* w_row, int64_t n, uint16_t s_bf16, double* D, double* R)
 {
     double s = eqo_bf16_to_double(s_bf16), d = 0.0, r = 0.0;
     for (int64_t j = 0; j < n; j++) {
         double w = eqo_bf16_to_double(w_row[j]);
-        double v = eqo_e4m3_value(eqo_quantize_value(w / s));
+        double v = eqo_grid_value(fmt, eqo_grid_quantize(fmt, w / s));
         d += fabs(w - s * v);
         r += fabs(v);
     }
     *D = d;
     *R = r;
+}
+
+void eqo_row_terms(const uint16_t* w_row, int64_t n, uint16_t s_bf16, double* D, double* R)
+{
+    eqo_row_terms_fmt(0, w_row, n, s_bf16, D, R);
 }
 
 double eqo_l1(const uint16_t* W, int64_t n)
@@ -210,17 +256,22 @@ double eqo_l1(const uint16_t* W, int64_t n)
 }
 
 /* Full-matrix objective (Eq. 4) for given per-row scales. */
-double eqo_objective(const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, double lambda)
+double eqo_objective_fmt(int fmt, const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, double lambda)
 {
     double l1 = eqo_l1(W, M * N), Dt = 0.0, Rt = 0.0;
     for (int64_t i = 0; i < M; i++) {
         double D, R;
-        eqo_row_terms(W + i * N, N, S[i], &D, &R);
+        eqo_row_terms_fmt(fmt, W + i * N, N, S[i], &D, &R);
         Dt += D;
         Rt += R;
     }
     double d = (l1 > 0.0) ? Dt / l1 : 0.0;
     return d + lambda * Rt / ((double)M * (double)N);
+}
+
+double eqo_objective(const uint16_t* W, int64_t M, int64_t N, const uint16_t* S, double lambda)
+{
+    return eqo_objective_fmt(0, W, M, N, S, lambda);
 }
 
 /* Candidate set for row search (reading, DESIGN.md §3 / SURVEY §8c.5): the contiguous
@@ -242,15 +293,15 @@ int64_t eqo_candidates(uint16_t s0, int32_t oct_lo, int32_t oct_hi, uint16_t* fi
  * candidate set (reading replacing L-BFGS+STE).  Tie rule: the
  * smallest candidate attaining the minimum.  All-zero rows keep s = 1.
  * obj_rows (nullable) receives f_i(s*_i). */
-void eqo_search_rows(const uint16_t* W, int64_t M, int64_t N, double lambda,
-                     int32_t oct_lo, int32_t oct_hi, int64_t row_begin, int64_t row_end,
-                     uint16_t* S, double* obj_rows)
+void eqo_search_rows_fmt(int fmt, const uint16_t* W, int64_t M, int64_t N, double lambda,
+                         int32_t oct_lo, int32_t oct_hi, int64_t row_begin, int64_t row_end,
+                         uint16_t* S, double* obj_rows)
 {
     double l1 = eqo_l1(W, M * N);
     double mn = (double)M * (double)N;
     for (int64_t i = row_begin; i < row_end; i++) {
         const uint16_t* row = W + i * N;
-        uint16_t s0 = eqo_absmax_scale(row, N);
+        uint16_t s0 = eqo_absmax_scale_fmt(fmt, row, N);
         int zero_row = 1;
         for (int64_t j = 0; j < N; j++)
             if ((row[j] & 0x7FFF) != 0) { zero_row = 0; break; }
@@ -266,7 +317,7 @@ void eqo_search_rows(const uint16_t* W, int64_t M, int64_t N, double lambda,
         for (int64_t k = 0; k < nc; k++) {
             uint16_t s = (uint16_t)(first + k);
             double D, R;
-            eqo_row_terms(row, N, s, &D, &R);
+            eqo_row_terms_fmt(fmt, row, N, s, &D, &R);
             double f = (l1 > 0.0 ? D / l1 : 0.0) + lambda * R / mn;
             if (f < best) { best = f; bests = s; }
         }
@@ -275,21 +326,28 @@ void eqo_search_rows(const uint16_t* W, int64_t M, int64_t N, double lambda,
     }
 }
 
+void eqo_search_rows(const uint16_t* W, int64_t M, int64_t N, double lambda,
+                     int32_t oct_lo, int32_t oct_hi, int64_t row_begin, int64_t row_end,
+                     uint16_t* S, double* obj_rows)
+{
+    eqo_search_rows_fmt(0, W, M, N, lambda, oct_lo, oct_hi, row_begin, row_end, S, obj_rows);
+}
+
 /* Per-candidate objective table of one row (used by tests to check GPU choices
  * against every candidate).  f[k] for candidate first+k.  Returns the count. */
-int64_t eqo_row_objectives(const uint16_t* W, int64_t M, int64_t N, int64_t row, double lambda,
-                           int32_t oct_lo, int32_t oct_hi, uint16_t* first_out, double* f,
-                           int64_t cap)
+int64_t eqo_row_objectives_fmt(int fmt, const uint16_t* W, int64_t M, int64_t N, int64_t row, double lambda,
+                               int32_t oct_lo, int32_t oct_hi, uint16_t* first_out, double* f,
+                               int64_t cap)
 {
     double l1 = eqo_l1(W, M * N);
     double mn = (double)M * (double)N;
     const uint16_t* r = W + row * N;
-    uint16_t s0 = eqo_absmax_scale(r, N), first;
+    uint16_t s0 = eqo_absmax_scale_fmt(fmt, r, N), first;
     int64_t nc = eqo_candidates(s0, oct_lo, oct_hi, &first);
     *first_out = first;
     for (int64_t k = 0; k < nc && k < cap; k++) {
         double D, R;
-        eqo_row_terms(r, N, (uint16_t)(first + k), &D, &R);
+        eqo_row_terms_fmt(fmt, r, N, (uint16_t)(first + k), &D, &R);
         f[k] = (l1 > 0.0 ? D / l1 : 0.0) + lambda * R / mn;
     }
     return nc;
@@ -586,4 +644,10 @@ int eqo_decode_dequant_layer_mt(const uint8_t* payload, const uint32_t* chunk_of
     free(th);
     free(jobs);
     return st;
+}
+
+int64_t eqo_row_objectives(const uint16_t* W, int64_t M, int64_t N, int64_t row, double lambda,
+                           int32_t oct_lo, int32_t oct_hi, uint16_t* first_out, double* f, int64_t cap)
+{
+    return eqo_row_objectives_fmt(0, W, M, N, row, lambda, oct_lo, oct_hi, first_out, f, cap);
 }
