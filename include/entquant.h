@@ -50,7 +50,9 @@ typedef enum {
 #define EQ_EF_BUFFER         0x10u
 
 #define EQ_FMT_E4M3   0u            /* Float8 E4M3 (torch float8_e4m3fn)            */
-#define EQ_OUT_FP8    0u            /* decode to raw E4M3 codes (scale left to the GEMM)   */
+#define EQ_FMT_INT8   1u            /* symmetric Int8, codes −127..127        */
+#define EQ_OUT_FP8    0u            /* decode to the raw 8-bit codes (E4M3 or Int8; scale  */
+                                    /* left to the GEMM epilogue)                          */
 #define EQ_OUT_BF16   1u            /* decode + fused per-row dequant to bf16      */
 
 #define EQ_SCALES_SEARCH 0u         /* exhaustive per-row Eq. 4 minimisation (R5)          */
@@ -70,12 +72,14 @@ typedef struct {
 } eq_tensor;
 
 typedef struct {
-    uint32_t format;                /* EQ_FMT_E4M3                                         */
+    uint32_t format;                /* EQ_FMT_E4M3 | EQ_FMT_INT8                           */
     uint32_t chunk_symbols;         /* 1 .. 262144; default EQ_DEFAULT_CHUNK       */
     uint32_t prob_bits;             /* must be 12                                          */
     uint32_t scale_mode;            /* EQ_SCALES_*                                         */
     double   lambda;                /* Eq. 4 λ ≥ 0, SPEC normalisation (R4)                */
     int32_t  oct_lo, oct_hi;        /* search bracket, octaves around AbsMax (R5): -1, 20  */
+    uint32_t exclude_mask;          /* bit l: layer l keeps AbsMax scales (λ = 0) — the    */
+                                    /* super-weight exclusion of P:393-396          */
 } eq_params;
 
 /* One compressed transformer block: all its layers in one bitstream with one table
@@ -91,6 +95,7 @@ typedef struct {
     uint16_t* freq;                 /* device: 256 normalised frequencies, Σ = 4096       */
     uint16_t* scales;               /* device: bf16 per-row scales, layers concatenated   */
     uint32_t  n_layers;
+    uint32_t  format;               /* EQ_FMT_* of the symbols (set by eq_quantize_encode) */
     int64_t   layer_rows[EQ_MAX_LAYERS];
     int64_t   layer_cols[EQ_MAX_LAYERS];
 } eq_block;
@@ -116,9 +121,9 @@ eq_status eq_arena_layout(const eq_block* blocks, uint32_t n_blocks, uint32_t ou
 /* ---------------------------------------------------------------- encode-side steps
  * §8(a) rows a1-a6; each is also used by eq_quantize_encode.  Asynchronous. */
 
-/* a1, Eq. (1), Alg. 1 l.1: s0_i = bf16_rne(max_j |W_ij| / 448); all-zero row -> 1
- * (S:67).  s0: device [rows] bf16. */
-eq_status eq_absmax(const eq_tensor* w, uint16_t* s0, eq_stream_t stream);
+/* a1, Eq. (1), Alg. 1 l.1: s0_i = bf16_rne(max_j |W_ij| / Q_max), Q_max = 448
+ * (E4M3) or 127 (Int8); all-zero row -> 1.  s0: device [rows] bf16. */
+eq_status eq_absmax(const eq_tensor* w, uint32_t format, uint16_t* s0, eq_stream_t stream);
 
 /* Scratch bytes eq_search_scales needs for `w`. */
 uint64_t eq_search_scratch_bytes(const eq_tensor* w);
@@ -130,16 +135,16 @@ uint64_t eq_search_scratch_bytes(const eq_tensor* w);
  * all-zero rows keep s = 1.  Outputs (device): scales[k*rows + i] and, if obj != NULL,
  * obj[k*rows + i] = f_i(s*).  Terms |W − s·v| are exact f32, sums f64 (deterministic
  * order).  n_lambda ≤ 32. */
-eq_status eq_search_scales(const eq_tensor* w, const double* lambdas_host, uint32_t n_lambda,
+eq_status eq_search_scales(const eq_tensor* w, uint32_t format, const double* lambdas_host, uint32_t n_lambda,
                            int32_t oct_lo, int32_t oct_hi, const uint32_t* rows, uint32_t n_rows,
                            uint16_t* scales, double* obj, void* scratch, uint64_t scratch_bytes,
                            eq_stream_t stream);
 
-/* a3 + a4, Alg. 1 l.3: codes = RNE_E4M3(clamp(W/s, ±448)) with
- * −0 → +0 for all rows (rows == NULL) or the listed rows, written row-major into `codes`
- * (device, rows*cols bytes; may be NULL to only count), and the 256-bin histogram
- * ACCUMULATED into hist (device uint64[256]). */
-eq_status eq_quantize_hist(const eq_tensor* w, const uint16_t* scales, const uint32_t* rows,
+/* a3 + a4, Alg. 1 l.3: codes = RNE_γ(clamp(W/s, ±Q_max)) — E4M3
+ * with −0 → +0, or Int8 (half to even, two's-complement byte) — for all rows (rows == NULL)
+ * or the listed rows, written row-major into `codes` (device, rows*cols bytes; may be NULL
+ * to only count), and the 256-bin histogram ACCUMULATED into hist (device uint64[256]). */
+eq_status eq_quantize_hist(const eq_tensor* w, uint32_t format, const uint16_t* scales, const uint32_t* rows,
                            uint32_t n_rows, uint8_t* codes, uint64_t* hist, eq_stream_t stream);
 
 /* a5 (R8): normalise hist (device uint64[256]) to freq (device uint16[256],
@@ -157,7 +162,8 @@ eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, uint32_t* ch
 
 /* ---------------------------------------------------------------- north-star calls */
 
-/* Alg. 1 for one block: scales (per p->scale_mode), FP8 quantisation, one
+/* Alg. 1 for one block: scales (per p->scale_mode; layers in p->exclude_mask
+ * keep AbsMax scales), 8-bit quantisation in p->format, one
  * histogram + table over the concatenated stream, chunked rANS.  Fills out->payload,
  * chunk_off, n_chunks, chunk_symbols, freq, scales (device, caller-allocated per
  * eq_encode_bounds) and out->payload_bytes.  SYNCHRONOUS: waits for the stream to read
@@ -170,7 +176,8 @@ eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_layers, const e
 /* Alg. 2 l.1-2 + App. A.1 arena: decode every chunk of `n_blocks`
  * blocks in ONE launch (chunk-parallel, lane per chunk) and write each layer, row-major,
  * into `arena` at the offsets of eq_arena_layout (views, no copies).  EQ_OUT_BF16 fuses
- * the dequantiser out = RNE_bf16(s_row · value(code)); EQ_OUT_FP8 writes the codes.
+ * the dequantiser out = RNE_bf16(s_row · value(code)) for the block's format (E4M3 or Int8);
+ * EQ_OUT_FP8 writes the codes.
  * Per-chunk integrity (final state == 2^23, every byte consumed) and offset bounds are
  * checked on the device and reported in d_err (EQ_EF_CORRUPT / EQ_EF_TRUNCATED).
  * Asynchronous; EQ_ERR_BUFFER if arena_bytes is below the layout's total. */

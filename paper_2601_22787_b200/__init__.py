@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("EQ_LIB") or os.path.join(_HERE, "libentquant.so")
 
 EQ_OK, EQ_ERR_ARG, EQ_ERR_SHAPE, EQ_ERR_EMPTY, EQ_ERR_BUFFER = 0, 1, 2, 3, 4
 EQ_ERR_CORRUPT, EQ_ERR_TRUNCATED, EQ_ERR_UNKNOWN_SYMBOL, EQ_ERR_UNREACHABLE_TARGET, EQ_ERR_CUDA = 5, 6, 7, 8, 9
-EQ_FMT_E4M3 = 0
+EQ_FMT_E4M3, EQ_FMT_INT8 = 0, 1
 EQ_OUT_FP8, EQ_OUT_BF16 = 0, 1
 EQ_SCALES_SEARCH, EQ_SCALES_ABSMAX, EQ_SCALES_GIVEN = 0, 1, 2
 EQ_MAX_LAYERS = 8
@@ -53,7 +53,8 @@ class eq_tensor(ctypes.Structure):
 class eq_params(ctypes.Structure):
     _fields_ = [("format", ctypes.c_uint32), ("chunk_symbols", ctypes.c_uint32),
                 ("prob_bits", ctypes.c_uint32), ("scale_mode", ctypes.c_uint32),
-                ("lambda_", ctypes.c_double), ("oct_lo", ctypes.c_int32), ("oct_hi", ctypes.c_int32)]
+                ("lambda_", ctypes.c_double), ("oct_lo", ctypes.c_int32), ("oct_hi", ctypes.c_int32),
+                ("exclude_mask", ctypes.c_uint32)]
 
 
 class eq_block(ctypes.Structure):
@@ -61,6 +62,7 @@ class eq_block(ctypes.Structure):
                 ("payload_bytes", ctypes.c_uint64), ("chunk_off", ctypes.c_void_p),
                 ("n_chunks", ctypes.c_uint32), ("chunk_symbols", ctypes.c_uint32),
                 ("freq", ctypes.c_void_p), ("scales", ctypes.c_void_p), ("n_layers", ctypes.c_uint32),
+                ("format", ctypes.c_uint32),
                 ("layer_rows", ctypes.c_int64 * EQ_MAX_LAYERS), ("layer_cols", ctypes.c_int64 * EQ_MAX_LAYERS)]
 
 
@@ -81,10 +83,10 @@ def lib() -> ctypes.CDLL:
             "eq_version": (ctypes.c_char_p, []),
             "eq_encode_bounds": (st, [P, u32, P, P, P, P]),
             "eq_arena_layout": (st, [P, u32, u32, P, P]),
-            "eq_absmax": (st, [P, P, P]),
+            "eq_absmax": (st, [P, u32, P, P]),
             "eq_search_scratch_bytes": (u64, [P]),
-            "eq_search_scales": (st, [P, P, u32, i32, i32, P, u32, P, P, P, u64, P]),
-            "eq_quantize_hist": (st, [P, P, P, u32, P, P, P]),
+            "eq_search_scales": (st, [P, u32, P, u32, i32, i32, P, u32, P, P, P, u64, P]),
+            "eq_quantize_hist": (st, [P, u32, P, P, u32, P, P, P]),
             "eq_build_table": (st, [P, P, P, P]),
             "eq_rans_encode": (st, [P, P, P, P, P, P]),
             "eq_quantize_encode": (st, [P, u32, P, P, P, u64, P]),
@@ -139,8 +141,12 @@ def _tensor(W: torch.Tensor) -> eq_tensor:
     return eq_tensor(W.data_ptr(), W.shape[0], W.shape[1])
 
 
-def _params(chunk_symbols=EQ_DEFAULT_CHUNK, scale_mode=EQ_SCALES_SEARCH, lam=0.0, oct_lo=-1, oct_hi=20) -> eq_params:
-    return eq_params(EQ_FMT_E4M3, chunk_symbols, EQ_PROB_BITS, scale_mode, float(lam), oct_lo, oct_hi)
+def _params(chunk_symbols=EQ_DEFAULT_CHUNK, scale_mode=EQ_SCALES_SEARCH, lam=0.0, oct_lo=-1, oct_hi=20,
+            fmt=EQ_FMT_E4M3, exclude=()) -> eq_params:
+    mask = 0
+    for i in exclude:
+        mask |= 1 << int(i)
+    return eq_params(fmt, chunk_symbols, EQ_PROB_BITS, scale_mode, float(lam), oct_lo, oct_hi, mask)
 
 
 # ---------------------------------------------------------------- compressed block
@@ -155,6 +161,7 @@ class Block:
     shapes: list                     # [(rows, cols)] in block order
     chunk_symbols: int = EQ_DEFAULT_CHUNK
     meta: dict = field(default_factory=dict)
+    format: int = EQ_FMT_E4M3
 
     @property
     def n_chunks(self) -> int:
@@ -175,6 +182,7 @@ class Block:
         b.freq = self.freq.data_ptr()
         b.scales = self.scales.data_ptr()
         b.n_layers = len(self.shapes)
+        b.format = self.format
         for i, (r, c) in enumerate(self.shapes):
             b.layer_rows[i] = r
             b.layer_cols[i] = c
@@ -206,13 +214,15 @@ def encode_bounds(layers, chunk_symbols=EQ_DEFAULT_CHUNK):
 
 def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH, scales: torch.Tensor | None = None,
                     chunk_symbols: int = EQ_DEFAULT_CHUNK, oct_lo: int = -1, oct_hi: int = 20,
-                    stream=None, scratch: torch.Tensor | None = None, shrink: bool = True) -> Block:
-    """Alg. 1 for one block of bf16 CUDA matrices.  Synchronous (reads payload size)."""
+                    stream=None, scratch: torch.Tensor | None = None, shrink: bool = True,
+                    format: int = EQ_FMT_E4M3, exclude=()) -> Block:
+    """Alg. 1 for one block of bf16 CUDA matrices.  Synchronous (reads payload size).
+    ``exclude``: layer indices kept at AbsMax scales (λ = 0)."""
     if scales is not None:
         scale_mode = EQ_SCALES_GIVEN
     dev = layers[0].device
     ts = (eq_tensor * len(layers))(*[_tensor(W) for W in layers])
-    p = _params(chunk_symbols, scale_mode, lam, oct_lo, oct_hi)
+    p = _params(chunk_symbols, scale_mode, lam, oct_lo, oct_hi, format, exclude)
     cap, nc, sb = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint64()
     _ck(lib().eq_encode_bounds(ts, len(layers), ctypes.byref(p), ctypes.byref(cap), ctypes.byref(nc), ctypes.byref(sb)),
         "eq_encode_bounds")
@@ -237,7 +247,7 @@ def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH
         keep = (nbytes + EQ_PAYLOAD_SLACK + 255) // 256 * 256
         payload = payload[:keep].clone()
     return Block(payload, nbytes, off, freq, scales, [tuple(W.shape) for W in layers], chunk_symbols,
-                 {"lambda": lam, "scale_mode": scale_mode})
+                 {"lambda": lam, "scale_mode": scale_mode, "exclude": tuple(exclude)}, format)
 
 
 def arena_layout(blocks, out_dtype=EQ_OUT_BF16):
@@ -334,15 +344,15 @@ class HostBlocks:
 
 
 # ---------------------------------------------------------------- step-level calls (a1-a6)
-def absmax(W: torch.Tensor, stream=None) -> torch.Tensor:
+def absmax(W: torch.Tensor, stream=None, format: int = EQ_FMT_E4M3) -> torch.Tensor:
     t = _tensor(W)
     s0 = torch.empty(W.shape[0], dtype=torch.bfloat16, device=W.device)
-    _ck(lib().eq_absmax(ctypes.byref(t), s0.data_ptr(), _stream(stream)), "eq_absmax")
+    _ck(lib().eq_absmax(ctypes.byref(t), format, s0.data_ptr(), _stream(stream)), "eq_absmax")
     return s0
 
 
 def search_scales(W: torch.Tensor, lambdas, oct_lo: int = -1, oct_hi: int = 20, rows: torch.Tensor | None = None,
-                  with_obj: bool = False, stream=None):
+                  with_obj: bool = False, stream=None, format: int = EQ_FMT_E4M3):
     """a2: scales [len(lambdas), rows] (bf16) and optionally the per-row objective (f64)."""
     t = _tensor(W)
     lam = list(lambdas) if hasattr(lambdas, "__len__") else [float(lambdas)]
@@ -353,14 +363,14 @@ def search_scales(W: torch.Tensor, lambdas, oct_lo: int = -1, oct_hi: int = 20, 
     scratch = torch.empty(sb, dtype=torch.uint8, device=W.device)
     if rows is not None:
         rows = rows.to(device=W.device, dtype=torch.int32).contiguous()
-    _ck(lib().eq_search_scales(ctypes.byref(t), la, len(lam), oct_lo, oct_hi, _ptr(rows),
+    _ck(lib().eq_search_scales(ctypes.byref(t), format, la, len(lam), oct_lo, oct_hi, _ptr(rows),
                                0 if rows is None else rows.numel(), sc.data_ptr(), _ptr(ob), scratch.data_ptr(), sb,
                                _stream(stream)), "eq_search_scales")
     return (sc, ob) if with_obj else sc
 
 
 def quantize_hist(W: torch.Tensor, scales: torch.Tensor, codes: bool = True, hist: torch.Tensor | None = None,
-                  rows: torch.Tensor | None = None, stream=None):
+                  rows: torch.Tensor | None = None, stream=None, format: int = EQ_FMT_E4M3):
     """a3+a4: (codes uint8 [M,N] or None, hist int64 [256] accumulated)."""
     t = _tensor(W)
     _require_cuda(scales)
@@ -369,7 +379,7 @@ def quantize_hist(W: torch.Tensor, scales: torch.Tensor, codes: bool = True, his
         hist = torch.zeros(256, dtype=torch.int64, device=W.device)
     if rows is not None:
         rows = rows.to(device=W.device, dtype=torch.int32).contiguous()
-    _ck(lib().eq_quantize_hist(ctypes.byref(t), scales.contiguous().data_ptr(), _ptr(rows),
+    _ck(lib().eq_quantize_hist(ctypes.byref(t), format, scales.contiguous().data_ptr(), _ptr(rows),
                                0 if rows is None else rows.numel(), _ptr(c), hist.data_ptr(), _stream(stream)),
         "eq_quantize_hist")
     return c, hist
@@ -407,10 +417,10 @@ def rans_encode(codes: torch.Tensor, shapes, freq: torch.Tensor, scales: torch.T
 
 
 def calibrate_lambda(layers, target_bits: float, row_stride: int = 8, chunk_symbols: int = EQ_DEFAULT_CHUNK,
-                     oct_lo: int = -1, oct_hi: int = 20, stream=None):
+                     oct_lo: int = -1, oct_hi: int = 20, stream=None, format: int = EQ_FMT_E4M3):
     """Global λ for a target effective rate.  Returns (λ, estimated bits)."""
     ts = (eq_tensor * len(layers))(*[_tensor(W) for W in layers])
-    p = _params(chunk_symbols, EQ_SCALES_SEARCH, 0.0, oct_lo, oct_hi)
+    p = _params(chunk_symbols, EQ_SCALES_SEARCH, 0.0, oct_lo, oct_hi, format)
     sb = lib().eq_calibrate_scratch_bytes(ts, len(layers), row_stride)
     scratch = torch.empty(sb, dtype=torch.uint8, device=layers[0].device)
     lam, est = ctypes.c_double(), ctypes.c_double()

@@ -29,7 +29,7 @@ eq_status check_layers(const eq_tensor* layers, uint32_t n_layers) {
 
 eq_status check_params(const eq_params* p) {
     if (!p) return EQ_ERR_ARG;
-    if (p->format != EQ_FMT_E4M3 || p->prob_bits != EQ_PROB_BITS) return EQ_ERR_ARG;
+    if (p->format > EQ_FMT_INT8 || p->prob_bits != EQ_PROB_BITS) return EQ_ERR_ARG;
     if (p->chunk_symbols == 0 || p->chunk_symbols > 262144u) return EQ_ERR_ARG;
     if (p->scale_mode > EQ_SCALES_GIVEN) return EQ_ERR_ARG;
     if (p->scale_mode == EQ_SCALES_SEARCH && !(p->lambda >= 0.0)) return EQ_ERR_ARG;
@@ -145,6 +145,7 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
     EncodeScratch S = carve(layers, n_layers, nc, (char*)scratch);
 
     out->n_layers = n_layers;
+    out->format = p->format;
     out->n_chunks = nc;
     out->chunk_symbols = p->chunk_symbols;
     for (uint32_t l = 0; l < EQ_MAX_LAYERS; ++l) {
@@ -157,13 +158,14 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
     uint64_t sym = 0, row = 0;
     for (uint32_t l = 0; l < n_layers; ++l) {
         uint16_t* sl = out->scales + row;
-        if (p->scale_mode == EQ_SCALES_SEARCH) {
-            EQ_TRY(eq_search_scales(&layers[l], &p->lambda, 1, p->oct_lo, p->oct_hi, nullptr, 0, sl, nullptr,
-                                    S.search, S.search_bytes, stream));
-        } else if (p->scale_mode == EQ_SCALES_ABSMAX) {
-            EQ_TRY(eq_absmax(&layers[l], sl, stream));
+        const bool excluded = (p->exclude_mask >> l) & 1u;        // λ = 0, still coded
+        if (p->scale_mode == EQ_SCALES_SEARCH && !excluded) {
+            EQ_TRY(eq_search_scales(&layers[l], p->format, &p->lambda, 1, p->oct_lo, p->oct_hi, nullptr, 0, sl,
+                                    nullptr, S.search, S.search_bytes, stream));
+        } else if (p->scale_mode == EQ_SCALES_ABSMAX || (p->scale_mode == EQ_SCALES_SEARCH && excluded)) {
+            EQ_TRY(eq_absmax(&layers[l], p->format, sl, stream));
         }
-        EQ_TRY(eq_quantize_hist(&layers[l], sl, nullptr, 0, S.codes + sym, S.hist, stream));
+        EQ_TRY(eq_quantize_hist(&layers[l], p->format, sl, nullptr, 0, S.codes + sym, S.hist, stream));
         sym += (uint64_t)layers[l].rows * (uint64_t)layers[l].cols;
         row += (uint64_t)layers[l].rows;
     }
@@ -332,10 +334,10 @@ extern "C" eq_status eq_calibrate_lambda(const eq_tensor* layers, uint32_t n_lay
         for (uint32_t l = 0; l < n_layers; ++l) {
             const uint32_t nr = (uint32_t)(rl_off[l + 1] - rl_off[l]);
             uint16_t* sc = C.scales + sc_off[l];
-            EQ_TRY(eq_search_scales(&layers[l], lam.data(), (uint32_t)lam.size(), p->oct_lo, p->oct_hi,
+            EQ_TRY(eq_search_scales(&layers[l], p->format, lam.data(), (uint32_t)lam.size(), p->oct_lo, p->oct_hi,
                                     C.rows + rl_off[l], nr, sc, nullptr, C.search, C.search_bytes, stream));
             for (size_t k = 0; k < lam.size(); ++k)
-                EQ_TRY(eq_quantize_hist(&layers[l], sc + k * layers[l].rows, C.rows + rl_off[l], nr, nullptr,
+                EQ_TRY(eq_quantize_hist(&layers[l], p->format, sc + k * layers[l].rows, C.rows + rl_off[l], nr, nullptr,
                                         C.hist + 256 * k, stream));
         }
         std::vector<uint64_t> h(256 * lam.size());

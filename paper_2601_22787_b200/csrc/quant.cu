@@ -20,12 +20,31 @@ constexpr int kMaxLambda = 32;
 // 2^-24 of the exact one and m/448 (m with 8 significant bits) is never within 2^-12
 // (relative) of a bf16 rounding midpoint unless exact, so bf16(fl32(max/448)) is the
 // exact RNE.  All-zero row -> 1.0.
-__device__ __forceinline__ uint16_t absmax_from_max(float m) {
-    return m == 0.f ? (uint16_t)0x3F80u : float_to_bf16_bits(__fdiv_rn(m, kQmax));
+__device__ __forceinline__ uint16_t absmax_from_max(float m, float qmax) {
+    return m == 0.f ? (uint16_t)0x3F80u : float_to_bf16_bits(__fdiv_rn(m, qmax));
+}
+
+// Int8: clamp to ±127, round half to even (the f32 quotient of bf16 values
+// is ≥ 2^-9 relative away from any half-integer unless exactly on it, so fl32 suffices)
+__device__ __forceinline__ uint32_t int8x2_from_float2(float a, float b) {
+    const int ia = __float2int_rn(fminf(fmaxf(a, -127.f), 127.f));
+    const int ib = __float2int_rn(fminf(fmaxf(b, -127.f), 127.f));
+    return ((uint32_t)ia & 0xFFu) | (((uint32_t)ib & 0xFFu) << 8);
+}
+__device__ __forceinline__ float2 int8x2_to_float2(uint32_t pair) {
+    return make_float2((float)(int8_t)(pair & 0xFFu), (float)(int8_t)((pair >> 8) & 0xFFu));
+}
+template <uint32_t FMT>
+__device__ __forceinline__ uint32_t codes2(float a, float b) {
+    return FMT == EQ_FMT_INT8 ? int8x2_from_float2(a, b) : e4m3x2_from_float2(a, b);
+}
+template <uint32_t FMT>
+__device__ __forceinline__ float2 values2(uint32_t pair) {
+    return FMT == EQ_FMT_INT8 ? int8x2_to_float2(pair) : e4m3x2_to_float2(pair);
 }
 
 __global__ void __launch_bounds__(kRedThreads)
-k_absmax(const uint16_t* __restrict__ W, int64_t rows, int64_t cols, uint16_t* __restrict__ s0) {
+k_absmax(const uint16_t* __restrict__ W, int64_t rows, int64_t cols, float qmax, uint16_t* __restrict__ s0) {
     const int64_t r = blockIdx.x;
     if (r >= rows) return;
     const uint16_t* row = W + r * cols;
@@ -38,7 +57,7 @@ k_absmax(const uint16_t* __restrict__ W, int64_t rows, int64_t cols, uint16_t* _
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < kRedThreads / 32; ++w) m = max(m, wm[w]);
-        s0[r] = absmax_from_max(bf16_bits_to_float(m));
+        s0[r] = absmax_from_max(bf16_bits_to_float(m), qmax);
     }
 }
 
@@ -73,6 +92,7 @@ __global__ void k_l1_final(const double* __restrict__ part, int n, double* __res
 // ---------------------------------------------------------------- a2: scale search
 struct SearchParams {
     const uint16_t* W;
+    float qmax;
     int64_t rows, cols;
     const uint32_t* row_list;   // nullable
     uint32_t n_rows;
@@ -85,9 +105,10 @@ struct SearchParams {
 };
 
 // one exact term pair: |w − s·v| in f32 (exact: see DESIGN.md §6 K-SRCH), |v|·512 integer
+template <uint32_t FMT>
 __device__ __forceinline__ void term2(float w0, float w1, float s, double& D, uint32_t& R) {
-    const uint32_t q = e4m3x2_from_float2(__fdiv_rn(w0, s), __fdiv_rn(w1, s));
-    const float2 v = e4m3x2_to_float2(q);
+    const uint32_t q = codes2<FMT>(__fdiv_rn(w0, s), __fdiv_rn(w1, s));
+    const float2 v = values2<FMT>(q);
     D += (double)fabsf(__fsub_rn(w0, __fmul_rn(s, v.x)));
     D += (double)fabsf(__fsub_rn(w1, __fmul_rn(s, v.y)));
     R += (uint32_t)__fmul_rn(fabsf(v.x), 512.f) + (uint32_t)__fmul_rn(fabsf(v.y), 512.f);
@@ -100,6 +121,7 @@ __device__ __forceinline__ bool better(double f, uint32_t k, double bf, uint32_t
 // One CTA per searched row.  The row is staged in shared memory as f32 (exact bf16
 // values); warps take candidates k = warp, warp+8, ...; lanes stride over the row; warp
 // reduction in fixed order; per-λ best kept by lane 0, merged over warps at the end.
+template <uint32_t FMT>
 __global__ void __launch_bounds__(kSearchThreads)
 k_search(const __grid_constant__ SearchParams P) {
     extern __shared__ float srow[];
@@ -128,7 +150,7 @@ k_search(const __grid_constant__ SearchParams P) {
     if (lane == 0) atomicMax(&s_max, m);
     __syncthreads();
     m = s_max;
-    const uint16_t s0 = absmax_from_max(bf16_bits_to_float(m));
+    const uint16_t s0 = absmax_from_max(bf16_bits_to_float(m), P.qmax);
     if (m == 0) {                                   // all-zero row keeps s = 1
         if (t < (int)P.n_lambda) {
             P.scales[(int64_t)t * P.rows + r] = 0x3F80u;
@@ -157,7 +179,7 @@ k_search(const __grid_constant__ SearchParams P) {
         uint32_t R = 0;
         for (int64_t p = lane; p < npair; p += 32) {
             const float2 w = reinterpret_cast<const float2*>(srow)[p];
-            term2(w.x, w.y, s, D, R);
+            term2<FMT>(w.x, w.y, s, D, R);
         }
         unsigned long long R64 = R;                 // a 28672-wide row overflows u32
         #pragma unroll
@@ -193,6 +215,7 @@ k_search(const __grid_constant__ SearchParams P) {
 // per-warp shared sub-histograms; the dominant zero symbol is counted in a register.
 constexpr int kQhThreads = 256;
 
+template <uint32_t FMT>
 __global__ void __launch_bounds__(kQhThreads)
 k_quant_hist(const uint16_t* __restrict__ W, int64_t rows, int64_t cols, const uint16_t* __restrict__ S,
              const uint32_t* __restrict__ row_list, uint32_t n_rows, uint8_t* __restrict__ codes,
@@ -214,7 +237,7 @@ k_quant_hist(const uint16_t* __restrict__ W, int64_t rows, int64_t cols, const u
             const float w0 = bf16_bits_to_float(wr[j]);
             const bool two = (j + 1 < cols);
             const float w1 = two ? bf16_bits_to_float(wr[j + 1]) : 0.f;
-            const uint32_t q = e4m3x2_from_float2(__fdiv_rn(w0, s), __fdiv_rn(w1, s));
+            const uint32_t q = codes2<FMT>(__fdiv_rn(w0, s), __fdiv_rn(w1, s));
             const uint32_t c0 = q & 0xFFu, c1 = q >> 8;
             if (cr) {
                 cr[j] = (uint8_t)c0;
@@ -245,11 +268,13 @@ static eq_status check_tensor(const eq_tensor* w) {
     return EQ_OK;
 }
 
-extern "C" eq_status eq_absmax(const eq_tensor* w, uint16_t* s0, eq_stream_t stream) {
+static float qmax_of(uint32_t format) { return format == EQ_FMT_INT8 ? 127.f : 448.f; }
+
+extern "C" eq_status eq_absmax(const eq_tensor* w, uint32_t format, uint16_t* s0, eq_stream_t stream) {
     EQ_TRY(check_tensor(w));
-    if (!s0) return EQ_ERR_ARG;
+    if (!s0 || format > EQ_FMT_INT8) return EQ_ERR_ARG;
     k_absmax<<<(unsigned)w->rows, kRedThreads, 0, (cudaStream_t)stream>>>(
-        (const uint16_t*)w->w, w->rows, w->cols, s0);
+        (const uint16_t*)w->w, w->rows, w->cols, qmax_of(format), s0);
     EQ_CUDA_TRY(cudaGetLastError());
     return EQ_OK;
 }
@@ -261,12 +286,13 @@ extern "C" uint64_t eq_search_scratch_bytes(const eq_tensor* w) {
     return 256 + 8ull * (uint64_t)l1_ctas(w->rows * w->cols);
 }
 
-extern "C" eq_status eq_search_scales(const eq_tensor* w, const double* lambdas_host, uint32_t n_lambda,
+extern "C" eq_status eq_search_scales(const eq_tensor* w, uint32_t format, const double* lambdas_host, uint32_t n_lambda,
                                       int32_t oct_lo, int32_t oct_hi, const uint32_t* rows, uint32_t n_rows,
                                       uint16_t* scales, double* obj, void* scratch, uint64_t scratch_bytes,
                                       eq_stream_t stream) {
     EQ_TRY(check_tensor(w));
     if (!lambdas_host || n_lambda == 0 || n_lambda > (uint32_t)kMaxLambda || !scales || !scratch) return EQ_ERR_ARG;
+    if (format > EQ_FMT_INT8) return EQ_ERR_ARG;
     if (oct_hi < oct_lo || oct_lo < -40 || oct_hi > 40) return EQ_ERR_ARG;
     for (uint32_t q = 0; q < n_lambda; ++q)
         if (!(lambdas_host[q] >= 0.0)) return EQ_ERR_ARG;
@@ -283,6 +309,7 @@ extern "C" eq_status eq_search_scales(const eq_tensor* w, const double* lambdas_
     k_l1_final<<<1, 32, 0, st>>>(part, nct, l1);
     SearchParams P;
     P.W = (const uint16_t*)w->w;
+    P.qmax = qmax_of(format);
     P.rows = w->rows;
     P.cols = w->cols;
     P.row_list = rows;
@@ -295,21 +322,30 @@ extern "C" eq_status eq_search_scales(const eq_tensor* w, const double* lambdas_
     P.scales = scales;
     P.obj = obj;
     if (P.n_rows == 0) return EQ_OK;
-    EQ_CUDA_TRY(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_search<<<P.n_rows, kSearchThreads, smem, st>>>(P);
+    if (format == EQ_FMT_INT8) {
+        EQ_CUDA_TRY(cudaFuncSetAttribute(k_search<EQ_FMT_INT8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_search<EQ_FMT_INT8><<<P.n_rows, kSearchThreads, smem, st>>>(P);
+    } else {
+        EQ_CUDA_TRY(cudaFuncSetAttribute(k_search<EQ_FMT_E4M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_search<EQ_FMT_E4M3><<<P.n_rows, kSearchThreads, smem, st>>>(P);
+    }
     EQ_CUDA_TRY(cudaGetLastError());
     return EQ_OK;
 }
 
-extern "C" eq_status eq_quantize_hist(const eq_tensor* w, const uint16_t* scales, const uint32_t* rows,
+extern "C" eq_status eq_quantize_hist(const eq_tensor* w, uint32_t format, const uint16_t* scales, const uint32_t* rows,
                                       uint32_t n_rows, uint8_t* codes, uint64_t* hist, eq_stream_t stream) {
     EQ_TRY(check_tensor(w));
-    if (!scales || !hist) return EQ_ERR_ARG;
+    if (!scales || !hist || format > EQ_FMT_INT8) return EQ_ERR_ARG;
     const uint32_t nr = rows ? n_rows : (uint32_t)w->rows;
     if (nr == 0) return EQ_OK;
     const int ctas = (int)std::min<int64_t>(148 * 8, nr);
-    k_quant_hist<<<ctas, kQhThreads, 0, (cudaStream_t)stream>>>((const uint16_t*)w->w, w->rows, w->cols, scales,
-                                                                 rows, nr, codes, (unsigned long long*)hist);
+    if (format == EQ_FMT_INT8)
+        k_quant_hist<EQ_FMT_INT8><<<ctas, kQhThreads, 0, (cudaStream_t)stream>>>(
+            (const uint16_t*)w->w, w->rows, w->cols, scales, rows, nr, codes, (unsigned long long*)hist);
+    else
+        k_quant_hist<EQ_FMT_E4M3><<<ctas, kQhThreads, 0, (cudaStream_t)stream>>>(
+            (const uint16_t*)w->w, w->rows, w->cols, scales, rows, nr, codes, (unsigned long long*)hist);
     EQ_CUDA_TRY(cudaGetLastError());
     return EQ_OK;
 }

@@ -46,7 +46,8 @@ struct DecBlock {
     const uint16_t* freq;
     const uint16_t* scales;
     uint64_t payload_bytes;
-    uint64_t word_end;     // unused by the kernel (kept for the layout)
+    uint32_t format;       // EQ_FMT_E4M3 | EQ_FMT_INT8 (bf16 dequant of the codes)
+    uint32_t pad0;
     uint32_t n_chunks;
     uint32_t cs;           // chunk symbols
     uint32_t n_layers;
@@ -232,6 +233,13 @@ __device__ __forceinline__ uint32_t dequant2_h(uint32_t pair, uint16_t s16) {
     return *reinterpret_cast<uint32_t*>(&r);
 }
 
+// Int8 base format: s · c is exact in f32 (8 + 8 significant bits), one RNE to bf16
+__device__ __forceinline__ uint32_t dequant2_i8(uint32_t pair, float s) {
+    const float a = (float)(int8_t)(pair & 0xFFu), b = (float)(int8_t)((pair >> 8) & 0xFFu);
+    __nv_bfloat162 r = __floats2bfloat162_rn(__fmul_rn(s, a), __fmul_rn(s, b));
+    return *reinterpret_cast<uint32_t*>(&r);
+}
+
 // f16 bits of a bf16 scale if exactly representable (normal f16 range), else 0
 __device__ __forceinline__ uint16_t scale_f16(float s) {
     const float a = fabsf(s);
@@ -264,10 +272,15 @@ __device__ __forceinline__ void st_out32(void* p, uint4 a, uint4 b) {
 }
 
 template <bool BF16>
-__device__ __forceinline__ void store_one(uint8_t* out, uint64_t i, uint32_t sym, float s) {
+__device__ __forceinline__ void store_one(uint8_t* out, uint64_t i, uint32_t sym, float s, bool i8) {
     if (BF16) {
-        __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)sym, __NV_E4M3);
-        float v = __half2float(*reinterpret_cast<__half*>(&h));
+        float v;
+        if (i8) {
+            v = (float)(int8_t)sym;
+        } else {
+            __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)sym, __NV_E4M3);
+            v = __half2float(*reinterpret_cast<__half*>(&h));
+        }
         reinterpret_cast<uint16_t*>(out)[i] = float_to_bf16_bits(__fmul_rn(s, v));
     } else {
         out[i] = (uint8_t)sym;
@@ -283,6 +296,7 @@ struct Chain {
     uint32_t row, col, cols;
     float s;
     uint16_t s16;          // f16 bits of s when exact, else 0 (FMUL path)
+    bool i8;               // Int8 base format
     uint32_t n, i;
     uint32_t a;            // chunk payload byte range [a, e)
     uint32_t e;
@@ -313,7 +327,12 @@ __device__ __forceinline__ void store16_bf16(Chain& c, const uint32_t q[4]) {
 
 __device__ __forceinline__ void store16_bf16_at(Chain& c, const uint32_t q[4], uint8_t* dst) {
     uint4 lo, hi;
-    if (c.s16) {
+    if (c.i8) {
+        lo = make_uint4(dequant2_i8(q[0], c.s), dequant2_i8(q[0] >> 16, c.s), dequant2_i8(q[1], c.s),
+                        dequant2_i8(q[1] >> 16, c.s));
+        hi = make_uint4(dequant2_i8(q[2], c.s), dequant2_i8(q[2] >> 16, c.s), dequant2_i8(q[3], c.s),
+                        dequant2_i8(q[3] >> 16, c.s));
+    } else if (c.s16) {
         lo = make_uint4(dequant2_h(q[0], c.s16), dequant2_h(q[0] >> 16, c.s16), dequant2_h(q[1], c.s16),
                         dequant2_h(q[1] >> 16, c.s16));
         hi = make_uint4(dequant2_h(q[2], c.s16), dequant2_h(q[2] >> 16, c.s16), dequant2_h(q[3], c.s16),
@@ -329,7 +348,7 @@ __device__ __forceinline__ void store16_bf16_at(Chain& c, const uint32_t q[4], u
         ++c.row;
         if (c.i + 16 < c.n) {
             c.s = bf16_bits_to_float(c.sc[c.row]);
-            c.s16 = scale_f16(c.s);
+            c.s16 = c.i8 ? 0 : scale_f16(c.s);
         }
     }
 }
@@ -367,7 +386,8 @@ __device__ __forceinline__ void chain_setup(Chain& c, const DecBlock& B, uint32_
     c.row = (uint32_t)(sym0 / Ly.cols);
     c.col = (uint32_t)(sym0 % Ly.cols);
     c.s = BF16 ? bf16_bits_to_float(c.sc[c.row]) : 0.f;
-    c.s16 = BF16 ? scale_f16(c.s) : 0;
+    c.i8 = B.format == EQ_FMT_INT8;
+    c.s16 = (BF16 && !c.i8) ? scale_f16(c.s) : 0;
     c.fast = BF16 ? ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) : ((B.cs & 31) == 0);
 }
 
@@ -443,7 +463,7 @@ __device__ __forceinline__ void chain_finish(Chain& c, const uint8_t* payload, c
         const uint32_t sym = decode_one(c.x, c.br, T) & 0xFFu;
         c.br.refill();
         if ((c.i & 7) == 7) { stage_wait_all(); ring_issue(c.br, payload); stage_commit(); }
-        store_one<BF16>(c.out, c.i, sym, c.s);
+        store_one<BF16>(c.out, c.i, sym, c.s, c.i8);
         if (BF16 && ++c.col == c.cols) {
             c.col = 0;
             ++c.row;
@@ -646,7 +666,8 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     d.freq = blk.freq;
     d.scales = blk.scales;
     d.payload_bytes = blk.payload_bytes;
-    d.word_end = blk.payload_cap / 4;
+    if (blk.format > EQ_FMT_INT8) return EQ_ERR_ARG;
+    d.format = blk.format;
     d.cs = blk.chunk_symbols;
     d.n_layers = blk.n_layers;
     d.cta0 = cta0;

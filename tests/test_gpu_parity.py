@@ -34,7 +34,7 @@ def oracle_block_to_gpu(blk: o.OracleBlock) -> eq.Block:
     freq = torch.from_numpy(blk.freq.view(np.int16).copy())
     scales = to_bf16(np.concatenate(blk.scales))
     return eq.Block(payload.to(DEV), len(blk.payload), off.to(DEV), freq.to(DEV), scales, list(blk.layer_shapes),
-                    blk.chunk_symbols)
+                    blk.chunk_symbols, format=blk.fmt)
 
 
 RAGGED = [(37, 53), (1, 1), (64, 64), (5, 4097), (16, 4096)]
@@ -284,3 +284,72 @@ def test_dequant_all_codes_all_scale_ranges():
     blk = o.encode_codes([C], [(M, 256)], [s_bits], cs=512)
     v = eq.decode_dequant([oracle_block_to_gpu(blk)], eq.EQ_OUT_BF16)[0][0]
     assert (u16(v) == o.dequant(C, s_bits)).all()
+
+
+# ------------------------------------------------------------------ NEXT row 4: Int8 + exclusion
+I8 = eq.EQ_FMT_INT8
+
+
+def test_int8_absmax_quantize_exhaustive():
+    bits = np.arange(0x10000, dtype=np.uint32).astype(np.uint16)
+    fin = ((bits & 0x7F80) != 0x7F80)
+    W = bits[fin][: (fin.sum() // 256) * 256].reshape(256, -1)
+    for s in [0x3F80, 0x3C00, 0x4040, 0x3700, 0x4430]:
+        S = np.full(256, s, dtype=np.uint16)
+        codes, hist = eq.quantize_hist(to_bf16(W), to_bf16(S), format=I8)
+        ref = o.quantize(W, S, o.FMT_INT8)
+        assert (codes.cpu().numpy() == ref).all(), hex(s)
+        assert (hist.cpu().numpy().astype(np.uint64) == o.histogram(ref)).all()
+    for Wt in small_layers():
+        assert (u16(eq.absmax(Wt.to(DEV), format=I8)) == o.absmax_scales(Wt, o.FMT_INT8)).all()
+
+
+@pytest.mark.parametrize("lam", [0.0, 120.0])
+def test_int8_search_vs_oracle(lam):
+    W = eqsynth.weights(16, 320, seed=13)
+    sc, ob = eq.search_scales(W.to(DEV), [lam], with_obj=True, format=I8)
+    S = u16(sc[0])
+    obj = ob[0].cpu().numpy()
+    near = 0
+    for r in range(16):
+        first, f = o.row_objectives(W, r, lam, fmt=o.FMT_INT8)
+        k = int(S[r]) - first
+        if k != int(np.argmin(f)):
+            near += 1
+            assert f[k] <= f.min() * (1 + 1e-9)
+        assert obj[r] == pytest.approx(f.min(), rel=1e-6)
+    assert near <= 1
+
+
+@pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16])
+def test_int8_decode_oracle_streams(out):
+    layers = small_layers(seed=21)
+    scales = [(o.absmax_scales(W, o.FMT_INT8).astype(np.int32) + 128 * 5).astype(np.uint16) for W in layers]
+    blk = o.quantize_encode(layers, scales=scales, cs=512, fmt=o.FMT_INT8)
+    views = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0]
+    a = 0
+    for (r, c), v, S in zip(blk.layer_shapes, views, blk.scales):
+        codes = blk.codes[a:a + r * c].reshape(r, c)
+        a += r * c
+        if out == eq.EQ_OUT_FP8:
+            assert (v.view(torch.uint8).cpu().numpy() == codes).all()
+        else:
+            assert (u16(v) == o.dequant(codes, S, o.FMT_INT8)).all()
+
+
+@pytest.mark.parametrize("fmt", [eq.EQ_FMT_E4M3, eq.EQ_FMT_INT8])
+def test_quantize_encode_format_and_exclusion(fmt):
+    layers = [eqsynth.weights(r, c, seed=22, layer=1, matrix=m) for m, (r, c) in enumerate([(48, 256), (32, 512), (8, 4096)])]
+    lam = 150.0
+    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=lam, format=fmt, exclude=(2,))
+    S_gpu = u16(g.scales)
+    assert (S_gpu[80:88] == o.absmax_scales(layers[2], fmt)).all()              # excluded layer: λ = 0
+    S_or = [o.search(W, lam, fmt=fmt)[0] for W in layers[:2]] + [o.absmax_scales(layers[2], fmt)]
+    sc = to_bf16(np.concatenate(S_or))
+    g2 = eq.quantize_encode([W.to(DEV) for W in layers], scales=sc, format=fmt)
+    ref = o.quantize_encode(layers, scales=S_or, fmt=fmt)
+    assert g2.payload[:g2.payload_bytes].cpu().numpy().tobytes() == ref.payload
+    for v, r in zip(eq.decode_dequant([g2], eq.EQ_OUT_BF16)[0], o.decode_dequant(ref)):
+        assert (u16(v) == r).all()
+    if (S_gpu == np.concatenate(S_or)).all():
+        assert g.payload[:g.payload_bytes].cpu().numpy().tobytes() == ref.payload
