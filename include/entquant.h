@@ -195,6 +195,17 @@ eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks,
                                  void* arena_host, uint64_t arena_bytes, void* workspace,
                                  uint64_t workspace_bytes, eq_stream_t stream);
 
+/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4): Y = X · Ŵᵀ for layer
+ * `layer` of block `blk`, Ŵ = the block's decoded + dequantised bf16 weights (never written
+ * to memory): each row's rANS chunks are decoded straight into tcgen05 shared-memory tiles
+ * and multiplied on the 5th-gen tensor cores (bf16 × bf16 → fp32 in TMEM).
+ * x: device bf16 [batch, cols] row-major (16-byte aligned); y: device fp32 [batch, rows].
+ * Requires row-aligned chunks (cols % chunk_symbols == 0), rows % 128 == 0,
+ * chunk_symbols % 64 == 0, 1 ≤ batch ≤ 256 (else EQ_ERR_SHAPE).  Stream integrity checks as
+ * eq_decode_dequant (d_err).  Asynchronous. */
+eq_status eq_qmatmul(const eq_block* blk, uint32_t layer, const void* x, uint32_t batch, float* y,
+                     uint32_t* d_err, eq_stream_t stream);
+
 /* SYNCHRONOUS: waits for `stream`, reads the device error word and maps its first set
  * bit to a status (EQ_OK when zero). */
 eq_status eq_check(const uint32_t* d_err, eq_stream_t stream);

@@ -37,6 +37,7 @@ EXPORTS = (
     "eq_search_scratch_bytes", "eq_search_scales", "eq_quantize_hist", "eq_build_table",
     "eq_rans_encode", "eq_quantize_encode", "eq_decode_dequant", "eq_decode_host_workspace_bytes",
     "eq_decode_dequant_host", "eq_check", "eq_calibrate_scratch_bytes", "eq_calibrate_lambda",
+    "eq_qmatmul",
 )
 
 
@@ -96,6 +97,7 @@ def lib() -> ctypes.CDLL:
             "eq_check": (st, [P, P]),
             "eq_calibrate_scratch_bytes": (u64, [P, u32, u32]),
             "eq_calibrate_lambda": (st, [P, u32, P, dbl, u32, P, P, P, u64, P]),
+            "eq_qmatmul": (st, [P, u32, P, u32, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -431,3 +433,26 @@ def calibrate_lambda(layers, target_bits: float, row_stride: int = 8, chunk_symb
 
 def check(err: torch.Tensor, stream=None) -> None:
     _ck(lib().eq_check(err.data_ptr(), _stream(stream)), "eq_check")
+
+
+def qmatmul(block: Block, layer: int, x: torch.Tensor, y: torch.Tensor | None = None, err: torch.Tensor | None = None,
+            stream=None, check: bool = True) -> torch.Tensor:
+    """Alg. 2 l.3 fused with decoding (NEXT row 1): y = x · Ŵᵀ, fp32 [batch, rows], for
+    ``layer`` of ``block``; the layer's weights are decoded straight into tcgen05 tiles."""
+    if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_contiguous():
+        raise ValueError("x must be contiguous 2-D bf16")
+    _require_cuda(x)
+    rows, cols = block.shapes[layer]
+    if x.shape[1] != cols:
+        raise EqError(EQ_ERR_SHAPE, "qmatmul")
+    if y is None:
+        y = torch.empty(x.shape[0], rows, dtype=torch.float32, device=x.device)
+    own = err is None
+    if own:
+        err = torch.zeros(1, dtype=torch.int32, device=x.device)
+    b = block.c_struct()
+    _ck(lib().eq_qmatmul(ctypes.byref(b), layer, x.data_ptr(), x.shape[0], y.data_ptr(), err.data_ptr(),
+                         _stream(stream)), "eq_qmatmul")
+    if check and own:
+        _ck(lib().eq_check(err.data_ptr(), _stream(stream)), "eq_qmatmul(check)")
+    return y

@@ -1,0 +1,68 @@
+"""Config 4: one Llama-3-8B decoder block (7 linears, chunk_symbols 2048 so every K is a
+multiple) — fused decode→tcgen05 GEMM (eq_qmatmul) vs decode-then-cuBLAS, batch 1 and 64."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import eqsynth  # noqa: E402
+import paper_2601_22787_b200 as eq  # noqa: E402
+
+
+def timed(fn, reps=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    dev = torch.device("cuda")
+    Ws = eqsynth.block_weights("llama-3-8b", 0, device=dev)
+    blk = eq.quantize_encode(Ws, lam=230.2, chunk_symbols=2048)
+    dec = eq.Decoder([blk])
+    out = {"workload": "config4: Llama-3-8B decoder block (q,k,v,o,gate,up,down), chunk 2048, ~2 bits",
+           "effective_bits": blk.effective_bits()}
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    for batch in (1, 64):
+        xs = [torch.randn(batch, c, device=dev, dtype=torch.bfloat16) * 0.1 for _, c in blk.shapes]
+        ys = [torch.empty(batch, r, device=dev) for r, _ in blk.shapes]
+
+        def fused():
+            for l in range(7):
+                eq.qmatmul(blk, l, xs[l], ys[l], err=err, check=False)
+
+        def unfused():
+            dec()
+            vs = dec.views()[0]
+            for l in range(7):
+                torch.matmul(xs[l], vs[l].t())
+
+        def dense():
+            for l in range(7):
+                torch.matmul(xs[l], Ws[l].t())
+        out[f"batch{batch}"] = {"fused_ms": timed(fused), "decode_then_cublas_ms": timed(unfused),
+                                "dense_bf16_cublas_ms": timed(dense)}
+        eq.check(err)
+        # correctness vs decode + fp32 matmul
+        dec()
+        vs = dec.views()[0]
+        for l in range(7):
+            eq.qmatmul(blk, l, xs[l], ys[l])
+            ref = xs[l].float() @ vs[l].float().t()
+            rel = ((ys[l] - ref).abs().max() / ref.abs().max()).item()
+            out[f"batch{batch}"][f"maxrel_layer{l}"] = rel
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,59 @@
+"""NEXT row 1 / config 4: decode fused into a tcgen05 GEMM.  y = x · Ŵᵀ where Ŵ is the
+oracle's exact dequantised weight matrix; fp32 tensor-core accumulation differs from the
+fp64 reference only by rounding (bound: 1e-4 · Σ_k |x_k ŵ_k| per output)."""
+import numpy as np
+import pytest
+import torch
+
+import eqsynth
+import oracle as o
+import paper_2601_22787_b200 as eq
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def to_gpu_block(blk):
+    cap = (len(blk.payload) + eq.EQ_PAYLOAD_SLACK + 255) // 256 * 256
+    payload = torch.zeros(cap, dtype=torch.uint8)
+    payload[:len(blk.payload)] = torch.frombuffer(bytearray(blk.payload), dtype=torch.uint8)
+    sc = torch.from_numpy(np.concatenate(blk.scales).view(np.int16)).view(torch.bfloat16)
+    return eq.Block(payload.to(DEV), len(blk.payload), torch.from_numpy(blk.chunk_off.astype(np.int64).astype(np.int32)).to(DEV),
+                    torch.from_numpy(blk.freq.view(np.int16).copy()).to(DEV), sc.to(DEV), list(blk.layer_shapes),
+                    blk.chunk_symbols, format=blk.fmt)
+
+
+@pytest.mark.parametrize("cs,fmt", [(4096, 0), (2048, 0), (1024, 1), (256, 0)])
+@pytest.mark.parametrize("batch", [1, 8, 61])
+def test_qmatmul_matches_fp64_reference(cs, fmt, batch):
+    shapes = [(256, 4096), (128, 2048 if cs <= 2048 else 4096)]
+    Ws = [eqsynth.weights(r, c, seed=31, layer=0, matrix=m) for m, (r, c) in enumerate(shapes)]
+    S = [(o.absmax_scales(W, fmt).astype(np.int32) + 128 * 12).astype(np.uint16) for W in Ws]
+    blk = o.quantize_encode(Ws, scales=S, cs=cs, fmt=fmt)
+    g = to_gpu_block(blk)
+    What = [d.view(np.int16) for d in o.decode_dequant(blk)]
+    for layer, (r, c) in enumerate(shapes):
+        x = (torch.randn(batch, c, generator=torch.Generator().manual_seed(layer + batch)) * 0.5).to(torch.bfloat16)
+        W64 = torch.from_numpy(What[layer]).view(torch.bfloat16).double().numpy()
+        X64 = x.double().numpy()
+        ref = X64 @ W64.T
+        bound = 1e-4 * (np.abs(X64) @ np.abs(W64).T) + 1e-30
+        for rep in range(3):              # repeated launches: catches staging races
+            y = eq.qmatmul(g, layer, x.to(DEV)).cpu().double().numpy()
+            assert (np.abs(y - ref) <= bound).all(), (layer, rep, float(np.max(np.abs(y - ref) / bound)))
+
+
+def test_qmatmul_shape_errors_and_corruption():
+    Ws = [eqsynth.weights(128, 4096, seed=3)]
+    blk = o.quantize_encode(Ws, scales=[o.absmax_scales(Ws[0])], cs=4096)
+    g = to_gpu_block(blk)
+    with pytest.raises(eq.EqError):
+        eq.qmatmul(g, 0, torch.zeros(2, 4000, dtype=torch.bfloat16, device=DEV))
+    blk2 = o.quantize_encode([eqsynth.weights(128, 4096, seed=4)], lam=None, cs=3000)
+    with pytest.raises(eq.EqError) as ei:
+        eq.qmatmul(to_gpu_block(blk2), 0, torch.zeros(2, 4096, dtype=torch.bfloat16, device=DEV))
+    assert ei.value.status == eq.EQ_ERR_SHAPE
+    g.payload[100] ^= 0x77
+    with pytest.raises(eq.EqError) as ei:
+        eq.qmatmul(g, 0, torch.ones(2, 4096, dtype=torch.bfloat16, device=DEV))
+    assert ei.value.status == eq.EQ_ERR_CORRUPT
