@@ -195,16 +195,28 @@ eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks,
                                  void* arena_host, uint64_t arena_bytes, void* workspace,
                                  uint64_t workspace_bytes, eq_stream_t stream);
 
-/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4): Y = X · Ŵᵀ for layer
- * `layer` of block `blk`, Ŵ = the block's decoded + dequantised bf16 weights (never written
- * to memory): each row's rANS chunks are decoded straight into tcgen05 shared-memory tiles
- * and multiplied on the 5th-gen tensor cores (bf16 × bf16 → fp32 in TMEM).
- * x: device bf16 [batch, cols] row-major (16-byte aligned); y: device fp32 [batch, rows].
+/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4): Y_q = X_q · Ŵ_qᵀ for
+ * n_jobs layers `layers[q]` of block `blk` in ONE launch, Ŵ = the layer's decoded +
+ * dequantised bf16 weights (never written to memory): each chunk is decoded straight into
+ * tcgen05 shared-memory tiles and multiplied on the 5th-gen tensor cores (bf16 × bf16 →
+ * fp32 accumulate in TMEM); a row split over several chunks yields per-chunk partial sums
+ * that a second kernel adds in chunk order (deterministic).
+ * layers: HOST array [n_jobs] (1 ≤ n_jobs ≤ EQ_MAX_LAYERS) of layer indices;
+ * x: HOST array of n_jobs DEVICE pointers, bf16 [batch, cols_q] row-major, 16-byte aligned;
+ * y: HOST array of n_jobs DEVICE pointers, fp32 [batch, rows_q], 16-byte aligned, disjoint.
+ * workspace: device, ≥ eq_qmatmul_workspace_bytes (0 when every row is one chunk), 16-byte
+ * aligned; caller-owned, reused freely after the stream passes the call.
  * Requires row-aligned chunks (cols % chunk_symbols == 0), rows % 128 == 0,
- * chunk_symbols % 64 == 0, 1 ≤ batch ≤ 256 (else EQ_ERR_SHAPE).  Stream integrity checks as
- * eq_decode_dequant (d_err).  Asynchronous. */
+ * chunk_symbols % 64 == 0, 1 ≤ batch ≤ 256 (else EQ_ERR_SHAPE); EQ_ERR_BUFFER for a short
+ * workspace.  Stream integrity checks as eq_decode_dequant (d_err).  Asynchronous. */
+uint64_t eq_qmatmul_workspace_bytes(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers,
+                                    uint32_t batch);
+eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers,
+                           const void* const* x, float* const* y, uint32_t batch, void* workspace,
+                           uint64_t workspace_bytes, uint32_t* d_err, eq_stream_t stream);
+/* Single-layer form of eq_qmatmul_group (x, y device pointers). */
 eq_status eq_qmatmul(const eq_block* blk, uint32_t layer, const void* x, uint32_t batch, float* y,
-                     uint32_t* d_err, eq_stream_t stream);
+                     void* workspace, uint64_t workspace_bytes, uint32_t* d_err, eq_stream_t stream);
 
 /* SYNCHRONOUS: waits for `stream`, reads the device error word and maps its first set
  * bit to a status (EQ_OK when zero). */

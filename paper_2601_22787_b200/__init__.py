@@ -38,6 +38,8 @@ EXPORTS = (
     "eq_rans_encode", "eq_quantize_encode", "eq_decode_dequant", "eq_decode_host_workspace_bytes",
     "eq_decode_dequant_host", "eq_check", "eq_calibrate_scratch_bytes", "eq_calibrate_lambda",
     "eq_qmatmul",
+    "eq_qmatmul_group",
+    "eq_qmatmul_workspace_bytes",
 )
 
 
@@ -97,7 +99,9 @@ def lib() -> ctypes.CDLL:
             "eq_check": (st, [P, P]),
             "eq_calibrate_scratch_bytes": (u64, [P, u32, u32]),
             "eq_calibrate_lambda": (st, [P, u32, P, dbl, u32, P, P, P, u64, P]),
-            "eq_qmatmul": (st, [P, u32, P, u32, P, P, P]),
+            "eq_qmatmul": (st, [P, u32, P, u32, P, P, u64, P, P]),
+            "eq_qmatmul_group": (st, [P, u32, P, P, P, u32, P, u64, P, P]),
+            "eq_qmatmul_workspace_bytes": (u64, [P, u32, P, u32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -435,24 +439,43 @@ def check(err: torch.Tensor, stream=None) -> None:
     _ck(lib().eq_check(err.data_ptr(), _stream(stream)), "eq_check")
 
 
-def qmatmul(block: Block, layer: int, x: torch.Tensor, y: torch.Tensor | None = None, err: torch.Tensor | None = None,
-            stream=None, check: bool = True) -> torch.Tensor:
-    """Alg. 2 l.3 fused with decoding (NEXT row 1): y = x · Ŵᵀ, fp32 [batch, rows], for
-    ``layer`` of ``block``; the layer's weights are decoded straight into tcgen05 tiles."""
-    if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_contiguous():
-        raise ValueError("x must be contiguous 2-D bf16")
-    _require_cuda(x)
-    rows, cols = block.shapes[layer]
-    if x.shape[1] != cols:
-        raise EqError(EQ_ERR_SHAPE, "qmatmul")
-    if y is None:
-        y = torch.empty(x.shape[0], rows, dtype=torch.float32, device=x.device)
+def qmatmul_group(block: Block, layers: list[int], xs: list[torch.Tensor], ys: list[torch.Tensor] | None = None,
+                  err: torch.Tensor | None = None, stream=None, check: bool = True,
+                  workspace: torch.Tensor | None = None) -> list[torch.Tensor]:
+    """Alg. 2 l.3 fused with decoding (NEXT row 1): ys[q] = xs[q] · Ŵ_{layers[q]}ᵀ, fp32
+    [batch, rows], for several layers of ``block`` in one launch; weights are decoded
+    straight into tcgen05 tiles."""
+    if len(layers) != len(xs) or not layers:
+        raise ValueError("one x per layer")
+    batch = xs[0].shape[0]
+    for x, l in zip(xs, layers):
+        if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_contiguous() or x.shape[0] != batch:
+            raise ValueError("xs must be contiguous 2-D bf16 with a common batch")
+        _require_cuda(x)
+        if not 0 <= l < len(block.shapes) or x.shape[1] != block.shapes[l][1]:
+            raise EqError(EQ_ERR_SHAPE, "qmatmul")
+    dev = xs[0].device
+    if ys is None:
+        ys = [torch.empty(batch, block.shapes[l][0], dtype=torch.float32, device=dev) for l in layers]
     own = err is None
     if own:
-        err = torch.zeros(1, dtype=torch.int32, device=x.device)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
     b = block.c_struct()
-    _ck(lib().eq_qmatmul(ctypes.byref(b), layer, x.data_ptr(), x.shape[0], y.data_ptr(), err.data_ptr(),
-                         _stream(stream)), "eq_qmatmul")
+    n = len(layers)
+    la = (ctypes.c_uint32 * n)(*layers)
+    xa = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
+    ya = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys])
+    need = lib().eq_qmatmul_workspace_bytes(ctypes.byref(b), n, la, batch)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+    _ck(lib().eq_qmatmul_group(ctypes.byref(b), n, la, xa, ya, batch, workspace.data_ptr(), workspace.numel(),
+                               err.data_ptr(), _stream(stream)), "eq_qmatmul_group")
     if check and own:
         _ck(lib().eq_check(err.data_ptr(), _stream(stream)), "eq_qmatmul(check)")
-    return y
+    return ys
+
+
+def qmatmul(block: Block, layer: int, x: torch.Tensor, y: torch.Tensor | None = None, err: torch.Tensor | None = None,
+            stream=None, check: bool = True, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Single-layer :func:`qmatmul_group`."""
+    return qmatmul_group(block, [layer], [x], None if y is None else [y], err, stream, check, workspace)[0]

@@ -4,39 +4,57 @@
 // FP8 GEMM (W8A16) on the buffer nvCOMP decoded into; here the decoded rows go
 // straight into tcgen05 shared-memory operand tiles.
 //
-// CTA = 128 threads = 128 output channels (lane = weight row = one rANS chunk sequence, which
-// needs row-aligned chunks: K % chunk_symbols == 0).  Per 64-column K step:
-//   1. each lane decodes + dequantises the next 64 symbols of its row into the A tile
-//      (bf16, K-major, SWIZZLE_128B canonical UMMA layout: 8-row × 128 B atoms, 16-byte
-//      chunk j of row r stored at chunk j ^ (r & 7));
+// One launch covers a GROUP of GEMMs of one block (e.g. all 7 linears, or q/k/v).  Chunks
+// must be row-aligned (K % chunk_symbols == 0), so the chunks of a row are independent K
+// slices: CTA = (GEMM, 128-row tile, chunk column j), 128 threads, lane r decodes chunk j of
+// row r.  Every CTA does identical work (one chunk per lane) and a Llama-3-8B block at
+// chunk 2048 gives 832 CTAs, one wave at 5-6 CTAs/SM.  Per 64-column K step:
+//   1. each lane decodes + dequantises its next 64 symbols into registers (overlapping the
+//      tensor cores' reads of the previous step), waits on the MMA mbarrier, and stores them
+//      into the A tile (bf16, K-major, SWIZZLE_128B canonical UMMA layout: 8-row × 128 B
+//      atoms, 16-byte chunk j of row r at chunk j ^ (r & 7));
 //   2. the 128 threads stage X[:, k0:k0+64] (bf16, K-major, same layout) as the B tile;
 //   3. fence.proxy.async, barrier; one thread issues 4 × tcgen05.mma.cta_group::1.kind::f16
 //      (M=128, N=batch padded to 8, K=16 each) accumulating fp32 in TMEM, then
-//      tcgen05.commit → mbarrier of the stage.  Two stages: the decode of step t+1 overlaps
-//      the MMAs of step t.
-// Epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32w..32w+31 = rows) → fp32 Y[b][row].
+//      tcgen05.commit → mbarrier.
+// Epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32w..32w+31 = rows) → fp32 partial
+// [j][b][row] (or Y directly when a row is one chunk); k_qmm_reduce sums the partials in a
+// fixed order (deterministic split-K).
 #include "common.cuh"
 #include "decode_core.cuh"
 
 #include <algorithm>
 #include <cstring>
 
+#ifndef EQ_QMM_MIN_CTAS
+#define EQ_QMM_MIN_CTAS 3
+#endif
+
 namespace eq {
 
-constexpr int kQThreads = 128;
+constexpr int kTileRows = 128;                // MMA M = TMEM lanes
+constexpr int kTiles = 2;                     // row tiles per CTA (share the LUT and the B tile)
+constexpr int kQThreads = kTileRows * kTiles;
 constexpr int kQK = 64;                       // K columns per step (one 128-byte swizzle row)
-constexpr int kATile = kQThreads * kQK * 2;   // 16 KB per stage
+constexpr int kATile = kTileRows * kQK * 2;   // 16 KB per row tile
+
+// one GEMM of the group: layer `layer` of the block, X [n_real][K] bf16, output fp32
+struct QmmJob {
+    const uint16_t* x;
+    float* out;               // cpr == 1: Y [n_real][rows]; else partials [cpr][n_real][rows]
+    const uint16_t* scales;   // the layer's first row
+    uint32_t chunk0, rows, K, cpr, tile_begin;
+};
 
 struct QmmParams {
+    QmmJob job[EQ_MAX_LAYERS];
+    uint32_t n_jobs;
     const uint8_t* payload;
     const uint32_t* off;
     const uint16_t* freq;
-    const uint16_t* scales;   // this layer's first row
     uint64_t payload_bytes;
-    const uint16_t* x;        // bf16 [n_real][K]
-    float* y;                 // fp32 [n_real][rows]
     uint32_t* err;
-    uint32_t format, cs, chunk0, rows, K, n_pad, n_real, idesc, tmem_cols;
+    uint32_t format, cs, n_pad, n_real, idesc, tmem_cols, acc_cols;
     uint32_t k2p20, k2p12, kneg2p14, k4;
 };
 
@@ -59,41 +77,31 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-// one lane's 64 decoded + dequantised symbols -> its row of the swizzled A tile
-__device__ __forceinline__ void decode_step(Chain& c, const DecTable& T, const uint8_t* payload, uint8_t* a_tile,
-                                            uint32_t r) {
-    uint8_t* row = a_tile + (r >> 3) * 1024 + (r & 7) * 128;
+__device__ __forceinline__ uint4 dequant8(const Chain& c, uint32_t q0, uint32_t q1) {
+    if (c.i8)
+        return make_uint4(dequant2_i8(q0, c.s), dequant2_i8(q0 >> 16, c.s), dequant2_i8(q1, c.s),
+                          dequant2_i8(q1 >> 16, c.s));
+    if (c.s16)
+        return make_uint4(dequant2_h(q0, c.s16), dequant2_h(q0 >> 16, c.s16), dequant2_h(q1, c.s16),
+                          dequant2_h(q1 >> 16, c.s16));
+    return make_uint4(dequant2(q0, c.s), dequant2(q0 >> 16, c.s), dequant2(q1, c.s), dequant2(q1 >> 16, c.s));
+}
+
+// one lane's next 64 decoded + dequantised symbols, held in registers (8 × 16 bytes) so the
+// decode of step t+1 overlaps the tensor-core reads of step t's tile
+__device__ __forceinline__ void decode_step(Chain& c, const DecTable& T, const uint8_t* payload, uint4 v[8]) {
     #pragma unroll
     for (int g = 0; g < 4; ++g) {                       // 4 × 16 symbols
-        uint32_t q[4];
-        q[0] = decode4(c, T);
-        q[1] = decode4(c, T);
+        const uint32_t q0 = decode4(c, T);
+        const uint32_t q1 = decode4(c, T);
         stage_wait_all(); ring_issue(c.br, payload); stage_commit();
-        q[2] = decode4(c, T);
-        q[3] = decode4(c, T);
+        const uint32_t q2 = decode4(c, T);
+        const uint32_t q3 = decode4(c, T);
         stage_wait_all(); ring_issue(c.br, payload); stage_commit();
-        uint4 lo, hi;
-        if (c.i8) {
-            lo = make_uint4(dequant2_i8(q[0], c.s), dequant2_i8(q[0] >> 16, c.s), dequant2_i8(q[1], c.s),
-                            dequant2_i8(q[1] >> 16, c.s));
-            hi = make_uint4(dequant2_i8(q[2], c.s), dequant2_i8(q[2] >> 16, c.s), dequant2_i8(q[3], c.s),
-                            dequant2_i8(q[3] >> 16, c.s));
-        } else if (c.s16) {
-            lo = make_uint4(dequant2_h(q[0], c.s16), dequant2_h(q[0] >> 16, c.s16), dequant2_h(q[1], c.s16),
-                            dequant2_h(q[1] >> 16, c.s16));
-            hi = make_uint4(dequant2_h(q[2], c.s16), dequant2_h(q[2] >> 16, c.s16), dequant2_h(q[3], c.s16),
-                            dequant2_h(q[3] >> 16, c.s16));
-        } else {
-            lo = make_uint4(dequant2(q[0], c.s), dequant2(q[0] >> 16, c.s), dequant2(q[1], c.s),
-                            dequant2(q[1] >> 16, c.s));
-            hi = make_uint4(dequant2(q[2], c.s), dequant2(q[2] >> 16, c.s), dequant2(q[3], c.s),
-                            dequant2(q[3] >> 16, c.s));
-        }
-        const uint32_t j0 = 2 * g, j1 = 2 * g + 1;     // 16-byte chunks of this 16-symbol group
-        *reinterpret_cast<uint4*>(row + ((j0 ^ (r & 7)) << 4)) = lo;
-        *reinterpret_cast<uint4*>(row + ((j1 ^ (r & 7)) << 4)) = hi;
-        c.i += 16;
+        v[2 * g] = dequant8(c, q0, q1);
+        v[2 * g + 1] = dequant8(c, q2, q3);
     }
+    c.i += 64;
 }
 
 // start decoding chunk `chunk` (payload bytes, ring staging, first state) for this lane
@@ -112,9 +120,6 @@ __device__ __forceinline__ bool chunk_begin(Chain& c, const QmmParams& P, uint32
     c.e = e;
     c.wlimit4 = ((e >> 2) + 16) * 4u;
     c.br.ring = ring;
-    // the previous chunk's look-ahead copies target the same ring slots and copies of
-    // different groups are not ordered: drain them before staging the new chunk
-    stage_wait_all();
     const uint32_t s0 = a >> 4;
     #pragma unroll
     for (int q = 0; q < 4; ++q) stage_segment(ring, P.payload, s0 + q);
@@ -141,25 +146,40 @@ __device__ __forceinline__ void chunk_end(const Chain& c, uint32_t* err) {
     if (c.br.wi4 > c.wlimit4 || c.x != kL || consumed != 8ll * (int64_t)(c.e - c.a)) atomicOr(err, EQ_EF_CORRUPT);
 }
 
-__global__ void __launch_bounds__(kQThreads, 1) k_qmatmul(const __grid_constant__ QmmParams P) {
+// CTA = (job, pair of 128-row tiles, chunk column j): lane r of half h decodes the j-th
+// chunk of row 128·(2p+h)+r — cs columns [j·cs, (j+1)·cs) — and each half accumulates that
+// K-slice of its 128 × batch output in its own TMEM columns.  Every CTA does the same work
+// (one chunk per lane), so one grouped launch over all GEMMs of a block fills the GPU evenly.
+__global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __grid_constant__ QmmParams P) {
     extern __shared__ __align__(1024) uint8_t dsm_raw[];
     // SWIZZLE_128B atoms are addressed by absolute shared-address bits: align the carve-out
     uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
-    // layout: [A stage 0 | A stage 1 | B stage 0 | B stage 1 | LUT | rings | cum | bars | tmem]
-    uint8_t* a_tiles = dsm;                                          // 2 × 16 KB, 1024-aligned
-    uint8_t* b_tiles = dsm + 2 * kATile;                             // 2 × n_pad × 128 B
-    const uint32_t b_tile_bytes = P.n_pad * 128u;
-    uint8_t* tail = b_tiles + 2 * ((b_tile_bytes + 1023) & ~1023u);
-    uint32_t* lut = reinterpret_cast<uint32_t*>(tail);               // 16 KB
-    uint32_t* rings = lut + kM;                                      // 128 × 64 B
-    uint32_t* cum = rings + kQThreads * kRingWords;                  // 257
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cum + 260);         // 2 mbarriers (8-aligned)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+    // layout: [A tiles 2 × 16 KB | B tile | LUT 16 KB | rings | wsum | bar | tmem slot]; the
+    // symbol prefix sums used while building the LUT live in the (not yet used) A tiles
+    uint8_t* a_tiles = dsm;
+    uint8_t* b_tile = dsm + kTiles * kATile;
+    const uint32_t b_tile_bytes = (P.n_pad * 128u + 1023u) & ~1023u;
+    uint32_t* lut = reinterpret_cast<uint32_t*>(b_tile + b_tile_bytes);
+    uint32_t* rings = lut + kM;                                      // 256 × 64 B
+    uint32_t* wsum = rings + kQThreads * kRingWords;                 // 8
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wsum + 8);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1);
+    uint32_t* cum = reinterpret_cast<uint32_t*>(a_tiles);            // 257 words
 
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const uint32_t row0 = blockIdx.x * kQThreads;
+    const uint32_t h = (uint32_t)t / kTileRows, r = (uint32_t)t % kTileRows;
 
-    // ---- TMEM accumulator (warp 0), mbarriers (thread 0)
+    // ---- which GEMM, row tiles and chunk column
+    uint32_t jb = 0;
+    for (uint32_t q = 1; q < P.n_jobs; ++q)
+        if (blockIdx.x >= P.job[q].tile_begin) jb = q;
+    const QmmJob& J = P.job[jb];
+    const uint32_t local = blockIdx.x - J.tile_begin;
+    const uint32_t pair = local / J.cpr, jcol = local - pair * J.cpr;
+    const uint32_t n_tiles = J.rows / kTileRows;
+    const bool my_on = kTiles * pair + h < n_tiles;                 // this half's tile exists
+
+    // ---- TMEM accumulators (warp 0), mbarrier (thread 0)
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(P.tmem_cols));
@@ -167,29 +187,21 @@ __global__ void __launch_bounds__(kQThreads, 1) k_qmatmul(const __grid_constant_
     }
     if (t == 0) {
         mbar_init(smem_u32(&bars[0]), 1);
-        mbar_init(smem_u32(&bars[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // ---- block LUT (as in k_decode)
     {
-        __shared__ uint32_t wsum[8];
-        for (int base = 0; base < 256; base += kQThreads) {
-            uint32_t v = P.freq[base + t];
-            #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
-                if (lane >= d) v += o;
-            }
-            if (lane == 31) wsum[(base >> 5) + warp] = v;
-            cum[base + t + 1] = v;
+        uint32_t v = P.freq[t];                      // 256 threads = 256 symbols
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+            if (lane >= d) v += o;
         }
+        if (lane == 31) wsum[warp] = v;
         __syncthreads();
-        for (int base = 0; base < 256; base += kQThreads) {
-            const int idx = base + t;
-            uint32_t add = 0;
-            for (int q = 0; q < (idx >> 5); ++q) add += wsum[q];
-            cum[idx + 1] += add;
-        }
+        uint32_t add = 0;
+        for (int q = 0; q < warp; ++q) add += wsum[q];
+        cum[t + 1] = v + add;
         if (t == 0) cum[0] = 0;
     }
     __syncthreads();
@@ -217,74 +229,90 @@ __global__ void __launch_bounds__(kQThreads, 1) k_qmatmul(const __grid_constant_
     T.lut_s = smem_u32(lut);
     T.f0 = cum[1];
     T.ez = (T.f0 - 1) << 8;
+    __syncthreads();                                 // cum (in the A tiles) read by everyone
 
-    // ---- this lane's row
-    const uint32_t r = (uint32_t)t;                 // row within the tile = TMEM lane
-    const uint32_t grow = row0 + r;
-    const uint32_t cpr = P.K / P.cs;                // chunks per row
+    // ---- this lane's row and chunk
+    const uint32_t grow = (kTiles * pair + h) * kTileRows + r;
     const uint32_t ring = smem_u32(rings + t * kRingWords);
     Chain c;
-    c.sc = P.scales;
+    c.sc = J.scales;
     c.i8 = P.format == EQ_FMT_INT8;
-    c.s = bf16_bits_to_float(P.scales[grow]);
-    c.s16 = c.i8 ? 0 : scale_f16(c.s);
     c.active = false;
-    const uint32_t steps = P.K / kQK, steps_per_chunk = P.cs / kQK;
+    c.s = 0.f;
+    c.s16 = 0;
+    if (my_on) {
+        c.s = bf16_bits_to_float(J.scales[grow]);
+        c.s16 = c.i8 ? 0 : scale_f16(c.s);
+        if (table_ok) chunk_begin(c, P, J.chunk0 + grow * J.cpr + jcol, ring);
+    }
+    const uint32_t steps = P.cs / kQK;
+    const uint32_t kbase = jcol * P.cs;
+    uint8_t* a_tile = a_tiles + h * kATile;
+    uint8_t* arow = a_tile + (r >> 3) * 1024 + (r & 7) * 128;
+    const uint32_t bar = smem_u32(&bars[0]);
 
     for (uint32_t st = 0; st < steps; ++st) {
-        const uint32_t s = st & 1;
-        if (st % steps_per_chunk == 0) {
-            if (st) chunk_end(c, P.err);
-            if (table_ok) chunk_begin(c, P, P.chunk0 + grow * cpr + st / steps_per_chunk, ring);
+        uint4 v[8];
+        if (c.active) {
+            decode_step(c, T, P.payload, v);
+        } else {
+            #pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = make_uint4(0, 0, 0, 0);
         }
-        if (st >= 2) mbar_wait(smem_u32(&bars[s]), ((st - 2) >> 1) & 1);   // MMA of step st-2 done
-        uint8_t* a_tile = a_tiles + s * kATile;
-        uint8_t* b_tile = b_tiles + s * ((b_tile_bytes + 1023) & ~1023u);
-        if (c.active) decode_step(c, T, P.payload, a_tile, r);
+        if (st > 0) mbar_wait(bar, (st - 1) & 1);     // tensor cores done reading step st-1
+        #pragma unroll
+        for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(arow + ((q ^ (r & 7)) << 4)) = v[q];
         // activations X[:, k0:k0+64] -> B tile (rows = batch, zero-padded)
-        const uint32_t k0 = st * kQK;
+        const uint32_t k0 = kbase + st * kQK;
         for (uint32_t piece = t; piece < P.n_pad * 8; piece += kQThreads) {
             const uint32_t b = piece >> 3, j = piece & 7;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (b < P.n_real) v = __ldg(reinterpret_cast<const uint4*>(P.x + (uint64_t)b * P.K + k0) + j);
-            *reinterpret_cast<uint4*>(b_tile + (b >> 3) * 1024 + (b & 7) * 128 + ((j ^ (b & 7)) << 4)) = v;
+            uint4 xv = make_uint4(0, 0, 0, 0);
+            if (b < P.n_real) xv = __ldg(reinterpret_cast<const uint4*>(J.x + (uint64_t)b * J.K + k0) + j);
+            *reinterpret_cast<uint4*>(b_tile + (b >> 3) * 1024 + (b & 7) * 128 + ((j ^ (b & 7)) << 4)) = xv;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (t == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t da = umma_desc_sw128(smem_u32(a_tile)), db = umma_desc_sw128(smem_u32(b_tile));
+            const uint64_t db = umma_desc_sw128(smem_u32(b_tile));
             #pragma unroll
-            for (int kk = 0; kk < kQK / 16; ++kk) {
-                const uint32_t acc = (st > 0 || kk > 0) ? 1u : 0u;
-                // +32 bytes per K=16 slice inside the swizzle atom (start address field in 16 B units)
-                asm volatile(
-                    "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
-                        tmem),
-                    "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(P.idesc), "r"(acc));
+            for (int hh = 0; hh < kTiles; ++hh) {
+                if (kTiles * pair + hh >= n_tiles) continue;
+                const uint64_t da = umma_desc_sw128(smem_u32(a_tiles + hh * kATile));
+                #pragma unroll
+                for (int kk = 0; kk < kQK / 16; ++kk) {
+                    const uint32_t acc = (st > 0 || kk > 0) ? 1u : 0u;
+                    // +32 bytes per K=16 slice inside the swizzle atom (start address in 16 B units)
+                    asm volatile(
+                        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+                            tmem + hh * P.acc_cols),
+                        "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(P.idesc), "r"(acc));
+                }
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(&bars[s]))
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                          : "memory");
         }
     }
     chunk_end(c, P.err);
     stage_wait_all();
-    // ---- wait for the last MMA, read the accumulator
-    const uint32_t last = steps - 1;
-    mbar_wait(smem_u32(&bars[last & 1]), (last >> 1) & 1);
+    // ---- wait for the last MMAs, read the accumulators
+    mbar_wait(bar, (steps - 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float* out = J.out + (uint64_t)jcol * P.n_real * J.rows;
     for (uint32_t col = 0; col < P.n_pad; col += 8) {
         uint32_t v[8];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + col;
+        // warp w reads TMEM lanes 32·(w % 4) .. +31 (= rows r of its half) of half h's columns
+        const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + h * P.acc_cols + col;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                      : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t b = col + q;
-            if (b < P.n_real) P.y[(uint64_t)b * P.rows + grow] = __uint_as_float(v[q]);
+        if (my_on) {
+            #pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t b = col + q;
+                if (b < P.n_real) out[(uint64_t)b * J.rows + grow] = __uint_as_float(v[q]);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -292,46 +320,141 @@ __global__ void __launch_bounds__(kQThreads, 1) k_qmatmul(const __grid_constant_
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols));
 }
 
+// Y = Σ_j partial_j in a fixed order (j = 0, 1, …): deterministic split-K reduction
+struct RedJob {
+    const float* part;
+    float* y;
+    uint32_t n, cpr;          // n = batch · rows (multiple of 4)
+};
+struct RedParams {
+    RedJob job[EQ_MAX_LAYERS];
+};
+
+__global__ void __launch_bounds__(256) k_qmm_reduce(const __grid_constant__ RedParams R) {
+    const RedJob& J = R.job[blockIdx.y];
+    const uint32_t n4 = J.n >> 2;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        float4 a = __ldcs(reinterpret_cast<const float4*>(J.part) + i);
+        for (uint32_t j = 1; j < J.cpr; ++j) {
+            const float4 b = __ldcs(reinterpret_cast<const float4*>(J.part + (uint64_t)j * J.n) + i);
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+        }
+        reinterpret_cast<float4*>(J.y)[i] = a;
+    }
+}
+
+struct QmmPlan {
+    uint32_t chunk0[EQ_MAX_LAYERS];
+    uint64_t srow[EQ_MAX_LAYERS];
+};
+
+static eq_status qmm_validate(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers, uint32_t batch,
+                              QmmPlan* plan) {
+    if (!blk || !layers || n_jobs < 1 || n_jobs > EQ_MAX_LAYERS) return EQ_ERR_ARG;
+    if (!blk->payload || !blk->chunk_off || !blk->freq || !blk->scales || blk->format > EQ_FMT_INT8) return EQ_ERR_ARG;
+    if (blk->n_layers < 1 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(blk->payload) & 15) != 0) return EQ_ERR_ARG;
+    if (blk->payload_cap < blk->payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;
+    const uint32_t cs = blk->chunk_symbols;
+    if (batch < 1 || batch > 256 || cs == 0 || cs % kQK != 0) return EQ_ERR_SHAPE;
+    uint32_t chunk0 = 0;
+    uint64_t srow = 0;
+    for (uint32_t l = 0; l < blk->n_layers; ++l) {
+        plan->chunk0[l] = chunk0;
+        plan->srow[l] = srow;
+        chunk0 += (uint32_t)(((uint64_t)blk->layer_rows[l] * blk->layer_cols[l] + cs - 1) / cs);
+        srow += (uint64_t)blk->layer_rows[l];
+    }
+    for (uint32_t q = 0; q < n_jobs; ++q) {
+        const uint32_t l = layers[q];
+        if (l >= blk->n_layers) return EQ_ERR_ARG;
+        const uint64_t rows = blk->layer_rows[l], K = blk->layer_cols[l];
+        if (rows == 0 || rows % kTileRows != 0 || K == 0 || K % cs != 0) return EQ_ERR_SHAPE;
+    }
+    return EQ_OK;
+}
+
+static uint64_t qmm_part_bytes(uint64_t cpr, uint64_t batch, uint64_t rows) {
+    return cpr > 1 ? (cpr * batch * rows * 4 + EQ_ARENA_ALIGN - 1) / EQ_ARENA_ALIGN * EQ_ARENA_ALIGN : 0;
+}
+
 }  // namespace eq
 
 using namespace eq;
 
-extern "C" eq_status eq_qmatmul(const eq_block* blk, uint32_t layer, const void* x, uint32_t batch, float* y,
-                                uint32_t* d_err, eq_stream_t stream) {
-    if (!blk || !x || !y || !d_err || layer >= blk->n_layers || layer >= EQ_MAX_LAYERS) return EQ_ERR_ARG;
-    if (!blk->payload || !blk->chunk_off || !blk->freq || !blk->scales || blk->format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if ((reinterpret_cast<uintptr_t>(blk->payload) & 15) != 0) return EQ_ERR_ARG;
-    if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return EQ_ERR_ARG;
-    if (blk->payload_cap < blk->payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;
-    const int64_t rows = blk->layer_rows[layer], K = blk->layer_cols[layer];
-    const uint32_t cs = blk->chunk_symbols;
-    if (batch < 1 || batch > 256) return EQ_ERR_SHAPE;
-    if (rows % kQThreads != 0 || K % kQK != 0 || cs % kQK != 0 || K % cs != 0) return EQ_ERR_SHAPE;
-    uint32_t chunk0 = 0;
-    uint64_t srow = 0;
-    for (uint32_t l = 0; l < layer; ++l) {
-        chunk0 += (uint32_t)(((uint64_t)blk->layer_rows[l] * blk->layer_cols[l] + cs - 1) / cs);
-        srow += (uint64_t)blk->layer_rows[l];
+extern "C" uint64_t eq_qmatmul_workspace_bytes(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers,
+                                               uint32_t batch) {
+    QmmPlan plan;
+    if (qmm_validate(blk, n_jobs, layers, batch, &plan) != EQ_OK) return 0;
+    uint64_t total = 0;
+    for (uint32_t q = 0; q < n_jobs; ++q) {
+        const uint32_t l = layers[q];
+        total += qmm_part_bytes(blk->layer_cols[l] / blk->chunk_symbols, batch, blk->layer_rows[l]);
     }
+    return total;
+}
+
+extern "C" eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers,
+                                      const void* const* x, float* const* y, uint32_t batch, void* workspace,
+                                      uint64_t workspace_bytes, uint32_t* d_err, eq_stream_t stream) {
+    QmmPlan plan;
+    const eq_status vs = qmm_validate(blk, n_jobs, layers, batch, &plan);
+    if (vs != EQ_OK) return vs;
+    if (!x || !y || !d_err) return EQ_ERR_ARG;
+    const uint64_t need = eq_qmatmul_workspace_bytes(blk, n_jobs, layers, batch);
+    if (need > 0 && (!workspace || workspace_bytes < need)) return EQ_ERR_BUFFER;
+    if ((reinterpret_cast<uintptr_t>(workspace) & 15) != 0) return EQ_ERR_ARG;
     QmmParams P;
     memset(&P, 0, sizeof(P));
+    RedParams R;
+    memset(&R, 0, sizeof(R));
+    uint32_t n_red = 0;
+    uint32_t max_red = 0;
+    uint64_t ws_off = 0;
+    uint32_t tiles = 0;
+    const uint32_t cs = blk->chunk_symbols;
+    for (uint32_t q = 0; q < n_jobs; ++q) {
+        const uint32_t l = layers[q];
+        if (!x[q] || !y[q] || (reinterpret_cast<uintptr_t>(x[q]) & 15) != 0 || (reinterpret_cast<uintptr_t>(y[q]) & 15) != 0)
+            return EQ_ERR_ARG;
+        QmmJob& J = P.job[q];
+        J.x = static_cast<const uint16_t*>(x[q]);
+        J.scales = blk->scales + plan.srow[l];
+        J.chunk0 = plan.chunk0[l];
+        J.rows = blk->layer_rows[l];
+        J.K = blk->layer_cols[l];
+        J.cpr = J.K / cs;
+        J.tile_begin = tiles;
+        tiles += (J.rows / kTileRows + kTiles - 1) / kTiles * J.cpr;
+        if (J.cpr == 1) {
+            J.out = y[q];
+        } else {
+            J.out = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + ws_off);
+            ws_off += qmm_part_bytes(J.cpr, batch, J.rows);
+            R.job[n_red].part = J.out;
+            R.job[n_red].y = y[q];
+            R.job[n_red].n = batch * J.rows;
+            R.job[n_red].cpr = J.cpr;
+            max_red = std::max(max_red, R.job[n_red].n);
+            ++n_red;
+        }
+    }
+    P.n_jobs = n_jobs;
     P.payload = blk->payload;
     P.off = blk->chunk_off;
     P.freq = blk->freq;
-    P.scales = blk->scales + srow;
     P.payload_bytes = blk->payload_bytes;
-    P.x = static_cast<const uint16_t*>(x);
-    P.y = y;
     P.err = d_err;
     P.format = blk->format;
     P.cs = cs;
-    P.chunk0 = chunk0;
-    P.rows = (uint32_t)rows;
-    P.K = (uint32_t)K;
     P.n_pad = (batch + 7) & ~7u;
     P.n_real = batch;
+    P.acc_cols = P.n_pad;                      // half h accumulates in columns [h·n_pad, (h+1)·n_pad)
     P.tmem_cols = 32;
-    while (P.tmem_cols < P.n_pad) P.tmem_cols <<= 1;
+    while (P.tmem_cols < kTiles * P.n_pad) P.tmem_cols <<= 1;
     // instruction descriptor, kind::f16: D f32, A = B = bf16, both K-major, N, M = 128
     P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((P.n_pad >> 3) << 17) | ((128u >> 4) << 24);
     P.k2p20 = 1u << 20;
@@ -339,9 +462,21 @@ extern "C" eq_status eq_qmatmul(const eq_block* blk, uint32_t layer, const void*
     P.kneg2p14 = 0u - (1u << 14);
     P.k4 = 4u;
     const uint32_t b_tile = ((P.n_pad * 128u + 1023u) & ~1023u);
-    const size_t smem = 2 * kATile + 2 * b_tile + kM * 4 + kQThreads * kRingWords * 4 + 260 * 4 + 2 * 8 + 16 + 1024;
+    const size_t smem = kTiles * kATile + b_tile + kM * 4 + kQThreads * kRingWords * 4 + 32 + 8 + 8 + 1024;
     EQ_CUDA_TRY(cudaFuncSetAttribute(k_qmatmul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_qmatmul<<<(unsigned)(rows / kQThreads), kQThreads, smem, (cudaStream_t)stream>>>(P);
+    k_qmatmul<<<tiles, kQThreads, smem, (cudaStream_t)stream>>>(P);
     EQ_CUDA_TRY(cudaGetLastError());
+    if (n_red) {
+        const uint32_t gx = std::min<uint32_t>((max_red / 4 + 255) / 256, 148u * 8u);
+        k_qmm_reduce<<<dim3(gx, n_red), 256, 0, (cudaStream_t)stream>>>(R);
+        EQ_CUDA_TRY(cudaGetLastError());
+    }
     return EQ_OK;
+}
+
+extern "C" eq_status eq_qmatmul(const eq_block* blk, uint32_t layer, const void* x, uint32_t batch, float* y,
+                                void* workspace, uint64_t workspace_bytes, uint32_t* d_err, eq_stream_t stream) {
+    const void* xs[1] = {x};
+    float* ys[1] = {y};
+    return eq_qmatmul_group(blk, 1, &layer, xs, ys, batch, workspace, workspace_bytes, d_err, stream);
 }

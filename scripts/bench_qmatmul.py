@@ -37,9 +37,20 @@ def main():
         xs = [torch.randn(batch, c, device=dev, dtype=torch.bfloat16) * 0.1 for _, c in blk.shapes]
         ys = [torch.empty(batch, r, device=dev) for r, _ in blk.shapes]
 
+        ws = torch.empty(1 << 26, dtype=torch.uint8, device=dev)
+        ys_grp = [torch.empty(batch, r, device=dev) for r, _ in blk.shapes]
+
+        def fused_group():                      # all 7 GEMMs of the block in one launch
+            eq.qmatmul_group(blk, list(range(7)), xs, ys_grp, err=err, check=False, workspace=ws)
+
+        def fused_chain():                      # Llama dataflow: {q,k,v} -> o -> {gate,up} -> down
+            for ls in ([0, 1, 2], [3], [4, 5], [6]):
+                eq.qmatmul_group(blk, ls, [xs[l] for l in ls], [ys[l] for l in ls], err=err, check=False,
+                                 workspace=ws)
+
         def fused():
             for l in range(7):
-                eq.qmatmul(blk, l, xs[l], ys[l], err=err, check=False)
+                eq.qmatmul(blk, l, xs[l], ys[l], err=err, check=False, workspace=ws)
 
         def unfused():
             dec()
@@ -50,7 +61,8 @@ def main():
         def dense():
             for l in range(7):
                 torch.matmul(xs[l], Ws[l].t())
-        out[f"batch{batch}"] = {"fused_ms": timed(fused), "decode_then_cublas_ms": timed(unfused),
+        out[f"batch{batch}"] = {"fused_group_ms": timed(fused_group), "fused_chain4_ms": timed(fused_chain),
+                                "fused_per_layer_ms": timed(fused), "decode_then_cublas_ms": timed(unfused),
                                 "dense_bf16_cublas_ms": timed(dense)}
         eq.check(err)
         # correctness vs decode + fp32 matmul
@@ -58,6 +70,7 @@ def main():
         vs = dec.views()[0]
         for l in range(7):
             eq.qmatmul(blk, l, xs[l], ys[l])
+            out[f"batch{batch}"][f"group_equals_single_layer{l}"] = bool(torch.equal(ys[l], ys_grp[l]))
             ref = xs[l].float() @ vs[l].float().t()
             rel = ((ys[l] - ref).abs().max() / ref.abs().max()).item()
             out[f"batch{batch}"][f"maxrel_layer{l}"] = rel

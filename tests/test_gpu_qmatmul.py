@@ -57,3 +57,45 @@ def test_qmatmul_shape_errors_and_corruption():
     with pytest.raises(eq.EqError) as ei:
         eq.qmatmul(g, 0, torch.ones(2, 4096, dtype=torch.bfloat16, device=DEV))
     assert ei.value.status == eq.EQ_ERR_CORRUPT
+
+
+@pytest.mark.parametrize("batch", [1, 24])
+def test_qmatmul_group_one_launch_deterministic(batch):
+    """All layers of a block in one grouped launch (mixed chunk counts per row: split-K
+    partials for some, direct output for others), bitwise repeatable, each vs fp64."""
+    shapes = [(256, 1024), (128, 2048), (384, 1024), (128, 3072)]
+    Ws = [eqsynth.weights(r, c, seed=77, layer=1, matrix=m) for m, (r, c) in enumerate(shapes)]
+    blk = o.quantize_encode(Ws, lam=None, cs=1024)
+    g = to_gpu_block(blk)
+    What = o.decode_dequant(blk)
+    xs = [(torch.randn(batch, c, generator=torch.Generator().manual_seed(5 + m)) * 0.3).to(torch.bfloat16)
+          for m, (_, c) in enumerate(shapes)]
+    order = [3, 0, 2, 1]                       # any order of layers
+    ys = eq.qmatmul_group(g, order, [xs[l].to(DEV) for l in order])
+    again = eq.qmatmul_group(g, order, [xs[l].to(DEV) for l in order])
+    for l, y, y2 in zip(order, ys, again):
+        assert torch.equal(y, y2)
+        W64 = torch.from_numpy(What[l]).view(torch.bfloat16).double().numpy()
+        X64 = xs[l].double().numpy()
+        ref = X64 @ W64.T
+        bound = 1e-4 * (np.abs(X64) @ np.abs(W64).T) + 1e-30
+        assert (np.abs(y.cpu().double().numpy() - ref) <= bound).all(), l
+
+
+def test_qmatmul_workspace_contract():
+    shapes = [(128, 2048)]
+    Ws = [eqsynth.weights(128, 2048, seed=9)]
+    g = to_gpu_block(o.quantize_encode(Ws, lam=None, cs=512))
+    x = torch.ones(3, 2048, dtype=torch.bfloat16, device=DEV)
+    small = torch.empty(16, dtype=torch.uint8, device=DEV)
+    b = g.c_struct()
+    import ctypes
+    la = (ctypes.c_uint32 * 1)(0)
+    need = eq.lib().eq_qmatmul_workspace_bytes(ctypes.byref(b), 1, la, 3)
+    assert need >= 4 * 3 * 128 * 4
+    y = torch.empty(3, 128, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    xa = (ctypes.c_void_p * 1)(x.data_ptr())
+    ya = (ctypes.c_void_p * 1)(y.data_ptr())
+    st = eq.lib().eq_qmatmul_group(ctypes.byref(b), 1, la, xa, ya, 3, small.data_ptr(), 16, err.data_ptr(), None)
+    assert st == eq.EQ_ERR_BUFFER
