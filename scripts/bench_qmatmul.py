@@ -26,11 +26,16 @@ def timed(fn, reps=20, warm=3):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cs", type=int, default=2048)
+    ap.add_argument("--profile", action="store_true", help="one grouped launch per batch (for ncu)")
+    args = ap.parse_args()
     dev = torch.device("cuda")
     Ws = eqsynth.block_weights("llama-3-8b", 0, device=dev)
-    blk = eq.quantize_encode(Ws, lam=230.2, chunk_symbols=2048)
+    blk = eq.quantize_encode(Ws, lam=230.2, chunk_symbols=args.cs)
     dec = eq.Decoder([blk])
-    out = {"workload": "config4: Llama-3-8B decoder block (q,k,v,o,gate,up,down), chunk 2048, ~2 bits",
+    out = {"workload": f"config4: Llama-3-8B decoder block (q,k,v,o,gate,up,down), chunk {args.cs}, ~2 bits",
            "effective_bits": blk.effective_bits()}
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     for batch in (1, 64):
@@ -47,6 +52,11 @@ def main():
             for ls in ([0, 1, 2], [3], [4, 5], [6]):
                 eq.qmatmul_group(blk, ls, [xs[l] for l in ls], [ys[l] for l in ls], err=err, check=False,
                                  workspace=ws)
+
+        if args.profile:
+            fused_group()
+            torch.cuda.synchronize()
+            continue
 
         def fused():
             for l in range(7):

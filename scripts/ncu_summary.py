@@ -19,6 +19,9 @@ KEYS = [
     "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
     "launch__registers_per_thread", "launch__occupancy_limit_registers", "sm__cycles_elapsed.avg",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum", "launch__grid_size", "launch__occupancy_limit_shared_mem",
 ]
 STALL = "smsp__average_warp_latency_issue_stalled_"
 
@@ -31,8 +34,10 @@ def summarize(path):
     for r in rows[2:]:
         d = {"kernel": r[hdr.index("Kernel Name")]}
         for k in KEYS:
-            if k in hdr:
-                d[k] = r[hdr.index(k)] + (" " + units[hdr.index(k)] if units[hdr.index(k)] else "")
+            for i, h in enumerate(hdr):
+                if h == k or h.endswith("." + k):      # some sections prefix the metric name
+                    d[k] = r[i] + (" " + units[i] if units[i] else "")
+                    break
         stalls = {}
         for i, h in enumerate(hdr):
             if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
