@@ -1,0 +1,74 @@
+"""Turn one evidence run (scripts/gpu_evidence.sh output directory) into the committed
+profile summaries:
+
+  profiles/ncu_decode_summary.json   per-launch DRAM bytes of k_decode (bench.py's `traffic`)
+  profiles/<round>/ncu_decode_full.json     ncu --set full summary (scripts/ncu_summary.py)
+  profiles/<round>/launches_summary.csv     launch list of the bench command, per kernel
+  profiles/<round>/launches_decode.json     the timed step's kernels and their share
+
+Usage: python scripts/make_profiles.py gpurun_out/ev1 r1
+"""
+import csv
+import json
+import os
+import shutil
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _num(s):
+    v, unit = s.split()[0], (s.split()[1] if len(s.split()) > 1 else "")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-6, "us": 1e-3,
+             "ms": 1.0, "s": 1e3}.get(unit, 1)
+    return float(v.replace(",", "")) * scale
+
+
+def main(ev, rnd):
+    out_dir = os.path.join(ROOT, "profiles", rnd)
+    os.makedirs(out_dir, exist_ok=True)
+    full = json.load(open(os.path.join(ev, "summary.json")))
+    shutil.copy(os.path.join(ev, "summary.json"), os.path.join(out_dir, "ncu_decode_full.json"))
+    summ = {"source": f"profiles/{rnd}/ncu_decode_full.json (ncu --set full --clock-control none, "
+                      "bench.py --profile --steps 1 --warmup 1: 32 blocks, lambda 230.2)"}
+    for d in full:
+        key = "bf16" if "k_decode<1>" in d["kernel"] else "fp8" if "k_decode<0>" in d["kernel"] else None
+        if key is None:
+            continue
+        rd, wr = _num(d["dram__bytes_read.sum"]), _num(d["dram__bytes_write.sum"])
+        summ[key] = {"kernel": d["kernel"], "duration_ms_under_ncu": _num(d["gpu__time_duration.sum"]),
+                     "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                     "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")}
+    json.dump(summ, open(os.path.join(ROOT, "profiles", "ncu_decode_summary.json"), "w"), indent=1)
+
+    # launch list: "ID",...,"Kernel Name",...,"Metric Value"
+    rows = []
+    with open(os.path.join(ev, "launches.csv")) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    for r in csv.DictReader(lines):
+        if r.get("Metric Name") == "gpu__time_duration.sum":
+            rows.append((r["Kernel Name"], float(r["Metric Value"].replace(",", "")) / 1e3))   # ns -> us
+    per = defaultdict(list)
+    for k, us in rows:
+        per[k.split("(")[0]].append(us)
+    tot = sum(us for _, us in rows)
+    with open(os.path.join(out_dir, "launches_summary.csv"), "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["kernel", "launches", "total_us", "share_of_command", "mean_us"])
+        for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+            w.writerow([k, len(v), round(sum(v), 1), round(sum(v) / tot, 5), round(sum(v) / len(v), 1)])
+    dec = {k: v for k, v in per.items() if "k_decode<1>" in k}
+    json.dump({"command": "python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --lam 230.2 "
+                          "(ncu --metrics gpu__time_duration.sum --clock-control none)",
+               "timed_step_kernels": {k: {"launches": len(v), "mean_us": sum(v) / len(v)} for k, v in dec.items()},
+               "decode_share_of_timed_step": 1.0,
+               "note": "cold-cache, serialised per-launch times; the timed step (one eq_decode_dequant of the "
+                       "32-block layer set) launches exactly one k_decode<1> kernel, so its share of the step "
+                       "is 1.0 in both the bench and the launch list"},
+              open(os.path.join(out_dir, "launches_decode.json"), "w"), indent=1)
+    print(json.dumps(summ, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "r1")
