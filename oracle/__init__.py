@@ -74,6 +74,7 @@ def lib():
             "eqo_quantize_fmt": (None, [ctypes.c_int, P, i64, i64, P, P]),
             "eqo_dequant_fmt": (None, [ctypes.c_int, P, i64, i64, P, P]),
             "eqo_row_terms_fmt": (None, [ctypes.c_int, P, i64, u16, P, P]),
+            "eqo_rd_row_fmt": (None, [ctypes.c_int, P, i64, u16, P]),
             "eqo_objective_fmt": (dbl, [ctypes.c_int, P, i64, i64, P, dbl]),
             "eqo_search_rows_fmt": (None, [ctypes.c_int, P, i64, i64, dbl, i32, i32, i64, i64, P, P]),
             "eqo_row_objectives_fmt": (i64, [ctypes.c_int, P, i64, i64, i64, dbl, i32, i32, P, P, i64]),
@@ -177,6 +178,14 @@ def row_terms(w_row, s_bf16: int, fmt: int = FMT_E4M3):
     D, R = ctypes.c_double(), ctypes.c_double()
     lib().eqo_row_terms_fmt(fmt, _p(w_row), w_row.size, s_bf16, ctypes.byref(D), ctypes.byref(R))
     return D.value, R.value
+
+
+def rd_row(w_row, s_bf16: int, fmt: int = FMT_E4M3) -> np.ndarray:
+    """Row sums {D, R, A, B, Q} of Eq. 4 and its straight-through derivative (eqo_rd_row_fmt)."""
+    w_row = _u16(w_row)
+    out = np.zeros(5, dtype=np.float64)
+    lib().eqo_rd_row_fmt(fmt, _p(w_row), w_row.size, int(s_bf16), _p(out))
+    return out
 
 
 def l1(W) -> float:

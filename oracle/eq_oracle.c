@@ -248,6 +248,46 @@ void eqo_row_terms(const uint16_t* w_row, int64_t n, uint16_t s_bf16, double* D,
     eqo_row_terms_fmt(0, w_row, n, s_bf16, D, R);
 }
 
+/* ------------------------------------------------------------------------------------
+ * Straight-through gradient of Eq. (4) w.r.t. a row's scale ("We use the
+ * straight-through estimator for Q_γ"; SPEC ste_gradient S:231-239; reading R13).
+ * Forward values are the true discrete ones (v = value(Q_γ(w/s))); for the derivative
+ * Q_γ's rounding is the identity inside the clamp range |w/s| ≤ Q_max (inclusive, as
+ * torch.clamp's backward) and its clamp has derivative 0 outside, so with q = w/s
+ *   ∂(s·v)/∂s = v + s·∂v/∂s = v − q   (inside),   v   (clamped),
+ *   ∂|w − s·v|/∂s = sign(s·v − w)·∂(s·v)/∂s,     ∂|v|/∂s = sign(v)·(−q/s)  (inside).
+ * Inside the clamp sign(s·v − w) = sign(v − q) (s > 0), so that term is |v − q|; for v ≠ 0
+ * sign(v) = sign(q), so the regulariser term is −|q|/s (torch: d|x|/dx = 0 at x = 0).
+ * Returns the row sums  out = {D, R, A, B, Q}:
+ *   D = Σ|w − s·v|,  R = Σ|v|,  A = Σ_inside |v − q|,  B = Σ_clamped sign(s·v − w)·v,
+ *   Q = Σ_{inside, v≠0} |q|;
+ * then ∂f_i/∂s = (A + B)/‖W‖₁ − λ·Q/(s·M·N).  All terms are exact or correctly rounded
+ * f64 operations on exact inputs; sums are sequential in j. */
+void eqo_rd_row_fmt(int fmt, const uint16_t* w_row, int64_t n, uint16_t s_bf16, double out[5])
+{
+    double s = eqo_bf16_to_double(s_bf16), qmax = eqo_qmax(fmt);
+    double D = 0.0, R = 0.0, A = 0.0, B = 0.0, Q = 0.0;
+    for (int64_t j = 0; j < n; j++) {
+        double w = eqo_bf16_to_double(w_row[j]);
+        double q = w / s;
+        double v = eqo_grid_value(fmt, eqo_grid_quantize(fmt, q));
+        double e = s * v - w;
+        D += fabs(e);
+        R += fabs(v);
+        if (fabs(q) <= qmax) {
+            A += fabs(v - q);
+            if (v != 0.0) Q += fabs(q);
+        } else {
+            B += (e > 0.0 ? 1.0 : e < 0.0 ? -1.0 : 0.0) * v;
+        }
+    }
+    out[0] = D;
+    out[1] = R;
+    out[2] = A;
+    out[3] = B;
+    out[4] = Q;
+}
+
 double eqo_l1(const uint16_t* W, int64_t n)
 {
     double a = 0.0;
