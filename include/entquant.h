@@ -218,6 +218,43 @@ eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, const uint32_t*
 eq_status eq_qmatmul(const eq_block* blk, uint32_t layer, const void* x, uint32_t batch, float* y,
                      void* workspace, uint64_t workspace_bytes, uint32_t* d_err, eq_stream_t stream);
 
+/* §8(f) NEXT row 3 — the paper's solver for Eq. 4: per layer, L-BFGS over
+ * the per-channel scales with straight-through gradients through Q_γ, from AbsMax.
+ * Reading R13: variables u = log2 s, evaluated scales RNE_bf16(2^u), Armijo
+ * backtracking on the true discrete objective (R4), two-loop recursion.
+ * lr ≤ 0 selects the paper's rule (0.25 for λ > 30, else 1.0); a steepest-descent step moves
+ * the largest log2-scale by lr, a quasi-Newton step starts at lr. */
+typedef struct {
+    uint32_t max_iters;       /* accepted steps per layer (default 100)                    */
+    uint32_t history;         /* curvature pairs kept, 1..32 (default 10)                  */
+    uint32_t trials;          /* backtracking step lengths evaluated per pass, 1..8 (4)    */
+    uint32_t max_backtracks;  /* Armijo trials per iteration before failing (32)          */
+    double lr;                /* initial step length; ≤ 0: P:507 rule                     */
+    double c1;                /* Armijo constant (1e-4)                                    */
+    double grad_tol;          /* stop when max |∂F/∂u| ≤ grad_tol (1e-7)                   */
+    double change_tol;        /* stop when |ΔF| or max |Δu| < change_tol (1e-9)            */
+} eq_lbfgs_params;
+
+void eq_lbfgs_default_params(eq_lbfgs_params* p);
+uint64_t eq_lbfgs_scratch_bytes(const eq_tensor* layers, uint32_t n_layers, const eq_lbfgs_params* p);
+/* Optimise the scales of n_layers (≤ EQ_MAX_LAYERS) layers, each independently with its own
+ * ‖W‖₁ and M·N (Eq. 4 per layer, "optimize each layer separately").  params may be
+ * NULL (defaults).  Outputs (device, caller-owned): scales bf16 bits [Σ rows] in layer
+ * order; trace (nullable) f64 [n_layers][max_iters+1] = objective after each accepted step
+ * (entry 0 = AbsMax objective; unused entries NaN); info (nullable) u32 [n_layers][4] =
+ * {accepted steps, converged, evaluation passes, done}.  Deterministic.  SYNCHRONOUS (polls
+ * completion).  EQ_ERR_BUFFER if scratch_bytes < eq_lbfgs_scratch_bytes. */
+eq_status eq_lbfgs_scales(const eq_tensor* layers, uint32_t n_layers, uint32_t format, double lambda,
+                          const eq_lbfgs_params* params, uint16_t* scales, double* trace,
+                          uint32_t* info, void* scratch, uint64_t scratch_bytes, eq_stream_t stream);
+/* Eq. 4 of one layer at given bf16 scales (device [rows]) and its straight-through gradient
+ * w.r.t. u = log2 s (SPEC ste_gradient): f_out (device, 1 double) = objective,
+ * g_out (device, rows doubles).  Scratch as eq_lbfgs_scratch_bytes(layer, 1, NULL).
+ * Asynchronous. */
+eq_status eq_rd_eval(const eq_tensor* layer, uint32_t format, double lambda, const uint16_t* scales,
+                     double* f_out, double* g_out, void* scratch, uint64_t scratch_bytes,
+                     eq_stream_t stream);
+
 /* SYNCHRONOUS: waits for `stream`, reads the device error word and maps its first set
  * bit to a status (EQ_OK when zero). */
 eq_status eq_check(const uint32_t* d_err, eq_stream_t stream);

@@ -40,6 +40,10 @@ EXPORTS = (
     "eq_qmatmul",
     "eq_qmatmul_group",
     "eq_qmatmul_workspace_bytes",
+    "eq_lbfgs_default_params",
+    "eq_lbfgs_scratch_bytes",
+    "eq_lbfgs_scales",
+    "eq_rd_eval",
 )
 
 
@@ -58,6 +62,12 @@ class eq_params(ctypes.Structure):
                 ("prob_bits", ctypes.c_uint32), ("scale_mode", ctypes.c_uint32),
                 ("lambda_", ctypes.c_double), ("oct_lo", ctypes.c_int32), ("oct_hi", ctypes.c_int32),
                 ("exclude_mask", ctypes.c_uint32)]
+
+
+class eq_lbfgs_params(ctypes.Structure):
+    _fields_ = [("max_iters", ctypes.c_uint32), ("history", ctypes.c_uint32), ("trials", ctypes.c_uint32),
+                ("max_backtracks", ctypes.c_uint32), ("lr", ctypes.c_double), ("c1", ctypes.c_double),
+                ("grad_tol", ctypes.c_double), ("change_tol", ctypes.c_double)]
 
 
 class eq_block(ctypes.Structure):
@@ -102,6 +112,10 @@ def lib() -> ctypes.CDLL:
             "eq_qmatmul": (st, [P, u32, P, u32, P, P, u64, P, P]),
             "eq_qmatmul_group": (st, [P, u32, P, P, P, u32, P, u64, P, P]),
             "eq_qmatmul_workspace_bytes": (u64, [P, u32, P, u32]),
+            "eq_lbfgs_default_params": (None, [P]),
+            "eq_lbfgs_scratch_bytes": (u64, [P, u32, P]),
+            "eq_lbfgs_scales": (st, [P, u32, u32, dbl, P, P, P, P, P, u64, P]),
+            "eq_rd_eval": (st, [P, u32, dbl, P, P, P, P, u64, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -433,6 +447,50 @@ def calibrate_lambda(layers, target_bits: float, row_stride: int = 8, chunk_symb
     _ck(lib().eq_calibrate_lambda(ts, len(layers), ctypes.byref(p), float(target_bits), row_stride, ctypes.byref(lam),
                                   ctypes.byref(est), scratch.data_ptr(), sb, _stream(stream)), "eq_calibrate_lambda")
     return lam.value, est.value
+
+
+def lbfgs_params(**kw) -> eq_lbfgs_params:
+    """eq_lbfgs_params with the library defaults, overridden by keyword."""
+    p = eq_lbfgs_params()
+    lib().eq_lbfgs_default_params(ctypes.byref(p))
+    for k, v in kw.items():
+        if v is not None:
+            setattr(p, k, v)
+    return p
+
+
+def lbfgs_scales(layers, lam: float, format: int = EQ_FMT_E4M3, stream=None, **params):
+    """Alg. 1 l.2 by the paper's solver: L-BFGS + STE on each layer's scales.
+    Returns (scales bf16 [Σ rows], trace f64 [n_layers, max_iters+1], info int [n_layers, 4])."""
+    dev = layers[0].device
+    ts = (eq_tensor * len(layers))(*[_tensor(W) for W in layers])
+    p = lbfgs_params(**params)
+    sb = lib().eq_lbfgs_scratch_bytes(ts, len(layers), ctypes.byref(p))
+    if sb == 0:
+        raise EqError(EQ_ERR_ARG, "eq_lbfgs_scratch_bytes")
+    scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+    R = sum(int(W.shape[0]) for W in layers)
+    scales = torch.empty(R, dtype=torch.bfloat16, device=dev)
+    trace = torch.empty(len(layers), p.max_iters + 1, dtype=torch.float64, device=dev)
+    info = torch.zeros(len(layers), 4, dtype=torch.int32, device=dev)
+    _ck(lib().eq_lbfgs_scales(ts, len(layers), format, float(lam), ctypes.byref(p), scales.data_ptr(),
+                              trace.data_ptr(), info.data_ptr(), scratch.data_ptr(), sb, _stream(stream)),
+        "eq_lbfgs_scales")
+    return scales, trace, info
+
+
+def rd_eval(W: torch.Tensor, scales: torch.Tensor, lam: float, format: int = EQ_FMT_E4M3, stream=None):
+    """Eq. 4 at given bf16 scales and its straight-through gradient w.r.t. log2 s:
+    (objective f64 [1], gradient f64 [rows])."""
+    _require_cuda(W, scales)
+    t = _tensor(W)
+    sb = lib().eq_lbfgs_scratch_bytes(ctypes.byref(t), 1, None)
+    scratch = torch.empty(sb, dtype=torch.uint8, device=W.device)
+    f = torch.empty(1, dtype=torch.float64, device=W.device)
+    g = torch.empty(W.shape[0], dtype=torch.float64, device=W.device)
+    _ck(lib().eq_rd_eval(ctypes.byref(t), format, float(lam), scales.contiguous().data_ptr(), f.data_ptr(),
+                         g.data_ptr(), scratch.data_ptr(), sb, _stream(stream)), "eq_rd_eval")
+    return f, g
 
 
 def check(err: torch.Tensor, stream=None) -> None:

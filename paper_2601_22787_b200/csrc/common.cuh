@@ -57,4 +57,24 @@ __device__ __forceinline__ float2 e4m3x2_to_float2(uint32_t pair) {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
+// Int8: clamp to ±127, round half to even (the f32 quotient of bf16 values
+// is ≥ 2^-9 relative away from any half-integer unless exactly on it, so fl32 suffices)
+__device__ __forceinline__ uint32_t int8x2_from_float2(float a, float b) {
+    const int ia = __float2int_rn(fminf(fmaxf(a, -127.f), 127.f));
+    const int ib = __float2int_rn(fminf(fmaxf(b, -127.f), 127.f));
+    return ((uint32_t)ia & 0xFFu) | (((uint32_t)ib & 0xFFu) << 8);
+}
+__device__ __forceinline__ float2 int8x2_to_float2(uint32_t pair) {
+    return make_float2((float)(int8_t)(pair & 0xFFu), (float)(int8_t)((pair >> 8) & 0xFFu));
+}
+template <uint32_t FMT>
+__device__ __forceinline__ uint32_t codes2(float a, float b) {
+    return FMT == EQ_FMT_INT8 ? int8x2_from_float2(a, b) : e4m3x2_from_float2(a, b);
+}
+template <uint32_t FMT>
+__device__ __forceinline__ float2 values2(uint32_t pair) {
+    return FMT == EQ_FMT_INT8 ? int8x2_to_float2(pair) : e4m3x2_to_float2(pair);
+}
+
+
 }  // namespace eq

@@ -4,6 +4,7 @@
 //   a3 FP8-E4M3 quantisation (clamp before RNE, −0 → +0 per P:509)
 //   a4 256-bin symbol histogram (metadata ℳ) fused into a3
 #include "common.cuh"
+#include "internal.h"
 
 #include <algorithm>
 #include <cmath>
@@ -22,25 +23,6 @@ constexpr int kMaxLambda = 32;
 // exact RNE.  All-zero row -> 1.0.
 __device__ __forceinline__ uint16_t absmax_from_max(float m, float qmax) {
     return m == 0.f ? (uint16_t)0x3F80u : float_to_bf16_bits(__fdiv_rn(m, qmax));
-}
-
-// Int8: clamp to ±127, round half to even (the f32 quotient of bf16 values
-// is ≥ 2^-9 relative away from any half-integer unless exactly on it, so fl32 suffices)
-__device__ __forceinline__ uint32_t int8x2_from_float2(float a, float b) {
-    const int ia = __float2int_rn(fminf(fmaxf(a, -127.f), 127.f));
-    const int ib = __float2int_rn(fminf(fmaxf(b, -127.f), 127.f));
-    return ((uint32_t)ia & 0xFFu) | (((uint32_t)ib & 0xFFu) << 8);
-}
-__device__ __forceinline__ float2 int8x2_to_float2(uint32_t pair) {
-    return make_float2((float)(int8_t)(pair & 0xFFu), (float)(int8_t)((pair >> 8) & 0xFFu));
-}
-template <uint32_t FMT>
-__device__ __forceinline__ uint32_t codes2(float a, float b) {
-    return FMT == EQ_FMT_INT8 ? int8x2_from_float2(a, b) : e4m3x2_from_float2(a, b);
-}
-template <uint32_t FMT>
-__device__ __forceinline__ float2 values2(uint32_t pair) {
-    return FMT == EQ_FMT_INT8 ? int8x2_to_float2(pair) : e4m3x2_to_float2(pair);
 }
 
 __global__ void __launch_bounds__(kRedThreads)
@@ -280,6 +262,18 @@ extern "C" eq_status eq_absmax(const eq_tensor* w, uint32_t format, uint16_t* s0
 }
 
 static int l1_ctas(int64_t n) { return (int)std::min<int64_t>(1184, (n + 4095) / 4096); }
+
+namespace eq {
+uint64_t l1_scratch_bytes(int64_t n) { return 8ull * (uint64_t)l1_ctas(n); }
+eq_status l1_device(const uint16_t* W, int64_t n, double* out, void* part, cudaStream_t st) {
+    const int nct = l1_ctas(n);
+    const int64_t per = (n + nct - 1) / nct;
+    k_l1_partial<<<nct, kRedThreads, 0, st>>>(W, n, per, (double*)part);
+    k_l1_final<<<1, 32, 0, st>>>((const double*)part, nct, out);
+    EQ_CUDA_TRY(cudaGetLastError());
+    return EQ_OK;
+}
+}  // namespace eq
 
 extern "C" uint64_t eq_search_scratch_bytes(const eq_tensor* w) {
     if (!w) return 0;
