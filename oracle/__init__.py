@@ -29,6 +29,7 @@ _SO = os.path.join(_HERE, "liboracle.so")
 PROB_BITS = 12
 CHUNK_SYMBOLS = 4096
 FMT_E4M3, FMT_INT8 = 0, 1
+CODEC_BYTE, CODEC_WORD = 0, 1      # rANS renormalisation: bytes (R9) / 16-bit words (R14)
 
 
 def build(force: bool = False) -> str:
@@ -88,6 +89,13 @@ def lib():
             "eqo_decode_block": (ctypes.c_int, [P, P, P, i32, i64, P, P]),
             "eqo_decode_chunks_mt": (ctypes.c_int, [P, P, P, P, i64, P, P, ctypes.c_int]),
             "eqo_decode_dequant_layer_mt": (ctypes.c_int, [P, P, i64, i64, i64, i64, P, P, P, ctypes.c_int]),
+            "eqo_encode_chunk_codec": (i64, [ctypes.c_int, P, i64, P, P, i64]),
+            "eqo_decode_chunk_codec": (ctypes.c_int, [ctypes.c_int, P, i64, P, P, i64]),
+            "eqo_encode_block_codec": (i64, [ctypes.c_int, P, P, i32, i64, P, P, i64, P]),
+            "eqo_decode_block_codec": (ctypes.c_int, [ctypes.c_int, P, P, P, i32, i64, P, P]),
+            "eqo_decode_chunks_mt_codec": (ctypes.c_int, [ctypes.c_int, P, P, P, P, i64, P, P, ctypes.c_int]),
+            "eqo_decode_dequant_layer_mt_codec": (ctypes.c_int, [ctypes.c_int, P, P, i64, i64, i64, i64, P, P, P,
+                                                                 ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -252,12 +260,12 @@ def entropy(hist: np.ndarray) -> float:
     return lib().eqo_entropy(_p(hist))
 
 
-def encode_chunk(sym: np.ndarray, freq: np.ndarray) -> bytes:
+def encode_chunk(sym: np.ndarray, freq: np.ndarray, codec: int = CODEC_BYTE) -> bytes:
     sym = np.ascontiguousarray(sym, dtype=np.uint8).reshape(-1)
     freq = np.ascontiguousarray(freq, dtype=np.uint16)
     cap = 4 + 2 * sym.size + 8
     out = np.zeros(cap, dtype=np.uint8)
-    n = lib().eqo_encode_chunk(_p(sym), sym.size, _p(freq), _p(out), cap)
+    n = lib().eqo_encode_chunk_codec(codec, _p(sym), sym.size, _p(freq), _p(out), cap)
     if n == -2:
         raise ValueError("unknown-symbol")
     if n < 0:
@@ -265,11 +273,11 @@ def encode_chunk(sym: np.ndarray, freq: np.ndarray) -> bytes:
     return out[:n].tobytes()
 
 
-def decode_chunk(data: bytes, freq: np.ndarray, n: int) -> np.ndarray:
+def decode_chunk(data: bytes, freq: np.ndarray, n: int, codec: int = CODEC_BYTE) -> np.ndarray:
     buf = np.frombuffer(data, dtype=np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
     freq = np.ascontiguousarray(freq, dtype=np.uint16)
     out = np.zeros(max(n, 1), dtype=np.uint8)
-    st = lib().eqo_decode_chunk(_p(buf), len(data), _p(freq), _p(out), n)
+    st = lib().eqo_decode_chunk_codec(codec, _p(buf), len(data), _p(freq), _p(out), n)
     if st == 1:
         raise ValueError("corrupt")
     if st == 2:
@@ -289,6 +297,7 @@ class OracleBlock:
     chunk_symbols: int = CHUNK_SYMBOLS
     codes: np.ndarray = field(default=None, repr=False)   # concatenated symbol stream
     fmt: int = FMT_E4M3
+    codec: int = CODEC_BYTE
 
     @property
     def n_params(self) -> int:
@@ -305,7 +314,8 @@ class OracleBlock:
         return 8.0 * b / self.n_params
 
 
-def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3) -> OracleBlock:
+def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3,
+                 codec: int = CODEC_BYTE) -> OracleBlock:
     """Alg. 1 l.4-5 + App. A.1: concatenate vec(W_q) of the block's layers, one table,
     chunked rANS."""
     stream = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1) for c in codes_list])
@@ -316,15 +326,16 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt:
     cap = 4 * n_chunks + 2 * stream.size + 64
     payload = np.zeros(cap, dtype=np.uint8)
     off = np.zeros(n_chunks + 1, dtype=np.uint32)
-    n = lib().eqo_encode_block(_p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(payload), cap, _p(off))
+    n = lib().eqo_encode_block_codec(codec, _p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(payload),
+                                     cap, _p(off))
     if n < 0:
         raise ValueError("encode failed %d" % n)
     return OracleBlock(list(layer_shapes), [np.asarray(s, dtype=np.uint16) for s in scales], freq, hist,
-                       payload[:n].tobytes(), off, cs, stream, fmt)
+                       payload[:n].tobytes(), off, cs, stream, fmt, codec)
 
 
 def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int = -1, oct_hi: int = 20,
-                    cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3, exclude=()) -> OracleBlock:
+                    cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3, exclude=(), codec: int = CODEC_BYTE) -> OracleBlock:
     """Alg. 1 for one block.  ``layers``: list of bf16 [M,N] arrays (uint16 bits or torch).
     Either ``scales`` (per layer) is given, or ``lam`` selects the exhaustive search
     (lam=None -> AbsMax scales, i.e. the λ=0 lossless-FP8 baseline of P:257).  Layers whose
@@ -339,7 +350,7 @@ def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int =
             else:
                 scales.append(search(W, lam, oct_lo, oct_hi, fmt=fmt)[0])
     codes = [quantize(W, S, fmt) for W, S in zip(Ws, scales)]
-    return encode_codes(codes, shapes, scales, cs, fmt)
+    return encode_codes(codes, shapes, scales, cs, fmt, codec)
 
 
 def decode_block(blk: OracleBlock) -> np.ndarray:
@@ -348,8 +359,8 @@ def decode_block(blk: OracleBlock) -> np.ndarray:
     out = np.zeros(int(sizes.sum()), dtype=np.uint8)
     payload = np.frombuffer(blk.payload, dtype=np.uint8).copy()
     off = np.ascontiguousarray(blk.chunk_off, dtype=np.uint32)
-    st = lib().eqo_decode_block(_p(payload), _p(off), _p(sizes), len(blk.layer_shapes), blk.chunk_symbols,
-                                _p(blk.freq), _p(out))
+    st = lib().eqo_decode_block_codec(blk.codec, _p(payload), _p(off), _p(sizes), len(blk.layer_shapes),
+                                      blk.chunk_symbols, _p(blk.freq), _p(out))
     if st:
         raise ValueError({1: "corrupt", 2: "truncated"}[st])
     return out
@@ -378,21 +389,21 @@ def chunk_table(layer_shapes, cs: int = CHUNK_SYMBOLS):
 
 
 def decode_chunks_mt(payload: np.ndarray, chunk_off: np.ndarray, sym0: np.ndarray, ns: np.ndarray,
-                     freq: np.ndarray, out: np.ndarray, threads: int) -> None:
+                     freq: np.ndarray, out: np.ndarray, threads: int, codec: int = CODEC_BYTE) -> None:
     """Multi-threaded oracle decode of selected chunks (CPU baseline timing only)."""
-    st = lib().eqo_decode_chunks_mt(_p(payload), _p(chunk_off), _p(sym0), _p(ns), ns.size,
+    st = lib().eqo_decode_chunks_mt_codec(codec, _p(payload), _p(chunk_off), _p(sym0), _p(ns), ns.size,
                                     _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(out), threads)
     if st:
         raise ValueError({1: "corrupt", 2: "truncated"}[st])
 
 
 def decode_dequant_layer_mt(payload: np.ndarray, chunk_off: np.ndarray, cs: int, rows: int, cols: int,
-                            scales: np.ndarray, freq: np.ndarray, threads: int) -> np.ndarray:
+                            scales: np.ndarray, freq: np.ndarray, threads: int, codec: int = CODEC_BYTE) -> np.ndarray:
     """Alg. 2 l.1-2 for one layer's chunks on ``threads`` host threads (CPU baseline)."""
     payload = np.ascontiguousarray(payload, dtype=np.uint8)
     off = np.ascontiguousarray(chunk_off, dtype=np.uint32)
     out = np.zeros(rows * cols, dtype=np.uint16)
-    st = lib().eqo_decode_dequant_layer_mt(_p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
+    st = lib().eqo_decode_dequant_layer_mt_codec(codec, _p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
                                            _p(np.ascontiguousarray(scales, dtype=np.uint16)),
                                            _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(out), threads)
     if st:

@@ -26,7 +26,6 @@
 #include <string.h>
 #include <pthread.h>
 
-#define EQO_L        (1u << 23)   /* rANS lower bound L = 2^23 */
 #define EQO_PROB_BITS 12          /* M = 2^12                                 */
 #define EQO_M        (1u << EQO_PROB_BITS)
 
@@ -465,37 +464,62 @@ double eqo_entropy(const uint64_t hist[256])
 }
 
 /* ------------------------------------------------------------------------------------
- * ANS (§2.1; Alg. 1 l.5 P:213; Alg. 2 l.1 P:229): byte-wise rANS, 32-bit state,
- * L = 2^23, M = 2^12, cumulative frequencies in code order.
- * Encoder: reverse symbol order from x = L; before coding s, emit low bytes while
- * x ≥ ((L>>12)<<8)·f_s; then x = ⌊x/f_s⌋·M + (x mod f_s) + c_s; finally the 4-byte state,
- * little-endian, precedes the renormalisation bytes in decode order.
+ * ANS (§2.1; Alg. 1 l.5 P:213; Alg. 2 l.1 P:229): rANS with a 32-bit state,
+ * M = 2^12, cumulative frequencies in code order.  Two
+ * renormalisation widths (the paper's coder, nvCOMP, does not document its own):
+ *
+ *   codec 0 (EQO_CODEC_BYTE, reading R9): L = 2^23, b = 2^8 — bytes;
+ *   codec 1 (EQO_CODEC_WORD, reading R14):           L = 2^16, b = 2^16 — 16-bit words,
+ *           each stored little-endian (low byte first).
+ *
+ * Encoder: reverse symbol order from x = L; before coding s, emit the low log2(b) bits
+ * while x ≥ ((L>>12)·b)·f_s and shift them out; then x = ⌊x/f_s⌋·M + (x mod f_s) + c_s;
+ * finally the 4-byte state, little-endian, precedes the renormalisation units in decode
+ * order.  Decoder: x = LE32; per symbol slot = x mod M, s with c_s ≤ slot < c_s + f_s,
+ * x = f_s·⌊x/M⌋ + slot − c_s, then while x < L: x = x·b + next unit.
  * ---------------------------------------------------------------------------------- */
+#define EQO_CODEC_BYTE 0
+#define EQO_CODEC_WORD 1
+
 static void eqo_cum(const uint16_t freq[256], uint32_t cum[257])
 {
     cum[0] = 0;
     for (int c = 0; c < 256; c++) cum[c + 1] = cum[c] + freq[c];
 }
 
-/* Encodes n symbols; writes into out[0..cap).  Returns the byte count, -1 if cap is too
- * small, -2 if a symbol has zero frequency ("unknown-symbol"). */
-int64_t eqo_encode_chunk(const uint8_t* sym, int64_t n, const uint16_t freq[256],
-                         uint8_t* out, int64_t cap)
+/* lower bound L and unit width (bits) of a codec; 0 width = unknown codec */
+static void eqo_codec_params(int codec, uint64_t* L, int* unit_bits)
 {
+    if (codec == EQO_CODEC_BYTE) { *L = 1u << 23; *unit_bits = 8; }
+    else if (codec == EQO_CODEC_WORD) { *L = 1u << 16; *unit_bits = 16; }
+    else { *L = 0; *unit_bits = 0; }
+}
+
+/* Encodes n symbols; writes into out[0..cap).  Returns the byte count, -1 if cap is too
+ * small, -2 if a symbol has zero frequency ("unknown-symbol"), -3 bad codec. */
+int64_t eqo_encode_chunk_codec(int codec, const uint8_t* sym, int64_t n, const uint16_t freq[256],
+                               uint8_t* out, int64_t cap)
+{
+    uint64_t L;
+    int ub;
+    eqo_codec_params(codec, &L, &ub);
+    if (ub == 0) return -3;
+    const int unit_bytes = ub / 8;
     uint32_t cum[257];
     eqo_cum(freq, cum);
-    /* bytes are produced back-to-front into a temporary of worst-case size */
+    /* units are produced back-to-front into a temporary of worst-case size */
     int64_t tcap = 4 + 2 * n + 8;
     uint8_t* tmp = (uint8_t*)malloc((size_t)tcap);
     int64_t pos = tcap;
-    uint64_t x = EQO_L;
+    uint64_t x = L;
     for (int64_t i = n - 1; i >= 0; i--) {
         uint32_t f = freq[sym[i]], c = cum[sym[i]];
         if (f == 0) { free(tmp); return -2; }
-        uint64_t x_max = (uint64_t)((EQO_L >> EQO_PROB_BITS) << 8) * f;
+        uint64_t x_max = ((L >> EQO_PROB_BITS) << ub) * f;
         while (x >= x_max) {
-            tmp[--pos] = (uint8_t)(x & 0xFF);
-            x >>= 8;
+            pos -= unit_bytes;
+            for (int k = 0; k < unit_bytes; k++) tmp[pos + k] = (uint8_t)((x >> (8 * k)) & 0xFF);
+            x >>= ub;
         }
         x = (x / f) * EQO_M + (x % f) + c;
     }
@@ -511,13 +535,17 @@ int64_t eqo_encode_chunk(const uint8_t* sym, int64_t n, const uint16_t freq[256]
     return len;
 }
 
-/* Decoder (Alg. 2 l.1): x = LE32; per symbol: slot = x mod M; s = the symbol with
- * cum[s] ≤ slot < cum[s+1] (linear scan); x = f_s·⌊x/M⌋ + slot − c_s; while x < L read
- * a byte.  Integrity: at the end x must equal L and every byte must have
- * been consumed.  Returns 0 ok, 1 corrupt, 2 truncated. */
-int eqo_decode_chunk(const uint8_t* in, int64_t nbytes, const uint16_t freq[256],
-                     uint8_t* sym, int64_t n)
+/* Decoder (Alg. 2 l.1): s found by a linear scan of the cumulative table.  Integrity
+ * (SURVEY §5): at the end x must equal L and every byte must have been consumed.
+ * Returns 0 ok, 1 corrupt, 2 truncated, 3 bad codec. */
+int eqo_decode_chunk_codec(int codec, const uint8_t* in, int64_t nbytes, const uint16_t freq[256],
+                           uint8_t* sym, int64_t n)
 {
+    uint64_t L;
+    int ub;
+    eqo_codec_params(codec, &L, &ub);
+    if (ub == 0) return 3;
+    const int unit_bytes = ub / 8;
     uint32_t cum[257];
     eqo_cum(freq, cum);
     if (nbytes < 4) return 2;
@@ -530,13 +558,26 @@ int eqo_decode_chunk(const uint8_t* in, int64_t nbytes, const uint16_t freq[256]
         while (!(cum[s] <= slot && slot < cum[s + 1])) s++;   /* cum[256] = M > slot */
         sym[i] = (uint8_t)s;
         x = (uint64_t)freq[s] * (x / EQO_M) + slot - cum[s];
-        while (x < EQO_L) {
-            if (p >= nbytes) return 2;
-            x = (x << 8) | in[p++];
+        while (x < L) {
+            if (p + unit_bytes > nbytes) return 2;
+            uint64_t u = 0;
+            for (int k = 0; k < unit_bytes; k++) u |= (uint64_t)in[p + k] << (8 * k);
+            p += unit_bytes;
+            x = (x << ub) | u;
         }
     }
-    if (x != EQO_L || p != nbytes) return 1;
+    if (x != L || p != nbytes) return 1;
     return 0;
+}
+
+int64_t eqo_encode_chunk(const uint8_t* sym, int64_t n, const uint16_t freq[256], uint8_t* out, int64_t cap)
+{
+    return eqo_encode_chunk_codec(EQO_CODEC_BYTE, sym, n, freq, out, cap);
+}
+
+int eqo_decode_chunk(const uint8_t* in, int64_t nbytes, const uint16_t freq[256], uint8_t* sym, int64_t n)
+{
+    return eqo_decode_chunk_codec(EQO_CODEC_BYTE, in, nbytes, freq, sym, n);
 }
 
 /* ------------------------------------------------------------------------------------
@@ -554,16 +595,16 @@ int64_t eqo_block_chunks(const int64_t* layer_sizes, int32_t n_layers, int64_t c
 }
 
 /* Returns payload bytes, or a negative error. */
-int64_t eqo_encode_block(const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers,
-                         int64_t cs, const uint16_t freq[256], uint8_t* payload, int64_t cap,
-                         uint32_t* chunk_off)
+int64_t eqo_encode_block_codec(int codec, const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers,
+                               int64_t cs, const uint16_t freq[256], uint8_t* payload, int64_t cap,
+                               uint32_t* chunk_off)
 {
     int64_t pos = 0, k = 0, sbase = 0;
     for (int32_t l = 0; l < n_layers; l++) {
         for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
             int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
             chunk_off[k++] = (uint32_t)pos;
-            int64_t len = eqo_encode_chunk(codes + sbase + a, n, freq, payload + pos, cap - pos);
+            int64_t len = eqo_encode_chunk_codec(codec, codes + sbase + a, n, freq, payload + pos, cap - pos);
             if (len < 0) return len;
             pos += len;
         }
@@ -573,22 +614,35 @@ int64_t eqo_encode_block(const uint8_t* codes, const int64_t* layer_sizes, int32
     return pos;
 }
 
+int64_t eqo_encode_block(const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers,
+                         int64_t cs, const uint16_t freq[256], uint8_t* payload, int64_t cap,
+                         uint32_t* chunk_off)
+{
+    return eqo_encode_block_codec(EQO_CODEC_BYTE, codes, layer_sizes, n_layers, cs, freq, payload, cap, chunk_off);
+}
+
 /* Decodes a whole block stream into codes; returns 0 / first failing status. */
-int eqo_decode_block(const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
-                     int32_t n_layers, int64_t cs, const uint16_t freq[256], uint8_t* codes)
+int eqo_decode_block_codec(int codec, const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
+                           int32_t n_layers, int64_t cs, const uint16_t freq[256], uint8_t* codes)
 {
     int64_t k = 0, sbase = 0;
     for (int32_t l = 0; l < n_layers; l++) {
         for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
             int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
-            int st = eqo_decode_chunk(payload + chunk_off[k], (int64_t)chunk_off[k + 1] - chunk_off[k],
-                                      freq, codes + sbase + a, n);
+            int st = eqo_decode_chunk_codec(codec, payload + chunk_off[k],
+                                            (int64_t)chunk_off[k + 1] - chunk_off[k], freq, codes + sbase + a, n);
             if (st) return st;
             k++;
         }
         sbase += layer_sizes[l];
     }
     return 0;
+}
+
+int eqo_decode_block(const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
+                     int32_t n_layers, int64_t cs, const uint16_t freq[256], uint8_t* codes)
+{
+    return eqo_decode_block_codec(EQO_CODEC_BYTE, payload, chunk_off, layer_sizes, n_layers, cs, freq, codes);
 }
 
 /* ------------------------------------------------------------------------------------
@@ -599,7 +653,7 @@ int eqo_decode_block(const uint8_t* payload, const uint32_t* chunk_off, const in
 typedef struct {
     const uint8_t* payload; const uint32_t* chunk_off; const uint64_t* chunk_sym0;
     const uint32_t* chunk_n; const uint16_t* freq; uint8_t* codes;
-    int64_t k0, k1; int status;
+    int64_t k0, k1; int status; int codec;
 } eqo_job;
 
 static void* eqo_worker(void* p)
@@ -607,24 +661,24 @@ static void* eqo_worker(void* p)
     eqo_job* j = (eqo_job*)p;
     j->status = 0;
     for (int64_t k = j->k0; k < j->k1; k++) {
-        int st = eqo_decode_chunk(j->payload + j->chunk_off[k],
-                                  (int64_t)j->chunk_off[k + 1] - j->chunk_off[k], j->freq,
-                                  j->codes + j->chunk_sym0[k], j->chunk_n[k]);
+        int st = eqo_decode_chunk_codec(j->codec, j->payload + j->chunk_off[k],
+                                        (int64_t)j->chunk_off[k + 1] - j->chunk_off[k], j->freq,
+                                        j->codes + j->chunk_sym0[k], j->chunk_n[k]);
         if (st && !j->status) j->status = st;
     }
     return NULL;
 }
 
-int eqo_decode_chunks_mt(const uint8_t* payload, const uint32_t* chunk_off,
-                         const uint64_t* chunk_sym0, const uint32_t* chunk_n, int64_t n_chunks,
-                         const uint16_t freq[256], uint8_t* codes, int threads)
+int eqo_decode_chunks_mt_codec(int codec, const uint8_t* payload, const uint32_t* chunk_off,
+                               const uint64_t* chunk_sym0, const uint32_t* chunk_n, int64_t n_chunks,
+                               const uint16_t freq[256], uint8_t* codes, int threads)
 {
     if (threads < 1) threads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
     eqo_job* jobs = (eqo_job*)malloc(sizeof(eqo_job) * (size_t)threads);
     for (int t = 0; t < threads; t++) {
         jobs[t] = (eqo_job){payload, chunk_off, chunk_sym0, chunk_n, freq, codes,
-                            n_chunks * t / threads, n_chunks * (t + 1) / threads, 0};
+                            n_chunks * t / threads, n_chunks * (t + 1) / threads, 0, codec};
         pthread_create(&th[t], NULL, eqo_worker, &jobs[t]);
     }
     int st = 0;
@@ -642,7 +696,7 @@ int eqo_decode_chunks_mt(const uint8_t* payload, const uint32_t* chunk_off,
  * (bf16 RNE of s_row·value(code)); chunks statically partitioned over POSIX threads. */
 typedef struct {
     const uint8_t* payload; const uint32_t* chunk_off; int64_t cs, size, cols;
-    const uint16_t* scales; const uint16_t* freq; uint16_t* out; int64_t k0, k1; int status;
+    const uint16_t* scales; const uint16_t* freq; uint16_t* out; int64_t k0, k1; int status; int codec;
 } eqo_ljob;
 
 static void* eqo_lworker(void* p)
@@ -652,8 +706,8 @@ static void* eqo_lworker(void* p)
     j->status = 0;
     for (int64_t k = j->k0; k < j->k1; k++) {
         int64_t a = k * j->cs, n = j->size - a < j->cs ? j->size - a : j->cs;
-        int st = eqo_decode_chunk(j->payload + j->chunk_off[k], (int64_t)j->chunk_off[k + 1] - j->chunk_off[k],
-                                  j->freq, sym, n);
+        int st = eqo_decode_chunk_codec(j->codec, j->payload + j->chunk_off[k],
+                                        (int64_t)j->chunk_off[k + 1] - j->chunk_off[k], j->freq, sym, n);
         if (st && !j->status) j->status = st;
         for (int64_t i = 0; i < n; i++) {
             int64_t row = (a + i) / j->cols;
@@ -664,16 +718,16 @@ static void* eqo_lworker(void* p)
     return NULL;
 }
 
-int eqo_decode_dequant_layer_mt(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks, int64_t cs,
-                                int64_t size, int64_t cols, const uint16_t* scales, const uint16_t freq[256],
-                                uint16_t* out, int threads)
+int eqo_decode_dequant_layer_mt_codec(int codec, const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks,
+                                      int64_t cs, int64_t size, int64_t cols, const uint16_t* scales,
+                                      const uint16_t freq[256], uint16_t* out, int threads)
 {
     if (threads < 1) threads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
     eqo_ljob* jobs = (eqo_ljob*)malloc(sizeof(eqo_ljob) * (size_t)threads);
     for (int t = 0; t < threads; t++) {
         jobs[t] = (eqo_ljob){payload, chunk_off, cs, size, cols, scales, freq, out,
-                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0};
+                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0, codec};
         pthread_create(&th[t], NULL, eqo_lworker, &jobs[t]);
     }
     int st = 0;
@@ -690,4 +744,20 @@ int64_t eqo_row_objectives(const uint16_t* W, int64_t M, int64_t N, int64_t row,
                            int32_t oct_lo, int32_t oct_hi, uint16_t* first_out, double* f, int64_t cap)
 {
     return eqo_row_objectives_fmt(0, W, M, N, row, lambda, oct_lo, oct_hi, first_out, f, cap);
+}
+
+int eqo_decode_chunks_mt(const uint8_t* payload, const uint32_t* chunk_off, const uint64_t* chunk_sym0,
+                         const uint32_t* chunk_n, int64_t n_chunks, const uint16_t freq[256], uint8_t* codes,
+                         int threads)
+{
+    return eqo_decode_chunks_mt_codec(EQO_CODEC_BYTE, payload, chunk_off, chunk_sym0, chunk_n, n_chunks, freq,
+                                      codes, threads);
+}
+
+int eqo_decode_dequant_layer_mt(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks, int64_t cs,
+                                int64_t size, int64_t cols, const uint16_t* scales, const uint16_t freq[256],
+                                uint16_t* out, int threads)
+{
+    return eqo_decode_dequant_layer_mt_codec(EQO_CODEC_BYTE, payload, chunk_off, n_chunks, cs, size, cols, scales,
+                                             freq, out, threads);
 }

@@ -91,73 +91,103 @@ def test_normalize_random_properties():
 
 
 # ------------------------------------------------------------------ rANS chunks
-def test_rans_worked_examples(golden):
-    for case in golden["rans_worked"]["cases"]:
+CODECS = [o.CODEC_BYTE, o.CODEC_WORD]
+GOLDEN_STREAMS = {o.CODEC_BYTE: "rans_worked", o.CODEC_WORD: "rans_word_worked"}
+L_OF = {o.CODEC_BYTE: 1 << 23, o.CODEC_WORD: 1 << 16}
+
+
+@pytest.mark.parametrize("codec", CODECS)
+def test_rans_worked_examples(golden, codec):
+    for case in golden[GOLDEN_STREAMS[codec]]["cases"]:
         freq = np.zeros(256, dtype=np.uint16)
         for k, v in case["freq"].items():
             freq[int(k)] = v
         sym = np.array(case["symbols"], dtype=np.uint8)
-        data = o.encode_chunk(sym, freq)
+        data = o.encode_chunk(sym, freq, codec)
         assert data.hex() == case["bytes_hex"], case["name"]
-        assert (o.decode_chunk(data, freq, sym.size) == sym).all()
+        assert (o.decode_chunk(data, freq, sym.size, codec) == sym).all()
 
 
+@pytest.mark.parametrize("codec", CODECS)
 @pytest.mark.parametrize("kind", ["skewed", "uniform", "subset130", "subset248", "subset2", "single"])
-def test_rans_round_trip_fuzz(kind):
+def test_rans_round_trip_fuzz(kind, codec):
     rng = np.random.default_rng(hash(kind) & 0xFFFF)
     for t in range(25):
         n = int(rng.choice([0, 1, 2, 3, 17, 4095, 4096, 4097, int(rng.integers(1, 70000))]))
         s = eqsynth.random_codes_stream(max(n, 1), int(rng.integers(1 << 30)), kind)[:n]
         freq = o.normalize(o.histogram(s)) if n else o.normalize(np.ones(256, np.uint64))
-        data = o.encode_chunk(s, freq)
-        assert (o.decode_chunk(data, freq, n) == s).all()
+        data = o.encode_chunk(s, freq, codec)
+        assert (o.decode_chunk(data, freq, n, codec) == s).all()
+        if codec == o.CODEC_WORD:
+            assert len(data) % 2 == 0                  # 4-byte state + whole 16-bit words
 
 
-def test_rans_empty_chunk_is_state_only():
+@pytest.mark.parametrize("codec", CODECS)
+def test_rans_empty_chunk_is_state_only(codec):
     freq = o.normalize(np.ones(256, np.uint64))
-    data = o.encode_chunk(np.zeros(0, np.uint8), freq)
-    assert data == (1 << 23).to_bytes(4, "little")
+    data = o.encode_chunk(np.zeros(0, np.uint8), freq, codec)
+    assert data == L_OF[codec].to_bytes(4, "little")
 
 
-def test_rans_rate_bounds():
+def test_rans_word_uniform_closed_form():
+    """Word codec, all 256 symbols at f = 16 (closed form, derived by hand): x = 16q + r
+    codes to 4096q + r + 16s.  From x = L = 2^16 the state alternates between
+    [2^16, 2^16 + 2^12) and [2^24, 2^24 + 2^20): a symbol coded from the lower range lands in
+    the upper one without output; the next one finds x ≥ 2^20·16 = 2^24, emits one word and
+    returns to the lower range.  So n symbols cost exactly 4 + 2·⌊n/2⌋ bytes."""
+    freq = np.full(256, 16, dtype=np.uint16)
+    rng = np.random.default_rng(3)
+    for n in [1, 2, 3, 4, 5, 20, 1001, 2000]:
+        s = rng.integers(0, 256, n).astype(np.uint8)
+        data = o.encode_chunk(s, freq, o.CODEC_WORD)
+        assert len(data) == 4 + 2 * (n // 2)
+        assert (o.decode_chunk(data, freq, s.size, o.CODEC_WORD) == s).all()
+
+
+@pytest.mark.parametrize("codec", CODECS)
+def test_rans_rate_bounds(codec):
     """Shannon lower bound and the table cross-entropy upper bound."""
     for kind, seed in [("skewed", 1), ("uniform", 2), ("subset40", 3)]:
         s = eqsynth.random_codes_stream(1 << 18, seed, kind)
         h = o.histogram(s)
         f = o.normalize(h)
-        data = o.encode_chunk(s, f)
+        data = o.encode_chunk(s, f, codec)
         bits = 8 * len(data)
         assert bits >= emp_entropy_bits(h) - 0.001 * s.size
         assert bits <= xent_bits(h, f) + 0.01 * s.size + 64
 
 
-def test_rans_degenerate_rates():
+@pytest.mark.parametrize("codec", CODECS)
+def test_rans_degenerate_rates(codec):
     # 2^20 copies of one symbol -> < 0.01 bits/symbol (S:323)
     s = np.full(1 << 20, 9, dtype=np.uint8)
     f = o.normalize(o.histogram(s))
-    assert 8 * len(o.encode_chunk(s, f)) / s.size < 0.01
+    assert 8 * len(o.encode_chunk(s, f, codec)) / s.size < 0.01
     # uniform random bytes -> within 1% above 8 bits/symbol (S:324)
     s = eqsynth.random_codes_stream(1 << 20, 5, "uniform")
     f = o.normalize(o.histogram(s))
-    r = 8 * len(o.encode_chunk(s, f)) / s.size
+    r = 8 * len(o.encode_chunk(s, f, codec)) / s.size
     assert 8.0 - 0.01 <= r <= 8.0 * 1.01
 
 
-def test_rans_unknown_symbol_and_corruption():
+@pytest.mark.parametrize("codec", CODECS)
+def test_rans_unknown_symbol_and_corruption(codec):
     f = o.normalize(hist_of({1: 5, 2: 5}))
     with pytest.raises(ValueError, match="unknown-symbol"):
-        o.encode_chunk(np.array([1, 3], np.uint8), f)
+        o.encode_chunk(np.array([1, 3], np.uint8), f, codec)
     s = eqsynth.random_codes_stream(5000, 9, "skewed")
     f = o.normalize(o.histogram(s))
-    data = bytearray(o.encode_chunk(s, f))
+    data = bytearray(o.encode_chunk(s, f, codec))
     with pytest.raises(ValueError, match="truncated"):
-        o.decode_chunk(bytes(data[:-3]), f, s.size)
+        o.decode_chunk(bytes(data[:-4]), f, s.size, codec)
+    with pytest.raises(ValueError, match="corrupt|truncated"):
+        o.decode_chunk(bytes(data) + b"\0\0", f, s.size, codec)     # unconsumed trailing bytes
     detected = 0
     for pos in range(4, len(data), max(1, len(data) // 40)):
         d2 = bytearray(data)
         d2[pos] ^= 0x5A
         try:
-            out = o.decode_chunk(bytes(d2), f, s.size)
+            out = o.decode_chunk(bytes(d2), f, s.size, codec)
             detected += int(not (out == s).all())      # wrong output at least
         except ValueError:
             detected += 1
@@ -165,12 +195,13 @@ def test_rans_unknown_symbol_and_corruption():
 
 
 # ------------------------------------------------------------------ block stream
-def test_block_round_trip_ragged_layers():
+@pytest.mark.parametrize("codec", CODECS)
+def test_block_round_trip_ragged_layers(codec):
     """Layer-restart chunking with ragged shapes and a tiny chunk size."""
     layers = [eqsynth.weights(r, c, seed=1, layer=0, matrix=m) for m, (r, c) in
               enumerate([(37, 53), (1, 1), (64, 64), (5, 4097)])]
     for cs in [4096, 100, 1]:
-        blk = o.quantize_encode(layers, lam=None, cs=cs)
+        blk = o.quantize_encode(layers, lam=None, cs=cs, codec=codec)
         stream = o.decode_block(blk)
         assert (stream == blk.codes).all()
         sym0, ns = o.chunk_table(blk.layer_shapes, cs)
@@ -178,7 +209,7 @@ def test_block_round_trip_ragged_layers():
         # chunk independence: any chunk decodes alone to its slice
         for k in [0, blk.n_chunks // 2, blk.n_chunks - 1]:
             a, b = int(blk.chunk_off[k]), int(blk.chunk_off[k + 1])
-            out = o.decode_chunk(blk.payload[a:b], blk.freq, int(ns[k]))
+            out = o.decode_chunk(blk.payload[a:b], blk.freq, int(ns[k]), codec)
             assert (out == stream[int(sym0[k]):int(sym0[k]) + int(ns[k])]).all()
         deq = o.decode_dequant(blk)
         for W, S, D in zip(layers, blk.scales, deq):
@@ -198,11 +229,12 @@ def test_block_lambda0_rate_near_paper_anchor():
     assert len(blk.payload) * 8 >= blk.n_params * H - 0.001 * blk.n_params
 
 
-def test_block_two_bits_unique_codes_and_budget():
+@pytest.mark.parametrize("codec", CODECS)
+def test_block_two_bits_unique_codes_and_budget(codec):
     """At ~2 bits: many more than 4 unique codes (Table 1) and coded size within
     1.02x of n·Ĥ (north_star)."""
     W = eqsynth.weights(64, 1024, seed=2)
-    blk = o.quantize_encode([W], lam=180.0)
+    blk = o.quantize_encode([W], lam=180.0, codec=codec)
     H = o.entropy(blk.hist)
     assert 1.3 < H < 3.0
     assert int((blk.hist > 0).sum()) > 12
