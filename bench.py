@@ -35,6 +35,9 @@ FALLBACK_HBM_GBS = 6650.0            # B200_PROFILING.md fallback, used only wit
 DEFAULT_LAMBDA = 230.2               # reference arm only: the GPU calibration of λ for 2.0 bits
 
 
+CODECS = {"byte": 0, "word": 1}     # EQ_CODEC_BYTE / EQ_CODEC_WORD (include/entquant.h)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -52,6 +55,8 @@ def parse():
     ap.add_argument("--no-fp8", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
+    ap.add_argument("--codec", default="byte", choices=["byte", "word"],
+                    help="rANS renormalisation: byte (SPEC S:355, R9) or 16-bit word (R14)")
     return ap.parse_args()
 
 
@@ -191,7 +196,7 @@ def run_reference(args, rank, world):
         layers.append(eqsynth.weights_rows(ids, r, c, seed=0, layer=0, matrix=m))
         full_shapes.append((r, c))
     t0 = time.time()
-    blk = o.quantize_encode(layers, lam=lam)
+    blk = o.quantize_encode(layers, lam=lam, codec=CODECS[args.codec])
     enc_s = time.time() - t0
     payload = np.frombuffer(blk.payload + b"\0" * 16, dtype=np.uint8)
     # per-layer chunk ranges of the sample block
@@ -204,7 +209,7 @@ def run_reference(args, rank, world):
 
     def one_pass():
         for off, r, c, S in per_layer:
-            o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, blk.freq, threads)
+            o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, blk.freq, threads, blk.codec)
 
     t = time.time()
     one_pass()
@@ -242,7 +247,7 @@ def workload_config(args, n_params, lam):
         "workload": f"config3: {args.model}-shaped layer set, {args.blocks or 'all'} blocks x 7 linear layers per rank, "
                     f"~{args.target_bits} effective bits/param, chunk-parallel rANS decode + fused dequant to bf16",
         "model_shapes": args.model, "blocks_per_rank": args.blocks, "params_per_rank": n_params,
-        "chunk_symbols": 4096, "lambda": lam, "target_bits": args.target_bits,
+        "chunk_symbols": 4096, "codec": args.codec, "lambda": lam, "target_bits": args.target_bits,
         "l2": "inputs larger than L2 (compressed in + decoded out per step >> 126 MB); no flush",
         "parallelism": f"block-sharded x{args.gpus} ({args.scaling})",
     }
@@ -291,7 +296,7 @@ def main():
         if scratch is None:
             _, _, sb = eq.encode_bounds(Ws)
             scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch))
+        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch, codec=CODECS[args.codec]))
         del Ws
     del scratch
     torch.cuda.synchronize()
@@ -435,7 +440,7 @@ def cpu_baseline(blocks, seconds: float):
             nk = (r * c + cs - 1) // cs
             off = off_all[k0:k0 + nk + 1]
             t = time.perf_counter()
-            o.decode_dequant_layer_mt(payload, off, cs, r, c, scales[r0:r0 + r], freq, threads)
+            o.decode_dequant_layer_mt(payload, off, cs, r, c, scales[r0:r0 + r], freq, threads, blk.codec)
             wall += time.perf_counter() - t
             done_bytes += int(off[-1] - off[0]) + 4 * (nk + 1) + 2 * r + 2 * r * c
             done_syms += r * c

@@ -3,7 +3,7 @@
  *
  * Paper: "Float8@2bits: Entropy Coding Enables Data-Free Model Compression",
  * arXiv 2601.22787.  P:<n> = line n of PAPER.md, S:<n> = line n of SPEC.md; the
- * readings of ambiguous passages are listed in DESIGN.md §3 and numbered R1..R12.
+ * readings of ambiguous passages are listed in DESIGN.md §3 and numbered R1..R14.
  *
  * Conventions (all entry points):
  *  - Tensor / array pointers are CUDA DEVICE pointers unless the parameter name ends in
@@ -55,6 +55,13 @@ typedef enum {
                                     /* left to the GEMM epilogue)                          */
 #define EQ_OUT_BF16   1u            /* decode + fused per-row dequant to bf16      */
 
+/* rANS renormalisation (the "ANS" of P:155/P:213/P:229; nvCOMP's own is undocumented).
+ * Both: 32-bit state, M = 2^12, cum in code order, chunk = 4-byte LE final state followed by
+ * the renormalisation units in decode order (R9, R14). */
+#define EQ_CODEC_BYTE 0u            /* L = 2^23, byte units (≤ 2 per symbol)    */
+#define EQ_CODEC_WORD 1u            /* R14: L = 2^16, 16-bit little-endian word units       */
+                                    /* (≤ 1 per symbol: the GPU decoder's fast path)         */
+
 #define EQ_SCALES_SEARCH 0u         /* exhaustive per-row Eq. 4 minimisation (R5)          */
 #define EQ_SCALES_ABSMAX 1u         /* AbsMax scales, Eq. 1 (the λ = 0 lossless-FP8 rate)  */
 #define EQ_SCALES_GIVEN  2u         /* caller supplies eq_block.scales                     */
@@ -80,6 +87,7 @@ typedef struct {
     int32_t  oct_lo, oct_hi;        /* search bracket, octaves around AbsMax (R5): -1, 20  */
     uint32_t exclude_mask;          /* bit l: layer l keeps AbsMax scales (λ = 0) — the    */
                                     /* super-weight exclusion of P:393-396          */
+    uint32_t codec;                 /* EQ_CODEC_BYTE (0, default) | EQ_CODEC_WORD          */
 } eq_params;
 
 /* One compressed transformer block: all its layers in one bitstream with one table
@@ -98,6 +106,8 @@ typedef struct {
     uint32_t  format;               /* EQ_FMT_* of the symbols (set by eq_quantize_encode) */
     int64_t   layer_rows[EQ_MAX_LAYERS];
     int64_t   layer_cols[EQ_MAX_LAYERS];
+    uint32_t  codec;                /* EQ_CODEC_* of the streams (set by eq_quantize_encode) */
+    uint32_t  reserved;             /* 0                                                   */
 } eq_block;
 
 /* ---------------------------------------------------------------- library info */
@@ -152,10 +162,10 @@ eq_status eq_quantize_hist(const eq_tensor* w, uint32_t format, const uint16_t* 
  * histogram sets EQ_EF_EMPTY in d_err. */
 eq_status eq_build_table(const uint64_t* hist, uint16_t* freq, uint32_t* d_err, eq_stream_t stream);
 
-/* a6 (Alg. 1 l.4-5, R9/R10): rANS-encode the concatenated symbol stream `codes`
- * of the block's layers (sizes rows*cols in block order, from `blk`), chunks of
+/* a6 (Alg. 1 l.4-5, R9/R10/R14): rANS-encode the concatenated symbol stream
+ * `codes` of the block's layers (sizes rows*cols in block order, from `blk`), chunks of
  * blk->chunk_symbols restarting at each layer, into blk->payload / blk->chunk_off with
- * table blk->freq.  chunk_sizes: device scratch uint32[n_chunks].  *payload_bytes_dev
+ * table blk->freq and renormalisation blk->codec (EQ_CODEC_*; else EQ_ERR_ARG).  chunk_sizes: device scratch uint32[n_chunks].  *payload_bytes_dev
  * (device uint64) receives the total.  A zero-frequency symbol sets EQ_EF_UNKNOWN_SYMBOL. */
 eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, uint32_t* chunk_sizes,
                          uint64_t* payload_bytes_dev, uint32_t* d_err, eq_stream_t stream);
@@ -177,9 +187,10 @@ eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_layers, const e
  * blocks in ONE launch (chunk-parallel, lane per chunk) and write each layer, row-major,
  * into `arena` at the offsets of eq_arena_layout (views, no copies).  EQ_OUT_BF16 fuses
  * the dequantiser out = RNE_bf16(s_row · value(code)) for the block's format (E4M3 or Int8);
- * EQ_OUT_FP8 writes the codes.
- * Per-chunk integrity (final state == 2^23, every byte consumed) and offset bounds are
- * checked on the device and reported in d_err (EQ_EF_CORRUPT / EQ_EF_TRUNCATED).
+ * EQ_OUT_FP8 writes the codes.  All blocks of one call must share one codec (EQ_ERR_ARG
+ * otherwise).
+ * Per-chunk integrity (final state == L of the codec, every byte consumed) and offset
+ * bounds are checked on the device and reported in d_err (EQ_EF_CORRUPT / EQ_EF_TRUNCATED).
  * Asynchronous; EQ_ERR_BUFFER if arena_bytes is below the layout's total. */
 eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks, uint32_t out_dtype,
                             void* arena, uint64_t arena_bytes, uint32_t* d_err,
@@ -195,7 +206,7 @@ eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks,
                                  void* arena_host, uint64_t arena_bytes, void* workspace,
                                  uint64_t workspace_bytes, eq_stream_t stream);
 
-/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4): Y_q = X_q · Ŵ_qᵀ for
+/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4; EQ_CODEC_BYTE blocks): Y_q = X_q · Ŵ_qᵀ for
  * n_jobs layers `layers[q]` of block `blk` in ONE launch, Ŵ = the layer's decoded +
  * dequantised bf16 weights (never written to memory): each chunk is decoded straight into
  * tcgen05 shared-memory tiles and multiplied on the 5th-gen tensor cores (bf16 × bf16 →

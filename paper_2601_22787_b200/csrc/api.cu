@@ -32,6 +32,7 @@ eq_status check_params(const eq_params* p) {
     if (p->format > EQ_FMT_INT8 || p->prob_bits != EQ_PROB_BITS) return EQ_ERR_ARG;
     if (p->chunk_symbols == 0 || p->chunk_symbols > 262144u) return EQ_ERR_ARG;
     if (p->scale_mode > EQ_SCALES_GIVEN) return EQ_ERR_ARG;
+    if (p->codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
     if (p->scale_mode == EQ_SCALES_SEARCH && !(p->lambda >= 0.0)) return EQ_ERR_ARG;
     return EQ_OK;
 }
@@ -115,6 +116,7 @@ extern "C" eq_status eq_encode_bounds(const eq_tensor* layers, uint32_t n_layers
     for (uint32_t l = 0; l < n_layers; ++l) syms += (uint64_t)layers[l].rows * (uint64_t)layers[l].cols;
     const uint64_t nc = count_chunks(layers, n_layers, p->chunk_symbols);
     // worst case per chunk: 4-byte state + at most 2 renormalisation bytes per symbol
+    // (two bytes, EQ_CODEC_BYTE, or one 16-bit word, EQ_CODEC_WORD)
     const uint64_t cap = align_up(4 * nc + 2 * syms + EQ_PAYLOAD_SLACK, 256);
     if (payload_cap) *payload_cap = cap;
     if (n_chunks) *n_chunks = (uint32_t)nc;
@@ -146,6 +148,8 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
 
     out->n_layers = n_layers;
     out->format = p->format;
+    out->codec = p->codec;
+    out->reserved = 0;
     out->n_chunks = nc;
     out->chunk_symbols = p->chunk_symbols;
     for (uint32_t l = 0; l < EQ_MAX_LAYERS; ++l) {

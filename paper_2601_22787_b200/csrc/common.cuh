@@ -11,7 +11,8 @@
 
 namespace eq {
 
-constexpr uint32_t kL = 1u << 23;            // rANS lower bound (R9)
+constexpr uint32_t kL = 1u << 23;            // rANS lower bound, EQ_CODEC_BYTE (R9)
+constexpr uint32_t kLw = 1u << 16;           // rANS lower bound, EQ_CODEC_WORD (R14)
 constexpr uint32_t kProbBits = 12;
 constexpr uint32_t kM = 1u << kProbBits;
 constexpr float kQmax = 448.0f;              // E4M3 Q_max

@@ -115,6 +115,7 @@ struct DecTable {
     uint32_t lut_s;        // shared address of the LUT
     uint32_t f0;           // frequency of code 0x00
     uint32_t ez;           // (f0 − 1) << 8
+    const uint32_t* lutp;  // the LUT (shared array; EQ_WADDR = 1 addressing)
 };
 
 // One rANS decode step (Alg. 2 l.1): slot lookup, state update, byte renormalisation.
@@ -263,14 +264,17 @@ __device__ __forceinline__ uint32_t decode4(Chain& c, const DecTable& T) {
 #ifndef EQ_UNROLL2
 #define EQ_UNROLL2 0
 #endif
-__device__ __forceinline__ void store16_bf16_at(Chain& c, const uint32_t q[4], uint8_t* dst);
+template <class C>
+__device__ __forceinline__ void store16_bf16_at(C& c, const uint32_t q[4], uint8_t* dst);
 
 // 16 symbols -> bf16 with one row scale (cols % 16 == 0), 32-byte store
-__device__ __forceinline__ void store16_bf16(Chain& c, const uint32_t q[4]) {
+template <class C>
+__device__ __forceinline__ void store16_bf16(C& c, const uint32_t q[4]) {
     store16_bf16_at(c, q, c.out + (uint64_t)c.i * 2);
 }
 
-__device__ __forceinline__ void store16_bf16_at(Chain& c, const uint32_t q[4], uint8_t* dst) {
+template <class C>
+__device__ __forceinline__ void store16_bf16_at(C& c, const uint32_t q[4], uint8_t* dst) {
     uint4 lo, hi;
     if (c.i8) {
         lo = make_uint4(dequant2_i8(q[0], c.s), dequant2_i8(q[0] >> 16, c.s), dequant2_i8(q[1], c.s),
@@ -298,5 +302,106 @@ __device__ __forceinline__ void store16_bf16_at(Chain& c, const uint32_t q[4], u
     }
 }
 
+// ================================================================ EQ_CODEC_WORD (R14)
+// 16-bit renormalisation: after a decode step at most ONE word is needed (x ≥ 16 always,
+// and (x << 16) ≥ 2^20 ≥ L), so the lane keeps no bit window: it holds the next unconsumed
+// word `w` in a register (prefetched from its shared-memory ring as soon as the previous one
+// is consumed, off the state's dependency chain) and renormalises with one predicated PRMT.
+#ifndef EQ_WRING
+#define EQ_WRING 64                 // bytes of staging ring per chunk (64 or 128; 64 measured faster:
+#endif                              // 6 CTAs/SM instead of 4)
+constexpr uint32_t kWRing = EQ_WRING;
+// Staging schedule: one 16-byte segment at most per 8-step boundary (a lane consumes at
+// most 8 words = 16 bytes per 8 steps, so the stage front keeps pace; right after the
+// initial fill it may trail its target gs·16 > q + kWRing − 16 by one segment, never more).
+// Hence every staged segment starts > q + kWRing − 48 when issued, the next 8 steps read
+// only [q, q + 16), and a segment issued k boundaries ago is not needed while
+// 16k ≤ kWRing − 64: cp.async groups (one per boundary) allowed in flight =
+// (kWRing − 64)/16 − 1 → 3 for a 128-byte ring, 0 (wait for all) for a 64-byte one.
+constexpr int kWWait = kWRing >= 128 ? 3 : 0;
+
+struct WordReader {
+    uint32_t q;            // payload byte offset of the next word to load into w
+    uint32_t w;            // the next unconsumed 16-bit word (low half)
+    uint32_t gs;           // next 16-byte payload segment to stage
+    uint32_t ring;         // shared address of this chunk's ring (kWRing-aligned)
+};
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void stage_segment_w(uint32_t ring, const uint8_t* payload, uint32_t seg) {
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(ring | ((seg * 16u) & (kWRing - 1))),
+                 "l"(payload + (uint64_t)seg * 16));
+}
+template <int N>
+__device__ __forceinline__ void stage_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Every 8 steps, after stage_wait_n<kWWait>: stage the next segment if the ring slot it
+// overwrites holds only bytes before the reader (gs·16 ≤ q + kWRing − 16).
+__device__ __forceinline__ void ring_issue_w(WordReader& r, const uint8_t* payload) {
+    if (r.gs * 16u <= r.q + (kWRing - 16u)) {
+        stage_segment_w(r.ring, payload, r.gs);
+        ++r.gs;
+    }
+}
+
+#ifndef EQ_WADDR
+#define EQ_WADDR 0       // LUT address: 0 = 4x − 2^14·xs + base (3 IMADs deep), 1 = (4x & 0x3FFC) + base
+#endif
+#ifndef EQ_WENTRY
+#define EQ_WENTRY 1      // LUT entry layout of build_lut<EQ_WENTRY> (0: f−1 in bits 8-19, 1: in 20-31)
+#endif
+// One rANS decode step (Alg. 2 l.1) with word renormalisation; returns the LUT entry
+// (symbol in the low byte).  State update with IMAD / IMAD.HI / LEA.HI forms; then
+// if x < 2^16: x = (x << 16) | w as one PRMT, and the next word is prefetched.
+__device__ __forceinline__ uint32_t decode_one_w(uint32_t& x, WordReader& r, const DecTable& T) {
+    const uint32_t xs = mad_hi(x, T.k2p20, 0u);                         // x >> 12
+#if EQ_WADDR
+    const uint32_t e = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(T.lutp) +
+                                                          (mad_lo(x, T.k4, 0u) & 0x3FFCu));
+#else
+    const uint32_t e = lds_u32(mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s)));
+#endif
+#if EQ_WENTRY
+    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
+    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
+#else
+    const uint32_t fm1 = mad_hi(mad_lo(e, T.k2p12, 0u), T.k2p12, 0u);   // (e >> 8) & 0xFFF
+    x = mad_lo(fm1, xs, xs + (e >> 20));                                // f·⌊x/M⌋ + slot − c (LEA.HI)
+#endif
+    if (x < kLw) {
+        x = __byte_perm(r.w, x, 0x5410);                                // (x << 16) | w
+        r.w = lds_u16(r.ring | (r.q & (kWRing - 1)));
+        r.q += 2;
+    }
+    return e;
+}
+
+struct ChainW {
+    uint32_t x;
+    WordReader r;
+    uint8_t* out;
+    const uint16_t* sc;
+    uint32_t row, col, cols;
+    float s;
+    uint16_t s16;
+    bool i8;
+    uint32_t n, i;
+    uint32_t a, e;         // chunk payload byte range [a, e)
+    bool active, runaway, fast;
+};
+
+// 4 symbols -> one word of codes (first symbol in the low byte)
+__device__ __forceinline__ uint32_t decode4_w(ChainW& c, const DecTable& T) {
+    const uint32_t a = decode_one_w(c.x, c.r, T);
+    const uint32_t b = decode_one_w(c.x, c.r, T);
+    const uint32_t d = decode_one_w(c.x, c.r, T);
+    const uint32_t f = decode_one_w(c.x, c.r, T);
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(d, f, 0x0040), 0x5410);
+}
 
 }  // namespace eq

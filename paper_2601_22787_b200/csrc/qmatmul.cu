@@ -355,6 +355,7 @@ static eq_status qmm_validate(const eq_block* blk, uint32_t n_jobs, const uint32
                               QmmPlan* plan) {
     if (!blk || !layers || n_jobs < 1 || n_jobs > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (!blk->payload || !blk->chunk_off || !blk->freq || !blk->scales || blk->format > EQ_FMT_INT8) return EQ_ERR_ARG;
+    if (blk->codec != EQ_CODEC_BYTE) return EQ_ERR_ARG;
     if (blk->n_layers < 1 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(blk->payload) & 15) != 0) return EQ_ERR_ARG;
     if (blk->payload_cap < blk->payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;

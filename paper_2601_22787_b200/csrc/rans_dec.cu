@@ -1,4 +1,5 @@
-// rans_dec.cu — §8(a) rows a7 + a8: chunk-parallel byte-wise rANS decode of E4M3 symbol
+// rans_dec.cu — §8(a) rows a7 + a8: chunk-parallel rANS decode (byte or 16-bit-word
+// renormalisation, R9 / R14) of E4M3 symbol
 // streams (Alg. 2 l.1) with the dequantiser Q† fused into the store, into
 // a per-device arena with one view per layer (App. A.1).
 //
@@ -44,7 +45,7 @@ struct DecBlock {
     const uint16_t* scales;
     uint64_t payload_bytes;
     uint32_t format;       // EQ_FMT_E4M3 | EQ_FMT_INT8 (bf16 dequant of the codes)
-    uint32_t pad0;
+    uint32_t codec;        // EQ_CODEC_BYTE | EQ_CODEC_WORD (one per launch)
     uint32_t n_chunks;
     uint32_t cs;           // chunk symbols
     uint32_t n_layers;
@@ -62,6 +63,59 @@ struct DecParams {
     uint32_t k2p20, k2p12, kneg2p14, k4;
     DecBlock b[kMaxDecBlocks];
 };
+
+// The block's decode LUT in shared memory from its 256 frequencies (all kDecThreads threads
+// call it): exclusive prefix cum[257], then per slot the largest s with cum[s] ≤ slot,
+// entry = s | (f_s − 1) << 8 | (slot − cum[s]) << 20 (LAYOUT 0) or
+//         s | (slot − cum[s]) << 8 | (f_s − 1) << 20 (LAYOUT 1, decode_one_w).
+// Returns false (EQ_EF_CORRUPT set once) if the frequencies do not sum to M.
+template <int LAYOUT = 0, int NT = kDecThreads>
+__device__ __forceinline__ bool build_lut(const DecBlock& B, uint32_t* lut, uint32_t* cum, uint32_t* err) {
+    static_assert(NT >= 256 || 256 % NT == 0, "thread count");
+    const int t = threadIdx.x;
+    {
+        __shared__ uint32_t wsum[8];
+        const int lane = t & 31, w = t >> 5;
+        for (int base = 0; base < 256; base += NT) {
+            if (base + t < 256) {
+                uint32_t v = B.freq[base + t];
+                #pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+                    if (lane >= d) v += o;
+                }
+                if (lane == 31) wsum[(base >> 5) + w] = v;
+                cum[base + t + 1] = v;              // warp-local inclusive prefix for now
+            }
+        }
+        __syncthreads();
+        for (int base = 0; base < 256; base += NT) {
+            const int idx = base + t;
+            if (idx < 256) {
+                uint32_t add = 0;
+                for (int q = 0; q < (idx >> 5); ++q) add += wsum[q];
+                cum[idx + 1] += add;
+            }
+        }
+        if (t == 0) cum[0] = 0;
+    }
+    __syncthreads();
+    if (cum[256] != kM) {                     // corrupt table: nothing decodable
+        if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
+        return false;
+    }
+    for (int slot = t; slot < (int)kM; slot += NT) {
+        int lo = 0, hi = 255;                  // largest s with cum[s] <= slot
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+        }
+        uint32_t fs = cum[lo + 1] - cum[lo];
+        lut[slot] = LAYOUT == 0 ? ((uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20))
+                                : ((uint32_t)lo | (((uint32_t)slot - cum[lo]) << 8) | ((fs - 1) << 20));
+    }
+    return true;
+}
 
 template <bool BF16>
 __device__ __forceinline__ void chain_setup(Chain& c, const DecBlock& B, uint32_t chunk, uint32_t ring,
@@ -210,42 +264,9 @@ k_decode(const __grid_constant__ DecParams P) {
     stage_commit();
 
     // ---- table: exclusive prefix of the 256 frequencies, then the slot LUT
-    {
-        __shared__ uint32_t wsum[8];
-        const int lane = t & 31, w = t >> 5;
-        for (int base = 0; base < 256; base += kDecThreads) {
-            uint32_t v = B.freq[base + t];
-            #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
-                if (lane >= d) v += o;
-            }
-            if (lane == 31) wsum[(base >> 5) + w] = v;
-            cum[base + t + 1] = v;                  // warp-local inclusive prefix for now
-        }
-        __syncthreads();
-        for (int base = 0; base < 256; base += kDecThreads) {
-            const int idx = base + t;
-            uint32_t add = 0;
-            for (int q = 0; q < (idx >> 5); ++q) add += wsum[q];
-            cum[idx + 1] += add;
-        }
-        if (t == 0) cum[0] = 0;
-    }
-    __syncthreads();
-    if (cum[256] != kM) {                     // corrupt table: nothing decodable
-        if (t == 0) atomicOr(P.err, EQ_EF_CORRUPT);
+    if (!build_lut(B, lut, cum, P.err)) {
         stage_wait_all();
         return;
-    }
-    for (int slot = t; slot < (int)kM; slot += kDecThreads) {
-        int lo = 0, hi = 255;                  // largest s with cum[s] <= slot
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
-        }
-        uint32_t fs = cum[lo + 1] - cum[lo];
-        lut[slot] = (uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20);
     }
     stage_wait_all();
     __syncthreads();
@@ -335,6 +356,151 @@ k_decode(const __grid_constant__ DecParams P) {
     }
 }
 
+
+// ================================================================ EQ_CODEC_WORD decoder
+// Same CTA/lane mapping, LUT and stores as k_decode; per lane a 128-byte (kWRing) staging
+// ring, and word renormalisation (decode_one_w): no bit window, no per-pair refill.
+template <bool BF16>
+__device__ __forceinline__ void chain_setup_w(ChainW& c, const DecBlock& B, uint32_t chunk, uint32_t ring,
+                                              uint8_t* arena, uint32_t* err) {
+    c.active = chunk < B.n_chunks;
+    c.runaway = false;
+    c.i = 0;
+    c.n = 0;
+    if (!c.active) return;
+    uint32_t l = 0;
+    while (l + 1 < B.n_layers && chunk >= B.layer[l + 1].chunk0) ++l;
+    const DecLayer& Ly = B.layer[l];
+    const uint64_t sym0 = (uint64_t)(chunk - Ly.chunk0) * B.cs;
+    c.n = (uint32_t)min((uint64_t)B.cs, Ly.size - sym0);
+    const uint32_t a = __ldg(B.off + chunk), e = __ldg(B.off + chunk + 1);
+    if (e < a || (uint64_t)e > B.payload_bytes || e - a < 4) {
+        atomicOr(err, EQ_EF_TRUNCATED);
+        c.active = false;
+        return;
+    }
+    c.a = a;
+    c.e = e;
+    c.r.ring = ring;
+    const uint32_t s0 = a >> 4;
+    #pragma unroll
+    for (uint32_t q = 0; q < kWRing / 16; ++q) stage_segment_w(ring, B.payload, s0 + q);
+    c.r.gs = s0 + kWRing / 16;
+    c.out = arena + Ly.out_off + sym0 * (BF16 ? 2 : 1);
+    c.sc = B.scales + Ly.scale_off;
+    c.cols = Ly.cols;
+    c.row = (uint32_t)(sym0 / Ly.cols);
+    c.col = (uint32_t)(sym0 % Ly.cols);
+    c.s = BF16 ? bf16_bits_to_float(c.sc[c.row]) : 0.f;
+    c.i8 = B.format == EQ_FMT_INT8;
+    c.s16 = (BF16 && !c.i8) ? scale_f16(c.s) : 0;
+    c.fast = BF16 ? ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) : ((B.cs & 31) == 0);
+}
+
+// after the initial segments landed: 4-byte little-endian state, then the first word
+__device__ __forceinline__ void chain_start_w(ChainW& c) {
+    if (!c.active) return;
+    const uint32_t m = kWRing - 1;
+    c.x = lds_u16(c.r.ring | (c.a & m)) | (lds_u16(c.r.ring | ((c.a + 2) & m)) << 16);
+    c.r.w = lds_u16(c.r.ring | ((c.a + 4) & m));
+    c.r.q = c.a + 6;
+}
+
+__device__ __forceinline__ void ring_step_w(ChainW& c, const uint8_t* payload) {
+    stage_wait_n<kWWait>();
+    ring_issue_w(c.r, payload);
+    stage_commit();
+}
+
+template <bool BF16>
+__device__ __forceinline__ void chain_finish_w(ChainW& c, const uint8_t* payload, const DecTable& T) {
+    if (!c.active || c.runaway) return;
+    if (c.fast) {
+        const uint32_t G = BF16 ? 16 : 32;
+        while (c.i + G <= c.n) {
+            if (BF16) {
+                uint32_t q[4];
+                q[0] = decode4_w(c, T);
+                q[1] = decode4_w(c, T);
+                ring_step_w(c, payload);
+                q[2] = decode4_w(c, T);
+                q[3] = decode4_w(c, T);
+                ring_step_w(c, payload);
+                store16_bf16(c, q);
+            } else {
+                uint32_t q[8];
+                #pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    q[k] = decode4_w(c, T);
+                    if (k & 1) ring_step_w(c, payload);
+                }
+                st_out32(c.out + c.i, make_uint4(q[0], q[1], q[2], q[3]), make_uint4(q[4], q[5], q[6], q[7]));
+            }
+            c.i += G;
+            if (c.r.q > c.e + 2) { c.runaway = true; return; }
+        }
+    }
+    for (; c.i < c.n; ++c.i) {                  // generic / ragged tail: one symbol at a time
+        const uint32_t sym = decode_one_w(c.x, c.r, T) & 0xFFu;
+        if ((c.i & 7) == 7) ring_step_w(c, payload);
+        store_one<BF16>(c.out, c.i, sym, c.s, c.i8);
+        if (BF16 && ++c.col == c.cols) {
+            c.col = 0;
+            ++c.row;
+            if (c.i + 1 < c.n) c.s = bf16_bits_to_float(c.sc[c.row]);
+        }
+        if (c.r.q > c.e + 2) { c.runaway = true; return; }
+    }
+}
+
+#ifndef EQ_WTHREADS
+#define EQ_WTHREADS 256             // chunks (= threads) per CTA of k_decode_w
+#endif
+#ifndef EQ_DECW_MIN_CTAS
+#define EQ_DECW_MIN_CTAS (EQ_WRING >= 128 ? 4 : 6)
+#endif
+constexpr int kWThreads = EQ_WTHREADS;
+constexpr uint32_t kDecWSmem = kWThreads * kWRing;          // dynamic: the staging rings
+
+template <bool BF16>
+__global__ void __launch_bounds__(kWThreads, EQ_DECW_MIN_CTAS)
+k_decode_w(const __grid_constant__ DecParams P) {
+    extern __shared__ __align__(128) uint8_t rings[];      // kWThreads × kWRing
+    __shared__ __align__(16) uint32_t lut[kM];
+    __shared__ uint32_t cum[257];
+
+    uint32_t bi = 0;
+    while (bi + 1 < P.n_blocks && blockIdx.x >= P.b[bi + 1].cta0) ++bi;
+    const DecBlock& B = P.b[bi];
+    const int t = threadIdx.x;
+
+    ChainW c;                   // setup first: the initial cp.async copies overlap the table build
+    chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kWThreads + t,
+                        (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
+    stage_commit();
+    if (!build_lut<EQ_WENTRY, kWThreads>(B, lut, cum, P.err)) {
+        stage_wait_all();
+        return;
+    }
+    stage_wait_all();
+    __syncthreads();
+    DecTable T;
+    T.k2p20 = P.k2p20;
+    T.k2p12 = P.k2p12;
+    T.kneg2p14 = P.kneg2p14;
+    T.k4 = P.k4;
+    T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
+    T.lutp = lut;
+    T.f0 = cum[1];
+    T.ez = (T.f0 - 1) << 8;
+
+    chain_start_w(c);
+    chain_finish_w<BF16>(c, B.payload, T);
+    stage_wait_all();
+    // integrity: final state L and every payload byte of the chunk consumed exactly
+    if (c.active && (c.runaway || c.x != kLw || c.r.q - 2u != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
+}
+
 }  // namespace eq
 
 using namespace eq;
@@ -377,7 +543,9 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     d.scales = blk.scales;
     d.payload_bytes = blk.payload_bytes;
     if (blk.format > EQ_FMT_INT8) return EQ_ERR_ARG;
+    if (blk.codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
     d.format = blk.format;
+    d.codec = blk.codec;
     d.cs = blk.chunk_symbols;
     d.n_layers = blk.n_layers;
     d.cta0 = cta0;
@@ -412,6 +580,9 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
     std::unique_ptr<uint64_t[]> all(new uint64_t[(size_t)n_blocks * EQ_MAX_LAYERS]);
     EQ_TRY(eq_arena_layout(blocks, n_blocks, out_dtype, all.get(), &total));
     if (arena_bytes < total) return EQ_ERR_BUFFER;
+    const uint32_t codec = blocks[0].codec;
+    for (uint32_t b = 1; b < n_blocks; ++b)
+        if (blocks[b].codec != codec) return EQ_ERR_ARG;       // one codec per call
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     for (uint32_t b0 = 0; b0 < n_blocks; b0 += kMaxDecBlocks) {
         const uint32_t nb = std::min<uint32_t>(kMaxDecBlocks, n_blocks - b0);
@@ -427,13 +598,27 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
         uint32_t ctas = 0;
         for (uint32_t k = 0; k < nb; ++k) {
             EQ_TRY(fill_desc(blocks[b0 + k], all.get() + (size_t)(b0 + k) * EQ_MAX_LAYERS, P.b[k], ctas));
-            ctas += (P.b[k].n_chunks + kChunksPerCta - 1) / kChunksPerCta;
+            const uint32_t per = codec == EQ_CODEC_WORD ? (uint32_t)kWThreads : (uint32_t)kChunksPerCta;
+            ctas += (P.b[k].n_chunks + per - 1) / per;
         }
         // blocks with zero chunks cannot exist (layers are non-empty); ctas > 0
-        if (out_dtype == EQ_OUT_BF16)
+        if (codec == EQ_CODEC_WORD) {
+            static bool attr_set[2] = {false, false};
+            const int bi = out_dtype == EQ_OUT_BF16 ? 1 : 0;
+            if (!attr_set[bi]) {
+                EQ_CUDA_TRY(cudaFuncSetAttribute(bi ? (const void*)k_decode_w<true> : (const void*)k_decode_w<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecWSmem));
+                attr_set[bi] = true;
+            }
+            if (bi)
+                k_decode_w<true><<<ctas, kWThreads, kDecWSmem, st>>>(P);
+            else
+                k_decode_w<false><<<ctas, kWThreads, kDecWSmem, st>>>(P);
+        } else if (out_dtype == EQ_OUT_BF16) {
             k_decode<true><<<ctas, kDecThreads, 0, st>>>(P);
-        else
+        } else {
             k_decode<false><<<ctas, kDecThreads, 0, st>>>(P);
+        }
         EQ_CUDA_TRY(cudaGetLastError());
     }
     return EQ_OK;

@@ -1,9 +1,10 @@
-// rans_enc.cu — §8(a) row a6: per-chunk byte-wise rANS encoding (Alg. 1 l.4-5, P:212-213;
+// rans_enc.cu — §8(a) row a6: per-chunk rANS encoding (Alg. 1 l.4-5, P:212-213;
 // S:316-324) of the block's concatenated E4M3 symbol stream (App. A.1).
-// Wire format (R9): 32-bit state, L = 2^23, M = 2^12, cum in code order; per chunk the
-// symbols are coded in reverse from x = L, bytes emitted while x ≥ ((L>>12)<<8)·f; the
-// final state is stored first (little-endian), followed by the renormalisation bytes in
-// decode order.  Chunks of cs symbols restart at each layer start (R10).
+// Wire formats: 32-bit state, M = 2^12, cum in code order; per chunk the symbols are coded
+// in reverse from x = L, units of b emitted while x ≥ ((L>>12)·b)·f; the final state is
+// stored first (little-endian), followed by the units in decode order.
+//   EQ_CODEC_BYTE (R9):  L = 2^23, b = 2^8;   EQ_CODEC_WORD (R14): L = 2^16, b = 2^16 (LE).
+// Chunks of cs symbols restart at each layer start (R10).
 //
 // Two passes, one thread per chunk: (1) exact byte count per chunk, (2) exclusive scan
 // into chunk offsets, (3) encode again writing back-to-front straight into the final
@@ -60,7 +61,7 @@ __device__ __forceinline__ void load_table(const EncParams& P, uint32_t* sf, uin
     __syncthreads();
 }
 
-template <bool WRITE>
+template <bool WRITE, bool WORD>
 __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ EncParams P) {
     __shared__ uint32_t sf[256], scum[256];
     load_table(P, sf, scum);
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
         }
         dst = P.payload + end;
     }
-    uint32_t x = kL, bytes = 0;
+    uint32_t x = WORD ? kLw : kL, bytes = 0;
     for (int64_t i = (int64_t)n - 1; i >= 0; --i) {
         const uint32_t s = sym[i];
         const uint32_t f = sf[s];
@@ -89,11 +90,24 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
             atomicOr(P.err, EQ_EF_UNKNOWN_SYMBOL);
             break;
         }
-        const uint32_t x_max = ((kL >> kProbBits) << 8) * f;
-        while (x >= x_max) {
-            if (WRITE) *--dst = (uint8_t)(x & 0xFFu);
-            ++bytes;
-            x >>= 8;
+        if (WORD) {
+            // x_max = 2^20·f ≤ 2^32: at most one word (x < 2^32 → x >> 16 < 2^16 ≤ 2^20·f)
+            if ((uint64_t)x >= ((uint64_t)(kLw >> kProbBits) << 16) * f) {
+                if (WRITE) {
+                    dst -= 2;
+                    dst[0] = (uint8_t)(x & 0xFFu);
+                    dst[1] = (uint8_t)((x >> 8) & 0xFFu);
+                }
+                bytes += 2;
+                x >>= 16;
+            }
+        } else {
+            const uint32_t x_max = ((kL >> kProbBits) << 8) * f;
+            while (x >= x_max) {
+                if (WRITE) *--dst = (uint8_t)(x & 0xFFu);
+                ++bytes;
+                x >>= 8;
+            }
         }
         x = (x / f) * kM + (x % f) + scum[s];
     }
@@ -153,6 +167,7 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     if (!blk->payload || !blk->chunk_off || !blk->freq) return EQ_ERR_ARG;
     if (blk->n_layers == 0 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (blk->chunk_symbols == 0 || blk->chunk_symbols > 262144u) return EQ_ERR_ARG;
+    if (blk->codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
     EncParams P;
     memset(&P, 0, sizeof(P));
     P.codes = codes;
@@ -181,9 +196,15 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     P.n_chunks = chunk;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g = (chunk + kEncThreads - 1) / kEncThreads;
-    k_encode<false><<<g, kEncThreads, 0, st>>>(P);
-    k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
-    k_encode<true><<<g, kEncThreads, 0, st>>>(P);
+    if (blk->codec == EQ_CODEC_WORD) {
+        k_encode<false, true><<<g, kEncThreads, 0, st>>>(P);
+        k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
+        k_encode<true, true><<<g, kEncThreads, 0, st>>>(P);
+    } else {
+        k_encode<false, false><<<g, kEncThreads, 0, st>>>(P);
+        k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
+        k_encode<true, false><<<g, kEncThreads, 0, st>>>(P);
+    }
     EQ_CUDA_TRY(cudaGetLastError());
     return EQ_OK;
 }

@@ -80,3 +80,35 @@ def test_product_never_imports_oracle():
                 src = open(os.path.join(dp, f)).read()
                 for pat in ("import oracle", "from oracle", "liboracle", "eq_oracle", "eqo_"):
                     assert pat not in src, (f, pat)
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of eq_params / eq_block / eq_lbfgs_params have the C layout
+    (sizes and every field offset, from a gcc-compiled probe of include/entquant.h)."""
+    import subprocess
+    structs = {"eq_params": eq.eq_params, "eq_block": eq.eq_block, "eq_lbfgs_params": eq.eq_lbfgs_params,
+               "eq_tensor": eq.eq_tensor}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "entquant.h"', 'int main(void) {']
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            cf = "lambda" if f == "lambda_" else f
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {cf}));')
+    lines.append("return 0; }")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = dict(l.split() for l in subprocess.check_output([str(exe)]).decode().splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, f"{name}.{f}"
+
+
+def test_codec_parameter_validated(lib):
+    t = (eq.eq_tensor * 1)(eq.eq_tensor(1, 64, 64))
+    p = eq._params(codec=eq.EQ_CODEC_WORD)
+    assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == 0
+    p.codec = 2
+    assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == eq.EQ_ERR_ARG
