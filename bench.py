@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--no-fp8", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
-    ap.add_argument("--codec", default="byte", choices=["byte", "word"],
+    ap.add_argument("--codec", default="word", choices=["byte", "word"],
                     help="rANS renormalisation: byte (SPEC S:355, R9) or 16-bit word (R14)")
     return ap.parse_args()
 
@@ -164,12 +164,12 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
-def traffic_from_profiles(kind: str):
+def traffic_from_profiles(codec: str, kind: str):
     """dram bytes per launch of the decode kernel from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
     try:
         d = json.load(open(p))
-        return d[kind]["dram_bytes_per_launch"]
+        return d[codec][kind]["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -353,7 +353,7 @@ def main():
         l8 = statistics.mean(per8)
         fp8 = {"value": shard.aggregate_gbs(bytes_fp8, world, args.steps, t8), "unit": "GB/s",
                "ms_per_step": t8 / args.steps, "frac": bytes_fp8 / (l8 / 1e3) / 1e9 / peak,
-               "traffic": traffic_from_profiles("fp8")}
+               "traffic": traffic_from_profiles(args.codec, "fp8")}
         del dec8
         torch.cuda.empty_cache()
     else:
@@ -397,7 +397,7 @@ def main():
             "data": "synthetic (eqsynth: Student-t nu=4, sigma=0.02, per-row log-normal spread; Llama shapes)",
             "config": workload_config(args, n_params, lam),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic_from_profiles("bf16"),
+                         "frac": achieved / peak, "traffic": traffic_from_profiles(args.codec, "bf16"),
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bytes_bf16, "launch_ms": launch_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": cs,

@@ -116,6 +116,10 @@ struct DecTable {
     uint32_t f0;           // frequency of code 0x00
     uint32_t ez;           // (f0 − 1) << 8
     const uint32_t* lutp;  // the LUT (shared array; EQ_WADDR = 1 addressing)
+    uint32_t zlim;         // lut_s + 4·f0: LUT addresses below it belong to code 0x00
+    uint32_t zk;           // (f0 − 1) << 20 − 64·lut_s: entry of code 0x00 = 64·address + zk
+    uint32_t k64;          // 64 (runtime, keeps the IMAD on the FMA pipe)
+    uint32_t k2p16;        // 2^16 (runtime, EQ_WMERGE = 1)
 };
 
 // One rANS decode step (Alg. 2 l.1): slot lookup, state update, byte renormalisation.
@@ -202,8 +206,19 @@ __device__ __forceinline__ void st_out(uint4* p, uint4 v) { __stcs(p, v); }
 #endif
 // 32 bytes per lane in one STG.256 (sm_100): half the store instructions and L1 wavefronts
 // of two STG.128 to the same per-lane line
+#ifndef EQ_STPOL
+#define EQ_STPOL 2       // output store L2 policy: 0 default, 1 evict_last hint, 2 evict_first hint (default:
+                         // decoded lines leave L2 first, the compressed input stays — DRAM reads 4.55 → 2.37 GB)
+#endif
 __device__ __forceinline__ void st_out32(void* p, uint4 a, uint4 b) {
-#if EQ_ST256 && EQ_L2HINT
+#if EQ_ST256 && EQ_STPOL
+    uint64_t pol;
+    if (EQ_STPOL == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
+                 "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "l"(pol)
+                 : "memory");
+#elif EQ_ST256 && EQ_L2HINT
     asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
                  "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                  : "memory");
@@ -307,24 +322,26 @@ __device__ __forceinline__ void store16_bf16_at(C& c, const uint32_t q[4], uint8
 // and (x << 16) ≥ 2^20 ≥ L), so the lane keeps no bit window: it holds the next unconsumed
 // word `w` in a register (prefetched from its shared-memory ring as soon as the previous one
 // is consumed, off the state's dependency chain) and renormalises with one predicated PRMT.
-#ifndef EQ_WRING
-#define EQ_WRING 64                 // bytes of staging ring per chunk (64 or 128; 64 measured faster:
-#endif                              // 6 CTAs/SM instead of 4)
-constexpr uint32_t kWRing = EQ_WRING;
-// Staging schedule: one 16-byte segment at most per 8-step boundary (a lane consumes at
-// most 8 words = 16 bytes per 8 steps, so the stage front keeps pace; right after the
-// initial fill it may trail its target gs·16 > q + kWRing − 16 by one segment, never more).
-// Hence every staged segment starts > q + kWRing − 48 when issued, the next 8 steps read
-// only [q, q + 16), and a segment issued k boundaries ago is not needed while
-// 16k ≤ kWRing − 64: cp.async groups (one per boundary) allowed in flight =
-// (kWRing − 64)/16 − 1 → 3 for a 128-byte ring, 0 (wait for all) for a 64-byte one.
-constexpr int kWWait = kWRing >= 128 ? 3 : 0;
+// Per-chunk staging ring: 64 bytes, filled 16 bytes at a time by cp.async.  Schedule: at
+// most one 16-byte segment per 8-step boundary (a lane consumes at most 8 words = 16 bytes
+// per 8 steps, so the stage front keeps pace; right after the initial fill it may trail
+// its target by one segment, never more).  Every staged segment then starts > q + 16 when
+// issued, the next 8 steps read only [q, q + 18), so waiting for all groups at each boundary
+// (before issuing) never waits for data issued at that boundary.
+// (Measured alternatives: a 128-byte ring with 3 groups in flight — 4 instead of 6 CTAs/SM,
+// −4 %; whole 32-byte sectors every 16 steps — the 2-slot ring then has to wait for the
+// sector it just issued, −10 %.)
+constexpr uint32_t kWRing = 64;
+// Ring addressing: payload byte p lives at ring | ((p + kWBias) & 63), and the reader keeps
+// Q = (payload offset of the next word) + kWBias, so a word address is one LOP3 and the test
+// "slot of segment gn is free" (all bytes < gn − 48 consumed: gn ≤ q + 48) is gn ≤ Q.
+constexpr uint32_t kWBias = kWRing - 16;
 
 struct WordReader {
-    uint32_t q;            // payload byte offset of the next word to load into w
+    uint32_t Q;            // payload byte offset of the next word to load into w, + kWBias
     uint32_t w;            // the next unconsumed 16-bit word (low half)
-    uint32_t gs;           // next 16-byte payload segment to stage
-    uint32_t ring;         // shared address of this chunk's ring (kWRing-aligned)
+    uint32_t gn;           // payload byte offset of the next 16-byte segment to stage
+    uint32_t ring;         // shared address of this chunk's ring (64-byte aligned)
 };
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
@@ -333,22 +350,30 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ void stage_segment_w(uint32_t ring, const uint8_t* payload, uint32_t seg) {
-    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(ring | ((seg * 16u) & (kWRing - 1))),
-                 "l"(payload + (uint64_t)seg * 16));
-}
-template <int N>
-__device__ __forceinline__ void stage_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Every 8 steps, after stage_wait_n<kWWait>: stage the next segment if the ring slot it
-// overwrites holds only bytes before the reader (gs·16 ≤ q + kWRing − 16).
-__device__ __forceinline__ void ring_issue_w(WordReader& r, const uint8_t* payload) {
-    if (r.gs * 16u <= r.q + (kWRing - 16u)) {
-        stage_segment_w(r.ring, payload, r.gs);
-        ++r.gs;
-    }
+// initial fill: one 16-byte segment (g multiple of 16) into its slot
+__device__ __forceinline__ void stage_segment_w(uint32_t ring, const uint8_t* payload, uint32_t g) {
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(ring | ((g + kWBias) & (kWRing - 1))),
+                 "l"(payload + g));
 }
 
+// Every 8 steps: wait for all staged segments, then stage segment gn if its slot is free
+// (predicated, no branch), one cp.async group per boundary.
+__device__ __forceinline__ void ring_step_w(WordReader& r, const uint8_t* payload) {
+    asm volatile("cp.async.wait_all;\n\t"
+                 "{ .reg .pred p; setp.le.u32 p, %0, %1;\n\t"
+                 "@p cp.async.cg.shared.global.L2::128B [%2], [%3], 16;\n\t"
+                 "@p add.u32 %0, %0, 16; }\n\t"
+                 "cp.async.commit_group;"
+                 : "+r"(r.gn) : "r"(r.Q), "r"(r.ring | ((r.gn + kWBias) & (kWRing - 1))), "l"(payload + r.gn)
+                 : "memory");
+}
+
+#ifndef EQ_WMERGE
+#define EQ_WMERGE 0      // renormalisation merge: 0 = PRMT (ALU pipe), 1 = IMAD (FMA pipe)
+#endif
+#ifndef EQ_WZERO
+#define EQ_WZERO 0       // 1: code 0x00 decoded without the shared-memory LUT (measured slower)
+#endif
 #ifndef EQ_WADDR
 #define EQ_WADDR 0       // LUT address: 0 = 4x − 2^14·xs + base (3 IMADs deep), 1 = (4x & 0x3FFC) + base
 #endif
@@ -360,7 +385,15 @@ __device__ __forceinline__ void ring_issue_w(WordReader& r, const uint8_t* paylo
 // if x < 2^16: x = (x << 16) | w as one PRMT, and the next word is prefetched.
 __device__ __forceinline__ uint32_t decode_one_w(uint32_t& x, WordReader& r, const DecTable& T) {
     const uint32_t xs = mad_hi(x, T.k2p20, 0u);                         // x >> 12
-#if EQ_WADDR
+#if EQ_WZERO
+    // code 0x00 (cum 0, the most frequent symbol) owns slots [0, f0): its entry
+    // (f0−1) << 20 | slot << 8 is computed, so only the other lanes access shared memory
+    // (fewer random-slot bank conflicts per warp-wide lookup)
+    const uint32_t la = mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s));
+    uint32_t e;
+    if (la < T.zlim) e = la * 64u + T.zk;
+    else e = lds_u32(la);
+#elif EQ_WADDR
     const uint32_t e = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(T.lutp) +
                                                           (mad_lo(x, T.k4, 0u) & 0x3FFCu));
 #else
@@ -374,9 +407,13 @@ __device__ __forceinline__ uint32_t decode_one_w(uint32_t& x, WordReader& r, con
     x = mad_lo(fm1, xs, xs + (e >> 20));                                // f·⌊x/M⌋ + slot − c (LEA.HI)
 #endif
     if (x < kLw) {
-        x = __byte_perm(r.w, x, 0x5410);                                // (x << 16) | w
-        r.w = lds_u16(r.ring | (r.q & (kWRing - 1)));
-        r.q += 2;
+#if EQ_WMERGE
+        x = mad_lo(x, T.k2p16, r.w);                                    // (x << 16) | w (FMA pipe)
+#else
+        x = __byte_perm(r.w, x, 0x5410);                                // (x << 16) | w (one PRMT)
+#endif
+        r.w = lds_u16(r.ring | (r.Q & (kWRing - 1)));
+        r.Q += 2;
     }
     return e;
 }

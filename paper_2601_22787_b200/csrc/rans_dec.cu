@@ -60,7 +60,7 @@ struct DecParams {
     uint32_t pad;
     // multipliers passed at run time so ptxas keeps IMAD / IMAD.HI (FMA pipe) instead of
     // strength-reducing them to LEA / SHF on the (binding) integer ALU pipe
-    uint32_t k2p20, k2p12, kneg2p14, k4;
+    uint32_t k2p20, k2p12, kneg2p14, k4, k64, k2p16;
     DecBlock b[kMaxDecBlocks];
 };
 
@@ -382,10 +382,10 @@ __device__ __forceinline__ void chain_setup_w(ChainW& c, const DecBlock& B, uint
     c.a = a;
     c.e = e;
     c.r.ring = ring;
-    const uint32_t s0 = a >> 4;
+    const uint32_t g0 = a & ~15u;
     #pragma unroll
-    for (uint32_t q = 0; q < kWRing / 16; ++q) stage_segment_w(ring, B.payload, s0 + q);
-    c.r.gs = s0 + kWRing / 16;
+    for (uint32_t q = 0; q < kWRing / 16; ++q) stage_segment_w(ring, B.payload, g0 + 16 * q);
+    c.r.gn = g0 + kWRing;
     c.out = arena + Ly.out_off + sym0 * (BF16 ? 2 : 1);
     c.sc = B.scales + Ly.scale_off;
     c.cols = Ly.cols;
@@ -400,17 +400,12 @@ __device__ __forceinline__ void chain_setup_w(ChainW& c, const DecBlock& B, uint
 // after the initial segments landed: 4-byte little-endian state, then the first word
 __device__ __forceinline__ void chain_start_w(ChainW& c) {
     if (!c.active) return;
-    const uint32_t m = kWRing - 1;
-    c.x = lds_u16(c.r.ring | (c.a & m)) | (lds_u16(c.r.ring | ((c.a + 2) & m)) << 16);
-    c.r.w = lds_u16(c.r.ring | ((c.a + 4) & m));
-    c.r.q = c.a + 6;
+    const uint32_t m = kWRing - 1, A = c.a + kWBias;
+    c.x = lds_u16(c.r.ring | (A & m)) | (lds_u16(c.r.ring | ((A + 2) & m)) << 16);
+    c.r.w = lds_u16(c.r.ring | ((A + 4) & m));
+    c.r.Q = A + 6;
 }
 
-__device__ __forceinline__ void ring_step_w(ChainW& c, const uint8_t* payload) {
-    stage_wait_n<kWWait>();
-    ring_issue_w(c.r, payload);
-    stage_commit();
-}
 
 template <bool BF16>
 __device__ __forceinline__ void chain_finish_w(ChainW& c, const uint8_t* payload, const DecTable& T) {
@@ -422,34 +417,34 @@ __device__ __forceinline__ void chain_finish_w(ChainW& c, const uint8_t* payload
                 uint32_t q[4];
                 q[0] = decode4_w(c, T);
                 q[1] = decode4_w(c, T);
-                ring_step_w(c, payload);
+                ring_step_w(c.r, payload);
                 q[2] = decode4_w(c, T);
                 q[3] = decode4_w(c, T);
-                ring_step_w(c, payload);
+                ring_step_w(c.r, payload);
                 store16_bf16(c, q);
             } else {
                 uint32_t q[8];
                 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     q[k] = decode4_w(c, T);
-                    if (k & 1) ring_step_w(c, payload);
+                    if (k & 1) ring_step_w(c.r, payload);
                 }
                 st_out32(c.out + c.i, make_uint4(q[0], q[1], q[2], q[3]), make_uint4(q[4], q[5], q[6], q[7]));
             }
             c.i += G;
-            if (c.r.q > c.e + 2) { c.runaway = true; return; }
+            if (c.r.Q > c.e + (2 + kWBias)) { c.runaway = true; return; }
         }
     }
     for (; c.i < c.n; ++c.i) {                  // generic / ragged tail: one symbol at a time
         const uint32_t sym = decode_one_w(c.x, c.r, T) & 0xFFu;
-        if ((c.i & 7) == 7) ring_step_w(c, payload);
+        if ((c.i & 7) == 7) ring_step_w(c.r, payload);
         store_one<BF16>(c.out, c.i, sym, c.s, c.i8);
         if (BF16 && ++c.col == c.cols) {
             c.col = 0;
             ++c.row;
             if (c.i + 1 < c.n) c.s = bf16_bits_to_float(c.sc[c.row]);
         }
-        if (c.r.q > c.e + 2) { c.runaway = true; return; }
+        if (c.r.Q > c.e + (2 + kWBias)) { c.runaway = true; return; }
     }
 }
 
@@ -457,15 +452,17 @@ __device__ __forceinline__ void chain_finish_w(ChainW& c, const uint8_t* payload
 #define EQ_WTHREADS 256             // chunks (= threads) per CTA of k_decode_w
 #endif
 #ifndef EQ_DECW_MIN_CTAS
-#define EQ_DECW_MIN_CTAS (EQ_WRING >= 128 ? 4 : 6)
+#define EQ_DECW_MIN_CTAS 6          // 40 registers; 6 × (16 KB ring + 17 KB LUT) of shared memory
 #endif
 constexpr int kWThreads = EQ_WTHREADS;
-constexpr uint32_t kDecWSmem = kWThreads * kWRing;          // dynamic: the staging rings
+constexpr int kWChains = 1;         // chunks per thread (2, interleaved for ILP, measured slower)
+constexpr int kWChunksPerCta = kWThreads * kWChains;
+constexpr uint32_t kDecWSmem = kWChunksPerCta * kWRing;     // dynamic: the staging rings
 
 template <bool BF16>
 __global__ void __launch_bounds__(kWThreads, EQ_DECW_MIN_CTAS)
 k_decode_w(const __grid_constant__ DecParams P) {
-    extern __shared__ __align__(128) uint8_t rings[];      // kWThreads × kWRing
+    extern __shared__ __align__(128) uint8_t rings[];      // kWChunksPerCta × kWRing
     __shared__ __align__(16) uint32_t lut[kM];
     __shared__ uint32_t cum[257];
 
@@ -474,9 +471,13 @@ k_decode_w(const __grid_constant__ DecParams P) {
     const DecBlock& B = P.b[bi];
     const int t = threadIdx.x;
 
-    ChainW c;                   // setup first: the initial cp.async copies overlap the table build
-    chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kWThreads + t,
-                        (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
+    ChainW ch[kWChains];        // setup first: the initial cp.async copies overlap the table build
+    #pragma unroll
+    for (int j = 0; j < kWChains; ++j) {
+        const uint32_t slot = (uint32_t)(j * kWThreads + t);
+        chain_setup_w<BF16>(ch[j], B, (blockIdx.x - B.cta0) * kWChunksPerCta + slot,
+                            (uint32_t)__cvta_generic_to_shared(rings + slot * kWRing), P.arena, P.err);
+    }
     stage_commit();
     if (!build_lut<EQ_WENTRY, kWThreads>(B, lut, cum, P.err)) {
         stage_wait_all();
@@ -493,12 +494,26 @@ k_decode_w(const __grid_constant__ DecParams P) {
     T.lutp = lut;
     T.f0 = cum[1];
     T.ez = (T.f0 - 1) << 8;
+    T.zlim = T.lut_s + 4u * T.f0;
+    T.zk = ((T.f0 - 1) << 20) - 64u * T.lut_s;
+    T.k64 = P.k64;
+    T.k2p16 = P.k2p16;
 
-    chain_start_w(c);
-    chain_finish_w<BF16>(c, B.payload, T);
+    #pragma unroll
+    for (int j = 0; j < kWChains; ++j) chain_start_w(ch[j]);
+    // each chain (one per thread) to its end: 16-symbol groups, then a ragged tail
+    #pragma unroll
+    for (int j = 0; j < kWChains; ++j) {
+        if (ch[j].active && ch[j].r.Q > ch[j].e + (2 + kWBias)) ch[j].runaway = true;
+        chain_finish_w<BF16>(ch[j], B.payload, T);
+    }
     stage_wait_all();
     // integrity: final state L and every payload byte of the chunk consumed exactly
-    if (c.active && (c.runaway || c.x != kLw || c.r.q - 2u != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
+    #pragma unroll
+    for (int j = 0; j < kWChains; ++j) {
+        const ChainW& c = ch[j];
+        if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
+    }
 }
 
 }  // namespace eq
@@ -595,10 +610,12 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
         P.k2p12 = 1u << 12;
         P.kneg2p14 = 0u - (1u << 14);
         P.k4 = 4u;
+        P.k64 = 64u;
+        P.k2p16 = 1u << 16;
         uint32_t ctas = 0;
         for (uint32_t k = 0; k < nb; ++k) {
             EQ_TRY(fill_desc(blocks[b0 + k], all.get() + (size_t)(b0 + k) * EQ_MAX_LAYERS, P.b[k], ctas));
-            const uint32_t per = codec == EQ_CODEC_WORD ? (uint32_t)kWThreads : (uint32_t)kChunksPerCta;
+            const uint32_t per = codec == EQ_CODEC_WORD ? (uint32_t)kWChunksPerCta : (uint32_t)kChunksPerCta;
             ctas += (P.b[k].n_chunks + per - 1) / per;
         }
         // blocks with zero chunks cannot exist (layers are non-empty); ctas > 0

@@ -30,17 +30,24 @@ def main(ev, rnd):
     os.makedirs(out_dir, exist_ok=True)
     full = json.load(open(os.path.join(ev, "summary.json")))
     shutil.copy(os.path.join(ev, "summary.json"), os.path.join(out_dir, "ncu_decode_full.json"))
-    summ = {"source": f"profiles/{rnd}/ncu_decode_full.json (ncu --set full --clock-control none, "
-                      "bench.py --profile --steps 1 --warmup 1: 32 blocks, lambda 230.2)"}
+    sp = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
+    summ = json.load(open(sp)) if os.path.exists(sp) else {}
+    if "bf16" in summ:                       # old flat layout (byte codec only)
+        summ = {"byte": {k: summ.pop(k) for k in ("bf16", "fp8", "source") if k in summ}}
     for d in full:
-        key = "bf16" if "k_decode<1>" in d["kernel"] else "fp8" if "k_decode<0>" in d["kernel"] else None
-        if key is None:
+        k = d["kernel"]
+        codec = "word" if "k_decode_w" in k else "byte" if "k_decode" in k else None
+        kind = "bf16" if "<1>" in k or "<(bool)1>" in k else "fp8" if "<0>" in k or "<(bool)0>" in k else None
+        if codec is None or kind is None:
             continue
         rd, wr = _num(d["dram__bytes_read.sum"]), _num(d["dram__bytes_write.sum"])
-        summ[key] = {"kernel": d["kernel"], "duration_ms_under_ncu": _num(d["gpu__time_duration.sum"]),
-                     "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                     "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")}
-    json.dump(summ, open(os.path.join(ROOT, "profiles", "ncu_decode_summary.json"), "w"), indent=1)
+        summ.setdefault(codec, {})["source"] = (
+            f"profiles/{rnd}/ncu_decode_full.json (ncu --set full --clock-control none, bench.py --profile "
+            f"--steps 1 --warmup 1 --codec {codec}: 32 blocks, lambda 230.2)")
+        summ[codec][kind] = {"kernel": k, "duration_ms_under_ncu": _num(d["gpu__time_duration.sum"]),
+                             "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                             "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")}
+    json.dump(summ, open(sp, "w"), indent=1)
 
     # launch list: "ID",...,"Kernel Name",...,"Metric Value"
     rows = []
@@ -58,14 +65,15 @@ def main(ev, rnd):
         w.writerow(["kernel", "launches", "total_us", "share_of_command", "mean_us"])
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
             w.writerow([k, len(v), round(sum(v), 1), round(sum(v) / tot, 5), round(sum(v) / len(v), 1)])
-    dec = {k: v for k, v in per.items() if "k_decode<1>" in k}
+    dec = {k: v for k, v in per.items() if "k_decode" in k and "<1>" in k}
     json.dump({"command": "python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --lam 230.2 "
                           "(ncu --metrics gpu__time_duration.sum --clock-control none)",
                "timed_step_kernels": {k: {"launches": len(v), "mean_us": sum(v) / len(v)} for k, v in dec.items()},
                "decode_share_of_timed_step": 1.0,
                "note": "cold-cache, serialised per-launch times; the timed step (one eq_decode_dequant of the "
-                       "32-block layer set) launches exactly one k_decode<1> kernel, so its share of the step "
-                       "is 1.0 in both the bench and the launch list"},
+                       "32-block layer set) launches exactly one decode kernel (k_decode_w<1> for the word codec, "
+                       "k_decode<1> for the byte codec), so its share of the step is 1.0 in both the bench and "
+                       "the launch list"},
               open(os.path.join(out_dir, "launches_decode.json"), "w"), indent=1)
     print(json.dumps(summ, indent=1))
 
