@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #ifndef EQ_QMM_MIN_CTAS
 #define EQ_QMM_MIN_CTAS 3
@@ -77,7 +78,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ uint4 dequant8(const Chain& c, uint32_t q0, uint32_t q1) {
+template <class C>
+__device__ __forceinline__ uint4 dequant8(const C& c, uint32_t q0, uint32_t q1) {
     if (c.i8)
         return make_uint4(dequant2_i8(q0, c.s), dequant2_i8(q0 >> 16, c.s), dequant2_i8(q1, c.s),
                           dequant2_i8(q1 >> 16, c.s));
@@ -102,6 +104,53 @@ __device__ __forceinline__ void decode_step(Chain& c, const DecTable& T, const u
         v[2 * g + 1] = dequant8(c, q2, q3);
     }
     c.i += 64;
+}
+
+// EQ_CODEC_WORD: the same 64 symbols with word renormalisation (decode_one_w)
+__device__ __forceinline__ void decode_step(ChainW& c, const DecTable& T, const uint8_t* payload, uint4 v[8]) {
+    #pragma unroll
+    for (int g = 0; g < 4; ++g) {                       // 4 × 16 symbols
+        const uint32_t q0 = decode4_w(c, T);
+        const uint32_t q1 = decode4_w(c, T);
+        ring_step_w(c.r, payload);
+        const uint32_t q2 = decode4_w(c, T);
+        const uint32_t q3 = decode4_w(c, T);
+        ring_step_w(c.r, payload);
+        v[2 * g] = dequant8(c, q0, q1);
+        v[2 * g + 1] = dequant8(c, q2, q3);
+    }
+    c.i += 64;
+}
+
+__device__ __forceinline__ bool chunk_begin(ChainW& c, const QmmParams& P, uint32_t chunk, uint32_t ring) {
+    c.i = 0;
+    c.n = P.cs;
+    c.runaway = false;
+    const uint32_t a = __ldg(P.off + chunk), e = __ldg(P.off + chunk + 1);
+    if (e < a || (uint64_t)e > P.payload_bytes || e - a < 4) {
+        atomicOr(P.err, EQ_EF_TRUNCATED);
+        c.active = false;
+        return false;
+    }
+    c.active = true;
+    c.a = a;
+    c.e = e;
+    c.r.ring = ring;
+    const uint32_t g0 = a & ~15u;
+    #pragma unroll
+    for (uint32_t q = 0; q < kWRing / 16; ++q) stage_segment_w(ring, P.payload, g0 + 16 * q);
+    c.r.gn = g0 + kWRing;
+    stage_commit();
+    stage_wait_all();
+    const uint32_t m = kWRing - 1, A = a + kWBias;
+    c.x = lds_u16(ring | (A & m)) | (lds_u16(ring | ((A + 2) & m)) << 16);
+    c.r.w = lds_u16(ring | ((A + 4) & m));
+    c.r.Q = A + 6;
+    return true;
+}
+
+__device__ __forceinline__ void chunk_end(const ChainW& c, uint32_t* err) {
+    if (c.active && (c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(err, EQ_EF_CORRUPT);
 }
 
 // start decoding chunk `chunk` (payload bytes, ring staging, first state) for this lane
@@ -150,6 +199,8 @@ __device__ __forceinline__ void chunk_end(const Chain& c, uint32_t* err) {
 // chunk of row 128·(2p+h)+r — cs columns [j·cs, (j+1)·cs) — and each half accumulates that
 // K-slice of its 128 × batch output in its own TMEM columns.  Every CTA does the same work
 // (one chunk per lane), so one grouped launch over all GEMMs of a block fills the GPU evenly.
+static_assert(EQ_WENTRY == 1, "k_qmatmul<true> builds the LUT in decode_one_w's entry layout");
+template <bool WORD>
 __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __grid_constant__ QmmParams P) {
     extern __shared__ __align__(1024) uint8_t dsm_raw[];
     // SWIZZLE_128B atoms are addressed by absolute shared-address bits: align the carve-out
@@ -214,7 +265,9 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
                 if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
             }
             uint32_t fs = cum[lo + 1] - cum[lo];
-            lut[slot] = (uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20);
+            // decode_one_w reads the (f−1)-on-top layout (EQ_WENTRY 1), decode_one the other
+            lut[slot] = WORD ? ((uint32_t)lo | (((uint32_t)slot - cum[lo]) << 8) | ((fs - 1) << 20))
+                             : ((uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20));
         }
     } else if (t == 0) {
         atomicOr(P.err, EQ_EF_CORRUPT);
@@ -234,7 +287,7 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
     // ---- this lane's row and chunk
     const uint32_t grow = (kTiles * pair + h) * kTileRows + r;
     const uint32_t ring = smem_u32(rings + t * kRingWords);
-    Chain c;
+    typename std::conditional<WORD, ChainW, Chain>::type c;
     c.sc = J.scales;
     c.i8 = P.format == EQ_FMT_INT8;
     c.active = false;
@@ -355,7 +408,7 @@ static eq_status qmm_validate(const eq_block* blk, uint32_t n_jobs, const uint32
                               QmmPlan* plan) {
     if (!blk || !layers || n_jobs < 1 || n_jobs > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (!blk->payload || !blk->chunk_off || !blk->freq || !blk->scales || blk->format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if (blk->codec != EQ_CODEC_BYTE) return EQ_ERR_ARG;
+    if (blk->codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
     if (blk->n_layers < 1 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(blk->payload) & 15) != 0) return EQ_ERR_ARG;
     if (blk->payload_cap < blk->payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;
@@ -464,8 +517,13 @@ extern "C" eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, cons
     P.k4 = 4u;
     const uint32_t b_tile = ((P.n_pad * 128u + 1023u) & ~1023u);
     const size_t smem = kTiles * kATile + b_tile + kM * 4 + kQThreads * kRingWords * 4 + 32 + 8 + 8 + 1024;
-    EQ_CUDA_TRY(cudaFuncSetAttribute(k_qmatmul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_qmatmul<<<tiles, kQThreads, smem, (cudaStream_t)stream>>>(P);
+    if (blk->codec == EQ_CODEC_WORD) {
+        EQ_CUDA_TRY(cudaFuncSetAttribute(k_qmatmul<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_qmatmul<true><<<tiles, kQThreads, smem, (cudaStream_t)stream>>>(P);
+    } else {
+        EQ_CUDA_TRY(cudaFuncSetAttribute(k_qmatmul<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_qmatmul<false><<<tiles, kQThreads, smem, (cudaStream_t)stream>>>(P);
+    }
     EQ_CUDA_TRY(cudaGetLastError());
     if (n_red) {
         const uint32_t gx = std::min<uint32_t>((max_red / 4 + 255) / 256, 148u * 8u);

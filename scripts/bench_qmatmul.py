@@ -30,12 +30,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cs", type=int, default=2048)
     ap.add_argument("--profile", action="store_true", help="one grouped launch per batch (for ncu)")
+    ap.add_argument("--codec", default="word", choices=["byte", "word"])
     args = ap.parse_args()
+    codec = {"byte": eq.EQ_CODEC_BYTE, "word": eq.EQ_CODEC_WORD}[args.codec]
     dev = torch.device("cuda")
     Ws = eqsynth.block_weights("llama-3-8b", 0, device=dev)
-    blk = eq.quantize_encode(Ws, lam=230.2, chunk_symbols=args.cs)
+    blk = eq.quantize_encode(Ws, lam=230.2, chunk_symbols=args.cs, codec=codec)
     dec = eq.Decoder([blk])
-    out = {"workload": f"config4: Llama-3-8B decoder block (q,k,v,o,gate,up,down), chunk {args.cs}, ~2 bits",
+    out = {"workload": f"config4: Llama-3-8B decoder block (q,k,v,o,gate,up,down), chunk {args.cs}, ~2 bits, "
+                       f"{args.codec} codec",
            "effective_bits": blk.effective_bits()}
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     for batch in (1, 64):

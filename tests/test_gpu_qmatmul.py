@@ -20,16 +20,17 @@ def to_gpu_block(blk):
     sc = torch.from_numpy(np.concatenate(blk.scales).view(np.int16)).view(torch.bfloat16)
     return eq.Block(payload.to(DEV), len(blk.payload), torch.from_numpy(blk.chunk_off.astype(np.int64).astype(np.int32)).to(DEV),
                     torch.from_numpy(blk.freq.view(np.int16).copy()).to(DEV), sc.to(DEV), list(blk.layer_shapes),
-                    blk.chunk_symbols, format=blk.fmt)
+                    blk.chunk_symbols, format=blk.fmt, codec=blk.codec)
 
 
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
 @pytest.mark.parametrize("cs,fmt", [(4096, 0), (2048, 0), (1024, 1), (256, 0)])
 @pytest.mark.parametrize("batch", [1, 8, 61])
-def test_qmatmul_matches_fp64_reference(cs, fmt, batch):
+def test_qmatmul_matches_fp64_reference(cs, fmt, batch, codec):
     shapes = [(256, 4096), (128, 2048 if cs <= 2048 else 4096)]
     Ws = [eqsynth.weights(r, c, seed=31, layer=0, matrix=m) for m, (r, c) in enumerate(shapes)]
     S = [(o.absmax_scales(W, fmt).astype(np.int32) + 128 * 12).astype(np.uint16) for W in Ws]
-    blk = o.quantize_encode(Ws, scales=S, cs=cs, fmt=fmt)
+    blk = o.quantize_encode(Ws, scales=S, cs=cs, fmt=fmt, codec=codec)
     g = to_gpu_block(blk)
     What = [d.view(np.int16) for d in o.decode_dequant(blk)]
     for layer, (r, c) in enumerate(shapes):
@@ -43,9 +44,10 @@ def test_qmatmul_matches_fp64_reference(cs, fmt, batch):
             assert (np.abs(y - ref) <= bound).all(), (layer, rep, float(np.max(np.abs(y - ref) / bound)))
 
 
-def test_qmatmul_shape_errors_and_corruption():
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
+def test_qmatmul_shape_errors_and_corruption(codec):
     Ws = [eqsynth.weights(128, 4096, seed=3)]
-    blk = o.quantize_encode(Ws, scales=[o.absmax_scales(Ws[0])], cs=4096)
+    blk = o.quantize_encode(Ws, scales=[o.absmax_scales(Ws[0])], cs=4096, codec=codec)
     g = to_gpu_block(blk)
     with pytest.raises(eq.EqError):
         eq.qmatmul(g, 0, torch.zeros(2, 4000, dtype=torch.bfloat16, device=DEV))
@@ -59,13 +61,14 @@ def test_qmatmul_shape_errors_and_corruption():
     assert ei.value.status == eq.EQ_ERR_CORRUPT
 
 
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
 @pytest.mark.parametrize("batch", [1, 24])
-def test_qmatmul_group_one_launch_deterministic(batch):
+def test_qmatmul_group_one_launch_deterministic(batch, codec):
     """All layers of a block in one grouped launch (mixed chunk counts per row: split-K
     partials for some, direct output for others), bitwise repeatable, each vs fp64."""
     shapes = [(256, 1024), (128, 2048), (384, 1024), (128, 3072)]
     Ws = [eqsynth.weights(r, c, seed=77, layer=1, matrix=m) for m, (r, c) in enumerate(shapes)]
-    blk = o.quantize_encode(Ws, lam=None, cs=1024)
+    blk = o.quantize_encode(Ws, lam=None, cs=1024, codec=codec)
     g = to_gpu_block(blk)
     What = o.decode_dequant(blk)
     xs = [(torch.randn(batch, c, generator=torch.Generator().manual_seed(5 + m)) * 0.3).to(torch.bfloat16)
