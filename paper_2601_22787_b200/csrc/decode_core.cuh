@@ -375,7 +375,8 @@ __device__ __forceinline__ void ring_step_w(WordReader& r, const uint8_t* payloa
 #define EQ_WZERO 0       // 1: code 0x00 decoded without the shared-memory LUT (measured slower)
 #endif
 #ifndef EQ_WADDR
-#define EQ_WADDR 0       // LUT address: 0 = 4x − 2^14·xs + base (3 IMADs deep), 1 = (4x & 0x3FFC) + base
+#define EQ_WADDR 2       // LUT address: 0 = 4x − 2^14·xs + base (IMAD.HI + 2 IMADs),
+                         // 2 = IMAD.WIDE x·2^20 (xs and slot together) + LEA.HI
 #endif
 #ifndef EQ_WENTRY
 #define EQ_WENTRY 1      // LUT entry layout of build_lut<EQ_WENTRY> (0: f−1 in bits 8-19, 1: in 20-31)
@@ -384,20 +385,24 @@ __device__ __forceinline__ void ring_step_w(WordReader& r, const uint8_t* payloa
 // (symbol in the low byte).  State update with IMAD / IMAD.HI / LEA.HI forms; then
 // if x < 2^16: x = (x << 16) | w as one PRMT, and the next word is prefetched.
 __device__ __forceinline__ uint32_t decode_one_w(uint32_t& x, WordReader& r, const DecTable& T) {
+#if EQ_WADDR == 2
+    // one IMAD.WIDE: x·2^20 = (x >> 12) : (slot << 20); LUT address = base + (lo >> 18) (LEA.HI)
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    const uint32_t la = T.lut_s + (lo >> 18);
+#else
     const uint32_t xs = mad_hi(x, T.k2p20, 0u);                         // x >> 12
+    const uint32_t la = mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s));
+#endif
 #if EQ_WZERO
     // code 0x00 (cum 0, the most frequent symbol) owns slots [0, f0): its entry
     // (f0−1) << 20 | slot << 8 is computed, so only the other lanes access shared memory
     // (fewer random-slot bank conflicts per warp-wide lookup)
-    const uint32_t la = mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s));
     uint32_t e;
     if (la < T.zlim) e = la * 64u + T.zk;
     else e = lds_u32(la);
-#elif EQ_WADDR
-    const uint32_t e = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(T.lutp) +
-                                                          (mad_lo(x, T.k4, 0u) & 0x3FFCu));
 #else
-    const uint32_t e = lds_u32(mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s)));
+    const uint32_t e = lds_u32(la);
 #endif
 #if EQ_WENTRY
     const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
