@@ -66,3 +66,62 @@ def test_single_process_identity_and_errors():
     assert shard.layer_ids(0, 1, 3) == [0, 1, 2]
     with pytest.raises(ValueError):
         shard.layer_ids(2, 2, 3)
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import numpy as np
+
+    import eqsynth
+    import oracle as o
+    import paper_2601_22787_b200 as eq
+    # rank r holds compressed blocks of layers 2r, 2r+1 (CPU tensors stand in for device memory)
+    mine = []
+    for lid in (2 * rank, 2 * rank + 1):
+        Ws = [eqsynth.weights(r_, c, seed=5, layer=lid, matrix=m) for m, (r_, c) in enumerate([(32, 256), (16, 384)])]
+        ob = o.quantize_encode(Ws, lam=None, cs=512, codec=o.CODEC_WORD if lid % 2 else o.CODEC_BYTE)
+        cap = len(ob.payload) + 256
+        pay = torch.zeros(cap, dtype=torch.uint8)
+        pay[:len(ob.payload)] = torch.frombuffer(bytearray(ob.payload), dtype=torch.uint8)
+        mine.append(eq.Block(pay, len(ob.payload), torch.from_numpy(ob.chunk_off.astype(np.int64).astype(np.int32)),
+                             torch.from_numpy(ob.freq.view(np.int16).copy()),
+                             torch.from_numpy(np.concatenate(ob.scales).view(np.int16)).view(torch.bfloat16),
+                             list(ob.layer_shapes), 512, {"layer": lid}, ob.fmt, ob.codec))
+    allb = shard.all_gather_blocks(mine, dist)
+    # decoded-row all-gather: rank r holds rows [4r, 4r+4) of an 8 x 6 tensor
+    full = torch.arange(48, dtype=torch.float32).view(8, 6)
+    rows = shard.all_gather_rows(full[4 * rank:4 * rank + 4].clone(), dist)
+    summary = []
+    for b in allb:
+        ob = o.OracleBlock(b.shapes, [], b.freq.numpy().view(np.uint16), None,
+                           b.payload[:b.payload_bytes].numpy().tobytes(), b.chunk_off.numpy().astype(np.uint32),
+                           b.chunk_symbols, None, b.format, b.codec)
+        stream = o.decode_block(ob)
+        summary.append((b.meta["layer"], b.codec, int(stream.sum()), b.payload_bytes,
+                        bytes(b.scales.view(torch.int16).numpy().tobytes())))
+    q.put((rank, summary, bool(torch.equal(rows, full))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_compressed_block_all_gather():
+    """Every rank ends with every rank's compressed blocks, byte-identical (streams decode
+    with the oracle to the same symbols on both ranks), plus the decoded-row all-gather."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    (_, s0, ok0), (_, s1, ok1) = res
+    assert ok0 and ok1
+    assert s0 == s1
+    assert [t[0] for t in s0] == [0, 1, 2, 3]                 # rank-major order
+    assert [t[1] for t in s0] == [0, 1, 0, 1]                 # codecs travel with the blocks
