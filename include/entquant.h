@@ -197,9 +197,12 @@ eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks, uint32_t 
                             eq_stream_t stream);
 
 /* End-to-end variant with HOST buffers: blocks_host[b].payload / chunk_off / freq / scales
- * are host pointers (pinned for full speed).  Copies them into `workspace` (device,
- * ≥ eq_decode_host_workspace_bytes), decodes, and copies the decoded arena to arena_host.
- * All on `stream`; SYNCHRONOUS (returns after the device→host copy, with eq_check). */
+ * are host pointers (pinned for full speed; arena_host too).  Copies them into `workspace`
+ * (device, ≥ eq_decode_host_workspace_bytes), decodes, and copies the decoded arena to
+ * arena_host, pipelined over ≤ 8 groups of blocks: the host→device copy of the next group
+ * and the device→host copy of the previous one overlap the decode of the current one (two
+ * copy streams created and destroyed inside the call, ordered after prior work on `stream`).
+ * SYNCHRONOUS (returns after the last device→host copy, with eq_check). */
 uint64_t eq_decode_host_workspace_bytes(const eq_block* blocks_host, uint32_t n_blocks,
                                         uint32_t out_dtype);
 eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks, uint32_t out_dtype,

@@ -210,7 +210,8 @@ extern "C" eq_status eq_decode_dequant_host(const eq_block* blocks, uint32_t n_b
     if (need == 0) return EQ_ERR_ARG;
     if (workspace_bytes < need) return EQ_ERR_BUFFER;
     uint64_t total = 0;
-    EQ_TRY(eq_arena_layout(blocks, n_blocks, out_dtype, nullptr, &total));
+    std::vector<uint64_t> offs((size_t)n_blocks * EQ_MAX_LAYERS);
+    EQ_TRY(eq_arena_layout(blocks, n_blocks, out_dtype, offs.data(), &total));
     if (arena_bytes < total) return EQ_ERR_BUFFER;
     cudaStream_t st = (cudaStream_t)stream;
     char* ws = (char*)workspace;
@@ -230,17 +231,70 @@ extern "C" eq_status eq_decode_dequant_host(const eq_block* blocks, uint32_t n_b
         pos += 512;
         d.scales = (uint16_t*)(ws + pos);
         pos += align_up(2 * rows, 256);
-        EQ_CUDA_TRY(cudaMemcpyAsync(d.payload, h.payload, h.payload_bytes, cudaMemcpyHostToDevice, st));
-        EQ_CUDA_TRY(cudaMemcpyAsync(d.chunk_off, h.chunk_off, 4ull * (h.n_chunks + 1), cudaMemcpyHostToDevice, st));
-        EQ_CUDA_TRY(cudaMemcpyAsync(d.freq, h.freq, 512, cudaMemcpyHostToDevice, st));
-        EQ_CUDA_TRY(cudaMemcpyAsync(d.scales, h.scales, 2 * rows, cudaMemcpyHostToDevice, st));
     }
     pos = align_up(pos, 256);
-    void* arena = ws + pos;
+    char* arena = ws + pos;
     uint32_t* err = (uint32_t*)(ws + pos + total);
-    EQ_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
-    EQ_TRY(eq_decode_dequant(dev.data(), n_blocks, out_dtype, arena, total, err, stream));
-    EQ_CUDA_TRY(cudaMemcpyAsync(arena_host, arena, total, cudaMemcpyDeviceToHost, st));
+    // Three-stage pipeline over groups of blocks: host→device copy of group g+1 (copy stream)
+    // and device→host copy of group g−1 (second copy stream) overlap the decode of group g
+    // (the caller's stream); PCIe is full duplex, so the step costs ≈ max(H2D, D2H) + one
+    // group's decode.  Streams and events live for this call only (the library keeps no state).
+    const uint32_t n_groups = std::min<uint32_t>(n_blocks, 8u);
+    const uint32_t per = (n_blocks + n_groups - 1) / n_groups;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev_in(n_groups, nullptr), ev_dec(n_groups, nullptr);
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+    eq_status rs = EQ_OK;
+    auto ck = [&](cudaError_t e) { if (e != cudaSuccess && rs == EQ_OK) rs = EQ_ERR_CUDA; return e == cudaSuccess; };
+    ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+    ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    ck(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    ck(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        ck(cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming));
+        ck(cudaEventCreateWithFlags(&ev_dec[g], cudaEventDisableTiming));
+    }
+    if (rs == EQ_OK) {
+        ck(cudaMemsetAsync(err, 0, 4, st));
+        ck(cudaEventRecord(ev_start, st));                        // work queued before this call
+        ck(cudaStreamWaitEvent(s_in, ev_start, 0));
+        for (uint32_t g = 0; g < n_groups && rs == EQ_OK; ++g) {
+            const uint32_t b0 = g * per, b1 = std::min(n_blocks, b0 + per);
+            if (b0 >= b1) break;
+            for (uint32_t b = b0; b < b1; ++b) {
+                const eq_block& h = blocks[b];
+                const eq_block& d = dev[b];
+                uint64_t rows = 0;
+                for (uint32_t l = 0; l < h.n_layers; ++l) rows += (uint64_t)h.layer_rows[l];
+                ck(cudaMemcpyAsync(d.payload, h.payload, h.payload_bytes, cudaMemcpyHostToDevice, s_in));
+                ck(cudaMemcpyAsync(d.chunk_off, h.chunk_off, 4ull * (h.n_chunks + 1), cudaMemcpyHostToDevice, s_in));
+                ck(cudaMemcpyAsync(d.freq, h.freq, 512, cudaMemcpyHostToDevice, s_in));
+                ck(cudaMemcpyAsync(d.scales, h.scales, 2 * rows, cudaMemcpyHostToDevice, s_in));
+            }
+            ck(cudaEventRecord(ev_in[g], s_in));
+            ck(cudaStreamWaitEvent(st, ev_in[g], 0));
+            const uint64_t a0 = offs[(size_t)b0 * EQ_MAX_LAYERS];
+            const uint64_t a1 = b1 < n_blocks ? offs[(size_t)b1 * EQ_MAX_LAYERS] : total;
+            const eq_status ds = eq_decode_dequant(dev.data() + b0, b1 - b0, out_dtype, arena + a0, a1 - a0, err, stream);
+            if (ds != EQ_OK && rs == EQ_OK) rs = ds;
+            ck(cudaEventRecord(ev_dec[g], st));
+            ck(cudaStreamWaitEvent(s_out, ev_dec[g], 0));
+            ck(cudaMemcpyAsync((char*)arena_host + a0, arena + a0, a1 - a0, cudaMemcpyDeviceToHost, s_out));
+        }
+        ck(cudaEventRecord(ev_done, s_out));
+        ck(cudaStreamWaitEvent(st, ev_done, 0));                  // the caller's stream sees the result
+    }
+    if (s_in) cudaStreamSynchronize(s_in);
+    if (s_out) cudaStreamSynchronize(s_out);
+    for (uint32_t g = 0; g < n_groups; ++g) {
+        if (ev_in[g]) cudaEventDestroy(ev_in[g]);
+        if (ev_dec[g]) cudaEventDestroy(ev_dec[g]);
+    }
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_done) cudaEventDestroy(ev_done);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    if (rs != EQ_OK) return rs;
     return eq_check(err, stream);
 }
 
