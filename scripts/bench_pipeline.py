@@ -38,10 +38,10 @@ def main():
     blocks, dense = [], []
     for lid in range(nb):
         Ws = eqsynth.block_weights(model, lid, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=lam))
+        blocks.append(eq.quantize_encode(Ws, lam=lam, codec=eq.EQ_CODEC_WORD))
         dense.append(Ws)
     hid = eqsynth.LLAMA[model]["hidden"]
-    out = {"workload": f"{model}-shaped linear forward over {nb} blocks (decode-in-the-loop, bf16 weights)"}
+    out = {"workload": f"{model}-shaped linear forward over {nb} blocks (decode-in-the-loop, bf16 weights, word codec)"}
     for batch in (1, 64):
         x0 = torch.randn(batch, hid, device=dev, dtype=torch.bfloat16) * 0.1
 

@@ -14,4 +14,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 ncu --set full --clock-control none --import-source on -k regex:k_decode -s 1 -c 2 -o $OUT/decode \
     python bench.py --profile --steps 1 --warmup 1 --no-e2e --no-cpu --lam 230.2 > $OUT/full_bench.log 2>&1; echo full=$?
 python scripts/ncu_summary.py $OUT/decode.ncu-rep > $OUT/summary.json 2>&1
+timeout 900 python scripts/bench_pipeline.py > $OUT/pipeline.json 2> $OUT/pipeline.err; echo pipeline=$?
 tail -c 1500 $OUT/bench.json

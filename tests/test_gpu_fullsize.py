@@ -1,7 +1,8 @@
 """Parity at BASELINE.json's full sizes, in bench.py's launch configuration.
 
 Config 3: the 32-block Llama-3-8B-shaped layer set is encoded on the GPU (search at the
-bench's λ) and decoded in ONE eq_decode_dequant launch into the bf16 arena.  The oracle
+bench's λ, word codec as in the bench and the byte codec) and decoded in ONE
+eq_decode_dequant launch into the bf16 arena.  The oracle
 recomputes sampled rows one by one from the INPUT weights (its own search, quantiser and
 dequantiser) and must equal the decoded rows bit for bit (rows whose GPU scale is a
 documented near-tie of the oracle's objective are checked for optimality instead).
@@ -31,8 +32,9 @@ def test_eqsynth_bit_identical_on_cuda():
         assert torch.equal(a.view(torch.int16), b.cpu().view(torch.int16)), dist
 
 
-@pytest.fixture(scope="module")
-def layer_set():
+@pytest.fixture(scope="module", params=[eq.EQ_CODEC_WORD, eq.EQ_CODEC_BYTE], ids=["word", "byte"])
+def layer_set(request):
+    """The bench's layer set in its codec (word, R14) and in SPEC's byte codec (R9)."""
     dev = torch.device("cuda")
     blocks, kept = [], {}
     scratch = None
@@ -40,7 +42,7 @@ def layer_set():
         Ws = eqsynth.block_weights("llama-3-8b", lid, device=dev)
         if scratch is None:
             scratch = torch.empty(eq.encode_bounds(Ws)[2], dtype=torch.uint8, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=LAM, scratch=scratch))
+        blocks.append(eq.quantize_encode(Ws, lam=LAM, scratch=scratch, codec=request.param))
         if lid in (0, 31):
             kept[lid] = [W.cpu() for W in Ws]          # the INPUT weights, for the oracle
         del Ws
@@ -94,7 +96,7 @@ def test_config3_lossless_and_rate_properties(layer_set):
         assert coded <= 1.02 * b.n_params * H / 8                     # north_star 1.02×
         assert 8 * b.payload_bytes >= b.n_params * H * (1 - 1e-3)    # Shannon
         # re-encoding the decoded codes with the same table reproduces the payload exactly
-        again = eq.rans_encode(codes, b.shapes, b.freq)
+        again = eq.rans_encode(codes, b.shapes, b.freq, codec=b.codec)
         assert again.payload_bytes == b.payload_bytes
         assert torch.equal(again.payload[:again.payload_bytes], b.payload[:b.payload_bytes])
         n += b.n_params
