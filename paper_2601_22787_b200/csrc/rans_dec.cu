@@ -104,15 +104,38 @@ __device__ __forceinline__ bool build_lut(const DecBlock& B, uint32_t* lut, uint
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
         return false;
     }
-    for (int slot = t; slot < (int)kM; slot += NT) {
-        int lo = 0, hi = 255;                  // largest s with cum[s] <= slot
+    auto entry = [&](uint32_t slot, int sym) -> uint32_t {
+        const uint32_t fs = cum[sym + 1] - cum[sym];
+        return LAYOUT == 0 ? ((uint32_t)sym | ((fs - 1) << 8) | ((slot - cum[sym]) << 20))
+                           : ((uint32_t)sym | ((slot - cum[sym]) << 8) | ((fs - 1) << 20));
+    };
+    if (NT == 256) {
+        // thread t fills slots [16t, 16t + 16): one binary search for the first slot's
+        // symbol, then a forward walk over the symbol boundaries; 4 × 16-byte stores
+        const uint32_t s0 = 16u * (uint32_t)t;
+        int lo = 0, hi = 255;                  // largest s with cum[s] <= s0
         while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
-            if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+            if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
         }
-        uint32_t fs = cum[lo + 1] - cum[lo];
-        lut[slot] = LAYOUT == 0 ? ((uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20))
-                                : ((uint32_t)lo | (((uint32_t)slot - cum[lo]) << 8) | ((fs - 1) << 20));
+        uint32_t v[16];
+        #pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            while (cum[lo + 1] <= s0 + k) ++lo;
+            v[k] = entry(s0 + k, lo);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(lut + s0);
+        #pragma unroll
+        for (int k = 0; k < 4; ++k) dst[k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    } else {
+        for (int slot = t; slot < (int)kM; slot += NT) {
+            int lo = 0, hi = 255;              // largest s with cum[s] <= slot
+            while (lo < hi) {
+                int mid = (lo + hi + 1) >> 1;
+                if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+            }
+            lut[slot] = entry((uint32_t)slot, lo);
+        }
     }
     return true;
 }
@@ -244,7 +267,7 @@ __device__ __forceinline__ void chain_finish(Chain& c, const uint8_t* payload, c
 template <bool BF16>
 __global__ void __launch_bounds__(kDecThreads, EQ_DEC_MIN_CTAS)
 k_decode(const __grid_constant__ DecParams P) {
-    __shared__ uint32_t lut[kM];
+    __shared__ __align__(16) uint32_t lut[kM];
     __shared__ uint32_t cum[257];
     __shared__ __align__(64) uint32_t rings[kChunksPerCta * kRingWords];
 
