@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 W16 = o.CODEC_WORD
 
 
-@pytest.mark.parametrize("cs", [4096, 1000, 64, 7, 1])
+@pytest.mark.parametrize("cs", [262144, 4096, 1000, 64, 7, 1])
 @pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16])
 def test_word_decode_oracle_streams(cs, out):
     layers = small_layers()
@@ -149,3 +149,15 @@ def test_word_rate_vs_byte_codec_at_two_bits():
     H = o.entropy(hist.cpu().numpy().astype(np.uint64))
     assert gw.payload_bytes + 4 * (gw.n_chunks + 1) <= 1.02 * W.numel() * H / 8
     assert abs(gw.payload_bytes - gb.payload_bytes) <= 0.005 * gb.payload_bytes
+
+
+def test_word_decode_max_chunk_full_rows():
+    """The largest chunk SPEC allows (262144 symbols) on rows of 14336 (a chunk spans
+    rows, so the per-group scale switch inside a chunk is exercised) and 8 such layers."""
+    shapes = [(32, 14336)] * 2 + [(64, 4096)]
+    layers = [eqsynth.weights(r, c, seed=21, layer=1, matrix=m) for m, (r, c) in enumerate(shapes)]
+    S = [(o.absmax_scales(W).astype(np.int32) + 1600).astype(np.uint16) for W in layers]
+    blk = o.quantize_encode(layers, scales=S, cs=262144, codec=W16)
+    g = oracle_block_to_gpu(blk)
+    for v, r in zip(eq.decode_dequant([g], eq.EQ_OUT_BF16)[0], o.decode_dequant(blk)):
+        assert (u16(v) == r).all()
