@@ -211,7 +211,12 @@ __device__ __forceinline__ void st_out(uint4* p, uint4 v) { __stcs(p, v); }
                          // decoded lines leave L2 first, the compressed input stays — DRAM reads 4.55 → 2.37 GB)
 #endif
 __device__ __forceinline__ void st_out32(void* p, uint4 a, uint4 b) {
-#if EQ_ST256 && EQ_STPOL
+#if EQ_ST256 && EQ_STPOL == 2
+    // evict-first in L2 as an instruction qualifier (STG.E.NA.EFL2): no policy register
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                 "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+#elif EQ_ST256 && EQ_STPOL
     uint64_t pol;
     if (EQ_STPOL == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
