@@ -452,9 +452,22 @@ def cpu_baseline(blocks, seconds: float):
         done_bytes += 512
         if wall >= seconds:
             break
+    # the same oracle on ONE host thread, on the first layer of block 0
+    blk = blocks[0]
+    r, c = blk.shapes[0]
+    nk = (r * c + blk.chunk_symbols - 1) // blk.chunk_symbols
+    off = blk.chunk_off.cpu().numpy().astype(np.uint32)[:nk + 1]
+    t = time.perf_counter()
+    o.decode_dequant_layer_mt(blk.payload.cpu().numpy(), off, blk.chunk_symbols, r, c,
+                              blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)[:r],
+                              blk.freq.cpu().numpy().view(np.uint16), 1, blk.codec)
+    w1 = time.perf_counter() - t
+    b1 = int(off[-1] - off[0]) + 4 * (nk + 1) + 2 * r + 2 * r * c
     return {"value": done_bytes / wall / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"{layers} whole layers ({done_syms} symbols) of the leading blocks, decode+dequant to bf16 "
-                      f"with eqo_decode_chunk on {threads} threads, {wall:.1f} s wall"}
+                      f"with eqo_decode_chunk on {threads} threads, {wall:.1f} s wall",
+            "value_1_thread": b1 / w1 / 1e9,
+            "sample_1_thread": f"layer 0 of block 0 ({r * c} symbols) on 1 thread, {w1:.1f} s wall"}
 
 
 if __name__ == "__main__":
