@@ -150,8 +150,13 @@ __device__ __forceinline__ bool chunk_begin(ChainW& c, const QmmParams& P, uint3
 }
 
 __device__ __forceinline__ void chunk_end(const ChainW& c, uint32_t* err) {
-    if (c.active && (c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(err, EQ_EF_CORRUPT);
+    if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(err, EQ_EF_CORRUPT);
 }
+
+// A corrupt stream can consume words past its chunk; checked before every 64-symbol step so
+// the ring never stages beyond the payload's readable slack (≤ 128 bytes per step + 48 ahead)
+__device__ __forceinline__ bool runaway_q(const ChainW& c) { return c.r.Q > c.e + (2u + kWBias); }
+__device__ __forceinline__ bool runaway_q(const Chain& c) { return c.br.wi4 > c.wlimit4; }
 
 // start decoding chunk `chunk` (payload bytes, ring staging, first state) for this lane
 __device__ __forceinline__ bool chunk_begin(Chain& c, const QmmParams& P, uint32_t chunk, uint32_t ring) {
@@ -192,7 +197,8 @@ __device__ __forceinline__ void chunk_end(const Chain& c, uint32_t* err) {
     if (!c.active) return;
     const int64_t inserted = 8ll * (int64_t)(c.br.wi4 - (c.a >> 2) * 4u) - 8ll * (int64_t)(c.a & 3);
     const int64_t consumed = inserted - c.br.nb;
-    if (c.br.wi4 > c.wlimit4 || c.x != kL || consumed != 8ll * (int64_t)(c.e - c.a)) atomicOr(err, EQ_EF_CORRUPT);
+    if (c.runaway || c.br.wi4 > c.wlimit4 || c.x != kL || consumed != 8ll * (int64_t)(c.e - c.a))
+        atomicOr(err, EQ_EF_CORRUPT);
 }
 
 // CTA = (job, pair of 128-row tiles, chunk column j): lane r of half h decodes the j-th
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
     c.sc = J.scales;
     c.i8 = P.format == EQ_FMT_INT8;
     c.active = false;
+    c.runaway = false;
     c.s = 0.f;
     c.s16 = 0;
     if (my_on) {
@@ -306,9 +313,10 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 
     for (uint32_t st = 0; st < steps; ++st) {
         uint4 v[8];
-        if (c.active) {
+        if (c.active && !runaway_q(c)) {
             decode_step(c, T, P.payload, v);
         } else {
+            c.runaway = c.runaway || c.active;           // stop reading a stream that overran its chunk
             #pragma unroll
             for (int q = 0; q < 8; ++q) v[q] = make_uint4(0, 0, 0, 0);
         }

@@ -102,3 +102,25 @@ def test_qmatmul_workspace_contract():
     ya = (ctypes.c_void_p * 1)(y.data_ptr())
     st = eq.lib().eq_qmatmul_group(ctypes.byref(b), 1, la, xa, ya, 3, small.data_ptr(), 16, err.data_ptr(), None)
     assert st == eq.EQ_ERR_BUFFER
+
+
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
+def test_qmatmul_runaway_stream_is_reported_not_overread(codec):
+    """A chunk whose state is forced to 1 consumes a renormalisation unit at every symbol and
+    runs far past its end: the fused kernel must stop reading it (no access beyond the
+    payload slack) and report EQ_ERR_CORRUPT; the other chunks still decode."""
+    Ws = [eqsynth.weights(128, 4096, seed=12)]
+    blk = o.quantize_encode(Ws, scales=[(o.absmax_scales(Ws[0]).astype(np.int32) + 1700).astype(np.uint16)],
+                            cs=2048, codec=codec)
+    g = to_gpu_block(blk)
+    last = blk.n_chunks - 1                                  # the chunk next to the payload end
+    a = int(blk.chunk_off[last])
+    g.payload[a:a + 4] = torch.tensor([1, 0, 0, 0], dtype=torch.uint8, device=DEV)
+    with pytest.raises(eq.EqError) as ei:
+        eq.qmatmul(g, 0, torch.ones(4, 4096, dtype=torch.bfloat16, device=DEV))
+    assert ei.value.status == eq.EQ_ERR_CORRUPT
+    d = eq.Decoder([g], eq.EQ_OUT_BF16)
+    d()
+    with pytest.raises(eq.EqError) as ei:
+        d.check()
+    assert ei.value.status == eq.EQ_ERR_CORRUPT
