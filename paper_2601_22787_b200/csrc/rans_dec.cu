@@ -118,15 +118,17 @@ __device__ __forceinline__ bool build_lut(const DecBlock& B, uint32_t* lut, uint
             int mid = (lo + hi + 1) >> 1;
             if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
         }
-        uint32_t v[16];
-        #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            while (cum[lo + 1] <= s0 + k) ++lo;
-            v[k] = entry(s0 + k, lo);
-        }
         uint4* dst = reinterpret_cast<uint4*>(lut + s0);
-        #pragma unroll
-        for (int k = 0; k < 4; ++k) dst[k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        #pragma unroll 1
+        for (int k = 0; k < 16; k += 4) {            // 4 entries per 16-byte store (few live registers)
+            uint32_t v[4];
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                while (cum[lo + 1] <= s0 + k + u) ++lo;
+                v[u] = entry(s0 + k + u, lo);
+            }
+            dst[k >> 2] = make_uint4(v[0], v[1], v[2], v[3]);
+        }
     } else {
         for (int slot = t; slot < (int)kM; slot += NT) {
             int lo = 0, hi = 255;              // largest s with cum[s] <= slot
