@@ -36,8 +36,20 @@ namespace eq {
 constexpr int kTileRows = 128;                // MMA M = TMEM lanes
 constexpr int kTiles = 2;                     // row tiles per CTA (share the LUT and the B tile)
 constexpr int kQThreads = kTileRows * kTiles;
-constexpr int kQK = 64;                       // K columns per step (one 128-byte swizzle row)
-constexpr int kATile = kTileRows * kQK * 2;   // 16 KB per row tile
+#ifndef EQ_QMM_K
+#define EQ_QMM_K 64
+#endif
+constexpr int kQK = EQ_QMM_K;                 // K columns per step: 64 (SWIZZLE_128B rows) or 32 (SWIZZLE_64B)
+constexpr int kRowB = kQK * 2;                // bytes per tile row = swizzle span
+constexpr int kAtom = 8 * kRowB;              // 8-row swizzle atom (1024 or 512 bytes)
+constexpr int kChunks = kRowB / 16;           // 16-byte chunks per row
+constexpr int kATile = kTileRows * kRowB;     // 16 KB (or 8 KB) per row tile
+static_assert(kQK == 64 || kQK == 32, "K step");
+// 16-byte chunk c of row r of a K-major swizzled tile: 128B mode XORs c with r & 7, 64B mode
+// with (r >> 1) & 3 (address bits [4,6) ^= bits [7,9))
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) {
+    return kQK == 64 ? (c ^ (r & 7)) : (c ^ ((r >> 1) & 3));
+}
 
 // one GEMM of the group: layer `layer` of the block, X [n_real][K] bf16, output fp32
 struct QmmJob {
@@ -67,6 +79,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
            ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
 }
+// K-major SWIZZLE_64B: SBO = 512 B between 8-row atoms, layout type 4
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(512u >> 4) << 32) |
+           ((uint64_t)1u << 46) | ((uint64_t)4u << 61);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    return kQK == 64 ? umma_desc_sw128(saddr) : umma_desc_sw64(saddr);
+}
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -91,9 +111,9 @@ __device__ __forceinline__ uint4 dequant8(const C& c, uint32_t q0, uint32_t q1) 
 
 // one lane's next 64 decoded + dequantised symbols, held in registers (8 × 16 bytes) so the
 // decode of step t+1 overlaps the tensor-core reads of step t's tile
-__device__ __forceinline__ void decode_step(Chain& c, const DecTable& T, const uint8_t* payload, uint4 v[8]) {
+__device__ __forceinline__ void decode_step(Chain& c, const DecTable& T, const uint8_t* payload, uint4 v[kQK / 8]) {
     #pragma unroll
-    for (int g = 0; g < 4; ++g) {                       // 4 × 16 symbols
+    for (int g = 0; g < kQK / 16; ++g) {                // kQK / 16 × 16 symbols
         const uint32_t q0 = decode4(c, T);
         const uint32_t q1 = decode4(c, T);
         stage_wait_all(); ring_issue(c.br, payload); stage_commit();
@@ -103,13 +123,13 @@ __device__ __forceinline__ void decode_step(Chain& c, const DecTable& T, const u
         v[2 * g] = dequant8(c, q0, q1);
         v[2 * g + 1] = dequant8(c, q2, q3);
     }
-    c.i += 64;
+    c.i += kQK;
 }
 
 // EQ_CODEC_WORD: the same 64 symbols with word renormalisation (decode_one_w)
-__device__ __forceinline__ void decode_step(ChainW& c, const DecTable& T, const uint8_t* payload, uint4 v[8]) {
+__device__ __forceinline__ void decode_step(ChainW& c, const DecTable& T, const uint8_t* payload, uint4 v[kQK / 8]) {
     #pragma unroll
-    for (int g = 0; g < 4; ++g) {                       // 4 × 16 symbols
+    for (int g = 0; g < kQK / 16; ++g) {                // kQK / 16 × 16 symbols
         const uint32_t q0 = decode4_w(c, T);
         const uint32_t q1 = decode4_w(c, T);
         ring_step_w(c.r, payload);
@@ -119,7 +139,7 @@ __device__ __forceinline__ void decode_step(ChainW& c, const DecTable& T, const 
         v[2 * g] = dequant8(c, q0, q1);
         v[2 * g + 1] = dequant8(c, q2, q3);
     }
-    c.i += 64;
+    c.i += kQK;
 }
 
 __device__ __forceinline__ bool chunk_begin(ChainW& c, const QmmParams& P, uint32_t chunk, uint32_t ring) {
@@ -215,7 +235,7 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
     // symbol prefix sums used while building the LUT live in the (not yet used) A tiles
     uint8_t* a_tiles = dsm;
     uint8_t* b_tile = dsm + kTiles * kATile;
-    const uint32_t b_tile_bytes = (P.n_pad * 128u + 1023u) & ~1023u;
+    const uint32_t b_tile_bytes = (P.n_pad * (uint32_t)kRowB + 1023u) & ~1023u;
     uint32_t* lut = reinterpret_cast<uint32_t*>(b_tile + b_tile_bytes);
     uint32_t* rings = lut + kM;                                      // 256 × 64 B
     uint32_t* wsum = rings + kQThreads * kRingWords;                 // 8
@@ -308,38 +328,38 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
     const uint32_t steps = P.cs / kQK;
     const uint32_t kbase = jcol * P.cs;
     uint8_t* a_tile = a_tiles + h * kATile;
-    uint8_t* arow = a_tile + (r >> 3) * 1024 + (r & 7) * 128;
+    uint8_t* arow = a_tile + (r >> 3) * kAtom + (r & 7) * kRowB;
     const uint32_t bar = smem_u32(&bars[0]);
 
     for (uint32_t st = 0; st < steps; ++st) {
-        uint4 v[8];
+        uint4 v[kQK / 8];
         if (c.active && !runaway_q(c)) {
             decode_step(c, T, P.payload, v);
         } else {
             c.runaway = c.runaway || c.active;           // stop reading a stream that overran its chunk
             #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = make_uint4(0, 0, 0, 0);
+            for (int q = 0; q < kQK / 8; ++q) v[q] = make_uint4(0, 0, 0, 0);
         }
         if (st > 0) mbar_wait(bar, (st - 1) & 1);     // tensor cores done reading step st-1
         #pragma unroll
-        for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(arow + ((q ^ (r & 7)) << 4)) = v[q];
-        // activations X[:, k0:k0+64] -> B tile (rows = batch, zero-padded)
+        for (int q = 0; q < kQK / 8; ++q) *reinterpret_cast<uint4*>(arow + (swz(r, q) << 4)) = v[q];
+        // activations X[:, k0:k0+kQK] -> B tile (rows = batch, zero-padded)
         const uint32_t k0 = kbase + st * kQK;
-        for (uint32_t piece = t; piece < P.n_pad * 8; piece += kQThreads) {
-            const uint32_t b = piece >> 3, j = piece & 7;
+        for (uint32_t piece = t; piece < P.n_pad * kChunks; piece += kQThreads) {
+            const uint32_t b = piece / kChunks, j = piece % kChunks;
             uint4 xv = make_uint4(0, 0, 0, 0);
             if (b < P.n_real) xv = __ldg(reinterpret_cast<const uint4*>(J.x + (uint64_t)b * J.K + k0) + j);
-            *reinterpret_cast<uint4*>(b_tile + (b >> 3) * 1024 + (b & 7) * 128 + ((j ^ (b & 7)) << 4)) = xv;
+            *reinterpret_cast<uint4*>(b_tile + (b >> 3) * kAtom + (b & 7) * kRowB + (swz(b, j) << 4)) = xv;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (t == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t db = umma_desc_sw128(smem_u32(b_tile));
+            const uint64_t db = umma_desc(smem_u32(b_tile));
             #pragma unroll
             for (int hh = 0; hh < kTiles; ++hh) {
                 if (kTiles * pair + hh >= n_tiles) continue;
-                const uint64_t da = umma_desc_sw128(smem_u32(a_tiles + hh * kATile));
+                const uint64_t da = umma_desc(smem_u32(a_tiles + hh * kATile));
                 #pragma unroll
                 for (int kk = 0; kk < kQK / 16; ++kk) {
                     const uint32_t acc = (st > 0 || kk > 0) ? 1u : 0u;
@@ -523,7 +543,7 @@ extern "C" eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, cons
     P.k2p12 = 1u << 12;
     P.kneg2p14 = 0u - (1u << 14);
     P.k4 = 4u;
-    const uint32_t b_tile = ((P.n_pad * 128u + 1023u) & ~1023u);
+    const uint32_t b_tile = ((P.n_pad * (uint32_t)kRowB + 1023u) & ~1023u);
     const size_t smem = kTiles * kATile + b_tile + kM * 4 + kQThreads * kRingWords * 4 + 32 + 8 + 8 + 1024;
     if (blk->codec == EQ_CODEC_WORD) {
         EQ_CUDA_TRY(cudaFuncSetAttribute(k_qmatmul<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
