@@ -161,3 +161,41 @@ def test_word_decode_max_chunk_full_rows():
     g = oracle_block_to_gpu(blk)
     for v, r in zip(eq.decode_dequant([g], eq.EQ_OUT_BF16)[0], o.decode_dequant(blk)):
         assert (u16(v) == r).all()
+
+
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
+def test_decode_under_random_corruption_matches_oracle_verdicts(codec):
+    """Fuzz: random byte flips in the payload.  The GPU decoder never faults; every chunk the
+    oracle rejects makes the launch report an error; when the oracle accepts every chunk of a
+    corrupted block (a flip can yield another valid stream), the GPU output equals the
+    oracle's decode of the same corrupted bytes."""
+    layers = small_layers(seed=40, shapes=[(32, 512), (16, 1024)])
+    S = [(o.absmax_scales(W).astype(np.int32) + 1600).astype(np.uint16) for W in layers]
+    blk = o.quantize_encode(layers, scales=S, cs=512, codec=codec)
+    rng = np.random.default_rng(codec)
+    base = bytearray(blk.payload)
+    accepted = rejected = 0
+    for trial in range(40):
+        data = bytearray(base)
+        for _ in range(int(rng.integers(1, 4))):
+            data[int(rng.integers(0, len(data)))] ^= int(rng.integers(1, 256))
+        cb = o.OracleBlock(blk.layer_shapes, blk.scales, blk.freq, blk.hist, bytes(data), blk.chunk_off,
+                           blk.chunk_symbols, None, blk.fmt, codec)
+        try:
+            ref = o.decode_dequant(cb)
+        except ValueError:
+            ref = None
+        g = oracle_block_to_gpu(cb)
+        d = eq.Decoder([g], eq.EQ_OUT_BF16)
+        d()
+        if ref is None:
+            with pytest.raises(eq.EqError) as ei:
+                d.check()
+            assert ei.value.status in (eq.EQ_ERR_CORRUPT, eq.EQ_ERR_TRUNCATED)
+            rejected += 1
+        else:
+            d.check()
+            for v, r in zip(d.views()[0], ref):
+                assert (u16(v) == r).all()
+            accepted += 1
+    assert rejected > 20
