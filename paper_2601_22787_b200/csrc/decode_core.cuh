@@ -104,7 +104,7 @@ __device__ __forceinline__ uint32_t renorm_bits(uint32_t x) {
 }
 
 #ifndef EQ_ZFAST
-#define EQ_ZFAST 0
+#define EQ_ZFAST 0       // 1: the old code-0x00 bypass with the (f−1)-in-bits-8-19 LUT layout (slower)
 #endif
 // Per-block constants of the decode step.  ez = the LUT entry of code 0x00 with slot 0:
 // code 0x00 is first in code order, so its slots are [0, f0) and its entry for slot s is
@@ -148,12 +148,18 @@ __device__ __forceinline__ uint32_t decode_one(uint32_t& x, BitReader& br, const
     uint32_t e = T.ez | (slot << 20);
     if (slot >= T.f0) e = lds_u32(T.lut_s + slot * 4u);
     const uint32_t xs = mad_hi(x, 1u << 20, 0u);
-#else
-    const uint32_t xs = mad_hi(x, T.k2p20, 0u);                         // x >> 12
-    const uint32_t e = lds_u32(mad_lo(x, T.k4, mad_lo(xs, T.kneg2p14, T.lut_s)));
-#endif
     const uint32_t fm1 = mad_hi(mad_lo(e, T.k2p12, 0u), T.k2p12, 0u);   // (e >> 8) & 0xFFF
     x = mad_lo(fm1, xs, xs + (e >> 20));                                // f·⌊x/M⌋ + slot − c
+#else
+    // as decode_one_w: one IMAD.WIDE x·2^20 gives x >> 12 and slot << 20, LEA.HI the LUT
+    // address; entry layout sym | (slot − c) << 8 | (f − 1) << 20 (build_lut<1>), so one
+    // IMAD.WIDE e·2^12 gives f − 1 and (slot − c) << 20
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    const uint32_t e = lds_u32(T.lut_s + (lo >> 18));
+    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
+    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
+#endif
     const uint32_t k = renorm_bits(x);
     x = __funnelshift_lc(br.hi, x, k);
     br.hi = __funnelshift_lc(br.lo, br.hi, k);

@@ -225,7 +225,7 @@ __device__ __forceinline__ void chunk_end(const Chain& c, uint32_t* err) {
 // chunk of row 128·(2p+h)+r — cs columns [j·cs, (j+1)·cs) — and each half accumulates that
 // K-slice of its 128 × batch output in its own TMEM columns.  Every CTA does the same work
 // (one chunk per lane), so one grouped launch over all GEMMs of a block fills the GPU evenly.
-static_assert(EQ_WENTRY == 1, "k_qmatmul<true> builds the LUT in decode_one_w's entry layout");
+static_assert(EQ_WENTRY == 1 && EQ_ZFAST == 0, "k_qmatmul builds the LUT in the (f−1)-on-top entry layout");
 template <bool WORD>
 __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __grid_constant__ QmmParams P) {
     extern __shared__ __align__(1024) uint8_t dsm_raw[];
@@ -291,9 +291,8 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
                 if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
             }
             uint32_t fs = cum[lo + 1] - cum[lo];
-            // decode_one_w reads the (f−1)-on-top layout (EQ_WENTRY 1), decode_one the other
-            lut[slot] = WORD ? ((uint32_t)lo | (((uint32_t)slot - cum[lo]) << 8) | ((fs - 1) << 20))
-                             : ((uint32_t)lo | ((fs - 1) << 8) | (((uint32_t)slot - cum[lo]) << 20));
+            // decode_one_w and decode_one both read the (f−1)-on-top layout
+            lut[slot] = (uint32_t)lo | (((uint32_t)slot - cum[lo]) << 8) | ((fs - 1) << 20);
         }
     } else if (t == 0) {
         atomicOr(P.err, EQ_EF_CORRUPT);

@@ -289,7 +289,7 @@ k_decode(const __grid_constant__ DecParams P) {
     stage_commit();
 
     // ---- table: exclusive prefix of the 256 frequencies, then the slot LUT
-    if (!build_lut(B, lut, cum, P.err)) {
+    if (!build_lut<EQ_ZFAST ? 0 : 1>(B, lut, cum, P.err)) {
         stage_wait_all();
         return;
     }
