@@ -30,6 +30,8 @@ PROB_BITS = 12
 CHUNK_SYMBOLS = 4096
 FMT_E4M3, FMT_INT8 = 0, 1
 CODEC_BYTE, CODEC_WORD = 0, 1      # rANS renormalisation: bytes (R9) / 16-bit words (R14)
+CODEC_PAIR = 2                      # word rANS over pairs of symbols with escapes (R15)
+PAIR_K = 15
 
 
 def build(force: bool = False) -> str:
@@ -90,6 +92,11 @@ def lib():
             "eqo_decode_chunks_mt": (ctypes.c_int, [P, P, P, P, i64, P, P, ctypes.c_int]),
             "eqo_decode_dequant_layer_mt": (ctypes.c_int, [P, P, i64, i64, i64, i64, P, P, P, ctypes.c_int]),
             "eqo_encode_chunk_codec": (i64, [ctypes.c_int, P, i64, P, P, i64]),
+            "eqo_pair_table": (ctypes.c_int, [P, P, P, P, P]),
+            "eqo_encode_chunk_pair": (i64, [P, i64, P, P, i32, P, u16, P, i64]),
+            "eqo_decode_chunk_pair": (ctypes.c_int, [P, i64, P, P, i32, P, u16, P, i64]),
+            "eqo_encode_block_pair": (i64, [P, P, i32, i64, P, P, i32, P, u16, P, i64, P]),
+            "eqo_decode_block_pair": (ctypes.c_int, [P, P, P, i32, i64, P, P, i32, P, u16, P]),
             "eqo_decode_chunk_codec": (ctypes.c_int, [ctypes.c_int, P, i64, P, P, i64]),
             "eqo_encode_block_codec": (i64, [ctypes.c_int, P, P, i32, i64, P, P, i64, P]),
             "eqo_decode_block_codec": (ctypes.c_int, [ctypes.c_int, P, P, P, i32, i64, P, P]),
@@ -285,6 +292,53 @@ def decode_chunk(data: bytes, freq: np.ndarray, n: int, codec: int = CODEC_BYTE)
     return out[:n]
 
 
+@dataclass
+class PairTable:
+    """Tables of the pair codec (R15): rank_code uint8[16], K ranked codes, pf uint16[225]
+    pair frequencies by (ra, rb) = ra*15 + rb (0 = not kept), fesc escape frequency."""
+    rank_code: np.ndarray
+    K: int
+    pf: np.ndarray
+    fesc: int
+
+
+def pair_table(hist: np.ndarray) -> PairTable:
+    hist = np.ascontiguousarray(hist, dtype=np.uint64)
+    rc = np.zeros(16, dtype=np.uint8)
+    K = ctypes.c_int32()
+    pf = np.zeros(225, dtype=np.uint16)
+    fe = ctypes.c_uint16()
+    if lib().eqo_pair_table(_p(hist), _p(rc), ctypes.byref(K), _p(pf), ctypes.byref(fe)) != 0:
+        raise ValueError("empty")
+    return PairTable(rc, K.value, pf, fe.value)
+
+
+def encode_chunk_pair(sym: np.ndarray, freq: np.ndarray, pt: PairTable) -> bytes:
+    sym = np.ascontiguousarray(sym, dtype=np.uint8).reshape(-1)
+    freq = np.ascontiguousarray(freq, dtype=np.uint16)
+    cap = 4 + 4 * sym.size + 8
+    out = np.zeros(cap, dtype=np.uint8)
+    n = lib().eqo_encode_chunk_pair(_p(sym), sym.size, _p(freq), _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc,
+                                    _p(out), cap)
+    if n == -2:
+        raise ValueError("unknown-symbol")
+    if n < 0:
+        raise ValueError("buffer")
+    return out[:n].tobytes()
+
+
+def decode_chunk_pair(data: bytes, freq: np.ndarray, pt: PairTable, n: int) -> np.ndarray:
+    buf = np.frombuffer(data, dtype=np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
+    out = np.zeros(max(n, 1), dtype=np.uint8)
+    st = lib().eqo_decode_chunk_pair(_p(buf), len(data), _p(np.ascontiguousarray(freq, dtype=np.uint16)),
+                                     _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc, _p(out), n)
+    if st == 1:
+        raise ValueError("corrupt")
+    if st == 2:
+        raise ValueError("truncated")
+    return out[:n]
+
+
 # ---------------------------------------------------------------- block (Alg. 1 / Alg. 2)
 @dataclass
 class OracleBlock:
@@ -298,6 +352,7 @@ class OracleBlock:
     codes: np.ndarray = field(default=None, repr=False)   # concatenated symbol stream
     fmt: int = FMT_E4M3
     codec: int = CODEC_BYTE
+    pair: object = None              # PairTable (codec CODEC_PAIR)
 
     @property
     def n_params(self) -> int:
@@ -326,12 +381,20 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt:
     cap = 4 * n_chunks + 2 * stream.size + 64
     payload = np.zeros(cap, dtype=np.uint8)
     off = np.zeros(n_chunks + 1, dtype=np.uint32)
-    n = lib().eqo_encode_block_codec(codec, _p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(payload),
-                                     cap, _p(off))
+    pt = None
+    if codec == CODEC_PAIR:
+        pt = pair_table(hist)
+        cap = 4 * n_chunks + 4 * stream.size + 64
+        payload = np.zeros(cap, dtype=np.uint8)
+        n = lib().eqo_encode_block_pair(_p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(pt.rank_code),
+                                        pt.K, _p(pt.pf), pt.fesc, _p(payload), cap, _p(off))
+    else:
+        n = lib().eqo_encode_block_codec(codec, _p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(payload),
+                                         cap, _p(off))
     if n < 0:
         raise ValueError("encode failed %d" % n)
     return OracleBlock(list(layer_shapes), [np.asarray(s, dtype=np.uint16) for s in scales], freq, hist,
-                       payload[:n].tobytes(), off, cs, stream, fmt, codec)
+                       payload[:n].tobytes(), off, cs, stream, fmt, codec, pt)
 
 
 def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int = -1, oct_hi: int = 20,
@@ -359,8 +422,13 @@ def decode_block(blk: OracleBlock) -> np.ndarray:
     out = np.zeros(int(sizes.sum()), dtype=np.uint8)
     payload = np.frombuffer(blk.payload, dtype=np.uint8).copy()
     off = np.ascontiguousarray(blk.chunk_off, dtype=np.uint32)
-    st = lib().eqo_decode_block_codec(blk.codec, _p(payload), _p(off), _p(sizes), len(blk.layer_shapes),
-                                      blk.chunk_symbols, _p(blk.freq), _p(out))
+    if blk.codec == CODEC_PAIR:
+        pt = blk.pair
+        st = lib().eqo_decode_block_pair(_p(payload), _p(off), _p(sizes), len(blk.layer_shapes), blk.chunk_symbols,
+                                         _p(blk.freq), _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc, _p(out))
+    else:
+        st = lib().eqo_decode_block_codec(blk.codec, _p(payload), _p(off), _p(sizes), len(blk.layer_shapes),
+                                          blk.chunk_symbols, _p(blk.freq), _p(out))
     if st:
         raise ValueError({1: "corrupt", 2: "truncated"}[st])
     return out

@@ -761,3 +761,270 @@ int eqo_decode_dequant_layer_mt(const uint8_t* payload, const uint32_t* chunk_of
     return eqo_decode_dequant_layer_mt_codec(EQO_CODEC_BYTE, payload, chunk_off, n_chunks, cs, size, cols, scales,
                                              freq, out, threads);
 }
+
+/* ------------------------------------------------------------------------------------
+ * Pair codec (codec 2, EQO_CODEC_PAIR; reading R15): the word codec's rANS
+ * (L = 2^16, 16-bit words, M = 2^12) over PAIRS of consecutive symbols of a chunk, for
+ * the block's most frequent symbols, with an escape to single symbols.  The paper fixes no
+ * wire format (nvCOMP's is undocumented); the symbols are modelled i.i.d. (the
+ * factorisation of P:160-168), so a pair's probability is the product of its symbols'.
+ *
+ * Tables (from the block histogram, integers only):
+ *  - ranks: present codes by count descending, ties by lower code; the first
+ *    K = min(15, #present) get ranks 0..K-1 (rank_code[r] = code);
+ *  - pair weights w(ra, rb) = c[code_ra]·c[code_rb] over the ranked codes (T = Σc, total T²);
+ *    a pair is KEPT when its ideal frequency is at least one slot, M·w ≥ T²;
+ *  - escape weight = T² − Σ kept w (all other pairs); the vector [kept pairs in (ra, rb)
+ *    lexicographic order, escape] is normalised to M by the R8 rule (eqo_normalize's rule on
+ *    128-bit numerators; escape present iff its weight is > 0); cum in that order, so the
+ *    escape owns the top slots;
+ *  - the single-symbol table is the R8 table of the histogram (eqo_normalize).
+ * Chunk of n symbols: pairs (s[2i], s[2i+1]), i < ⌊n/2⌋, in order, then s[n−1] with the
+ * single table if n is odd.  A pair whose two codes are ranked and whose (ra, rb) is kept is
+ * one pair-table symbol; otherwise the escape (pair table) followed by the two codes
+ * (single table).  The encoder works in reverse (for an escaped pair: b, a, then escape).
+ * ---------------------------------------------------------------------------------- */
+#define EQO_CODEC_PAIR 2
+#define EQO_PAIR_K 15
+
+/* R8 normalisation of n weights (total W) to M; pres[i] = weight > 0. */
+static void eqo_normalize_w(const unsigned __int128* w, int n, unsigned __int128 W, int64_t* f)
+{
+    unsigned __int128 r[EQO_PAIR_K * EQO_PAIR_K + 1];
+    int64_t sum = 0;
+    for (int i = 0; i < n; i++) {
+        if (w[i] == 0) { f[i] = 0; r[i] = 0; continue; }
+        unsigned __int128 num = (unsigned __int128)EQO_M * w[i];
+        unsigned __int128 q = num / W;
+        r[i] = num % W;
+        f[i] = q < 1 ? 1 : (int64_t)q;
+        sum += f[i];
+    }
+    int64_t D = (int64_t)EQO_M - sum;
+    if (D > 0) {
+        int taken[EQO_PAIR_K * EQO_PAIR_K + 1] = {0};
+        for (int64_t k = 0; k < D; k++) {
+            int b = -1;
+            for (int i = 0; i < n; i++) {
+                if (w[i] == 0 || taken[i]) continue;
+                if (b < 0 || r[i] > r[b] || (r[i] == r[b] && w[i] > w[b])) b = i;
+            }
+            taken[b] = 1;
+            f[b] += 1;
+        }
+    }
+    while (D < 0) {
+        int b = -1;
+        for (int i = 0; i < n; i++)
+            if (f[i] > 1 && (b < 0 || f[i] > f[b])) b = i;
+        f[b] -= 1;
+        D += 1;
+    }
+}
+
+/* Builds the pair tables.  rank_code[16] (unused ranks 0), *K, pf[15*15] = pair frequency
+ * by (ra, rb) (0 = not kept), *fesc = escape frequency.  Returns 0, or -1 for an empty
+ * histogram. */
+int eqo_pair_table(const uint64_t hist[256], uint8_t rank_code[16], int32_t* K_out, uint16_t pf[225],
+                   uint16_t* fesc)
+{
+    uint64_t T = 0;
+    for (int c = 0; c < 256; c++) T += hist[c];
+    if (T == 0) return -1;
+    /* ranks: repeated selection of the largest count, lower code first on ties */
+    int used[256] = {0}, K = 0;
+    memset(rank_code, 0, 16);
+    for (; K < EQO_PAIR_K; K++) {
+        int b = -1;
+        for (int c = 0; c < 256; c++)
+            if (hist[c] && !used[c] && (b < 0 || hist[c] > hist[b])) b = c;
+        if (b < 0) break;
+        used[b] = 1;
+        rank_code[K] = (uint8_t)b;
+    }
+    const unsigned __int128 W = (unsigned __int128)T * T;
+    unsigned __int128 w[EQO_PAIR_K * EQO_PAIR_K + 1];
+    int idx[EQO_PAIR_K * EQO_PAIR_K];
+    int n = 0;
+    unsigned __int128 kept = 0;
+    for (int ra = 0; ra < K; ra++)
+        for (int rb = 0; rb < K; rb++) {
+            unsigned __int128 x = (unsigned __int128)hist[rank_code[ra]] * hist[rank_code[rb]];
+            if ((unsigned __int128)EQO_M * x >= W) {
+                w[n] = x;
+                idx[n] = ra * EQO_PAIR_K + rb;
+                kept += x;
+                n++;
+            }
+        }
+    w[n] = W - kept;                 /* escape: every other pair */
+    int64_t f[EQO_PAIR_K * EQO_PAIR_K + 1];
+    eqo_normalize_w(w, n + 1, W, f);
+    for (int i = 0; i < 225; i++) pf[i] = 0;
+    for (int i = 0; i < n; i++) pf[idx[i]] = (uint16_t)f[i];
+    *fesc = (uint16_t)f[n];
+    *K_out = K;
+    return 0;
+}
+
+/* cumulative pair table in cum order: kept pairs lexicographic by (ra, rb), escape last */
+static void eqo_pair_cum(const uint16_t pf[225], int K, uint32_t pcum[225], uint32_t* cesc)
+{
+    uint32_t run = 0;
+    for (int ra = 0; ra < EQO_PAIR_K; ra++)
+        for (int rb = 0; rb < EQO_PAIR_K; rb++) {
+            int i = ra * EQO_PAIR_K + rb;
+            pcum[i] = run;
+            if (ra < K && rb < K) run += pf[i];
+        }
+    *cesc = run;
+}
+
+/* one rANS encode step with the word codec's renormalisation (units emitted back to front) */
+static void eqo_w_put(uint64_t* x, uint32_t f, uint32_t c, uint8_t* tmp, int64_t* pos)
+{
+    const uint64_t L = 1u << 16;
+    uint64_t x_max = ((L >> EQO_PROB_BITS) << 16) * f;
+    while (*x >= x_max) {
+        *pos -= 2;
+        tmp[*pos] = (uint8_t)(*x & 0xFF);
+        tmp[*pos + 1] = (uint8_t)((*x >> 8) & 0xFF);
+        *x >>= 16;
+    }
+    *x = (*x / f) * EQO_M + (*x % f) + c;
+}
+
+int64_t eqo_encode_chunk_pair(const uint8_t* sym, int64_t n, const uint16_t freq[256], const uint8_t rank_code[16],
+                              int32_t K, const uint16_t pf[225], uint16_t fesc, uint8_t* out, int64_t cap)
+{
+    uint32_t cum[257], pcum[225], cesc;
+    eqo_cum(freq, cum);
+    eqo_pair_cum(pf, K, pcum, &cesc);
+    int rank[256];
+    for (int c = 0; c < 256; c++) rank[c] = -1;
+    for (int r = 0; r < K; r++) rank[rank_code[r]] = r;
+    int64_t tcap = 4 + 4 * n + 8;
+    uint8_t* tmp = (uint8_t*)malloc((size_t)tcap);
+    int64_t pos = tcap;
+    uint64_t x = 1u << 16;
+    if (n & 1) {
+        uint8_t s = sym[n - 1];
+        if (freq[s] == 0) { free(tmp); return -2; }
+        eqo_w_put(&x, freq[s], cum[s], tmp, &pos);
+    }
+    for (int64_t i = n / 2 - 1; i >= 0; i--) {
+        uint8_t a = sym[2 * i], b = sym[2 * i + 1];
+        if (freq[a] == 0 || freq[b] == 0) { free(tmp); return -2; }
+        int ra = rank[a], rb = rank[b];
+        if (ra >= 0 && rb >= 0 && pf[ra * EQO_PAIR_K + rb] > 0) {
+            eqo_w_put(&x, pf[ra * EQO_PAIR_K + rb], pcum[ra * EQO_PAIR_K + rb], tmp, &pos);
+        } else {
+            if (fesc == 0) { free(tmp); return -2; }
+            eqo_w_put(&x, freq[b], cum[b], tmp, &pos);
+            eqo_w_put(&x, freq[a], cum[a], tmp, &pos);
+            eqo_w_put(&x, fesc, cesc, tmp, &pos);
+        }
+    }
+    pos -= 4;
+    for (int k = 0; k < 4; k++) tmp[pos + k] = (uint8_t)((x >> (8 * k)) & 0xFF);
+    int64_t len = tcap - pos;
+    if (len > cap) { free(tmp); return -1; }
+    memcpy(out, tmp + pos, (size_t)len);
+    free(tmp);
+    return len;
+}
+
+/* one rANS decode step: slot, then the caller's symbol lookup, state update, renormalise */
+static int eqo_w_get(uint64_t* x, uint32_t f, uint32_t c, uint32_t slot, const uint8_t* in, int64_t nbytes,
+                     int64_t* p)
+{
+    *x = (uint64_t)f * (*x / EQO_M) + slot - c;
+    while (*x < (1u << 16)) {
+        if (*p + 2 > nbytes) return 2;
+        *x = (*x << 16) | (uint64_t)in[*p] | ((uint64_t)in[*p + 1] << 8);
+        *p += 2;
+    }
+    return 0;
+}
+
+int eqo_decode_chunk_pair(const uint8_t* in, int64_t nbytes, const uint16_t freq[256], const uint8_t rank_code[16],
+                          int32_t K, const uint16_t pf[225], uint16_t fesc, uint8_t* sym, int64_t n)
+{
+    uint32_t cum[257], pcum[225], cesc;
+    eqo_cum(freq, cum);
+    eqo_pair_cum(pf, K, pcum, &cesc);
+    if (nbytes < 4) return 2;
+    uint64_t x = (uint64_t)in[0] | ((uint64_t)in[1] << 8) | ((uint64_t)in[2] << 16) | ((uint64_t)in[3] << 24);
+    int64_t p = 4;
+    for (int64_t i = 0; i < n / 2; i++) {
+        uint32_t slot = (uint32_t)(x % EQO_M);
+        if (slot >= cesc) {                                   /* escape, then two singles */
+            if (eqo_w_get(&x, fesc, cesc, slot, in, nbytes, &p)) return 2;
+            for (int k = 0; k < 2; k++) {
+                uint32_t sl = (uint32_t)(x % EQO_M);
+                int s = 0;
+                while (!(cum[s] <= sl && sl < cum[s + 1])) s++;
+                sym[2 * i + k] = (uint8_t)s;
+                if (eqo_w_get(&x, freq[s], cum[s], sl, in, nbytes, &p)) return 2;
+            }
+        } else {
+            int j = -1;                                      /* the kept pair owning slot */
+            for (int q = 0; q < 225 && j < 0; q++) {
+                int ra = q / EQO_PAIR_K, rb = q % EQO_PAIR_K;
+                if (ra < K && rb < K && pf[q] && pcum[q] <= slot && slot < pcum[q] + pf[q]) j = q;
+            }
+            if (j < 0) return 1;
+            sym[2 * i] = rank_code[j / EQO_PAIR_K];
+            sym[2 * i + 1] = rank_code[j % EQO_PAIR_K];
+            if (eqo_w_get(&x, pf[j], pcum[j], slot, in, nbytes, &p)) return 2;
+        }
+    }
+    if (n & 1) {
+        uint32_t sl = (uint32_t)(x % EQO_M);
+        int s = 0;
+        while (!(cum[s] <= sl && sl < cum[s + 1])) s++;
+        sym[n - 1] = (uint8_t)s;
+        if (eqo_w_get(&x, freq[s], cum[s], sl, in, nbytes, &p)) return 2;
+    }
+    if (x != (1u << 16) || p != nbytes) return 1;
+    return 0;
+}
+
+/* block stream of the pair codec (same chunking as eqo_encode_block) */
+int64_t eqo_encode_block_pair(const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers, int64_t cs,
+                              const uint16_t freq[256], const uint8_t rank_code[16], int32_t K, const uint16_t pf[225],
+                              uint16_t fesc, uint8_t* payload, int64_t cap, uint32_t* chunk_off)
+{
+    int64_t pos = 0, k = 0, sbase = 0;
+    for (int32_t l = 0; l < n_layers; l++) {
+        for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
+            int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
+            chunk_off[k++] = (uint32_t)pos;
+            int64_t len = eqo_encode_chunk_pair(codes + sbase + a, n, freq, rank_code, K, pf, fesc, payload + pos,
+                                                cap - pos);
+            if (len < 0) return len;
+            pos += len;
+        }
+        sbase += layer_sizes[l];
+    }
+    chunk_off[k] = (uint32_t)pos;
+    return pos;
+}
+
+int eqo_decode_block_pair(const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
+                          int32_t n_layers, int64_t cs, const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
+                          const uint16_t pf[225], uint16_t fesc, uint8_t* codes)
+{
+    int64_t k = 0, sbase = 0;
+    for (int32_t l = 0; l < n_layers; l++) {
+        for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
+            int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
+            int st = eqo_decode_chunk_pair(payload + chunk_off[k], (int64_t)chunk_off[k + 1] - chunk_off[k], freq,
+                                           rank_code, K, pf, fesc, codes + sbase + a, n);
+            if (st) return st;
+            k++;
+        }
+        sbase += layer_sizes[l];
+    }
+    return 0;
+}

@@ -240,3 +240,56 @@ def test_block_two_bits_unique_codes_and_budget(codec):
     assert int((blk.hist > 0).sum()) > 12
     coded = len(blk.payload) + 4 * (blk.n_chunks + 1)
     assert coded <= 1.02 * blk.n_params * H / 8
+
+
+# ------------------------------------------------------------------ pair codec (R15; round-2 groundwork)
+def test_pair_table_rules():
+    """Integer table rules: ranks by count (ties: lower code), pairs kept iff M·c_a·c_b ≥ T²,
+    the R8 rule over [kept pairs, escape] sums to M, escape present iff some pair is not
+    kept; a single-symbol histogram gives one pair of frequency M."""
+    h = hist_of({7: 10})
+    pt = o.pair_table(h)
+    assert pt.K == 1 and pt.rank_code[0] == 7 and pt.pf[0] == 4096 and pt.fesc == 0
+    h = hist_of({3: 50, 9: 50, 200: 1})
+    pt = o.pair_table(h)
+    assert list(pt.rank_code[:3]) == [3, 9, 200]                      # tie 3/9 -> lower code first
+    T = 101
+    for ra in range(pt.K):
+        for rb in range(pt.K):
+            w = int(h[pt.rank_code[ra]]) * int(h[pt.rank_code[rb]])
+            assert (pt.pf[ra * 15 + rb] > 0) == (4096 * w >= T * T)
+    assert int(pt.pf.sum()) + pt.fesc == 4096 and pt.fesc > 0
+    # 20 equiprobable codes: only the top 15 are ranked; everything else escapes
+    h = np.zeros(256, np.uint64)
+    h[np.arange(20) * 7] = 1000
+    pt = o.pair_table(h)
+    assert pt.K == 15 and int(pt.pf.sum()) + pt.fesc == 4096 and (pt.pf > 0).sum() == 225
+
+
+@pytest.mark.parametrize("kind", ["skewed", "uniform", "subset2", "single", "subset40"])
+def test_pair_codec_round_trip_and_rate(kind):
+    rng = np.random.default_rng(hash(kind) & 0xFFFF)
+    for t in range(6):
+        n = int(rng.choice([1, 2, 3, 17, 4095, 4097, int(rng.integers(1, 12000))]))
+        s = eqsynth.random_codes_stream(n, int(rng.integers(1 << 30)), kind)
+        h = o.histogram(s)
+        f = o.normalize(h)
+        pt = o.pair_table(h)
+        data = o.encode_chunk_pair(s, f, pt)
+        assert (o.decode_chunk_pair(data, f, pt, n) == s).all()
+        assert 8 * len(data) >= emp_entropy_bits(h) - 0.001 * n - 32     # Shannon (i.i.d. pairs)
+    with pytest.raises(ValueError):
+        o.decode_chunk_pair(data[:-2], f, pt, n)
+
+
+def test_pair_codec_block_rate_at_two_bits():
+    """Pair coding of the bench's synthetic 2-bit weights: lossless, and within 1.5 % of the
+    word codec's payload (the pair table's quantisation and the escapes cost ~1 %)."""
+    W = eqsynth.weights(32, 4096, seed=2)
+    S = o.search(W, 230.0)[0]
+    bw = o.quantize_encode([W], scales=[S], codec=o.CODEC_WORD)
+    bp = o.quantize_encode([W], scales=[S], codec=o.CODEC_PAIR)
+    assert (o.decode_block(bp) == bp.codes).all()
+    assert len(bp.payload) <= 1.015 * len(bw.payload)
+    H = o.entropy(bp.hist)
+    assert len(bp.payload) + 4 * (bp.n_chunks + 1) <= 1.025 * W.numel() * H / 8
