@@ -35,7 +35,7 @@ FALLBACK_HBM_GBS = 6650.0            # B200_PROFILING.md fallback, used only wit
 DEFAULT_LAMBDA = 230.2               # reference arm only: the GPU calibration of λ for 2.0 bits
 
 
-CODECS = {"byte": 0, "word": 1}     # EQ_CODEC_BYTE / EQ_CODEC_WORD (include/entquant.h)
+CODECS = {"byte": 0, "word": 1, "pair": 2}     # EQ_CODEC_* (include/entquant.h)
 
 
 def parse():
@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--no-fp8", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
-    ap.add_argument("--codec", default="word", choices=["byte", "word"],
+    ap.add_argument("--codec", default="word", choices=["byte", "word", "pair"],
                     help="rANS renormalisation: byte (SPEC S:355, R9) or 16-bit word (R14)")
     return ap.parse_args()
 
@@ -385,8 +385,8 @@ def main():
 
     # ---- CPU baseline: the oracle on the host cores, rank 0, N=1, bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cpu = cpu_baseline(blocks, args.cpu_seconds)
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile and args.codec != "pair":
+        cpu = cpu_baseline(blocks, args.cpu_seconds)       # (the oracle's pair decoder has no mt timing helper)
 
     if rank == 0:
         cs = clocks.summary() if clocks is not None else None

@@ -61,6 +61,11 @@ typedef enum {
 #define EQ_CODEC_BYTE 0u            /* L = 2^23, byte units (≤ 2 per symbol)    */
 #define EQ_CODEC_WORD 1u            /* R14: L = 2^16, 16-bit little-endian word units       */
                                     /* (≤ 1 per symbol: the GPU decoder's fast path)         */
+#define EQ_CODEC_PAIR 2u            /* R15: the word codec over PAIRS of the block's top-15   */
+                                    /* codes, escape to singles; eq_block.freq then holds   */
+                                    /* 512 u16: [0,256) single table, [256,481) pair table  */
+                                    /* by ra*15+rb, [481] escape, [482] K, [484,492) rank   */
+                                    /* codes as bytes                                        */
 
 #define EQ_SCALES_SEARCH 0u         /* exhaustive per-row Eq. 4 minimisation (R5)          */
 #define EQ_SCALES_ABSMAX 1u         /* AbsMax scales, Eq. 1 (the λ = 0 lossless-FP8 rate)  */
@@ -87,7 +92,7 @@ typedef struct {
     int32_t  oct_lo, oct_hi;        /* search bracket, octaves around AbsMax (R5): -1, 20  */
     uint32_t exclude_mask;          /* bit l: layer l keeps AbsMax scales (λ = 0) — the    */
                                     /* super-weight exclusion of P:393-396          */
-    uint32_t codec;                 /* EQ_CODEC_BYTE (0, default) | EQ_CODEC_WORD          */
+    uint32_t codec;                 /* EQ_CODEC_BYTE (0, default) | _WORD | _PAIR          */
 } eq_params;
 
 /* One compressed transformer block: all its layers in one bitstream with one table
@@ -101,6 +106,7 @@ typedef struct {
     uint32_t  n_chunks;
     uint32_t  chunk_symbols;        /* chunk length used when encoding                     */
     uint16_t* freq;                 /* device: 256 normalised frequencies, Σ = 4096       */
+                                    /* (512 u16 for EQ_CODEC_PAIR, see above)             */
     uint16_t* scales;               /* device: bf16 per-row scales, layers concatenated   */
     uint32_t  n_layers;
     uint32_t  format;               /* EQ_FMT_* of the symbols (set by eq_quantize_encode) */

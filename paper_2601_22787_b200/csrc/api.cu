@@ -32,7 +32,7 @@ eq_status check_params(const eq_params* p) {
     if (p->format > EQ_FMT_INT8 || p->prob_bits != EQ_PROB_BITS) return EQ_ERR_ARG;
     if (p->chunk_symbols == 0 || p->chunk_symbols > 262144u) return EQ_ERR_ARG;
     if (p->scale_mode > EQ_SCALES_GIVEN) return EQ_ERR_ARG;
-    if (p->codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
+    if (p->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
     if (p->scale_mode == EQ_SCALES_SEARCH && !(p->lambda >= 0.0)) return EQ_ERR_ARG;
     return EQ_OK;
 }
@@ -88,6 +88,79 @@ eq_status err_to_status(uint32_t e) {
     return EQ_OK;
 }
 
+// EQ_CODEC_PAIR tables (reading R15) from the block histogram, host integer arithmetic:
+// ranks = the 15 most frequent codes (ties: lower code); pair (ra, rb) kept iff
+// M·c_a·c_b ≥ T²; escape weight = T² − Σ kept; the R8 largest-remainder rule over
+// [kept pairs in (ra, rb) order, escape] to M.  Writes table[256..511] (include/entquant.h).
+void pair_table_host(const uint64_t hist[256], uint16_t table_hi[256]) {
+    typedef unsigned __int128 u128;
+    uint64_t T = 0;
+    for (int c = 0; c < 256; ++c) T += hist[c];
+    memset(table_hi, 0, 512);
+    if (T == 0) return;
+    int rank_code[15], K = 0;
+    bool used[256] = {false};
+    for (; K < 15; ++K) {
+        int b = -1;
+        for (int c = 0; c < 256; ++c)
+            if (hist[c] && !used[c] && (b < 0 || hist[c] > hist[b])) b = c;
+        if (b < 0) break;
+        used[b] = true;
+        rank_code[K] = b;
+    }
+    const u128 W = (u128)T * T;
+    std::vector<u128> w;
+    std::vector<int> idx;
+    u128 kept = 0;
+    for (int ra = 0; ra < K; ++ra)
+        for (int rb = 0; rb < K; ++rb) {
+            const u128 x = (u128)hist[rank_code[ra]] * hist[rank_code[rb]];
+            if ((u128)kM * x >= W) {
+                w.push_back(x);
+                idx.push_back(ra * 15 + rb);
+                kept += x;
+            }
+        }
+    w.push_back(W - kept);
+    const int n = (int)w.size();
+    std::vector<int64_t> f(n);
+    std::vector<u128> r(n);
+    int64_t sum = 0;
+    for (int i = 0; i < n; ++i) {
+        if (w[i] == 0) { f[i] = 0; r[i] = 0; continue; }
+        const u128 num = (u128)kM * w[i];
+        const u128 q = num / W;
+        r[i] = num % W;
+        f[i] = q < 1 ? 1 : (int64_t)q;
+        sum += f[i];
+    }
+    int64_t D = (int64_t)kM - sum;
+    if (D > 0) {
+        std::vector<bool> taken(n, false);
+        for (int64_t k = 0; k < D; ++k) {
+            int b = -1;
+            for (int i = 0; i < n; ++i) {
+                if (w[i] == 0 || taken[i]) continue;
+                if (b < 0 || r[i] > r[b] || (r[i] == r[b] && w[i] > w[b])) b = i;
+            }
+            taken[b] = true;
+            f[b] += 1;
+        }
+    }
+    while (D < 0) {
+        int b = -1;
+        for (int i = 0; i < n; ++i)
+            if (f[i] > 1 && (b < 0 || f[i] > f[b])) b = i;
+        f[b] -= 1;
+        D += 1;
+    }
+    for (int i = 0; i + 1 < n; ++i) table_hi[idx[i]] = (uint16_t)f[i];   // [256 + q] -> hi[q]
+    table_hi[225] = (uint16_t)f[n - 1];                                 // [481] escape
+    table_hi[226] = (uint16_t)K;                                        // [482]
+    uint8_t* rc = reinterpret_cast<uint8_t*>(table_hi + 228);           // [484, 492)
+    for (int i = 0; i < K; ++i) rc[i] = (uint8_t)rank_code[i];
+}
+
 }  // namespace
 
 extern "C" const char* eq_status_string(eq_status s) {
@@ -117,7 +190,8 @@ extern "C" eq_status eq_encode_bounds(const eq_tensor* layers, uint32_t n_layers
     const uint64_t nc = count_chunks(layers, n_layers, p->chunk_symbols);
     // worst case per chunk: 4-byte state + at most 2 renormalisation bytes per symbol
     // (two bytes, EQ_CODEC_BYTE, or one 16-bit word, EQ_CODEC_WORD)
-    const uint64_t cap = align_up(4 * nc + 2 * syms + EQ_PAYLOAD_SLACK, 256);
+    // (EQ_CODEC_PAIR: an escaped pair is three words for two symbols)
+    const uint64_t cap = align_up(4 * nc + (p->codec == EQ_CODEC_PAIR ? 3 : 2) * syms + EQ_PAYLOAD_SLACK, 256);
     if (payload_cap) *payload_cap = cap;
     if (n_chunks) *n_chunks = (uint32_t)nc;
     if (scratch_bytes) *scratch_bytes = carve(layers, n_layers, (uint32_t)nc, nullptr).bytes;
@@ -175,6 +249,15 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
     }
     // metadata ℳ and Alg. 1 l.4-5
     EQ_TRY(eq_build_table(S.hist, out->freq, S.err, stream));
+    if (p->codec == EQ_CODEC_PAIR) {               // the pair table is built on the host (R15)
+        uint64_t h[256];
+        uint16_t hi[256];
+        EQ_CUDA_TRY(cudaMemcpyAsync(h, S.hist, sizeof(h), cudaMemcpyDeviceToHost, st));
+        EQ_CUDA_TRY(cudaStreamSynchronize(st));
+        pair_table_host(h, hi);
+        EQ_CUDA_TRY(cudaMemcpyAsync(out->freq + 256, hi, sizeof(hi), cudaMemcpyHostToDevice, st));
+        EQ_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     EQ_TRY(eq_rans_encode(S.codes, out, S.sizes, S.total, S.err, stream));
     uint64_t total = 0;
     uint32_t e = 0;

@@ -69,8 +69,10 @@ struct DecParams {
 // entry = s | (f_s − 1) << 8 | (slot − cum[s]) << 20 (LAYOUT 0) or
 //         s | (slot − cum[s]) << 8 | (f_s − 1) << 20 (LAYOUT 1, decode_one_w).
 // Returns false (EQ_EF_CORRUPT set once) if the frequencies do not sum to M.
-template <int LAYOUT = 0, int NT = kDecThreads>
-__device__ __forceinline__ bool build_lut(const DecBlock& B, uint32_t* lut, uint32_t* cum, uint32_t* err) {
+// cum[257] = exclusive prefix of the block's 256 single-symbol frequencies (all NT threads);
+// false (EQ_EF_CORRUPT set once) if they do not sum to M
+template <int NT>
+__device__ __forceinline__ bool build_cum(const DecBlock& B, uint32_t* cum, uint32_t* err) {
     static_assert(NT >= 256 || 256 % NT == 0, "thread count");
     const int t = threadIdx.x;
     {
@@ -104,6 +106,13 @@ __device__ __forceinline__ bool build_lut(const DecBlock& B, uint32_t* lut, uint
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
         return false;
     }
+    return true;
+}
+
+template <int LAYOUT = 0, int NT = kDecThreads>
+__device__ __forceinline__ bool build_lut(const DecBlock& B, uint32_t* lut, uint32_t* cum, uint32_t* err) {
+    const int t = threadIdx.x;
+    if (!build_cum<NT>(B, cum, err)) return false;
     auto entry = [&](uint32_t slot, int sym) -> uint32_t {
         const uint32_t fs = cum[sym + 1] - cum[sym];
         return LAYOUT == 0 ? ((uint32_t)sym | ((fs - 1) << 8) | ((slot - cum[sym]) << 20))
@@ -541,6 +550,225 @@ k_decode_w(const __grid_constant__ DecParams P) {
     }
 }
 
+
+// ================================================================ EQ_CODEC_PAIR decoder (R15)
+// Word-codec rANS over pairs of symbols: one LUT lookup and at most one 16-bit word per TWO
+// symbols for the block's top-15 codes; an escape (top slots) decodes two singles by binary
+// search over the single table.  Table buffer (u16[512], see include/entquant.h): [0,256)
+// single frequencies, [256,481) pair frequencies by ra·15 + rb, [481] escape frequency,
+// [482] K, [484,492) the 16 rank codes as bytes.
+constexpr int kPairOff = 256, kFescIdx = 481, kKIdx = 482, kRankIdx = 484;
+
+struct PairTab {
+    uint32_t lut_s;        // shared address of the pair LUT (4096 × u32: nib | bias << 8 | (f−1) << 20)
+    uint32_t lut1_s;       // shared address of the single-symbol LUT (escapes; EQ_PAIR_LUT1)
+    uint32_t esc_lo;       // slot << 20 at and above which a pair step is the escape (0xFFFFFFFF: none)
+    uint32_t fesc, cesc;   // escape frequency and cumulative start
+    uint32_t rc0, rc1, rc2, rc3;   // rank codes 0..15 as bytes
+    uint32_t k2p20, k2p12;
+    const uint32_t* cum;   // single-table cumulative frequencies (shared, 257)
+};
+
+__device__ __forceinline__ void renorm_w(uint32_t& x, WordReader& r) {
+    if (x < kLw) {
+        x = __byte_perm(r.w, x, 0x5410);                                // (x << 16) | w
+        r.w = lds_u16(r.ring | (r.Q & (kWRing - 1)));
+        r.Q += 2;
+    }
+}
+
+#ifndef EQ_PAIR_LUT1
+#define EQ_PAIR_LUT1 1   // escapes decode their two singles with a single-symbol LUT (else binary search)
+#endif
+// a single-table symbol (escape path and odd tails)
+__device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, const PairTab& T) {
+#if EQ_PAIR_LUT1
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    const uint32_t e = lds_u32(T.lut1_s + (lo >> 18));
+    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);
+    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));
+    renorm_w(x, r);
+    return e & 0xFFu;
+#else
+    const uint32_t slot = x & (kM - 1);
+    int lo = 0, hi = 255;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (T.cum[mid] <= slot) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t c = T.cum[lo], f = T.cum[lo + 1] - c;
+    x = f * (x >> 12) + slot - c;
+    renorm_w(x, r);
+    return (uint32_t)lo;
+#endif
+}
+
+// one pair step; returns the two codes in the low 16 bits (first symbol in the low byte)
+__device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, const PairTab& T, const uint8_t* payload) {
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    if (lo >= T.esc_lo) {                          // escape: its step, then two singles
+        x = T.fesc * xs + (lo >> 20) - T.cesc;
+        renorm_w(x, r);
+#ifndef EQ_PAIR_ESCRING
+#define EQ_PAIR_ESCRING 1
+#endif
+        if (EQ_PAIR_ESCRING) ring_step_w(r, payload);   // up to 2 more words follow: keep the ring ahead
+        const uint32_t a = decode_single_p(x, r, T);
+        const uint32_t b = decode_single_p(x, r, T);
+        return a | (b << 8);
+    }
+    const uint32_t e = lds_u32(T.lut_s + (lo >> 18));
+    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
+    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
+    renorm_w(x, r);
+    // rank nibbles -> codes: bytes of {rc0, rc1} for ranks 0-7, of {rc2, rc3} for 8-15,
+    // chosen per byte by the nibble's bit 3 (PRMT sign-replicate of bits 3 and 7 of e)
+    const uint32_t sel = e & 0x77u;
+    const uint32_t t1 = __byte_perm(T.rc0, T.rc1, sel), t2 = __byte_perm(T.rc2, T.rc3, sel);
+    uint32_t m;                                    // PTX prmt: selector bit 3 = replicate the msb
+    asm("prmt.b32 %0, %1, %2, 0xC8;" : "=r"(m) : "r"(e << 4), "r"(e));
+    return (t1 & ~m) | (t2 & m);
+}
+
+// the pair LUT (and the single cum for escapes) of one block, all NT threads
+template <int NT>
+__device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut, uint32_t* cum, uint32_t* pcum,
+                                               uint32_t* err) {
+    const int t = threadIdx.x;
+    if (!build_cum<NT>(B, cum, err)) return false;
+    const uint32_t K = B.freq[kKIdx];
+    if (t == 0) {                                  // 226-entry pair cum: (ra, rb) order, escape last
+        uint32_t run = 0;
+        for (int q = 0; q < 225; ++q) {
+            pcum[q] = run;
+            if ((uint32_t)(q / 15) < K && (uint32_t)(q % 15) < K) run += B.freq[kPairOff + q];
+        }
+        pcum[225] = run;
+        pcum[226] = run + B.freq[kFescIdx];
+    }
+    __syncthreads();
+    if (pcum[226] != kM || K > 15) {
+        if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
+        return false;
+    }
+    for (int slot = t; slot < (int)kM; slot += NT) {
+        int lo = 0, hi = 225;                      // largest q with pcum[q] <= slot
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pcum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t f = lo < 225 ? B.freq[kPairOff + lo] : B.freq[kFescIdx];
+        const uint32_t nib = lo < 225 ? (uint32_t)((lo / 15) | ((lo % 15) << 4)) : 0xFFu;
+        lut[slot] = nib | (((uint32_t)slot - pcum[lo]) << 8) | ((f - 1) << 20);
+    }
+    return true;
+}
+
+template <bool BF16>
+__device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload, const PairTab& T) {
+    if (!c.active || c.runaway) return;
+    const uint32_t qlim = c.e + (2 + kWBias);
+    if (c.fast) {
+        const uint32_t G = BF16 ? 16 : 32;
+        while (c.i + G <= c.n) {
+            uint32_t q[8];
+            #pragma unroll
+            for (int k = 0; k < (BF16 ? 4 : 8); ++k) {
+                const uint32_t a = decode_pair(c.x, c.r, T, payload);
+                const uint32_t b = decode_pair(c.x, c.r, T, payload);
+                q[k] = __byte_perm(a, b, 0x5410);
+                if ((k & 3) == 3) ring_step_w(c.r, payload);
+            }
+            if (BF16) store16_bf16(c, q);
+            else st_out32(c.out + c.i, make_uint4(q[0], q[1], q[2], q[3]), make_uint4(q[4], q[5], q[6], q[7]));
+            c.i += G;
+            if (c.r.Q > qlim) { c.runaway = true; return; }
+        }
+    }
+    uint32_t k = 0;                                // generic / ragged tail
+    for (; c.i + 2 <= c.n; c.i += 2) {
+        const uint32_t ab = decode_pair(c.x, c.r, T, payload);
+        if ((++k & 7) == 0) ring_step_w(c.r, payload);
+        #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            store_one<BF16>(c.out, c.i + h, (ab >> (8 * h)) & 0xFFu, c.s, c.i8);
+            if (BF16 && ++c.col == c.cols) {
+                c.col = 0;
+                ++c.row;
+                if (c.i + h + 1 < c.n) c.s = bf16_bits_to_float(c.sc[c.row]);
+            }
+        }
+        if (c.r.Q > qlim) { c.runaway = true; return; }
+    }
+    if (c.i < c.n) {                               // odd chunk: the last symbol is a single
+        const uint32_t s1 = decode_single_p(c.x, c.r, T);
+        store_one<BF16>(c.out, c.i, s1, c.s, c.i8);
+        ++c.i;
+    }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kWThreads, EQ_DECW_MIN_CTAS)
+k_decode_p(const __grid_constant__ DecParams P) {
+    extern __shared__ __align__(128) uint8_t rings[];      // kWThreads × kWRing
+    __shared__ __align__(16) uint32_t lut[kM];
+    __shared__ uint32_t cum[257];
+    __shared__ uint32_t pcum[227];
+#if EQ_PAIR_LUT1
+    __shared__ __align__(16) uint32_t lut1[kM];
+#endif
+
+    uint32_t bi = 0;
+    while (bi + 1 < P.n_blocks && blockIdx.x >= P.b[bi + 1].cta0) ++bi;
+    const DecBlock& B = P.b[bi];
+    const int t = threadIdx.x;
+    ChainW c;
+    chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kWThreads + t,
+                        (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
+    stage_commit();
+    if (!build_pair_lut<kWThreads>(B, lut, cum, pcum, P.err)) {
+        stage_wait_all();
+        return;
+    }
+#if EQ_PAIR_LUT1
+    {                                              // single LUT in decode_one_w's entry layout
+        auto entry = [&](uint32_t slot, int sym) -> uint32_t {
+            const uint32_t fs = cum[sym + 1] - cum[sym];
+            return (uint32_t)sym | ((slot - cum[sym]) << 8) | ((fs - 1) << 20);
+        };
+        for (int slot = t; slot < (int)kM; slot += kWThreads) {
+            int lo = 0, hi = 255;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+            }
+            lut1[slot] = entry((uint32_t)slot, lo);
+        }
+    }
+#endif
+    stage_wait_all();
+    __syncthreads();
+    PairTab T;
+    T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
+#if EQ_PAIR_LUT1
+    T.lut1_s = (uint32_t)__cvta_generic_to_shared(lut1);
+#endif
+    T.fesc = B.freq[kFescIdx];
+    T.cesc = pcum[225];
+    T.esc_lo = T.fesc ? (T.cesc << 20) : 0xFFFFFFFFu;
+    const uint32_t* rk = reinterpret_cast<const uint32_t*>(B.freq + kRankIdx);
+    T.rc0 = rk[0]; T.rc1 = rk[1]; T.rc2 = rk[2]; T.rc3 = rk[3];
+    T.k2p20 = P.k2p20;
+    T.k2p12 = P.k2p12;
+    T.cum = cum;
+    chain_start_w(c);
+    chain_finish_p<BF16>(c, B.payload, T);
+    stage_wait_all();
+    if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
+}
+
 }  // namespace eq
 
 using namespace eq;
@@ -583,7 +811,7 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     d.scales = blk.scales;
     d.payload_bytes = blk.payload_bytes;
     if (blk.format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if (blk.codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
+    if (blk.codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
     d.format = blk.format;
     d.codec = blk.codec;
     d.cs = blk.chunk_symbols;
@@ -640,11 +868,20 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
         uint32_t ctas = 0;
         for (uint32_t k = 0; k < nb; ++k) {
             EQ_TRY(fill_desc(blocks[b0 + k], all.get() + (size_t)(b0 + k) * EQ_MAX_LAYERS, P.b[k], ctas));
-            const uint32_t per = codec == EQ_CODEC_WORD ? (uint32_t)kWChunksPerCta : (uint32_t)kChunksPerCta;
+            const uint32_t per = codec != EQ_CODEC_BYTE ? (uint32_t)kWChunksPerCta : (uint32_t)kChunksPerCta;
             ctas += (P.b[k].n_chunks + per - 1) / per;
         }
         // blocks with zero chunks cannot exist (layers are non-empty); ctas > 0
-        if (codec == EQ_CODEC_WORD) {
+        if (codec == EQ_CODEC_PAIR) {
+            const int bi = out_dtype == EQ_OUT_BF16 ? 1 : 0;
+            const uint32_t dyn = kDecWSmem;
+            EQ_CUDA_TRY(cudaFuncSetAttribute(bi ? (const void*)k_decode_p<true> : (const void*)k_decode_p<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+            if (bi)
+                k_decode_p<true><<<ctas, kWThreads, dyn, st>>>(P);
+            else
+                k_decode_p<false><<<ctas, kWThreads, dyn, st>>>(P);
+        } else if (codec == EQ_CODEC_WORD) {
             const int bi = out_dtype == EQ_OUT_BF16 ? 1 : 0;
             // (6 CTAs/SM: for the 8B layer set 7.5 waves; forcing 5 CTAs/SM for exactly 9 waves
             // measured 2.3 % slower — the tail wave runs faster, the lost latency hiding costs more)

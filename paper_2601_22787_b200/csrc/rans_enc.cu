@@ -126,6 +126,108 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
     }
 }
 
+// EQ_CODEC_PAIR (R15): pairs (s[2i], s[2i+1]) of ranked codes whose pair is kept are one
+// pair-table symbol, other pairs the escape followed by the two codes (single table), an
+// odd tail one single; all word-codec rANS steps, in reverse (escaped pair: b, a, escape).
+// Table buffer layout as in include/entquant.h (P.freq points at 512 u16).
+struct WordEmitter {
+    uint32_t x, bytes;
+    uint8_t* dst;
+    template <bool WRITE>
+    __device__ __forceinline__ void put(uint32_t f, uint32_t c) {
+        if ((uint64_t)x >= ((uint64_t)(kLw >> kProbBits) << 16) * f) {
+            if (WRITE) {
+                dst -= 2;
+                dst[0] = (uint8_t)(x & 0xFFu);
+                dst[1] = (uint8_t)((x >> 8) & 0xFFu);
+            }
+            bytes += 2;
+            x >>= 16;
+        }
+        x = (x / f) * kM + (x % f) + c;
+    }
+};
+
+template <bool WRITE>
+__global__ void __launch_bounds__(kEncThreads) k_encode_pair(const __grid_constant__ EncParams P) {
+    __shared__ uint32_t sf[256], scum[256];
+    __shared__ uint32_t pf[225], pcum[225];
+    __shared__ int32_t rank[256];
+    __shared__ uint32_t fesc_s, cesc_s;
+    load_table(P, sf, scum);
+    const uint32_t K = P.freq[482];
+    const uint8_t* rc = reinterpret_cast<const uint8_t*>(P.freq + 484);
+    for (int i = threadIdx.x; i < 256; i += kEncThreads) rank[i] = -1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t r = 0; r < K; ++r) rank[rc[r]] = (int32_t)r;
+        uint32_t run = 0;
+        for (int q = 0; q < 225; ++q) {
+            const bool on = (uint32_t)(q / 15) < K && (uint32_t)(q % 15) < K;
+            pf[q] = on ? P.freq[256 + q] : 0;
+            pcum[q] = run;
+            run += pf[q];
+        }
+        cesc_s = run;
+        fesc_s = P.freq[481];
+    }
+    __syncthreads();
+    const uint32_t c = blockIdx.x * kEncThreads + threadIdx.x;
+    if (c >= P.n_chunks) return;
+    uint64_t base;
+    uint32_t n;
+    chunk_range(P, c, base, n);
+    const uint8_t* sym = P.codes + base;
+    uint64_t end = 0, beg = 0;
+    WordEmitter E{kLw, 0, nullptr};
+    if (WRITE) {
+        beg = P.chunk_off[c];
+        end = P.chunk_off[c + 1];
+        if (end + EQ_PAYLOAD_SLACK > P.payload_cap) {
+            atomicOr(P.err, EQ_EF_BUFFER);
+            return;
+        }
+        E.dst = P.payload + end;
+    }
+    bool bad = false;
+    if (n & 1) {
+        const uint32_t s = sym[n - 1];
+        if (sf[s] == 0) bad = true;
+        else E.put<WRITE>(sf[s], scum[s]);
+    }
+    for (int64_t i = (int64_t)(n / 2) - 1; i >= 0 && !bad; --i) {
+        const uint32_t a = sym[2 * i], b = sym[2 * i + 1];
+        if (sf[a] == 0 || sf[b] == 0) { bad = true; break; }
+        const int ra = rank[a], rb = rank[b];
+        const int q = ra * 15 + rb;
+        if (ra >= 0 && rb >= 0 && pf[q] > 0) {
+            E.put<WRITE>(pf[q], pcum[q]);
+        } else {
+            if (fesc_s == 0) { bad = true; break; }
+            E.put<WRITE>(sf[b], scum[b]);
+            E.put<WRITE>(sf[a], scum[a]);
+            E.put<WRITE>(fesc_s, cesc_s);
+        }
+    }
+    if (bad) {
+        atomicOr(P.err, EQ_EF_UNKNOWN_SYMBOL);
+        return;
+    }
+    if (WRITE) {
+        if (end - beg != (uint64_t)E.bytes + 4) {
+            atomicOr(P.err, EQ_EF_BUFFER);
+            return;
+        }
+        uint8_t* d = E.dst - 4;
+        d[0] = (uint8_t)E.x;
+        d[1] = (uint8_t)(E.x >> 8);
+        d[2] = (uint8_t)(E.x >> 16);
+        d[3] = (uint8_t)(E.x >> 24);
+    } else {
+        P.sizes[c] = E.bytes + 4;
+    }
+}
+
 // exclusive scan of sizes -> chunk_off[0..n], total; one CTA, fixed segments (deterministic)
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ sizes, uint32_t n,
                                                uint32_t* __restrict__ off, unsigned long long* total,
@@ -167,7 +269,7 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     if (!blk->payload || !blk->chunk_off || !blk->freq) return EQ_ERR_ARG;
     if (blk->n_layers == 0 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (blk->chunk_symbols == 0 || blk->chunk_symbols > 262144u) return EQ_ERR_ARG;
-    if (blk->codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
+    if (blk->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
     EncParams P;
     memset(&P, 0, sizeof(P));
     P.codes = codes;
@@ -196,7 +298,11 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     P.n_chunks = chunk;
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g = (chunk + kEncThreads - 1) / kEncThreads;
-    if (blk->codec == EQ_CODEC_WORD) {
+    if (blk->codec == EQ_CODEC_PAIR) {
+        k_encode_pair<false><<<g, kEncThreads, 0, st>>>(P);
+        k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
+        k_encode_pair<true><<<g, kEncThreads, 0, st>>>(P);
+    } else if (blk->codec == EQ_CODEC_WORD) {
         k_encode<false, true><<<g, kEncThreads, 0, st>>>(P);
         k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
         k_encode<true, true><<<g, kEncThreads, 0, st>>>(P);

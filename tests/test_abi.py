@@ -110,5 +110,7 @@ def test_codec_parameter_validated(lib):
     t = (eq.eq_tensor * 1)(eq.eq_tensor(1, 64, 64))
     p = eq._params(codec=eq.EQ_CODEC_WORD)
     assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == 0
-    p.codec = 2
+    p.codec = eq.EQ_CODEC_PAIR
+    assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == 0
+    p.codec = 3
     assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == eq.EQ_ERR_ARG

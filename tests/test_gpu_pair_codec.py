@@ -1,0 +1,67 @@
+"""GPU parity for the pair codec (EQ_CODEC_PAIR, reading R15): decode of
+oracle-encoded streams (symbols and bf16 bit-exact), incl. escapes, odd chunk lengths and
+ragged layers; GPU encode byte-identical to the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import eqsynth
+import oracle as o
+import paper_2601_22787_b200 as eq
+from test_gpu_parity import DEV, oracle_block_to_gpu, small_layers, to_bf16, u16
+
+pytestmark = pytest.mark.gpu
+PAIR = o.CODEC_PAIR
+
+
+@pytest.mark.parametrize("cs", [4096, 1000, 64, 7, 1])
+@pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16])
+def test_pair_decode_oracle_streams(cs, out):
+    layers = small_layers()
+    scales = [o.absmax_scales(W) for W in layers]
+    scales[2] = (scales[2].astype(np.int32) + 1700).astype(np.uint16)
+    scales[4] = (scales[4].astype(np.int32) + 2000).astype(np.uint16)
+    blk = o.quantize_encode(layers, scales=scales, cs=cs, codec=PAIR)
+    views = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0]
+    a = 0
+    for (r, c), v, S in zip(blk.layer_shapes, views, blk.scales):
+        codes = blk.codes[a:a + r * c].reshape(r, c)
+        a += r * c
+        if out == eq.EQ_OUT_FP8:
+            assert (v.view(torch.uint8).cpu().numpy() == codes).all()
+        else:
+            assert (u16(v) == o.dequant(codes, S)).all()
+
+
+@pytest.mark.parametrize("kind", ["uniform", "subset2", "single", "skewed", "subset40"])
+def test_pair_decode_extreme_streams(kind):
+    """Escape-heavy (uniform bytes: 15 of 256 codes ranked), single-code and two-code tables."""
+    s = eqsynth.random_codes_stream(64 * 4096, 3, kind)
+    blk = o.encode_codes([s.reshape(64, 4096)], [(64, 4096)], [np.full(64, 0x3F80, np.uint16)], 4096, codec=PAIR)
+    v = eq.decode_dequant([oracle_block_to_gpu(blk)], eq.EQ_OUT_FP8)[0][0]
+    assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == s).all()
+
+
+@pytest.mark.parametrize("cs", [4096, 333, 1])
+def test_pair_quantize_encode_byte_identical(cs):
+    """Alg. 1 on the GPU with the pair codec, given the oracle's scales: the table buffer
+    (single + pair tables, host-built on the product side) and the stream are the oracle's."""
+    from test_gpu_parity import table_u16
+    layers = small_layers(seed=5)
+    S = [(o.absmax_scales(W).astype(np.int32) + 1500).astype(np.uint16) for W in layers]
+    g = eq.quantize_encode([W.to(DEV) for W in layers], scales=to_bf16(np.concatenate(S)), chunk_symbols=cs,
+                           codec=eq.EQ_CODEC_PAIR)
+    ref = o.quantize_encode(layers, scales=S, cs=cs, codec=PAIR)
+    assert (g.freq.cpu().numpy().view(np.uint16) == table_u16(ref)).all()
+    assert g.payload_bytes == len(ref.payload)
+    assert g.payload[:g.payload_bytes].cpu().numpy().tobytes() == ref.payload
+    for v, r in zip(eq.decode_dequant([g], eq.EQ_OUT_BF16)[0], o.decode_dequant(ref)):
+        assert (u16(v) == r).all()
+
+
+def test_pair_rate_at_two_bits_gpu():
+    W = eqsynth.weights(512, 4096, seed=6)
+    gp = eq.quantize_encode([W.to(DEV)], lam=230.0, codec=eq.EQ_CODEC_PAIR)
+    codes, hist = eq.quantize_hist(W.to(DEV), gp.scales)
+    H = o.entropy(hist.cpu().numpy().astype(np.uint64))
+    assert gp.payload_bytes + 4 * (gp.n_chunks + 1) <= 1.025 * W.numel() * H / 8

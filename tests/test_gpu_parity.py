@@ -26,12 +26,26 @@ def to_bf16(bits: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(DEV)
 
 
+def table_u16(blk: o.OracleBlock) -> np.ndarray:
+    """The block's table buffer in the device layout of include/entquant.h: the 256 single
+    frequencies, plus for EQ_CODEC_PAIR the pair table, escape, K and the rank codes."""
+    if blk.codec != o.CODEC_PAIR:
+        return np.ascontiguousarray(blk.freq, dtype=np.uint16)
+    t = np.zeros(512, dtype=np.uint16)
+    t[:256] = blk.freq
+    t[256:481] = blk.pair.pf
+    t[481] = blk.pair.fesc
+    t[482] = blk.pair.K
+    t.view(np.uint8)[968:984] = blk.pair.rank_code
+    return t
+
+
 def oracle_block_to_gpu(blk: o.OracleBlock) -> eq.Block:
     cap = (len(blk.payload) + eq.EQ_PAYLOAD_SLACK + 255) // 256 * 256
     payload = torch.zeros(cap, dtype=torch.uint8)
     payload[:len(blk.payload)] = torch.frombuffer(bytearray(blk.payload), dtype=torch.uint8) if blk.payload else payload[:0]
     off = torch.from_numpy(blk.chunk_off.astype(np.int64).astype(np.int32))
-    freq = torch.from_numpy(blk.freq.view(np.int16).copy())
+    freq = torch.from_numpy(table_u16(blk).view(np.int16).copy())
     scales = to_bf16(np.concatenate(blk.scales))
     return eq.Block(payload.to(DEV), len(blk.payload), off.to(DEV), freq.to(DEV), scales, list(blk.layer_shapes),
                     blk.chunk_symbols, format=blk.fmt, codec=blk.codec)
