@@ -90,7 +90,7 @@ eq_status err_to_status(uint32_t e) {
 
 // EQ_CODEC_PAIR tables (reading R15) from the block histogram, host integer arithmetic:
 // ranks = the 15 most frequent codes (ties: lower code); pair (ra, rb) kept iff
-// M·c_a·c_b ≥ T²; escape weight = T² − Σ kept; the R8 largest-remainder rule over
+// 8·M·c_a·c_b ≥ T² (ideal frequency ≥ 1/8 slot); escape weight = T² − Σ kept; the R8 largest-remainder rule over
 // [kept pairs in (ra, rb) order, escape] to M.  Writes table[256..511] (include/entquant.h).
 void pair_table_host(const uint64_t hist[256], uint16_t table_hi[256]) {
     typedef unsigned __int128 u128;
@@ -115,7 +115,7 @@ void pair_table_host(const uint64_t hist[256], uint16_t table_hi[256]) {
     for (int ra = 0; ra < K; ++ra)
         for (int rb = 0; rb < K; ++rb) {
             const u128 x = (u128)hist[rank_code[ra]] * hist[rank_code[rb]];
-            if ((u128)kM * x >= W) {
+            if ((u128)8 * kM * x >= W) {                 // ideal frequency ≥ 1/8 slot
                 w.push_back(x);
                 idx.push_back(ra * 15 + rb);
                 kept += x;
