@@ -608,7 +608,11 @@ __device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, 
 __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, const PairTab& T, const uint8_t* payload) {
     uint32_t lo, xs;
     asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
-    if (lo >= T.esc_lo) {                          // escape: its step, then two singles
+    const bool esc = lo >= T.esc_lo;
+#ifndef EQ_PAIR_VOTE
+#define EQ_PAIR_VOTE 0   // 1: test for escapes warp-wide first (measured: more SASS, not less)
+#endif
+    if ((!EQ_PAIR_VOTE || __any_sync(__activemask(), esc)) && esc) {   // escape: its step, then two singles
         x = T.fesc * xs + (lo >> 20) - T.cesc;
         renorm_w(x, r);
 #ifndef EQ_PAIR_ESCRING
@@ -625,8 +629,10 @@ __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, cons
     renorm_w(x, r);
     // rank nibbles -> codes: bytes of {rc0, rc1} for ranks 0-7, of {rc2, rc3} for 8-15,
     // chosen per byte by the nibble's bit 3 (PRMT sign-replicate of bits 3 and 7 of e)
-    const uint32_t sel = e & 0x77u;
-    const uint32_t t1 = __byte_perm(T.rc0, T.rc1, sel), t2 = __byte_perm(T.rc2, T.rc3, sel);
+    // (t1 may take e's nibbles as they are: a rank ≥ 8 byte of t1 is replaced by t2's)
+    uint32_t t1;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(t1) : "r"(T.rc0), "r"(T.rc1), "r"(e));
+    const uint32_t t2 = __byte_perm(T.rc2, T.rc3, e & 0x77u);
     uint32_t m;                                    // PTX prmt: selector bit 3 = replicate the msb
     asm("prmt.b32 %0, %1, %2, 0xC8;" : "=r"(m) : "r"(e << 4), "r"(e));
     return (t1 & ~m) | (t2 & m);
