@@ -385,8 +385,8 @@ def main():
 
     # ---- CPU baseline: the oracle on the host cores, rank 0, N=1, bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and not args.profile and args.codec != "pair":
-        cpu = cpu_baseline(blocks, args.cpu_seconds)       # (the oracle's pair decoder has no mt timing helper)
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
+        cpu = cpu_baseline(blocks, args.cpu_seconds)
 
     if rank == 0:
         cs = clocks.summary() if clocks is not None else None
@@ -433,14 +433,19 @@ def cpu_baseline(blocks, seconds: float):
         cs = blk.chunk_symbols
         off_all = blk.chunk_off.cpu().numpy().astype(np.uint32)
         payload = blk.payload.cpu().numpy()
-        freq = blk.freq.cpu().numpy().view(np.uint16)
+        table = blk.freq.cpu().numpy().view(np.uint16)
+        freq = table[:256]
+        pair = None
+        if blk.codec == CODECS["pair"]:                    # the table buffer layout of include/entquant.h
+            pair = o.PairTable(table.view(np.uint8)[968:984].copy(), int(table[482]), table[256:481].copy(),
+                               int(table[481]))
         scales = blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)
         k0, r0 = 0, 0
         for (r, c) in blk.shapes:
             nk = (r * c + cs - 1) // cs
             off = off_all[k0:k0 + nk + 1]
             t = time.perf_counter()
-            o.decode_dequant_layer_mt(payload, off, cs, r, c, scales[r0:r0 + r], freq, threads, blk.codec)
+            o.decode_dequant_layer_mt(payload, off, cs, r, c, scales[r0:r0 + r], freq, threads, blk.codec, pair)
             wall += time.perf_counter() - t
             done_bytes += int(off[-1] - off[0]) + 4 * (nk + 1) + 2 * r + 2 * r * c
             done_syms += r * c
@@ -458,9 +463,13 @@ def cpu_baseline(blocks, seconds: float):
     nk = (r * c + blk.chunk_symbols - 1) // blk.chunk_symbols
     off = blk.chunk_off.cpu().numpy().astype(np.uint32)[:nk + 1]
     t = time.perf_counter()
+    table = blk.freq.cpu().numpy().view(np.uint16)
+    pair = None
+    if blk.codec == CODECS["pair"]:
+        pair = o.PairTable(table.view(np.uint8)[968:984].copy(), int(table[482]), table[256:481].copy(), int(table[481]))
     o.decode_dequant_layer_mt(blk.payload.cpu().numpy(), off, blk.chunk_symbols, r, c,
                               blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)[:r],
-                              blk.freq.cpu().numpy().view(np.uint16), 1, blk.codec)
+                              table[:256], 1, blk.codec, pair)
     w1 = time.perf_counter() - t
     b1 = int(off[-1] - off[0]) + 4 * (nk + 1) + 2 * r + 2 * r * c
     return {"value": done_bytes / wall / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",

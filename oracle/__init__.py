@@ -92,6 +92,8 @@ def lib():
             "eqo_decode_chunks_mt": (ctypes.c_int, [P, P, P, P, i64, P, P, ctypes.c_int]),
             "eqo_decode_dequant_layer_mt": (ctypes.c_int, [P, P, i64, i64, i64, i64, P, P, P, ctypes.c_int]),
             "eqo_encode_chunk_codec": (i64, [ctypes.c_int, P, i64, P, P, i64]),
+            "eqo_decode_dequant_layer_mt_pair": (ctypes.c_int, [P, P, i64, i64, i64, i64, P, P, P, i32, P, u16, P,
+                                                                ctypes.c_int]),
             "eqo_pair_table": (ctypes.c_int, [P, P, P, P, P]),
             "eqo_encode_chunk_pair": (i64, [P, i64, P, P, i32, P, u16, P, i64]),
             "eqo_decode_chunk_pair": (ctypes.c_int, [P, i64, P, P, i32, P, u16, P, i64]),
@@ -466,11 +468,20 @@ def decode_chunks_mt(payload: np.ndarray, chunk_off: np.ndarray, sym0: np.ndarra
 
 
 def decode_dequant_layer_mt(payload: np.ndarray, chunk_off: np.ndarray, cs: int, rows: int, cols: int,
-                            scales: np.ndarray, freq: np.ndarray, threads: int, codec: int = CODEC_BYTE) -> np.ndarray:
+                            scales: np.ndarray, freq: np.ndarray, threads: int, codec: int = CODEC_BYTE,
+                            pair: PairTable | None = None) -> np.ndarray:
     """Alg. 2 l.1-2 for one layer's chunks on ``threads`` host threads (CPU baseline)."""
     payload = np.ascontiguousarray(payload, dtype=np.uint8)
     off = np.ascontiguousarray(chunk_off, dtype=np.uint32)
     out = np.zeros(rows * cols, dtype=np.uint16)
+    if codec == CODEC_PAIR:
+        st = lib().eqo_decode_dequant_layer_mt_pair(_p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
+                                                    _p(np.ascontiguousarray(scales, dtype=np.uint16)),
+                                                    _p(np.ascontiguousarray(freq, dtype=np.uint16)),
+                                                    _p(pair.rank_code), pair.K, _p(pair.pf), pair.fesc, _p(out), threads)
+        if st:
+            raise ValueError({1: "corrupt", 2: "truncated"}[st])
+        return out.reshape(rows, cols)
     st = lib().eqo_decode_dequant_layer_mt_codec(codec, _p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
                                            _p(np.ascontiguousarray(scales, dtype=np.uint16)),
                                            _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(out), threads)

@@ -1029,3 +1029,53 @@ int eqo_decode_block_pair(const uint8_t* payload, const uint32_t* chunk_off, con
     }
     return 0;
 }
+
+/* CPU baseline (bench.py only) for the pair codec: as eqo_decode_dequant_layer_mt, with
+ * eqo_decode_chunk_pair per chunk. */
+typedef struct {
+    const uint8_t* payload; const uint32_t* chunk_off; int64_t cs, size, cols;
+    const uint16_t* scales; const uint16_t* freq; const uint8_t* rank_code; int32_t K; const uint16_t* pf;
+    uint16_t fesc; uint16_t* out; int64_t k0, k1; int status;
+} eqo_pjob;
+
+static void* eqo_pworker(void* p)
+{
+    eqo_pjob* j = (eqo_pjob*)p;
+    uint8_t* sym = (uint8_t*)malloc((size_t)j->cs);
+    j->status = 0;
+    for (int64_t k = j->k0; k < j->k1; k++) {
+        int64_t a = k * j->cs, n = j->size - a < j->cs ? j->size - a : j->cs;
+        int st = eqo_decode_chunk_pair(j->payload + j->chunk_off[k], (int64_t)j->chunk_off[k + 1] - j->chunk_off[k],
+                                       j->freq, j->rank_code, j->K, j->pf, j->fesc, sym, n);
+        if (st && !j->status) j->status = st;
+        for (int64_t i = 0; i < n; i++) {
+            int64_t row = (a + i) / j->cols;
+            j->out[a + i] = eqo_bf16_from_double(eqo_bf16_to_double(j->scales[row]) * eqo_e4m3_value(sym[i]));
+        }
+    }
+    free(sym);
+    return NULL;
+}
+
+int eqo_decode_dequant_layer_mt_pair(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks, int64_t cs,
+                                     int64_t size, int64_t cols, const uint16_t* scales, const uint16_t freq[256],
+                                     const uint8_t rank_code[16], int32_t K, const uint16_t pf[225], uint16_t fesc,
+                                     uint16_t* out, int threads)
+{
+    if (threads < 1) threads = 1;
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    eqo_pjob* jobs = (eqo_pjob*)malloc(sizeof(eqo_pjob) * (size_t)threads);
+    for (int t = 0; t < threads; t++) {
+        jobs[t] = (eqo_pjob){payload, chunk_off, cs, size, cols, scales, freq, rank_code, K, pf, fesc, out,
+                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0};
+        pthread_create(&th[t], NULL, eqo_pworker, &jobs[t]);
+    }
+    int st = 0;
+    for (int t = 0; t < threads; t++) {
+        pthread_join(th[t], NULL);
+        if (jobs[t].status && !st) st = jobs[t].status;
+    }
+    free(th);
+    free(jobs);
+    return st;
+}

@@ -297,3 +297,15 @@ def test_pair_codec_block_rate_at_two_bits():
     assert len(bp.payload) <= 1.015 * len(bw.payload)
     H = o.entropy(bp.hist)
     assert len(bp.payload) + 4 * (bp.n_chunks + 1) <= 1.025 * W.numel() * H / 8
+
+
+def test_cpu_baseline_helpers_match_block_decode():
+    """bench.py's multi-threaded CPU baseline decodes exactly what decode_dequant does (all
+    three codecs): timing helper, same arithmetic."""
+    W = eqsynth.weights(64, 1024, seed=9)
+    S = (o.absmax_scales(W).astype(np.int32) + 1600).astype(np.uint16)
+    for codec in (o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR):
+        blk = o.quantize_encode([W], scales=[S], cs=512, codec=codec)
+        payload = np.frombuffer(blk.payload + b"\0" * 16, dtype=np.uint8)
+        out = o.decode_dequant_layer_mt(payload, blk.chunk_off, 512, 64, 1024, S, blk.freq, 3, codec, blk.pair)
+        assert (out == o.decode_dequant(blk)[0]).all(), codec
