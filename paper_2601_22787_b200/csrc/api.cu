@@ -115,7 +115,10 @@ void pair_table_host(const uint64_t hist[256], uint16_t table_hi[256]) {
     for (int ra = 0; ra < K; ++ra)
         for (int rb = 0; rb < K; ++rb) {
             const u128 x = (u128)hist[rank_code[ra]] * hist[rank_code[rb]];
-            if ((u128)8 * kM * x >= W) {                 // ideal frequency ≥ 1/8 slot
+#ifndef EQ_PAIR_KEEP
+#define EQ_PAIR_KEEP 8   // keep a pair whose ideal frequency is ≥ 1/EQ_PAIR_KEEP slot (R15: 8)
+#endif
+            if ((u128)EQ_PAIR_KEEP * kM * x >= W) {       // ideal frequency ≥ 1/8 slot
                 w.push_back(x);
                 idx.push_back(ra * 15 + rb);
                 kept += x;
