@@ -213,9 +213,10 @@ class Block:
         return b
 
     def compressed_bytes(self) -> int:
-        """payload + chunk offsets + bf16 scales + 256×u16 table."""
+        """payload + chunk offsets + bf16 scales + table: 256×u16, 512×u16 with the pair table
+        (S:413-417)."""
         rows = sum(r for r, _ in self.shapes)
-        return self.payload_bytes + 4 * (self.n_chunks + 1) + 2 * rows + 512
+        return self.payload_bytes + 4 * (self.n_chunks + 1) + 2 * rows + 2 * self.freq.numel()
 
     def effective_bits(self) -> float:
         return 8.0 * self.compressed_bytes() / self.n_params
@@ -357,7 +358,7 @@ class HostBlocks:
 
     def h2d_bytes(self) -> int:
         """Bytes copied host->device per decode: payload + offsets + table + scales."""
-        return sum(b.payload_bytes + 4 * (b.n_chunks + 1) + 512 + 2 * b.scales.numel() for b in self.blocks)
+        return sum(b.payload_bytes + 4 * (b.n_chunks + 1) + 2 * b.freq.numel() + 2 * b.scales.numel() for b in self.blocks)
 
     def decode(self, stream=None) -> torch.Tensor:
         if self.workspace is None:

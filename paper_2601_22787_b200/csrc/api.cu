@@ -274,6 +274,8 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
 }
 
 // ---------------------------------------------------------------- e2e with host buffers
+// bytes of a block's table buffer: 256 u16, or 512 for EQ_CODEC_PAIR (include/entquant.h)
+static uint64_t table_bytes(const eq_block& b) { return b.codec == EQ_CODEC_PAIR ? 1024 : 512; }
 extern "C" uint64_t eq_decode_host_workspace_bytes(const eq_block* blocks, uint32_t n_blocks, uint32_t out_dtype) {
     if (!blocks || n_blocks == 0) return 0;
     uint64_t total = 0, pos = 0;
@@ -283,7 +285,7 @@ extern "C" uint64_t eq_decode_host_workspace_bytes(const eq_block* blocks, uint3
         for (uint32_t l = 0; l < blocks[b].n_layers; ++l) rows += (uint64_t)blocks[b].layer_rows[l];
         pos += align_up(blocks[b].payload_bytes + EQ_PAYLOAD_SLACK, 256);
         pos += align_up(4ull * (blocks[b].n_chunks + 1), 256);
-        pos += 512 + align_up(2 * rows, 256);
+        pos += table_bytes(blocks[b]) + align_up(2 * rows, 256);
     }
     return align_up(pos, 256) + total + 256;
 }
@@ -314,7 +316,7 @@ extern "C" eq_status eq_decode_dequant_host(const eq_block* blocks, uint32_t n_b
         d.chunk_off = (uint32_t*)(ws + pos);
         pos += align_up(4ull * (h.n_chunks + 1), 256);
         d.freq = (uint16_t*)(ws + pos);
-        pos += 512;
+        pos += table_bytes(h);
         d.scales = (uint16_t*)(ws + pos);
         pos += align_up(2 * rows, 256);
     }
@@ -354,7 +356,7 @@ extern "C" eq_status eq_decode_dequant_host(const eq_block* blocks, uint32_t n_b
                 for (uint32_t l = 0; l < h.n_layers; ++l) rows += (uint64_t)h.layer_rows[l];
                 ck(cudaMemcpyAsync(d.payload, h.payload, h.payload_bytes, cudaMemcpyHostToDevice, s_in));
                 ck(cudaMemcpyAsync(d.chunk_off, h.chunk_off, 4ull * (h.n_chunks + 1), cudaMemcpyHostToDevice, s_in));
-                ck(cudaMemcpyAsync(d.freq, h.freq, 512, cudaMemcpyHostToDevice, s_in));
+                ck(cudaMemcpyAsync(d.freq, h.freq, table_bytes(h), cudaMemcpyHostToDevice, s_in));
                 ck(cudaMemcpyAsync(d.scales, h.scales, 2 * rows, cudaMemcpyHostToDevice, s_in));
             }
             ck(cudaEventRecord(ev_in[g], s_in));

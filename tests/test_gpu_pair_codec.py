@@ -65,3 +65,14 @@ def test_pair_rate_at_two_bits_gpu():
     codes, hist = eq.quantize_hist(W.to(DEV), gp.scales)
     H = o.entropy(hist.cpu().numpy().astype(np.uint64))
     assert gp.payload_bytes + 4 * (gp.n_chunks + 1) <= 1.025 * W.numel() * H / 8
+
+
+def test_pair_host_buffer_e2e_decode():
+    layers = small_layers(seed=8, shapes=[(64, 256), (32, 512)])
+    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=80.0, codec=eq.EQ_CODEC_PAIR)
+    hb = eq.HostBlocks([g], eq.EQ_OUT_BF16)
+    arena = hb.decode()
+    dev = eq.Decoder([g], eq.EQ_OUT_BF16)
+    dev()
+    dev.check()
+    assert torch.equal(arena[:dev.total], dev.arena[:dev.total].cpu())
