@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--no-fp8", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
-    ap.add_argument("--codec", default="word", choices=["byte", "word", "pair"],
-                    help="rANS renormalisation: byte (SPEC S:355, R9) or 16-bit word (R14)")
+    ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"],
+                    help="wire format: byte rANS (SPEC S:355, R9), 16-bit-word rANS (R14), or the word "
+                         "rANS over symbol pairs with escapes (R15, default: fastest, smallest)")
     return ap.parse_args()
 
 
@@ -209,7 +210,7 @@ def run_reference(args, rank, world):
 
     def one_pass():
         for off, r, c, S in per_layer:
-            o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, blk.freq, threads, blk.codec)
+            o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, blk.freq, threads, blk.codec, blk.pair)
 
     t = time.time()
     one_pass()

@@ -773,8 +773,9 @@ int eqo_decode_dequant_layer_mt(const uint8_t* payload, const uint32_t* chunk_of
  *  - ranks: present codes by count descending, ties by lower code; the first
  *    K = min(15, #present) get ranks 0..K-1 (rank_code[r] = code);
  *  - pair weights w(ra, rb) = c[code_ra]·c[code_rb] over the ranked codes (T = Σc, total T²);
- *    a pair is KEPT when its ideal frequency is at least 1/8 slot, 8·M·w ≥ T² (it then gets
- *    ≥ 1 slot: cheaper than an escape followed by two singles, and 3× fewer escapes);
+ *    a pair is KEPT when its ideal frequency is at least 1/32 slot, 32·M·w ≥ T² (it then
+ *    gets ≥ 1 slot: about as cheap as an escape followed by two singles, and escapes — the
+ *    decoder's divergent path — become 5× rarer);
  *  - escape weight = T² − Σ kept w (all other pairs); the vector [kept pairs in (ra, rb)
  *    lexicographic order, escape] is normalised to M by the R8 rule (eqo_normalize's rule on
  *    128-bit numerators; escape present iff its weight is > 0); cum in that order, so the
@@ -851,7 +852,7 @@ int eqo_pair_table(const uint64_t hist[256], uint8_t rank_code[16], int32_t* K_o
     for (int ra = 0; ra < K; ra++)
         for (int rb = 0; rb < K; rb++) {
             unsigned __int128 x = (unsigned __int128)hist[rank_code[ra]] * hist[rank_code[rb]];
-            if ((unsigned __int128)8 * EQO_M * x >= W) {      /* ideal frequency ≥ 1/8 slot */
+            if ((unsigned __int128)32 * EQO_M * x >= W) {     /* ideal frequency ≥ 1/32 slot */
                 w[n] = x;
                 idx[n] = ra * EQO_PAIR_K + rb;
                 kept += x;

@@ -90,7 +90,7 @@ eq_status err_to_status(uint32_t e) {
 
 // EQ_CODEC_PAIR tables (reading R15) from the block histogram, host integer arithmetic:
 // ranks = the 15 most frequent codes (ties: lower code); pair (ra, rb) kept iff
-// 8·M·c_a·c_b ≥ T² (ideal frequency ≥ 1/8 slot); escape weight = T² − Σ kept; the R8 largest-remainder rule over
+// 32·M·c_a·c_b ≥ T² (ideal frequency ≥ 1/32 slot); escape weight = T² − Σ kept; the R8 largest-remainder rule over
 // [kept pairs in (ra, rb) order, escape] to M.  Writes table[256..511] (include/entquant.h).
 void pair_table_host(const uint64_t hist[256], uint16_t table_hi[256]) {
     typedef unsigned __int128 u128;
@@ -116,9 +116,9 @@ void pair_table_host(const uint64_t hist[256], uint16_t table_hi[256]) {
         for (int rb = 0; rb < K; ++rb) {
             const u128 x = (u128)hist[rank_code[ra]] * hist[rank_code[rb]];
 #ifndef EQ_PAIR_KEEP
-#define EQ_PAIR_KEEP 8   // keep a pair whose ideal frequency is ≥ 1/EQ_PAIR_KEEP slot (R15: 8)
+#define EQ_PAIR_KEEP 32  // keep a pair whose ideal frequency is ≥ 1/EQ_PAIR_KEEP slot (R15: 32)
 #endif
-            if ((u128)EQ_PAIR_KEEP * kM * x >= W) {       // ideal frequency ≥ 1/8 slot
+            if ((u128)EQ_PAIR_KEEP * kM * x >= W) {       // ideal frequency ≥ 1/32 slot
                 w.push_back(x);
                 idx.push_back(ra * 15 + rb);
                 kept += x;

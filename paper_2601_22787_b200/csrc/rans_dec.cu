@@ -715,8 +715,11 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
     }
 }
 
+#ifndef EQ_DECP_MIN_CTAS
+#define EQ_DECP_MIN_CTAS 4          // shared memory allows 4 CTAs/SM (pair + single LUT, rings): 64 registers
+#endif
 template <bool BF16>
-__global__ void __launch_bounds__(kWThreads, EQ_DECW_MIN_CTAS)
+__global__ void __launch_bounds__(kWThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) uint8_t rings[];      // kWThreads × kWRing
     __shared__ __align__(16) uint32_t lut[kM];

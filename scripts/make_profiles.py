@@ -36,7 +36,7 @@ def main(ev, rnd):
         summ = {"byte": {k: summ.pop(k) for k in ("bf16", "fp8", "source") if k in summ}}
     for d in full:
         k = d["kernel"]
-        codec = "word" if "k_decode_w" in k else "byte" if "k_decode" in k else None
+        codec = "word" if "k_decode_w" in k else "pair" if "k_decode_p" in k else "byte" if "k_decode" in k else None
         kind = "bf16" if "<1>" in k or "<(bool)1>" in k else "fp8" if "<0>" in k or "<(bool)0>" in k else None
         if codec is None or kind is None:
             continue
@@ -71,9 +71,9 @@ def main(ev, rnd):
                "timed_step_kernels": {k: {"launches": len(v), "mean_us": sum(v) / len(v)} for k, v in dec.items()},
                "decode_share_of_timed_step": 1.0,
                "note": "cold-cache, serialised per-launch times; the timed step (one eq_decode_dequant of the "
-                       "32-block layer set) launches exactly one decode kernel (k_decode_w<1> for the word codec, "
-                       "k_decode<1> for the byte codec), so its share of the step is 1.0 in both the bench and "
-                       "the launch list"},
+                       "32-block layer set) launches exactly one decode kernel (k_decode_p<1> for the pair codec, "
+                       "k_decode_w<1> for the word codec, k_decode<1> for the byte codec), so its share of the "
+                       "step is 1.0 in both the bench and the launch list"},
               open(os.path.join(out_dir, "launches_decode.json"), "w"), indent=1)
     print(json.dumps(summ, indent=1))
 

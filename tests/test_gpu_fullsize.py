@@ -32,9 +32,11 @@ def test_eqsynth_bit_identical_on_cuda():
         assert torch.equal(a.view(torch.int16), b.cpu().view(torch.int16)), dist
 
 
-@pytest.fixture(scope="module", params=[eq.EQ_CODEC_WORD, eq.EQ_CODEC_BYTE], ids=["word", "byte"])
+@pytest.fixture(scope="module", params=[eq.EQ_CODEC_PAIR, eq.EQ_CODEC_WORD, eq.EQ_CODEC_BYTE],
+                ids=["pair", "word", "byte"])
 def layer_set(request):
-    """The bench's layer set in its codec (word, R14) and in SPEC's byte codec (R9)."""
+    """The bench's layer set in its codec (pair, R15), the word codec (R14) and SPEC's byte
+    codec (R9)."""
     dev = torch.device("cuda")
     blocks, kept = [], {}
     scratch = None

@@ -76,3 +76,19 @@ def test_pair_host_buffer_e2e_decode():
     dev()
     dev.check()
     assert torch.equal(arena[:dev.total], dev.arena[:dev.total].cpu())
+
+
+def test_pair_runaway_stream_is_reported():
+    """A chunk whose state is forced to 1 (every step then escapes or renormalises) runs past
+    its end: reported as CORRUPT, never read beyond the payload slack (see memcheck runs)."""
+    Ws = [eqsynth.weights(128, 4096, seed=12)]
+    blk = o.quantize_encode(Ws, scales=[(o.absmax_scales(Ws[0]).astype(np.int32) + 1700).astype(np.uint16)],
+                            cs=2048, codec=PAIR)
+    g = oracle_block_to_gpu(blk)
+    a = int(blk.chunk_off[blk.n_chunks - 1])
+    g.payload[a:a + 4] = torch.tensor([1, 0, 0, 0], dtype=torch.uint8, device=DEV)
+    d = eq.Decoder([g], eq.EQ_OUT_BF16)
+    d()
+    with pytest.raises(eq.EqError) as ei:
+        d.check()
+    assert ei.value.status == eq.EQ_ERR_CORRUPT

@@ -163,7 +163,7 @@ def test_word_decode_max_chunk_full_rows():
         assert (u16(v) == r).all()
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
 def test_decode_under_random_corruption_matches_oracle_verdicts(codec):
     """Fuzz: random byte flips in the payload.  The GPU decoder never faults; every chunk the
     oracle rejects makes the launch report an error; when the oracle accepts every chunk of a
@@ -180,7 +180,7 @@ def test_decode_under_random_corruption_matches_oracle_verdicts(codec):
         for _ in range(int(rng.integers(1, 4))):
             data[int(rng.integers(0, len(data)))] ^= int(rng.integers(1, 256))
         cb = o.OracleBlock(blk.layer_shapes, blk.scales, blk.freq, blk.hist, bytes(data), blk.chunk_off,
-                           blk.chunk_symbols, None, blk.fmt, codec)
+                           blk.chunk_symbols, None, blk.fmt, codec, blk.pair)
         try:
             ref = o.decode_dequant(cb)
         except ValueError:

@@ -244,7 +244,7 @@ def test_block_two_bits_unique_codes_and_budget(codec):
 
 # ------------------------------------------------------------------ pair codec (R15; round-2 groundwork)
 def test_pair_table_rules():
-    """Integer table rules: ranks by count (ties: lower code), pairs kept iff 8·M·c_a·c_b ≥ T²,
+    """Integer table rules: ranks by count (ties: lower code), pairs kept iff 32·M·c_a·c_b ≥ T²,
     the R8 rule over [kept pairs, escape] sums to M, escape present iff some pair is not
     kept; a single-symbol histogram gives one pair of frequency M."""
     h = hist_of({7: 10})
@@ -257,9 +257,9 @@ def test_pair_table_rules():
     for ra in range(pt.K):
         for rb in range(pt.K):
             w = int(h[pt.rank_code[ra]]) * int(h[pt.rank_code[rb]])
-            assert (pt.pf[ra * 15 + rb] > 0) == (8 * 4096 * w >= T * T)
+            assert (pt.pf[ra * 15 + rb] > 0) == (32 * 4096 * w >= T * T)
     assert int(pt.pf.sum()) + pt.fesc == 4096 and pt.fesc == 0          # every pair kept: no escape
-    h = hist_of({3: 5000, 9: 5000, 200: 1})                              # (200, 200) below 1/8 slot
+    h = hist_of({3: 50000, 9: 50000, 200: 1})                            # (200, 200) below 1/32 slot
     pt = o.pair_table(h)
     assert pt.pf[2 * 15 + 2] == 0 and pt.pf[0] > 0 and pt.fesc >= 1
     assert int(pt.pf.sum()) + pt.fesc == 4096
