@@ -567,7 +567,12 @@ struct PairTab {
     uint32_t rc0, rc1, rc2, rc3;   // rank codes 0..15 as bytes
     uint32_t k2p20, k2p12;
     const uint32_t* cum;   // single-table cumulative frequencies (shared, 257)
+    uint32_t ctab_s;       // shared address of the 256 × u16 nibble-pair -> codes table (EQ_PAIR_CODETAB)
 };
+
+#ifndef EQ_PAIR_CODETAB
+#define EQ_PAIR_CODETAB 1   // pair codes from a 512-B shared table (1 LDS) instead of 6 ALU ops over rc0..rc3
+#endif
 
 __device__ __forceinline__ void renorm_w(uint32_t& x, WordReader& r) {
     if (x < kLw) {
@@ -627,6 +632,9 @@ __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, cons
     const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
     x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
     renorm_w(x, r);
+#if EQ_PAIR_CODETAB
+    return lds_u16(T.ctab_s + ((e & 0xFFu) << 1));                    // rank nibbles -> codes
+#endif
     // rank nibbles -> codes: bytes of {rc0, rc1} for ranks 0-7, of {rc2, rc3} for 8-15,
     // chosen per byte by the nibble's bit 3 (PRMT sign-replicate of bits 3 and 7 of e)
     // (t1 may take e's nibbles as they are: a rank ≥ 8 byte of t1 is replaced by t2's)
@@ -645,6 +653,37 @@ __device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut,
     const int t = threadIdx.x;
     if (!build_cum<NT>(B, cum, err)) return false;
     const uint32_t K = B.freq[kKIdx];
+#ifndef EQ_PAIR_PSCAN
+#define EQ_PAIR_PSCAN 1  // the 226-entry pair cum by one warp scan (else one thread's serial loop)
+#endif
+#if EQ_PAIR_PSCAN
+    if (t < 32) {                                  // 226-entry pair cum: (ra, rb) order, escape last
+        uint32_t v[8], s = 0;                      // lane t: q in [8t, 8t + 8)
+        #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int q = t * 8 + j;
+            v[j] = (q < 225 && (uint32_t)(q / 15) < K && (uint32_t)(q % 15) < K) ? B.freq[kPairOff + q] : 0u;
+            s += v[j];
+        }
+        uint32_t inc = s;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (t >= d) inc += o;
+        }
+        uint32_t run = inc - s;
+        #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int q = t * 8 + j;
+            if (q < 225) pcum[q] = run;
+            run += v[j];
+        }
+        if (t == 31) {
+            pcum[225] = inc;
+            pcum[226] = inc + B.freq[kFescIdx];
+        }
+    }
+#else
     if (t == 0) {                                  // 226-entry pair cum: (ra, rb) order, escape last
         uint32_t run = 0;
         for (int q = 0; q < 225; ++q) {
@@ -654,6 +693,7 @@ __device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut,
         pcum[225] = run;
         pcum[226] = run + B.freq[kFescIdx];
     }
+#endif
     __syncthreads();
     if (pcum[226] != kM || K > 15) {
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
@@ -728,6 +768,9 @@ k_decode_p(const __grid_constant__ DecParams P) {
 #if EQ_PAIR_LUT1
     __shared__ __align__(16) uint32_t lut1[kM];
 #endif
+#if EQ_PAIR_CODETAB
+    __shared__ uint16_t ctab[256];
+#endif
 
     uint32_t bi = 0;
     while (bi + 1 < P.n_blocks && blockIdx.x >= P.b[bi + 1].cta0) ++bi;
@@ -757,6 +800,12 @@ k_decode_p(const __grid_constant__ DecParams P) {
         }
     }
 #endif
+#if EQ_PAIR_CODETAB
+    {                                              // nibble pair (ra | rb << 4) -> code(ra) | code(rb) << 8
+        const uint8_t* rcb = reinterpret_cast<const uint8_t*>(B.freq + kRankIdx);
+        for (int i = t; i < 256; i += kWThreads) ctab[i] = (uint16_t)(rcb[i & 15] | (rcb[i >> 4] << 8));
+    }
+#endif
     stage_wait_all();
     __syncthreads();
     PairTab T;
@@ -772,6 +821,9 @@ k_decode_p(const __grid_constant__ DecParams P) {
     T.k2p20 = P.k2p20;
     T.k2p12 = P.k2p12;
     T.cum = cum;
+#if EQ_PAIR_CODETAB
+    T.ctab_s = (uint32_t)__cvta_generic_to_shared(ctab);
+#endif
     chain_start_w(c);
     chain_finish_p<BF16>(c, B.payload, T);
     stage_wait_all();
