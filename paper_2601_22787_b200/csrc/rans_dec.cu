@@ -646,6 +646,33 @@ __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, cons
     return (t1 & ~m) | (t2 & m);
 }
 
+#ifndef EQ_PAIR_WALK
+#define EQ_PAIR_WALK 1   // LUT fills: one binary search per 16 slots + a forward walk (else one per slot)
+#endif
+// lut[slot] = entry(slot, s) for the s with cm[s] <= slot < cm[s + 1] (cm[0..NS], cm[NS] = kM),
+// 256 threads: thread t fills slots [16t, 16t + 16), one binary search then a forward walk
+// over the symbol boundaries (zero-width symbols are stepped over), 4 × 16-byte stores
+template <int NS, class F>
+__device__ __forceinline__ void lut_walk256(uint32_t* lut, const uint32_t* cm, F entry) {
+    const uint32_t s0 = 16u * (uint32_t)threadIdx.x;
+    int lo = 0, hi = NS - 1;                       // largest s with cm[s] <= s0
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cm[mid] <= s0) lo = mid; else hi = mid - 1;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(lut + s0);
+    #pragma unroll 1
+    for (int k = 0; k < 16; k += 4) {
+        uint32_t v[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            while (cm[lo + 1] <= s0 + k + u) ++lo;
+            v[u] = entry(s0 + k + u, lo);
+        }
+        dst[k >> 2] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 // the pair LUT (and the single cum for escapes) of one block, all NT threads
 template <int NT>
 __device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut, uint32_t* cum, uint32_t* pcum,
@@ -699,17 +726,26 @@ __device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut,
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
         return false;
     }
-    for (int slot = t; slot < (int)kM; slot += NT) {
-        int lo = 0, hi = 225;                      // largest q with pcum[q] <= slot
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (pcum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+    if constexpr (NT == 256 && EQ_PAIR_WALK) {
+        lut_walk256<226>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
+            const uint32_t f = pcum[q + 1] - pcum[q];
+            const uint32_t nib = q < 225 ? (uint32_t)((q / 15) | ((q % 15) << 4)) : 0xFFu;
+            return nib | ((slot - pcum[q]) << 8) | ((f - 1) << 20);
+        });
+        return true;
+    } else {
+        for (int slot = t; slot < (int)kM; slot += NT) {
+            int lo = 0, hi = 225;                  // largest q with pcum[q] <= slot
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (pcum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t f = lo < 225 ? B.freq[kPairOff + lo] : B.freq[kFescIdx];
+            const uint32_t nib = lo < 225 ? (uint32_t)((lo / 15) | ((lo % 15) << 4)) : 0xFFu;
+            lut[slot] = nib | (((uint32_t)slot - pcum[lo]) << 8) | ((f - 1) << 20);
         }
-        const uint32_t f = lo < 225 ? B.freq[kPairOff + lo] : B.freq[kFescIdx];
-        const uint32_t nib = lo < 225 ? (uint32_t)((lo / 15) | ((lo % 15) << 4)) : 0xFFu;
-        lut[slot] = nib | (((uint32_t)slot - pcum[lo]) << 8) | ((f - 1) << 20);
+        return true;
     }
-    return true;
 }
 
 template <bool BF16>
@@ -790,13 +826,17 @@ k_decode_p(const __grid_constant__ DecParams P) {
             const uint32_t fs = cum[sym + 1] - cum[sym];
             return (uint32_t)sym | ((slot - cum[sym]) << 8) | ((fs - 1) << 20);
         };
-        for (int slot = t; slot < (int)kM; slot += kWThreads) {
-            int lo = 0, hi = 255;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+        if constexpr (kWThreads == 256 && EQ_PAIR_WALK) {
+            lut_walk256<256>(lut1, cum, entry);
+        } else {
+            for (int slot = t; slot < (int)kM; slot += kWThreads) {
+                int lo = 0, hi = 255;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
+                }
+                lut1[slot] = entry((uint32_t)slot, lo);
             }
-            lut1[slot] = entry((uint32_t)slot, lo);
         }
     }
 #endif
