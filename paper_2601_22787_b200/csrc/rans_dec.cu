@@ -864,6 +864,10 @@ k_decode_p(const __grid_constant__ DecParams P) {
 #if EQ_PAIR_CODETAB
     T.ctab_s = (uint32_t)__cvta_generic_to_shared(ctab);
 #endif
+#ifdef EQ_PAIR_PROLOGUE_ONLY
+    stage_wait_all();
+    return;                                        // timing experiment: table builds only
+#endif
     chain_start_w(c);
     chain_finish_p<BF16>(c, B.payload, T);
     stage_wait_all();
