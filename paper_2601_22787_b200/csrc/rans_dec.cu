@@ -567,8 +567,25 @@ struct PairTab {
     uint32_t rc0, rc1, rc2, rc3;   // rank codes 0..15 as bytes
     uint32_t k2p20, k2p12;
     const uint32_t* cum;   // single-table cumulative frequencies (shared, 257)
-    uint32_t ctab_s;       // shared address of the 256 × u16 nibble-pair -> codes table (EQ_PAIR_CODETAB)
+    uint32_t ctab_s;       // shared address of the 256 × u16 pair id -> codes table (EQ_PAIR_CODETAB)
+    uint32_t cum_s;        // shared address of cum (EQ_PAIR_LUT1 == 2)
 };
+
+#ifndef EQ_PAIR_DIAG
+#define EQ_PAIR_DIAG 1   // pair ids in anti-diagonal order of (ra, rb): the frequent pairs (small ranks)
+                         // get consecutive ids, so their codes-table words fall in distinct banks
+#endif
+// the LUT entry's 8-bit pair id of rank pair (ra, rb), ra, rb < 15 (a bijection onto [0, 225))
+__device__ __forceinline__ uint32_t pair_id(uint32_t ra, uint32_t rb) {
+#if EQ_PAIR_DIAG && EQ_PAIR_CODETAB
+    const uint32_t d = ra + rb;
+    if (d <= 14) return d * (d + 1) / 2 + ra;
+    const uint32_t e = 28 - d;
+    return 225 - (e + 1) * (e + 2) / 2 + ra - (d - 14);
+#else
+    return ra | (rb << 4);
+#endif
+}
 
 #ifndef EQ_PAIR_CODETAB
 #define EQ_PAIR_CODETAB 1   // pair codes from a 512-B shared table (1 LDS) instead of 6 ALU ops over rc0..rc3
@@ -583,11 +600,26 @@ __device__ __forceinline__ void renorm_w(uint32_t& x, WordReader& r) {
 }
 
 #ifndef EQ_PAIR_LUT1
-#define EQ_PAIR_LUT1 1   // escapes decode their two singles with a single-symbol LUT (else binary search)
+#define EQ_PAIR_LUT1 2   // escapes decode their two singles from a u8 symbol per slot + the cum table
+                         // (1: u32 LUT entries, 12 KB more shared memory -> 4 CTAs/SM; 0: binary search)
 #endif
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
 // a single-table symbol (escape path and odd tails)
 __device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, const PairTab& T) {
-#if EQ_PAIR_LUT1
+#if EQ_PAIR_LUT1 == 2
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    const uint32_t slot = lo >> 20;
+    const uint32_t s = lds_u8(T.lut1_s + slot);
+    const uint32_t cs = lds_u32(T.cum_s + 4 * s), ce = lds_u32(T.cum_s + 4 * s + 4);
+    x = (ce - cs) * xs + slot - cs;
+    renorm_w(x, r);
+    return s;
+#elif EQ_PAIR_LUT1
     uint32_t lo, xs;
     asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
     const uint32_t e = lds_u32(T.lut1_s + (lo >> 18));
@@ -729,7 +761,7 @@ __device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut,
     if constexpr (NT == 256 && EQ_PAIR_WALK) {
         lut_walk256<226>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
             const uint32_t f = pcum[q + 1] - pcum[q];
-            const uint32_t nib = q < 225 ? (uint32_t)((q / 15) | ((q % 15) << 4)) : 0xFFu;
+            const uint32_t nib = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : 0xFFu;
             return nib | ((slot - pcum[q]) << 8) | ((f - 1) << 20);
         });
         return true;
@@ -741,7 +773,7 @@ __device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut,
                 if (pcum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
             }
             const uint32_t f = lo < 225 ? B.freq[kPairOff + lo] : B.freq[kFescIdx];
-            const uint32_t nib = lo < 225 ? (uint32_t)((lo / 15) | ((lo % 15) << 4)) : 0xFFu;
+            const uint32_t nib = lo < 225 ? pair_id((uint32_t)lo / 15, (uint32_t)lo % 15) : 0xFFu;
             lut[slot] = nib | (((uint32_t)slot - pcum[lo]) << 8) | ((f - 1) << 20);
         }
         return true;
@@ -792,7 +824,7 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
 }
 
 #ifndef EQ_DECP_MIN_CTAS
-#define EQ_DECP_MIN_CTAS 4          // shared memory allows 4 CTAs/SM (pair + single LUT, rings): 64 registers
+#define EQ_DECP_MIN_CTAS 5          // shared memory (40 KB: pair LUT, byte single LUT, rings) allows 5 CTAs/SM: 48 registers
 #endif
 template <bool BF16>
 __global__ void __launch_bounds__(kWThreads, EQ_DECP_MIN_CTAS)
@@ -801,7 +833,9 @@ k_decode_p(const __grid_constant__ DecParams P) {
     __shared__ __align__(16) uint32_t lut[kM];
     __shared__ uint32_t cum[257];
     __shared__ uint32_t pcum[227];
-#if EQ_PAIR_LUT1
+#if EQ_PAIR_LUT1 == 2
+    __shared__ __align__(16) uint8_t lut1[kM];
+#elif EQ_PAIR_LUT1
     __shared__ __align__(16) uint32_t lut1[kM];
 #endif
 #if EQ_PAIR_CODETAB
@@ -820,7 +854,25 @@ k_decode_p(const __grid_constant__ DecParams P) {
         stage_wait_all();
         return;
     }
-#if EQ_PAIR_LUT1
+#if EQ_PAIR_LUT1 == 2
+    {                                              // symbol per slot: thread t fills [16t, 16t + 16)
+        static_assert(kWThreads == 256, "byte single LUT fill assumes 256 threads");
+        const uint32_t s0 = 16u * (uint32_t)t;
+        int lo = 0, hi = 255;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
+        }
+        uint32_t w[4];
+        #pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            while (cum[lo + 1] <= s0 + k) ++lo;
+            if ((k & 3) == 0) w[k >> 2] = 0;
+            w[k >> 2] |= (uint32_t)lo << (8 * (k & 3));
+        }
+        *reinterpret_cast<uint4*>(lut1 + s0) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+#elif EQ_PAIR_LUT1
     {                                              // single LUT in decode_one_w's entry layout
         auto entry = [&](uint32_t slot, int sym) -> uint32_t {
             const uint32_t fs = cum[sym + 1] - cum[sym];
@@ -841,9 +893,10 @@ k_decode_p(const __grid_constant__ DecParams P) {
     }
 #endif
 #if EQ_PAIR_CODETAB
-    {                                              // nibble pair (ra | rb << 4) -> code(ra) | code(rb) << 8
+    {                                              // pair id of (ra, rb) -> code(ra) | code(rb) << 8
         const uint8_t* rcb = reinterpret_cast<const uint8_t*>(B.freq + kRankIdx);
-        for (int i = t; i < 256; i += kWThreads) ctab[i] = (uint16_t)(rcb[i & 15] | (rcb[i >> 4] << 8));
+        for (int q = t; q < 225; q += kWThreads)
+            ctab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = (uint16_t)(rcb[q / 15] | (rcb[q % 15] << 8));
     }
 #endif
     stage_wait_all();
@@ -861,6 +914,7 @@ k_decode_p(const __grid_constant__ DecParams P) {
     T.k2p20 = P.k2p20;
     T.k2p12 = P.k2p12;
     T.cum = cum;
+    T.cum_s = (uint32_t)__cvta_generic_to_shared(cum);
 #if EQ_PAIR_CODETAB
     T.ctab_s = (uint32_t)__cvta_generic_to_shared(ctab);
 #endif
