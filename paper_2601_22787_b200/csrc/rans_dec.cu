@@ -610,7 +610,21 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
 }
 // a single-table symbol (escape path and odd tails)
 __device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, const PairTab& T) {
-#if EQ_PAIR_LUT1 == 2
+#if EQ_PAIR_LUT1 == 3
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    const uint32_t slot = lo >> 20;
+    uint32_t s = lds_u8(T.lut1_s + (slot >> 4));   // first symbol of the slot's 16-slot bucket
+    uint32_t ce = lds_u32(T.cum_s + 4 * s + 4);
+    while (ce <= slot) {                           // walk the bucket's symbol boundaries
+        ++s;
+        ce = lds_u32(T.cum_s + 4 * s + 4);
+    }
+    const uint32_t cs = lds_u32(T.cum_s + 4 * s);
+    x = (ce - cs) * xs + slot - cs;
+    renorm_w(x, r);
+    return s;
+#elif EQ_PAIR_LUT1 == 2
     uint32_t lo, xs;
     asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
     const uint32_t slot = lo >> 20;
@@ -833,7 +847,9 @@ k_decode_p(const __grid_constant__ DecParams P) {
     __shared__ __align__(16) uint32_t lut[kM];
     __shared__ uint32_t cum[257];
     __shared__ uint32_t pcum[227];
-#if EQ_PAIR_LUT1 == 2
+#if EQ_PAIR_LUT1 == 3
+    __shared__ __align__(16) uint8_t lut1[kM / 16];
+#elif EQ_PAIR_LUT1 == 2
     __shared__ __align__(16) uint8_t lut1[kM];
 #elif EQ_PAIR_LUT1
     __shared__ __align__(16) uint32_t lut1[kM];
@@ -854,7 +870,18 @@ k_decode_p(const __grid_constant__ DecParams P) {
         stage_wait_all();
         return;
     }
-#if EQ_PAIR_LUT1 == 2
+#if EQ_PAIR_LUT1 == 3
+    {                                              // bucket t (slots [16t, 16t + 16)): its first symbol
+        static_assert(kWThreads == 256, "bucket fill assumes 256 threads");
+        const uint32_t s0 = 16u * (uint32_t)t;
+        int lo = 0, hi = 255;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
+        }
+        lut1[t] = (uint8_t)lo;
+    }
+#elif EQ_PAIR_LUT1 == 2
     {                                              // symbol per slot: thread t fills [16t, 16t + 16)
         static_assert(kWThreads == 256, "byte single LUT fill assumes 256 threads");
         const uint32_t s0 = 16u * (uint32_t)t;
