@@ -90,6 +90,108 @@ def test_normalize_random_properties():
             assert xent_bits(h, f) <= emp_entropy_bits(h) + 0.06 * h.sum() + 1e-6
 
 
+def _expand(d: dict) -> dict:
+    """{"5": v, "100..399": v} -> {5: v, 100: v, ..., 399: v} (golden shorthand)."""
+    out = {}
+    for k, v in d.items():
+        if ".." in k:
+            a, b = (int(x) for x in k.split(".."))
+            out.update({c: v for c in range(a, b + 1)})
+        else:
+            out[int(k)] = v
+    return out
+
+
+def test_normalize_worked_examples(golden):
+    """Hand-derived R8 tables (tests/golden/normalize_worked.json): D > 0 with remainder, count
+    and code tie-breaks; D < 0 with two give-back candidates that interleave, and an odd split."""
+    for case in golden["normalize_worked"]["cases"]:
+        f = o.normalize(hist_of(_expand(case["counts"])))
+        want = np.zeros(256, np.int64)
+        for c, v in _expand(case["freq"]).items():
+            want[c] = v
+        assert (f.astype(np.int64) == want).all(), case["name"]
+
+
+def _r8_reference_parts(h):
+    """floor / remainder of 4096·c/T in exact integers (Python ints, independent of the oracle)."""
+    T = int(h.sum())
+    q = {c: max(1, 4096 * int(h[c]) // T) for c in range(256) if h[c]}
+    r = {c: (4096 * int(h[c])) % T for c in range(256) if h[c]}
+    return q, r
+
+
+def test_normalize_selection_properties():
+    """Which symbols the R8 rule adjusts, checked against exact integer floors/remainders:
+    D > 0 — exactly D present symbols get +1 and each of them ranks (r, c, -code) above every
+    present symbol that did not; D < 0 — only symbols with f > 1 lose, and the losers end at
+    the final maximum or one below it (take-from-the-largest water-filling)."""
+    rng = np.random.default_rng(11)
+    seen_pos = seen_neg = 0
+    for t in range(400):
+        k = int(rng.integers(2, 257))
+        h = np.zeros(256, dtype=np.uint64)
+        idx = rng.permutation(256)[:k]
+        h[idx] = (rng.pareto(0.5 + rng.uniform(0, 3), k) * rng.choice([3, 30, 3000])).astype(np.uint64) + 1
+        if t % 3 == 0:                      # many count-1 symbols under a heavy head: D < 0
+            h[idx[: k // 2]] = 1
+            h[idx[0]] += np.uint64(rng.integers(4096, 40000))
+        f = o.normalize(h).astype(np.int64)
+        q, r = _r8_reference_parts(h)
+        D = 4096 - sum(q.values())
+        pres = sorted(q)
+        if D > 0:
+            seen_pos += 1
+            up = [c for c in pres if f[c] == q[c] + 1]
+            assert len(up) == D and all(f[c] in (q[c], q[c] + 1) for c in pres)
+            key = lambda c: (r[c], int(h[c]), -c)
+            rest = [c for c in pres if f[c] == q[c]]
+            if rest:
+                assert min(key(c) for c in up) > max(key(c) for c in rest)
+        elif D < 0:
+            seen_neg += 1
+            down = [c for c in pres if f[c] < q[c]]
+            m = int(f.max())
+            assert all(q[c] > 1 and f[c] >= max(m - 1, 1) for c in down)
+            assert all(q[c] <= m for c in pres if c not in down)
+            assert all(f[c] == q[c] for c in pres if c not in down)
+        else:
+            assert all(f[c] == q[c] for c in pres)
+    assert seen_pos > 50 and seen_neg > 20
+
+
+def test_pair_table_worked_examples(golden):
+    """Hand-derived pair tables (R15): ranks with a count tie, D > 0 over pair weights (largest
+    remainder), and a dropped pair with an escape and D < 0."""
+    for case in golden["normalize_worked"]["pair_cases"]:
+        pt = o.pair_table(hist_of(_expand(case["counts"])))
+        assert pt.K == case["K"], case["name"]
+        assert list(pt.rank_code[:pt.K]) == case["rank_code"], case["name"]
+        want = np.zeros(225, np.int64)
+        for k, v in case["pairs"].items():
+            ra, rb = (int(x) for x in k.split(","))
+            want[ra * 15 + rb] = v
+        assert (pt.pf.astype(np.int64) == want).all(), case["name"]
+        assert pt.fesc == case["fesc"], case["name"]
+
+
+def test_pair_codec_worked_streams(golden):
+    """Hand-derived pair-codec chunks (tests/golden/rans_pair_worked.json): an escaped pair, a kept
+    pair and an odd tail; and a renormalisation-free two-pair chunk."""
+    for case in golden["rans_pair_worked"]["cases"]:
+        h = hist_of(_expand(case["counts"]))
+        f = o.normalize(h)
+        want = np.zeros(256, np.int64)
+        for c, v in _expand(case["single_freq"]).items():
+            want[c] = v
+        assert (f.astype(np.int64) == want).all(), case["name"]
+        pt = o.pair_table(h)
+        sym = np.array(case["symbols"], dtype=np.uint8)
+        data = o.encode_chunk_pair(sym, f, pt)
+        assert data.hex() == case["bytes_hex"], case["name"]
+        assert (o.decode_chunk_pair(data, f, pt, sym.size) == sym).all()
+
+
 # ------------------------------------------------------------------ rANS chunks
 CODECS = [o.CODEC_BYTE, o.CODEC_WORD]
 GOLDEN_STREAMS = {o.CODEC_BYTE: "rans_worked", o.CODEC_WORD: "rans_word_worked"}
@@ -296,7 +398,7 @@ def test_pair_codec_block_rate_at_two_bits():
     assert (o.decode_block(bp) == bp.codes).all()
     assert len(bp.payload) <= 1.015 * len(bw.payload)
     H = o.entropy(bp.hist)
-    assert len(bp.payload) + 4 * (bp.n_chunks + 1) <= 1.025 * W.numel() * H / 8
+    assert len(bp.payload) + 4 * (bp.n_chunks + 1) <= 1.02 * W.numel() * H / 8
 
 
 def test_cpu_baseline_helpers_match_block_decode():
