@@ -3,7 +3,7 @@
  *
  * Paper: "Float8@2bits: Entropy Coding Enables Data-Free Model Compression",
  * arXiv 2601.22787.  P:<n> = line n of PAPER.md, S:<n> = line n of SPEC.md; the
- * readings of ambiguous passages are listed in DESIGN.md §3 and numbered R1..R14.
+ * readings of ambiguous passages are listed in DESIGN.md §3 and numbered R1..R15.
  *
  * Conventions (all entry points):
  *  - Tensor / array pointers are CUDA DEVICE pointers unless the parameter name ends in
@@ -121,8 +121,9 @@ const char* eq_status_string(eq_status s);
 const char* eq_version(void);
 
 /* ---------------------------------------------------------------- sizing (host only)
- * Sizes for encoding `n_layers` tensors as one block: payload capacity (worst case
- * 4 + 2 bytes per symbol per chunk, plus slack), chunk count, and the scratch bytes
+ * Sizes for encoding `n_layers` tensors as one block: payload capacity (worst case 4 bytes
+ * per chunk + 2 bytes per symbol for EQ_CODEC_BYTE / _WORD, 3 bytes per symbol for
+ * EQ_CODEC_PAIR — an escaped pair is three words — plus slack), chunk count, and the scratch bytes
  * eq_quantize_encode needs (codes stream + tables + chunk sizes).  EQ_ERR_SHAPE for
  * rows/cols < 1 or > 2^31, EQ_ERR_ARG for n_layers outside 1..EQ_MAX_LAYERS. */
 eq_status eq_encode_bounds(const eq_tensor* layers, uint32_t n_layers, const eq_params* p,
@@ -168,6 +169,16 @@ eq_status eq_quantize_hist(const eq_tensor* w, uint32_t format, const uint16_t* 
  * histogram sets EQ_EF_EMPTY in d_err. */
 eq_status eq_build_table(const uint64_t* hist, uint16_t* freq, uint32_t* d_err, eq_stream_t stream);
 
+/* a5 for EQ_CODEC_PAIR (reading R15; one table per block): from the
+ * block histogram hist (device uint64[256]) write the pair half of the table buffer,
+ * table[256..512) (device uint16, the layout of EQ_CODEC_PAIR above): ranks = the 15 most
+ * frequent present codes (ties: lower code); pair (ra, rb) kept iff 32·M·c_a·c_b ≥ T²; the R8
+ * rule over [kept pairs in (ra, rb) order, escape = T² − Σ kept] to M = 4096; unused entries 0.
+ * table[0..256) (the single table, eq_build_table) is not touched.  Block counts must stay
+ * below 2^50 (always true within eq_encode_bounds' limits).  An empty histogram sets
+ * EQ_EF_EMPTY in d_err.  Asynchronous; one CTA. */
+eq_status eq_build_pair_table(const uint64_t* hist, uint16_t* table, uint32_t* d_err, eq_stream_t stream);
+
 /* a6 (Alg. 1 l.4-5, R9/R10/R14): rANS-encode the concatenated symbol stream
  * `codes` of the block's layers (sizes rows*cols in block order, from `blk`), chunks of
  * blk->chunk_symbols restarting at each layer, into blk->payload / blk->chunk_off with
@@ -202,6 +213,13 @@ eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks, uint32_t 
                             void* arena, uint64_t arena_bytes, uint32_t* d_err,
                             eq_stream_t stream);
 
+/* Chunks the decoder of `codec` (EQ_CODEC_*) / `out_dtype` keeps in flight at once on CUDA
+ * device `device` (SMs × resident CTAs per SM × chunks per CTA; one chunk per lane).  A
+ * launch with n chunks runs ceil(n / lanes) rounds of one chunk-length serial chain each, so
+ * callers choose chunk_symbols to keep n / lanes near a whole number of rounds.
+ * Host only; EQ_ERR_ARG for bad enums. */
+eq_status eq_decode_lanes(uint32_t codec, uint32_t out_dtype, int device, uint64_t* lanes);
+
 /* End-to-end variant with HOST buffers: blocks_host[b].payload / chunk_off / freq / scales
  * are host pointers (pinned for full speed; arena_host too).  Copies them into `workspace`
  * (device, ≥ eq_decode_host_workspace_bytes), decodes, and copies the decoded arena to
@@ -215,7 +233,8 @@ eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks,
                                  void* arena_host, uint64_t arena_bytes, void* workspace,
                                  uint64_t workspace_bytes, eq_stream_t stream);
 
-/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4; EQ_CODEC_BYTE blocks): Y_q = X_q · Ŵ_qᵀ for
+/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4; EQ_CODEC_BYTE or EQ_CODEC_WORD
+ * blocks — EQ_CODEC_PAIR blocks return EQ_ERR_ARG): Y_q = X_q · Ŵ_qᵀ for
  * n_jobs layers `layers[q]` of block `blk` in ONE launch, Ŵ = the layer's decoded +
  * dequantised bf16 weights (never written to memory): each chunk is decoded straight into
  * tcgen05 shared-memory tiles and multiplied on the 5th-gen tensor cores (bf16 × bf16 →

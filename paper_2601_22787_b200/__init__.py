@@ -35,7 +35,8 @@ EQ_ARENA_ALIGN = 256
 
 EXPORTS = (
     "eq_status_string", "eq_version", "eq_encode_bounds", "eq_arena_layout", "eq_absmax",
-    "eq_search_scratch_bytes", "eq_search_scales", "eq_quantize_hist", "eq_build_table",
+    "eq_search_scratch_bytes", "eq_search_scales", "eq_quantize_hist", "eq_build_table", "eq_build_pair_table",
+    "eq_decode_lanes",
     "eq_rans_encode", "eq_quantize_encode", "eq_decode_dequant", "eq_decode_host_workspace_bytes",
     "eq_decode_dequant_host", "eq_check", "eq_calibrate_scratch_bytes", "eq_calibrate_lambda",
     "eq_qmatmul",
@@ -103,6 +104,8 @@ def lib() -> ctypes.CDLL:
             "eq_search_scales": (st, [P, u32, P, u32, i32, i32, P, u32, P, P, P, u64, P]),
             "eq_quantize_hist": (st, [P, u32, P, P, u32, P, P, P]),
             "eq_build_table": (st, [P, P, P, P]),
+            "eq_build_pair_table": (st, [P, P, P, P]),
+            "eq_decode_lanes": (st, [u32, u32, ctypes.c_int, P]),
             "eq_rans_encode": (st, [P, P, P, P, P, P]),
             "eq_quantize_encode": (st, [P, u32, P, P, P, u64, P]),
             "eq_decode_dequant": (st, [P, u32, u32, P, u64, P, P]),
@@ -321,6 +324,15 @@ class Decoder:
         return out
 
 
+def decode_lanes(codec: int = EQ_CODEC_PAIR, out_dtype: int = EQ_OUT_BF16, device: int | None = None) -> int:
+    """Chunks the decoder keeps in flight at once on a device (one chunk per lane)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    n = ctypes.c_uint64()
+    _ck(lib().eq_decode_lanes(codec, out_dtype, device, ctypes.byref(n)), "eq_decode_lanes")
+    return int(n.value)
+
+
 def decode_dequant(blocks, out_dtype=EQ_OUT_BF16, stream=None, check: bool = True):
     """Decodes blocks (one launch) and returns per-block lists of per-layer views."""
     d = Decoder(blocks, out_dtype)
@@ -420,6 +432,18 @@ def build_table(hist: torch.Tensor, stream=None):
     return freq, err
 
 
+def build_pair_table(hist: torch.Tensor, stream=None):
+    """a5 for EQ_CODEC_PAIR (R15): (table int16 [512] — [0,256) the single table of
+    build_table, [256,512) the pair table — and the device error word)."""
+    _require_cuda(hist)
+    tab = torch.zeros(512, dtype=torch.int16, device=hist.device)
+    err = torch.zeros(1, dtype=torch.int32, device=hist.device)
+    _ck(lib().eq_build_table(hist.data_ptr(), tab.data_ptr(), err.data_ptr(), _stream(stream)), "eq_build_table")
+    _ck(lib().eq_build_pair_table(hist.data_ptr(), tab.data_ptr(), err.data_ptr(), _stream(stream)),
+        "eq_build_pair_table")
+    return tab, err
+
+
 def rans_encode(codes: torch.Tensor, shapes, freq: torch.Tensor, scales: torch.Tensor | None = None,
                 chunk_symbols: int = EQ_DEFAULT_CHUNK, stream=None, codec: int = EQ_CODEC_BYTE) -> Block:
     """a6 alone: encode a concatenated symbol stream (uint8 CUDA) with a given table."""
@@ -443,10 +467,12 @@ def rans_encode(codes: torch.Tensor, shapes, freq: torch.Tensor, scales: torch.T
 
 
 def calibrate_lambda(layers, target_bits: float, row_stride: int = 8, chunk_symbols: int = EQ_DEFAULT_CHUNK,
-                     oct_lo: int = -1, oct_hi: int = 20, stream=None, format: int = EQ_FMT_E4M3):
-    """Global λ for a target effective rate.  Returns (λ, estimated bits)."""
+                     oct_lo: int = -1, oct_hi: int = 20, stream=None, format: int = EQ_FMT_E4M3,
+                     codec: int = EQ_CODEC_BYTE):
+    """Global λ for a target effective rate (P:192, P:507).  Returns (λ, estimated bits);
+    ``codec`` sizes the per-block table in the side information."""
     ts = (eq_tensor * len(layers))(*[_tensor(W) for W in layers])
-    p = _params(chunk_symbols, EQ_SCALES_SEARCH, 0.0, oct_lo, oct_hi, format)
+    p = _params(chunk_symbols, EQ_SCALES_SEARCH, 0.0, oct_lo, oct_hi, format, codec=codec)
     sb = lib().eq_calibrate_scratch_bytes(ts, len(layers), row_stride)
     scratch = torch.empty(sb, dtype=torch.uint8, device=layers[0].device)
     lam, est = ctypes.c_double(), ctypes.c_double()

@@ -4,6 +4,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -35,8 +36,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), so: str | None
     if not force and not defines and not stale():
         return SO
     objs = []
+    tmp = tempfile.mkdtemp(prefix="eqbuild_")       # per-build object dir: parallel variant builds never collide
     for s in SOURCES:
-        o = os.path.join(CSRC, s.replace(".cu", ".o"))
+        o = os.path.join(tmp, s.replace(".cu", ".o"))
         cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
@@ -47,6 +49,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), so: str | None
     os.replace(target + ".tmp", target)
     for o in objs:
         os.remove(o)
+    os.rmdir(tmp)
     return target
 
 

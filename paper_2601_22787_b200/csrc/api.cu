@@ -88,82 +88,6 @@ eq_status err_to_status(uint32_t e) {
     return EQ_OK;
 }
 
-// EQ_CODEC_PAIR tables (reading R15) from the block histogram, host integer arithmetic:
-// ranks = the 15 most frequent codes (ties: lower code); pair (ra, rb) kept iff
-// 32·M·c_a·c_b ≥ T² (ideal frequency ≥ 1/32 slot); escape weight = T² − Σ kept; the R8 largest-remainder rule over
-// [kept pairs in (ra, rb) order, escape] to M.  Writes table[256..511] (include/entquant.h).
-void pair_table_host(const uint64_t hist[256], uint16_t table_hi[256]) {
-    typedef unsigned __int128 u128;
-    uint64_t T = 0;
-    for (int c = 0; c < 256; ++c) T += hist[c];
-    memset(table_hi, 0, 512);
-    if (T == 0) return;
-    int rank_code[15], K = 0;
-    bool used[256] = {false};
-    for (; K < 15; ++K) {
-        int b = -1;
-        for (int c = 0; c < 256; ++c)
-            if (hist[c] && !used[c] && (b < 0 || hist[c] > hist[b])) b = c;
-        if (b < 0) break;
-        used[b] = true;
-        rank_code[K] = b;
-    }
-    const u128 W = (u128)T * T;
-    std::vector<u128> w;
-    std::vector<int> idx;
-    u128 kept = 0;
-    for (int ra = 0; ra < K; ++ra)
-        for (int rb = 0; rb < K; ++rb) {
-            const u128 x = (u128)hist[rank_code[ra]] * hist[rank_code[rb]];
-#ifndef EQ_PAIR_KEEP
-#define EQ_PAIR_KEEP 32  // keep a pair whose ideal frequency is ≥ 1/EQ_PAIR_KEEP slot (R15: 32)
-#endif
-            if ((u128)EQ_PAIR_KEEP * kM * x >= W) {       // ideal frequency ≥ 1/32 slot
-                w.push_back(x);
-                idx.push_back(ra * 15 + rb);
-                kept += x;
-            }
-        }
-    w.push_back(W - kept);
-    const int n = (int)w.size();
-    std::vector<int64_t> f(n);
-    std::vector<u128> r(n);
-    int64_t sum = 0;
-    for (int i = 0; i < n; ++i) {
-        if (w[i] == 0) { f[i] = 0; r[i] = 0; continue; }
-        const u128 num = (u128)kM * w[i];
-        const u128 q = num / W;
-        r[i] = num % W;
-        f[i] = q < 1 ? 1 : (int64_t)q;
-        sum += f[i];
-    }
-    int64_t D = (int64_t)kM - sum;
-    if (D > 0) {
-        std::vector<bool> taken(n, false);
-        for (int64_t k = 0; k < D; ++k) {
-            int b = -1;
-            for (int i = 0; i < n; ++i) {
-                if (w[i] == 0 || taken[i]) continue;
-                if (b < 0 || r[i] > r[b] || (r[i] == r[b] && w[i] > w[b])) b = i;
-            }
-            taken[b] = true;
-            f[b] += 1;
-        }
-    }
-    while (D < 0) {
-        int b = -1;
-        for (int i = 0; i < n; ++i)
-            if (f[i] > 1 && (b < 0 || f[i] > f[b])) b = i;
-        f[b] -= 1;
-        D += 1;
-    }
-    for (int i = 0; i + 1 < n; ++i) table_hi[idx[i]] = (uint16_t)f[i];   // [256 + q] -> hi[q]
-    table_hi[225] = (uint16_t)f[n - 1];                                 // [481] escape
-    table_hi[226] = (uint16_t)K;                                        // [482]
-    uint8_t* rc = reinterpret_cast<uint8_t*>(table_hi + 228);           // [484, 492)
-    for (int i = 0; i < K; ++i) rc[i] = (uint8_t)rank_code[i];
-}
-
 }  // namespace
 
 extern "C" const char* eq_status_string(eq_status s) {
@@ -252,15 +176,7 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
     }
     // metadata ℳ and Alg. 1 l.4-5
     EQ_TRY(eq_build_table(S.hist, out->freq, S.err, stream));
-    if (p->codec == EQ_CODEC_PAIR) {               // the pair table is built on the host (R15)
-        uint64_t h[256];
-        uint16_t hi[256];
-        EQ_CUDA_TRY(cudaMemcpyAsync(h, S.hist, sizeof(h), cudaMemcpyDeviceToHost, st));
-        EQ_CUDA_TRY(cudaStreamSynchronize(st));
-        pair_table_host(h, hi);
-        EQ_CUDA_TRY(cudaMemcpyAsync(out->freq + 256, hi, sizeof(hi), cudaMemcpyHostToDevice, st));
-        EQ_CUDA_TRY(cudaStreamSynchronize(st));
-    }
+    if (p->codec == EQ_CODEC_PAIR) EQ_TRY(eq_build_pair_table(S.hist, out->freq, S.err, stream));   // R15
     EQ_TRY(eq_rans_encode(S.codes, out, S.sizes, S.total, S.err, stream));
     uint64_t total = 0;
     uint32_t e = 0;
@@ -447,14 +363,19 @@ extern "C" eq_status eq_calibrate_lambda(const eq_tensor* layers, uint32_t n_lay
     if (!layers || n_layers == 0 || !p || !lambda_out || !scratch || row_stride == 0) return EQ_ERR_ARG;
     for (uint32_t l = 0; l < n_layers; ++l)
         if (!layers[l].w || layers[l].rows < 1 || layers[l].cols < 1) return EQ_ERR_SHAPE;
-    if (p->chunk_symbols == 0) return EQ_ERR_ARG;
+    {
+        eq_params q = *p;                          // λ is the output here: validate everything else
+        q.lambda = 0.0;
+        EQ_TRY(check_params(&q));
+    }
     if (!(target_bits > 0.0)) return EQ_ERR_ARG;
     if (scratch_bytes < eq_calibrate_scratch_bytes(layers, n_layers, row_stride)) return EQ_ERR_BUFFER;
     cudaStream_t st = (cudaStream_t)stream;
     CalibScratch C = carve_calib(layers, n_layers, row_stride, (char*)scratch);
 
     // side information per parameter of the full layer set: chunk offsets,
-    // bf16 scales, and one 256 x u16 table per 7 layers (a block), + 4-byte states.
+    // bf16 scales, one table per 7 layers (a block: 256 x u16, or 512 x u16 for the pair
+    // codec), + 4-byte states.
     double params = 0, rows_total = 0, chunks = 0;
     for (uint32_t l = 0; l < n_layers; ++l) {
         const double sz = (double)layers[l].rows * (double)layers[l].cols;
@@ -462,7 +383,7 @@ extern "C" eq_status eq_calibrate_lambda(const eq_tensor* layers, uint32_t n_lay
         rows_total += (double)layers[l].rows;
         chunks += std::ceil(sz / p->chunk_symbols);
     }
-    const double side = (8.0 * (4.0 * chunks + 4.0 * chunks + 2.0 * rows_total) + 4096.0 * std::ceil(n_layers / 7.0)) / params;
+    const double side = (8.0 * (4.0 * chunks + 4.0 * chunks + 2.0 * rows_total) + (p->codec == EQ_CODEC_PAIR ? 8192.0 : 4096.0) * std::ceil(n_layers / 7.0)) / params;
 
     // sampled row lists
     std::vector<uint32_t> rl;

@@ -369,7 +369,22 @@ __device__ __forceinline__ void stage_segment_w(uint32_t ring, const uint8_t* pa
 
 // Every 8 steps: wait for all staged segments, then stage segment gn if its slot is free
 // (predicated, no branch), one cp.async group per boundary.
+#ifndef EQ_RING_ISSUE_FIRST
+#define EQ_RING_ISSUE_FIRST 1   // stage, commit, then wait for all but the newest group (same data
+                                // guarantee as wait-all-then-stage: the segment issued at this
+                                // boundary is never read before the next one); avoids the LDGDEPBAR
+                                // of wait_all and the dummy LDS ptxas pads between DEPBAR and LDGSTS
+#endif
 __device__ __forceinline__ void ring_step_w(WordReader& r, const uint8_t* payload) {
+#if EQ_RING_ISSUE_FIRST
+    asm volatile("{ .reg .pred p; setp.le.u32 p, %0, %1;\n\t"
+                 "@p cp.async.cg.shared.global.L2::128B [%2], [%3], 16;\n\t"
+                 "@p add.u32 %0, %0, 16; }\n\t"
+                 "cp.async.commit_group;\n\t"
+                 "cp.async.wait_group 1;"
+                 : "+r"(r.gn) : "r"(r.Q), "r"(r.ring | ((r.gn + kWBias) & (kWRing - 1))), "l"(payload + r.gn)
+                 : "memory");
+#else
     asm volatile("cp.async.wait_all;\n\t"
                  "{ .reg .pred p; setp.le.u32 p, %0, %1;\n\t"
                  "@p cp.async.cg.shared.global.L2::128B [%2], [%3], 16;\n\t"
@@ -377,6 +392,7 @@ __device__ __forceinline__ void ring_step_w(WordReader& r, const uint8_t* payloa
                  "cp.async.commit_group;"
                  : "+r"(r.gn) : "r"(r.Q), "r"(r.ring | ((r.gn + kWBias) & (kWRing - 1))), "l"(payload + r.gn)
                  : "memory");
+#endif
 }
 
 #ifndef EQ_WMERGE

@@ -45,7 +45,7 @@ struct DecBlock {
     const uint16_t* scales;
     uint64_t payload_bytes;
     uint32_t format;       // EQ_FMT_E4M3 | EQ_FMT_INT8 (bf16 dequant of the codes)
-    uint32_t codec;        // EQ_CODEC_BYTE | EQ_CODEC_WORD (one per launch)
+    uint32_t codec;        // EQ_CODEC_BYTE | EQ_CODEC_WORD | EQ_CODEC_PAIR (one per launch)
     uint32_t n_chunks;
     uint32_t cs;           // chunk symbols
     uint32_t n_layers;
@@ -567,10 +567,12 @@ struct PairTab {
     uint32_t rc0, rc1, rc2, rc3;   // rank codes 0..15 as bytes
     uint32_t k2p20, k2p12;
     const uint32_t* cum;   // single-table cumulative frequencies (shared, 257)
-    uint32_t ctab_s;       // shared address of the 256 × u16 pair id -> codes table (EQ_PAIR_CODETAB)
     uint32_t cum_s;        // shared address of cum (EQ_PAIR_LUT1 == 2)
 };
 
+#ifndef EQ_PAIR_CODETAB
+#define EQ_PAIR_CODETAB 1   // pair codes from a 512-B shared table (1 LDS) instead of 6 ALU ops over rc0..rc3
+#endif
 #ifndef EQ_PAIR_DIAG
 #define EQ_PAIR_DIAG 1   // pair ids in anti-diagonal order of (ra, rb): the frequent pairs (small ranks)
                          // get consecutive ids, so their codes-table words fall in distinct banks
@@ -587,9 +589,6 @@ __device__ __forceinline__ uint32_t pair_id(uint32_t ra, uint32_t rb) {
 #endif
 }
 
-#ifndef EQ_PAIR_CODETAB
-#define EQ_PAIR_CODETAB 1   // pair codes from a 512-B shared table (1 LDS) instead of 6 ALU ops over rc0..rc3
-#endif
 
 __device__ __forceinline__ void renorm_w(uint32_t& x, WordReader& r) {
     if (x < kLw) {
@@ -679,7 +678,10 @@ __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, cons
     x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
     renorm_w(x, r);
 #if EQ_PAIR_CODETAB
-    return lds_u16(T.ctab_s + ((e & 0xFFu) << 1));                    // rank nibbles -> codes
+    // the codes table sits right after the 16 KB LUT in one shared array: its address is the
+    // LUT's uniform base + a constant (a separate array's address was rematerialised per step
+    // with S2UR / UMOV / UIADD3 / ULEA — four issue slots per pair)
+    return lds_u16(T.lut_s + 4 * kM + ((e & 0xFFu) << 1));            // pair id -> codes
 #endif
     // rank nibbles -> codes: bytes of {rc0, rc1} for ranks 0-7, of {rc2, rc3} for 8-15,
     // chosen per byte by the nibble's bit 3 (PRMT sign-replicate of bits 3 and 7 of e)
@@ -844,7 +846,7 @@ template <bool BF16>
 __global__ void __launch_bounds__(kWThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) uint8_t rings[];      // kWThreads × kWRing
-    __shared__ __align__(16) uint32_t lut[kM];
+    __shared__ __align__(16) uint32_t lut[kM + 128];       // pair LUT, then the 256 × u16 codes table
     __shared__ uint32_t cum[257];
     __shared__ uint32_t pcum[227];
 #if EQ_PAIR_LUT1 == 3
@@ -855,7 +857,7 @@ k_decode_p(const __grid_constant__ DecParams P) {
     __shared__ __align__(16) uint32_t lut1[kM];
 #endif
 #if EQ_PAIR_CODETAB
-    __shared__ uint16_t ctab[256];
+    uint16_t* ctab = reinterpret_cast<uint16_t*>(lut + kM);
 #endif
 
     uint32_t bi = 0;
@@ -942,9 +944,6 @@ k_decode_p(const __grid_constant__ DecParams P) {
     T.k2p12 = P.k2p12;
     T.cum = cum;
     T.cum_s = (uint32_t)__cvta_generic_to_shared(cum);
-#if EQ_PAIR_CODETAB
-    T.ctab_s = (uint32_t)__cvta_generic_to_shared(ctab);
-#endif
 #ifdef EQ_PAIR_PROLOGUE_ONLY
     stage_wait_all();
     return;                                        // timing experiment: table builds only
@@ -1021,6 +1020,29 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     }
     if (chunk != blk.n_chunks) return EQ_ERR_SHAPE;
     d.n_chunks = chunk;
+    return EQ_OK;
+}
+
+extern "C" eq_status eq_decode_lanes(uint32_t codec, uint32_t out_dtype, int device, uint64_t* lanes) {
+    if (!lanes || codec > EQ_CODEC_PAIR || (out_dtype != EQ_OUT_FP8 && out_dtype != EQ_OUT_BF16)) return EQ_ERR_ARG;
+    const bool bf = out_dtype == EQ_OUT_BF16;
+    const void* fn;
+    int threads, per;
+    size_t dyn;
+    if (codec == EQ_CODEC_PAIR) {
+        fn = bf ? (const void*)k_decode_p<true> : (const void*)k_decode_p<false>;
+        threads = kWThreads, per = kWChunksPerCta, dyn = kDecWSmem;
+    } else if (codec == EQ_CODEC_WORD) {
+        fn = bf ? (const void*)k_decode_w<true> : (const void*)k_decode_w<false>;
+        threads = kWThreads, per = kWChunksPerCta, dyn = kDecWSmem;
+    } else {
+        fn = bf ? (const void*)k_decode<true> : (const void*)k_decode<false>;
+        threads = kDecThreads, per = kChunksPerCta, dyn = 0;
+    }
+    int sms = 0, ctas = 0;
+    EQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    EQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, threads, dyn));
+    *lanes = (uint64_t)sms * (uint64_t)ctas * (uint64_t)per;
     return EQ_OK;
 }
 

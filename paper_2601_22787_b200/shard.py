@@ -1,26 +1,30 @@
 """Multi-GPU sharding of the decode hot path.
 
 The work shards by transformer block: blocks are independent (own table, own chunks), so
-the decode itself needs no data-path collective (the bench: weak scaling, barrier + MAX
-timing only).  Where a consumer needs blocks or tensors another rank holds, the exchange is
+the decode itself needs no data-path collective (the bench: §8(e)'s contiguous 32/G split of
+one layer set, barrier + MAX timing only).  Where a consumer needs blocks or tensors another rank holds, the exchange is
 one all-gather: of compressed blocks (all_gather_blocks, decode locally) or of decoded row
 shards (all_gather_rows).
 """
 from __future__ import annotations
 
 
-def layer_ids(rank: int, world: int, blocks: int, scaling: str = "weak") -> list[int]:
+def layer_ids(rank: int, world: int, blocks: int, scaling: str = "strong") -> list[int]:
     """Block (layer) ids decoded by ``rank``.
 
+    strong (default, SURVEY §8(e) for config 3): ONE ``blocks``-block layer set split into
+            contiguous ranges, ``blocks``/world per rank (the first ``blocks`` % world ranks
+            take one more) — 32/G blocks per GPU for Llama-3-8B; total work fixed as N grows.
     weak:   every rank decodes its own ``blocks``-block layer set (distinct ids
-            rank*blocks .. rank*blocks+blocks-1) — per-GPU work fixed as N grows.
-    strong: one ``blocks``-block layer set split round-robin over the ranks."""
+            rank*blocks .. rank*blocks+blocks-1) — per-GPU work fixed as N grows."""
     if world < 1 or not (0 <= rank < world) or blocks < 1:
         raise ValueError("bad rank/world/blocks")
     if scaling == "weak":
         return [rank * blocks + i for i in range(blocks)]
     if scaling == "strong":
-        return [i for i in range(blocks) if i % world == rank]
+        base, extra = divmod(blocks, world)
+        lo = rank * base + min(rank, extra)
+        return list(range(lo, lo + base + (1 if rank < extra else 0)))
     raise ValueError(scaling)
 
 

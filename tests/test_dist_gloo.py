@@ -55,7 +55,8 @@ def test_two_rank_sharding_and_timing(scaling):
         assert flat == list(range(world * blocks))           # each rank its own layer set
         assert all(len(ids) == blocks for ids in gathered)
     else:
-        assert sorted(flat) == list(range(blocks))           # one layer set split
+        assert flat == list(range(blocks))                   # one layer set, contiguous ranges
+        assert [len(ids) for ids in gathered] == [4, 3]      # 7 blocks: the first rank takes the extra
     for rank, _, m, v in res:
         assert m == 15.0                                     # MAX over ranks
         assert v == pytest.approx(1e9 * world * 4 / 0.015 / 1e9)
@@ -64,6 +65,11 @@ def test_two_rank_sharding_and_timing(scaling):
 def test_single_process_identity_and_errors():
     assert shard.max_over_ranks(3.5) == 3.5
     assert shard.layer_ids(0, 1, 3) == [0, 1, 2]
+    # 32 Llama-3-8B blocks over G = 2, 4, 8 ranks -> contiguous 16 / 8 / 4-block ranges
+    for G in (2, 4, 8):
+        parts = [shard.layer_ids(r, G, 32) for r in range(G)]
+        assert [i for p in parts for i in p] == list(range(32))
+        assert all(p == list(range(r * 32 // G, (r + 1) * 32 // G)) for r, p in enumerate(parts))
     with pytest.raises(ValueError):
         shard.layer_ids(2, 2, 3)
 

@@ -42,10 +42,57 @@ def test_pair_decode_extreme_streams(kind):
     assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == s).all()
 
 
+def _pair_hists():
+    """Histograms for the pair-table kernel: the hand-derived golden cases, escape-heavy and
+    single-code streams, heavy heads over many count-1 codes (D < 0), random Pareto counts,
+    and a 2-bit weight matrix."""
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "normalize_worked.json")))
+    from test_oracle_codec import _expand, hist_of
+    hs = [hist_of(_expand(c["counts"])) for c in g["pair_cases"] + g["cases"]]
+    for kind in ["uniform", "subset2", "single", "skewed", "subset40", "subset130", "subset248"]:
+        hs.append(o.histogram(eqsynth.random_codes_stream(50000, 7, kind)))
+    rng = np.random.default_rng(5)
+    for t in range(40):
+        k = int(rng.integers(1, 257))
+        h = np.zeros(256, np.uint64)
+        idx = rng.permutation(256)[:k]
+        h[idx] = (rng.pareto(0.3 + rng.uniform(0, 3), k) * rng.choice([1, 10, 1000, 1e6])).astype(np.uint64) + 1
+        if t % 4 == 0:
+            h[idx[: k // 2]] = 1
+        hs.append(h)
+    W = eqsynth.weights(256, 4096, seed=6)
+    hs.append(o.histogram(o.quantize(W, (o.absmax_scales(W).astype(np.int32) + 1900).astype(np.uint16))))
+    big = np.zeros(256, np.uint64)                   # block-sized counts (8B down_proj scale)
+    big[[0, 1, 255, 8, 136]] = [91_000_000, 40_000_000, 39_000_000, 3_000_000, 1]
+    hs.append(big)
+    return hs
+
+
+def test_pair_table_kernel_vs_oracle():
+    """k_build_pair_table (device, R15 written as rank counting + water-filling) equals the
+    oracle's pair_table on every histogram, entry for entry, incl. K, escape and rank codes."""
+    for i, h in enumerate(_pair_hists()):
+        tab, err = eq.build_pair_table(torch.from_numpy(h.astype(np.int64)).to(DEV))
+        eq.check(err)
+        pt = o.pair_table(h)
+        want = np.zeros(512, np.uint16)
+        want[:256] = o.normalize(h)
+        want[256:481] = pt.pf
+        want[481] = pt.fesc
+        want[482] = pt.K
+        want.view(np.uint8)[968:984] = pt.rank_code
+        got = tab.cpu().numpy().view(np.uint16)
+        assert (got == want).all(), (i, np.nonzero(got != want))
+    _, err = eq.build_pair_table(torch.zeros(256, dtype=torch.int64, device=DEV))
+    with pytest.raises(eq.EqError):
+        eq.check(err)
+
+
 @pytest.mark.parametrize("cs", [4096, 333, 1])
 def test_pair_quantize_encode_byte_identical(cs):
     """Alg. 1 on the GPU with the pair codec, given the oracle's scales: the table buffer
-    (single + pair tables, host-built on the product side) and the stream are the oracle's."""
+    (single + pair tables, both built by device kernels) and the stream are the oracle's."""
     from test_gpu_parity import table_u16
     layers = small_layers(seed=5)
     S = [(o.absmax_scales(W).astype(np.int32) + 1500).astype(np.uint16) for W in layers]
