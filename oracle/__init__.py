@@ -31,6 +31,7 @@ CHUNK_SYMBOLS = 4096
 FMT_E4M3, FMT_INT8 = 0, 1
 CODEC_BYTE, CODEC_WORD = 0, 1      # rANS renormalisation: bytes (R9) / 16-bit words (R14)
 CODEC_PAIR = 2                      # word rANS over pairs of symbols with escapes (R15)
+CHUNK_LAYER, CHUNK_ROW = 0, 1       # chunks restart at every layer start / also at every row start (§8c.10)
 PAIR_K = 15
 
 
@@ -105,6 +106,10 @@ def lib():
             "eqo_decode_chunks_mt_codec": (ctypes.c_int, [ctypes.c_int, P, P, P, P, i64, P, P, ctypes.c_int]),
             "eqo_decode_dequant_layer_mt_codec": (ctypes.c_int, [ctypes.c_int, P, P, i64, i64, i64, i64, P, P, P,
                                                                  ctypes.c_int]),
+            "eqo_decode_dequant_layer_mt_codec_seg": (ctypes.c_int, [ctypes.c_int, P, P, i64, i64, i64, i64, i64, P, P,
+                                                                     P, ctypes.c_int]),
+            "eqo_decode_dequant_layer_mt_pair_seg": (ctypes.c_int, [P, P, i64, i64, i64, i64, i64, P, P, P, i32, P, u16,
+                                                                    P, ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -355,6 +360,7 @@ class OracleBlock:
     fmt: int = FMT_E4M3
     codec: int = CODEC_BYTE
     pair: object = None              # PairTable (codec CODEC_PAIR)
+    chunk_mode: int = CHUNK_LAYER
 
     @property
     def n_params(self) -> int:
@@ -371,15 +377,27 @@ class OracleBlock:
         return 8.0 * b / self.n_params
 
 
+def segment_sizes(layer_shapes, chunk_mode: int = CHUNK_LAYER) -> np.ndarray:
+    """Lengths of the stream segments at whose starts chunking restarts: one per layer
+    (CHUNK_LAYER), or one per row (CHUNK_ROW: every row of a layer with K
+    columns is split into ⌈K/cs⌉ chunks, e.g. 4096 + 4096 + 4096 + 2048 for K = 14336, so a
+    row's chunks are independent K slices of the fused GEMM, §8(f) row 1)."""
+    if chunk_mode == CHUNK_LAYER:
+        return np.array([r * c for r, c in layer_shapes], dtype=np.int64)
+    if chunk_mode == CHUNK_ROW:
+        return np.concatenate([np.full(r, c, dtype=np.int64) for r, c in layer_shapes])
+    raise ValueError("chunk_mode")
+
+
 def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3,
-                 codec: int = CODEC_BYTE) -> OracleBlock:
+                 codec: int = CODEC_BYTE, chunk_mode: int = CHUNK_LAYER) -> OracleBlock:
     """Alg. 1 l.4-5 + App. A.1: concatenate vec(W_q) of the block's layers, one table,
-    chunked rANS."""
+    chunked rANS (chunks restart at every segment of ``segment_sizes``)."""
     stream = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1) for c in codes_list])
     hist = histogram(stream)
     freq = normalize(hist)
-    sizes = np.array([r * c for r, c in layer_shapes], dtype=np.int64)
-    n_chunks = lib().eqo_block_chunks(_p(sizes), len(layer_shapes), cs)
+    sizes = segment_sizes(layer_shapes, chunk_mode)
+    n_chunks = lib().eqo_block_chunks(_p(sizes), sizes.size, cs)
     cap = 4 * n_chunks + 2 * stream.size + 64
     payload = np.zeros(cap, dtype=np.uint8)
     off = np.zeros(n_chunks + 1, dtype=np.uint32)
@@ -388,19 +406,20 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt:
         pt = pair_table(hist)
         cap = 4 * n_chunks + 4 * stream.size + 64
         payload = np.zeros(cap, dtype=np.uint8)
-        n = lib().eqo_encode_block_pair(_p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(pt.rank_code),
+        n = lib().eqo_encode_block_pair(_p(stream), _p(sizes), sizes.size, cs, _p(freq), _p(pt.rank_code),
                                         pt.K, _p(pt.pf), pt.fesc, _p(payload), cap, _p(off))
     else:
-        n = lib().eqo_encode_block_codec(codec, _p(stream), _p(sizes), len(layer_shapes), cs, _p(freq), _p(payload),
+        n = lib().eqo_encode_block_codec(codec, _p(stream), _p(sizes), sizes.size, cs, _p(freq), _p(payload),
                                          cap, _p(off))
     if n < 0:
         raise ValueError("encode failed %d" % n)
     return OracleBlock(list(layer_shapes), [np.asarray(s, dtype=np.uint16) for s in scales], freq, hist,
-                       payload[:n].tobytes(), off, cs, stream, fmt, codec, pt)
+                       payload[:n].tobytes(), off, cs, stream, fmt, codec, pt, chunk_mode)
 
 
 def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int = -1, oct_hi: int = 20,
-                    cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3, exclude=(), codec: int = CODEC_BYTE) -> OracleBlock:
+                    cs: int = CHUNK_SYMBOLS, fmt: int = FMT_E4M3, exclude=(), codec: int = CODEC_BYTE,
+                    chunk_mode: int = CHUNK_LAYER) -> OracleBlock:
     """Alg. 1 for one block.  ``layers``: list of bf16 [M,N] arrays (uint16 bits or torch).
     Either ``scales`` (per layer) is given, or ``lam`` selects the exhaustive search
     (lam=None -> AbsMax scales, i.e. the λ=0 lossless-FP8 baseline of P:257).  Layers whose
@@ -415,21 +434,21 @@ def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int =
             else:
                 scales.append(search(W, lam, oct_lo, oct_hi, fmt=fmt)[0])
     codes = [quantize(W, S, fmt) for W, S in zip(Ws, scales)]
-    return encode_codes(codes, shapes, scales, cs, fmt, codec)
+    return encode_codes(codes, shapes, scales, cs, fmt, codec, chunk_mode)
 
 
 def decode_block(blk: OracleBlock) -> np.ndarray:
     """Alg. 2 l.1: concatenated symbol stream."""
-    sizes = np.array([r * c for r, c in blk.layer_shapes], dtype=np.int64)
+    sizes = segment_sizes(blk.layer_shapes, blk.chunk_mode)
     out = np.zeros(int(sizes.sum()), dtype=np.uint8)
     payload = np.frombuffer(blk.payload, dtype=np.uint8).copy()
     off = np.ascontiguousarray(blk.chunk_off, dtype=np.uint32)
     if blk.codec == CODEC_PAIR:
         pt = blk.pair
-        st = lib().eqo_decode_block_pair(_p(payload), _p(off), _p(sizes), len(blk.layer_shapes), blk.chunk_symbols,
+        st = lib().eqo_decode_block_pair(_p(payload), _p(off), _p(sizes), sizes.size, blk.chunk_symbols,
                                          _p(blk.freq), _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc, _p(out))
     else:
-        st = lib().eqo_decode_block_codec(blk.codec, _p(payload), _p(off), _p(sizes), len(blk.layer_shapes),
+        st = lib().eqo_decode_block_codec(blk.codec, _p(payload), _p(off), _p(sizes), sizes.size,
                                           blk.chunk_symbols, _p(blk.freq), _p(out))
     if st:
         raise ValueError({1: "corrupt", 2: "truncated"}[st])
@@ -446,11 +465,10 @@ def decode_dequant(blk: OracleBlock) -> list:
     return outs
 
 
-def chunk_table(layer_shapes, cs: int = CHUNK_SYMBOLS):
-    """(sym0, n) per chunk of a block stream (layer-restart chunking)."""
+def chunk_table(layer_shapes, cs: int = CHUNK_SYMBOLS, chunk_mode: int = CHUNK_LAYER):
+    """(sym0, n) per chunk of a block stream (chunks restart at every segment)."""
     sym0, ns, base = [], [], 0
-    for r, c in layer_shapes:
-        n = r * c
+    for n in segment_sizes(layer_shapes, chunk_mode).tolist():
         for a in range(0, n, cs):
             sym0.append(base + a)
             ns.append(min(cs, n - a))
@@ -469,20 +487,22 @@ def decode_chunks_mt(payload: np.ndarray, chunk_off: np.ndarray, sym0: np.ndarra
 
 def decode_dequant_layer_mt(payload: np.ndarray, chunk_off: np.ndarray, cs: int, rows: int, cols: int,
                             scales: np.ndarray, freq: np.ndarray, threads: int, codec: int = CODEC_BYTE,
-                            pair: PairTable | None = None) -> np.ndarray:
+                            pair: PairTable | None = None, chunk_mode: int = CHUNK_LAYER) -> np.ndarray:
     """Alg. 2 l.1-2 for one layer's chunks on ``threads`` host threads (CPU baseline)."""
+    seg = rows * cols if chunk_mode == CHUNK_LAYER else cols
     payload = np.ascontiguousarray(payload, dtype=np.uint8)
     off = np.ascontiguousarray(chunk_off, dtype=np.uint32)
     out = np.zeros(rows * cols, dtype=np.uint16)
     if codec == CODEC_PAIR:
-        st = lib().eqo_decode_dequant_layer_mt_pair(_p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
+        st = lib().eqo_decode_dequant_layer_mt_pair_seg(_p(payload), _p(off), off.size - 1, cs, rows * cols, cols, seg,
                                                     _p(np.ascontiguousarray(scales, dtype=np.uint16)),
                                                     _p(np.ascontiguousarray(freq, dtype=np.uint16)),
                                                     _p(pair.rank_code), pair.K, _p(pair.pf), pair.fesc, _p(out), threads)
         if st:
             raise ValueError({1: "corrupt", 2: "truncated"}[st])
         return out.reshape(rows, cols)
-    st = lib().eqo_decode_dequant_layer_mt_codec(codec, _p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
+    st = lib().eqo_decode_dequant_layer_mt_codec_seg(codec, _p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
+                                                     seg,
                                            _p(np.ascontiguousarray(scales, dtype=np.uint16)),
                                            _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(out), threads)
     if st:

@@ -583,7 +583,10 @@ int eqo_decode_chunk(const uint8_t* in, int64_t nbytes, const uint16_t freq[256]
 /* ------------------------------------------------------------------------------------
  * Block stream (App. A.1): the vec'd code matrices of a block's
  * layers are concatenated in order; one table over the whole stream; the stream is
- * split into chunks of `cs` symbols that restart at each layer start;
+ * split into chunks of `cs` symbols that restart at each segment start:
+ * `layer_sizes` lists the segments — one per layer (layer-restart chunking), or one per
+ * row (EQ_CHUNK_ROW: a K-column row splits into ⌈K/cs⌉ chunks; the Python wrapper
+ * expands the layers into rows);
  * payload = chunk streams back to back; chunk_off[k] = byte offset of chunk k,
  * chunk_off[n_chunks] = payload bytes.
  * ---------------------------------------------------------------------------------- */
@@ -696,8 +699,19 @@ int eqo_decode_chunks_mt_codec(int codec, const uint8_t* payload, const uint32_t
  * (bf16 RNE of s_row·value(code)); chunks statically partitioned over POSIX threads. */
 typedef struct {
     const uint8_t* payload; const uint32_t* chunk_off; int64_t cs, size, cols;
-    const uint16_t* scales; const uint16_t* freq; uint16_t* out; int64_t k0, k1; int status; int codec;
+    const uint16_t* scales; const uint16_t* freq; uint16_t* out; int64_t k0, k1; int status; int codec; int64_t seg;
 } eqo_ljob;
+
+/* Chunk k of a layer whose chunking restarts every `seg` symbols (seg = the layer size:
+ * layer-restart chunking; seg = cols: EQ_CHUNK_ROW, boundaries also at every
+ * row start): its first symbol, and its length in *n. */
+static int64_t eqo_chunk_start(int64_t k, int64_t cs, int64_t seg, int64_t* n)
+{
+    int64_t cps = (seg + cs - 1) / cs;          /* chunks per segment */
+    int64_t s = k / cps, j = k % cps;
+    *n = seg - j * cs < cs ? seg - j * cs : cs;
+    return s * seg + j * cs;
+}
 
 static void* eqo_lworker(void* p)
 {
@@ -705,7 +719,7 @@ static void* eqo_lworker(void* p)
     uint8_t* sym = (uint8_t*)malloc((size_t)j->cs);
     j->status = 0;
     for (int64_t k = j->k0; k < j->k1; k++) {
-        int64_t a = k * j->cs, n = j->size - a < j->cs ? j->size - a : j->cs;
+        int64_t n, a = eqo_chunk_start(k, j->cs, j->seg, &n);
         int st = eqo_decode_chunk_codec(j->codec, j->payload + j->chunk_off[k],
                                         (int64_t)j->chunk_off[k + 1] - j->chunk_off[k], j->freq, sym, n);
         if (st && !j->status) j->status = st;
@@ -718,16 +732,16 @@ static void* eqo_lworker(void* p)
     return NULL;
 }
 
-int eqo_decode_dequant_layer_mt_codec(int codec, const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks,
-                                      int64_t cs, int64_t size, int64_t cols, const uint16_t* scales,
-                                      const uint16_t freq[256], uint16_t* out, int threads)
+int eqo_decode_dequant_layer_mt_codec_seg(int codec, const uint8_t* payload, const uint32_t* chunk_off,
+                                          int64_t n_chunks, int64_t cs, int64_t size, int64_t cols, int64_t seg,
+                                          const uint16_t* scales, const uint16_t freq[256], uint16_t* out, int threads)
 {
     if (threads < 1) threads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
     eqo_ljob* jobs = (eqo_ljob*)malloc(sizeof(eqo_ljob) * (size_t)threads);
     for (int t = 0; t < threads; t++) {
         jobs[t] = (eqo_ljob){payload, chunk_off, cs, size, cols, scales, freq, out,
-                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0, codec};
+                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0, codec, seg};
         pthread_create(&th[t], NULL, eqo_lworker, &jobs[t]);
     }
     int st = 0;
@@ -738,6 +752,14 @@ int eqo_decode_dequant_layer_mt_codec(int codec, const uint8_t* payload, const u
     free(th);
     free(jobs);
     return st;
+}
+
+int eqo_decode_dequant_layer_mt_codec(int codec, const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks,
+                                      int64_t cs, int64_t size, int64_t cols, const uint16_t* scales,
+                                      const uint16_t freq[256], uint16_t* out, int threads)
+{
+    return eqo_decode_dequant_layer_mt_codec_seg(codec, payload, chunk_off, n_chunks, cs, size, cols, size, scales,
+                                                 freq, out, threads);
 }
 
 int64_t eqo_row_objectives(const uint16_t* W, int64_t M, int64_t N, int64_t row, double lambda,
@@ -1036,7 +1058,7 @@ int eqo_decode_block_pair(const uint8_t* payload, const uint32_t* chunk_off, con
 typedef struct {
     const uint8_t* payload; const uint32_t* chunk_off; int64_t cs, size, cols;
     const uint16_t* scales; const uint16_t* freq; const uint8_t* rank_code; int32_t K; const uint16_t* pf;
-    uint16_t fesc; uint16_t* out; int64_t k0, k1; int status;
+    uint16_t fesc; uint16_t* out; int64_t k0, k1; int status; int64_t seg;
 } eqo_pjob;
 
 static void* eqo_pworker(void* p)
@@ -1045,7 +1067,7 @@ static void* eqo_pworker(void* p)
     uint8_t* sym = (uint8_t*)malloc((size_t)j->cs);
     j->status = 0;
     for (int64_t k = j->k0; k < j->k1; k++) {
-        int64_t a = k * j->cs, n = j->size - a < j->cs ? j->size - a : j->cs;
+        int64_t n, a = eqo_chunk_start(k, j->cs, j->seg, &n);
         int st = eqo_decode_chunk_pair(j->payload + j->chunk_off[k], (int64_t)j->chunk_off[k + 1] - j->chunk_off[k],
                                        j->freq, j->rank_code, j->K, j->pf, j->fesc, sym, n);
         if (st && !j->status) j->status = st;
@@ -1058,17 +1080,17 @@ static void* eqo_pworker(void* p)
     return NULL;
 }
 
-int eqo_decode_dequant_layer_mt_pair(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks, int64_t cs,
-                                     int64_t size, int64_t cols, const uint16_t* scales, const uint16_t freq[256],
-                                     const uint8_t rank_code[16], int32_t K, const uint16_t pf[225], uint16_t fesc,
-                                     uint16_t* out, int threads)
+int eqo_decode_dequant_layer_mt_pair_seg(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks,
+                                         int64_t cs, int64_t size, int64_t cols, int64_t seg, const uint16_t* scales,
+                                         const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
+                                         const uint16_t pf[225], uint16_t fesc, uint16_t* out, int threads)
 {
     if (threads < 1) threads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
     eqo_pjob* jobs = (eqo_pjob*)malloc(sizeof(eqo_pjob) * (size_t)threads);
     for (int t = 0; t < threads; t++) {
         jobs[t] = (eqo_pjob){payload, chunk_off, cs, size, cols, scales, freq, rank_code, K, pf, fesc, out,
-                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0};
+                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0, seg};
         pthread_create(&th[t], NULL, eqo_pworker, &jobs[t]);
     }
     int st = 0;
@@ -1079,4 +1101,13 @@ int eqo_decode_dequant_layer_mt_pair(const uint8_t* payload, const uint32_t* chu
     free(th);
     free(jobs);
     return st;
+}
+
+int eqo_decode_dequant_layer_mt_pair(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks, int64_t cs,
+                                     int64_t size, int64_t cols, const uint16_t* scales, const uint16_t freq[256],
+                                     const uint8_t rank_code[16], int32_t K, const uint16_t pf[225], uint16_t fesc,
+                                     uint16_t* out, int threads)
+{
+    return eqo_decode_dequant_layer_mt_pair_seg(payload, chunk_off, n_chunks, cs, size, cols, size, scales, freq,
+                                                rank_code, K, pf, fesc, out, threads);
 }

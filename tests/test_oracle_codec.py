@@ -411,3 +411,61 @@ def test_cpu_baseline_helpers_match_block_decode():
         payload = np.frombuffer(blk.payload + b"\0" * 16, dtype=np.uint8)
         out = o.decode_dequant_layer_mt(payload, blk.chunk_off, 512, 64, 1024, S, blk.freq, 3, codec, blk.pair)
         assert (out == o.decode_dequant(blk)[0]).all(), codec
+
+
+# ------------------------------------------------------------------ EQ_CHUNK_ROW
+ALL_CODECS = [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR]
+
+
+def _chunk_alone(blk, k, n):
+    data = blk.payload[int(blk.chunk_off[k]):int(blk.chunk_off[k + 1])]
+    if blk.codec == o.CODEC_PAIR:
+        return o.decode_chunk_pair(data, blk.freq, blk.pair, n)
+    return o.decode_chunk(data, blk.freq, n, blk.codec)
+
+
+@pytest.mark.parametrize("codec", ALL_CODECS)
+def test_row_chunking_layout_by_brute_force(codec):
+    """Row chunking: a row of K columns is ⌈K/cs⌉ chunks (full chunks, then the remainder);
+    chunk k, decoded ALONE from its byte range, is exactly the codes of its (row, column
+    range) — 10 columns at cs = 4 give 4 + 4 + 2, 7 columns give 4 + 3."""
+    rng = np.random.default_rng(codec)
+    shapes = [(6, 10), (3, 7), (2, 4)]
+    codes = [eqsynth.random_codes_stream(r * c, int(rng.integers(1 << 30)), "skewed").reshape(r, c) for r, c in shapes]
+    S = [np.full(r, 0x3F80, np.uint16) for r, _ in shapes]
+    blk = o.encode_codes(codes, shapes, S, 4, codec=codec, chunk_mode=o.CHUNK_ROW)
+    assert blk.n_chunks == 6 * 3 + 3 * 2 + 2 * 1
+    k = 0
+    for C, (r, c) in zip(codes, shapes):
+        for row in range(r):
+            for j0 in range(0, c, 4):
+                want = C[row, j0:min(c, j0 + 4)]
+                assert (_chunk_alone(blk, k, want.size) == want).all(), (k, row, j0)
+                k += 1
+    assert k == blk.n_chunks
+    assert (o.decode_block(blk) == np.concatenate([C.reshape(-1) for C in codes])).all()
+
+
+@pytest.mark.parametrize("codec", ALL_CODECS)
+def test_row_chunking_equals_layer_chunking_when_rows_are_whole_chunks(codec):
+    """K % cs == 0: row boundaries already are chunk boundaries, so the two modes give the
+    same bytes (the Llama-3-8B layers with K = 4096 at cs = 4096 / 2048)."""
+    W = eqsynth.weights(24, 512, seed=3)
+    S = (o.absmax_scales(W).astype(np.int32) + 1700).astype(np.uint16)
+    a = o.quantize_encode([W], scales=[S], cs=256, codec=codec)
+    b = o.quantize_encode([W], scales=[S], cs=256, codec=codec, chunk_mode=o.CHUNK_ROW)
+    assert a.payload == b.payload and (a.chunk_off == b.chunk_off).all()
+
+
+@pytest.mark.parametrize("codec", ALL_CODECS)
+def test_row_chunking_threaded_dequant_helper(codec):
+    """The threaded decode + dequant helper (bench CPU baseline, full-size parity) follows the
+    row layout: equal to decode_dequant for K = 700 at cs = 256 (256 + 256 + 188 per row)."""
+    W = eqsynth.weights(40, 700, seed=5)
+    S = (o.absmax_scales(W).astype(np.int32) + 1600).astype(np.uint16)
+    blk = o.quantize_encode([W], scales=[S], cs=256, codec=codec, chunk_mode=o.CHUNK_ROW)
+    assert blk.n_chunks == 40 * 3
+    payload = np.frombuffer(blk.payload + b"\0" * 16, dtype=np.uint8)
+    out = o.decode_dequant_layer_mt(payload, blk.chunk_off, 256, 40, 700, S, blk.freq, 3, codec, blk.pair,
+                                    chunk_mode=o.CHUNK_ROW)
+    assert (out == o.decode_dequant(blk)[0]).all()
