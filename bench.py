@@ -2,19 +2,25 @@
 """bench.py — EntQuant decode hot path on B200 (BASELINE config 3 by default).
 
 One step = one pass of the whole hot path over one batch: eq_decode_dequant of every
-chunk of the rank's Llama-3-8B-shaped layer set (32 blocks × 7 linear layers, ~2.0
-effective bits/param) into the per-device bf16 arena — §8(a) rows a7+a8.  The encode side
-(rows a1-a6) runs once before timing to produce the streams (its time is reported as
-``encode_s``).  Inputs are synthetic (eqsynth), resident in HBM; the 1.76 GB compressed
-input and 13.96 GB decoded output per step are both far larger than the 126 MB L2, so no
-flush is needed between steps.
+chunk of the rank's share of the Llama-3-8B-shaped layer set (32 blocks × 7 linear
+layers, ~2.0 effective bits/param) into the per-device bf16 arena — §8(a) rows a7+a8.
+The encode side (rows a1-a6) runs once before timing to produce the streams (its time is
+reported as ``encode_s``).  Inputs are synthetic (eqsynth), resident in HBM; the 1.76 GB
+compressed input and 13.96 GB decoded output per step are both far larger than the 126 MB
+L2, so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
-Multi-GPU: weak scaling — every rank decodes its own 32-block layer set (distinct layers),
-no data-path collective (the work shards by block); a barrier brackets the
-timed region and the time is the max over ranks.
+Multi-GPU: strong scaling by default — ONE 32-block layer set split into
+contiguous ranges of 32/G blocks per rank, no data-path collective (blocks are
+independent); a barrier brackets the timed region and the time is the max over ranks.
+``--scaling weak`` gives every rank its own 32-block set.  ``--as-rank R/G`` runs rank R's
+share of a G-GPU split on one GPU (the per-rank lines of profiles/r2).
+
+After timing: every decoded bf16 layer that the CPU-baseline leg decodes with the oracle is
+compared with the GPU arena bit for bit (the run fails on a mismatch), and the line carries
+the rate statistics of the encoded layer set (Ĥ, coded / n·Ĥ, unique codes, p(0), relative ℓ1).
 """
 from __future__ import annotations
 
@@ -45,14 +51,19 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="llama-3-8b")
-    ap.add_argument("--blocks", type=int, default=0, help="blocks per rank (default: all layers of the model)")
+    ap.add_argument("--blocks", type=int, default=0, help="blocks of the layer set (default: all layers of the model)")
     ap.add_argument("--target-bits", type=float, default=2.0)
     ap.add_argument("--lam", type=float, default=None, help="fixed λ (skips calibration)")
     ap.add_argument("--calib-stride", type=int, default=16)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
+    ap.add_argument("--as-rank", default=None, help="R/G: run rank R's share of a G-GPU split on this one GPU")
+    ap.add_argument("--chunk-symbols", type=int, default=0,
+                    help="symbols per chunk (0: auto — 4096 unless the rank's share is too few chunks "
+                         "for whole rounds of the decoder's lanes, DESIGN.md §7)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp8", action="store_true")
+    ap.add_argument("--no-stats", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
     ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"],
@@ -165,93 +176,189 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
-def traffic_from_profiles(codec: str, kind: str):
-    """dram bytes per launch of the decode kernel from the committed ncu --set full summary."""
+DECODER_SOURCES = ("rans_dec.cu", "decode_core.cuh", "common.cuh")
+
+
+def decoder_source_sha() -> str:
+    """sha256 (16 hex) of the decode kernels' sources: ties a committed ncu traffic figure
+    to the kernel it was measured on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in DECODER_SOURCES:
+        h.update(open(os.path.join(ROOT, "paper_2601_22787_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def traffic_from_profiles(codec: str, kind: str, blocks: int, chunk_symbols: int):
+    """DRAM bytes per launch of the decode kernel from the committed ncu --set full summary —
+    only if it was captured on THIS kernel source (sha) and launch (blocks, chunk size);
+    otherwise None (a stale figure is never reported)."""
     p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
     try:
-        d = json.load(open(p))
-        return d[codec][kind]["dram_bytes_per_launch"]
+        c = json.load(open(p))[codec]
+        e = dict(c[kind], **{k: c.get(k) for k in ("kernel_sha", "blocks", "chunk_symbols", "when", "source")})
     except Exception:
-        return None
+        return None, "no ncu capture"
+    if e.get("kernel_sha") != decoder_source_sha():
+        return None, f"ncu capture stale (kernel sha {e.get('kernel_sha')} != {decoder_source_sha()})"
+    if e.get("blocks") != blocks or e.get("chunk_symbols") != chunk_symbols:
+        return None, "ncu capture of another launch"
+    return e["dram_bytes_per_launch"], f"{e.get('source', p)} (kernel sha {e['kernel_sha']}, {e.get('when', '?')})"
+
+
+# ---------------------------------------------------------------- shared: the workload
+def share_ids(args, rank: int, world: int):
+    """(block ids of this process, simulated (rank, world)) — --as-rank R/G runs rank R's share
+    of a G-GPU split on this one GPU."""
+    from paper_2601_22787_b200 import shard
+    if args.as_rank:
+        r, g = (int(x) for x in args.as_rank.split("/"))
+        return shard.layer_ids(r, g, args.blocks, args.scaling), (r, g)
+    return shard.layer_ids(rank, world, args.blocks, args.scaling), (rank, world)
+
+
+def choose_chunk(args, layer_ids, lanes: int) -> int:
+    """Chunk length for the rank's share: a launch runs ceil(chunks / lanes)
+    rounds of one serial chunk-length chain, so a share of 1.1 rounds at 4096 symbols wastes
+    almost half the GPU.  Among 4096 / 2048 / 1024 take the one with the shortest
+    rounds × (length + per-chunk overhead); 4096 (the smallest rate) wins ties."""
+    import eqsynth
+    if args.chunk_symbols:
+        return args.chunk_symbols
+    sizes = [r * c for r, c in eqsynth.block_shapes(args.model)] * len(layer_ids)
+    best, best_t = 4096, None
+    for cs in (4096, 2048, 1024):
+        n = sum((x + cs - 1) // cs for x in sizes)
+        t = -(-n // lanes) * (cs + CHUNK_OVERHEAD_SYMBOLS)
+        if best_t is None or t < best_t:
+            best, best_t = cs, t
+    return best
+
+
+CHUNK_OVERHEAD_SYMBOLS = 256        # per-chunk setup (staging, table-build share, stores) in symbol-steps
+
+
+def encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist=None):
+    """λ calibration (global; one deterministic calibration on block 0) and Alg. 1 per
+    block of the share.  Returns (blocks, λ, estimated bits, encode seconds)."""
+    import torch
+    t0 = time.time()
+    lam, est = args.lam, None
+    if lam is None:
+        calib = eqsynth.block_weights(args.model, 0, device=dev)
+        lam, est = eq.calibrate_lambda(calib, args.target_bits, row_stride=args.calib_stride, chunk_symbols=cs,
+                                       codec=CODECS[args.codec])
+        del calib
+    if dist is not None:
+        t = torch.tensor([lam], dtype=torch.float64, device=dev)
+        dist.broadcast(t, 0)
+        lam = float(t.item())
+    blocks, scratch = [], None
+    for lid in layer_ids:
+        Ws = eqsynth.block_weights(args.model, lid, device=dev)
+        if scratch is None:
+            _, _, sb = eq.encode_bounds(Ws, chunk_symbols=cs)
+            scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch, chunk_symbols=cs, codec=CODECS[args.codec]))
+        del Ws
+    del scratch
+    torch.cuda.synchronize()
+    return blocks, lam, est, time.time() - t0
+
+
+def workload_config(args, n_blocks, n_params, cs, world):
+    return {
+        "workload": f"config3: {args.model}-shaped layer set of {args.blocks} blocks x 7 linear layers, "
+                    f"{n_blocks} blocks per rank, ~{args.target_bits} effective bits/param, chunk-parallel rANS "
+                    f"decode + fused dequant to bf16",
+        "model_shapes": args.model, "blocks_per_rank": n_blocks, "params_per_rank": n_params,
+        "chunk_symbols": cs, "codec": args.codec, "target_bits": args.target_bits,
+        "l2": "inputs larger than L2 (compressed in + decoded out per step >> 126 MB); no flush",
+        "parallelism": f"block-sharded x{world} ({args.scaling}, contiguous ranges)" if args.scaling == "strong"
+                       else f"block-sharded x{world} (weak)",
+    }
+
+
+def oracle_pair_table(table, o):
+    """The pair-codec tables of a block's table buffer (layout of include/entquant.h)."""
+    import numpy as np
+    return o.PairTable(table.view(np.uint8)[968:984].copy(), int(table[482]), table[256:481].copy(), int(table[481]))
+
+
+def oracle_layers(blk, o):
+    """Host copies of one GPU-encoded block for the oracle, and its per-layer chunk ranges."""
+    import numpy as np
+    import torch
+    cs = blk.chunk_symbols
+    off_all = blk.chunk_off.cpu().numpy().astype(np.uint32)
+    payload = blk.payload.cpu().numpy()
+    table = blk.freq.cpu().numpy().view(np.uint16)
+    pair = oracle_pair_table(table, o) if blk.codec == CODECS["pair"] else None
+    scales = blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)
+    out, k0, r0 = [], 0, 0
+    for (r, c) in blk.shapes:
+        nk = (r * c + cs - 1) // cs
+        out.append((off_all[k0:k0 + nk + 1], r, c, scales[r0:r0 + r]))
+        k0 += nk
+        r0 += r
+    return payload, table[:256], pair, out
 
 
 # ---------------------------------------------------------------- reference arm (oracle)
 def run_reference(args, rank, world):
+    """The oracle, as it stands, timed on the host cores on OUR arm's config: the streams
+    of block 0 of the same layer set (λ calibrated and encoded exactly as our arm does —
+    untimed input preparation), and per step the oracle's decode + dequant of all 7 whole
+    layers of that block.  Rank 0 only; other ranks exit without work."""
     if rank != 0:
         return
-    import eqsynth as _es
-    if args.blocks <= 0:                     # same workload config as our arm
-        args.blocks = _es.LLAMA[args.model]["layers"]
-    n_params_full = args.blocks * sum(r * c for r, c in _es.block_shapes(args.model))
     import numpy as np
+    import torch
 
     import eqsynth
     import oracle as o
-    lam = args.lam if args.lam is not None else DEFAULT_LAMBDA
+    import paper_2601_22787_b200 as eq
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    if args.blocks <= 0:
+        args.blocks = eqsynth.LLAMA[args.model]["layers"]
+    ids, (r, g) = share_ids(args, rank, world)
+    cs = choose_chunk(args, ids, eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, 0))
+    n_params = len(ids) * sum(a * b for a, b in eqsynth.block_shapes(args.model))
+    blocks, lam, est, enc_s = encode_share(args, eq, eqsynth, dev, [0], cs)
+    blk = blocks[0]
+    payload, freq, pair, layers = oracle_layers(blk, o)
     threads = os.cpu_count() or 1
-    shapes = eqsynth.block_shapes(args.model)
-    rows_per = 16
-    layers, full_shapes = [], []
-    for m, (r, c) in enumerate(shapes):
-        ids = list(range(0, r, max(1, r // rows_per)))[:rows_per]
-        layers.append(eqsynth.weights_rows(ids, r, c, seed=0, layer=0, matrix=m))
-        full_shapes.append((r, c))
-    t0 = time.time()
-    blk = o.quantize_encode(layers, lam=lam, codec=CODECS[args.codec])
-    enc_s = time.time() - t0
-    payload = np.frombuffer(blk.payload + b"\0" * 16, dtype=np.uint8)
-    # per-layer chunk ranges of the sample block
-    sym0, ns = o.chunk_table(blk.layer_shapes, blk.chunk_symbols)
-    per_layer, k = [], 0
-    for (r, c), S in zip(blk.layer_shapes, blk.scales):
-        nk = (r * c + blk.chunk_symbols - 1) // blk.chunk_symbols
-        per_layer.append((blk.chunk_off[k:k + nk + 1].copy(), r, c, S))
-        k += nk
 
     def one_pass():
-        for off, r, c, S in per_layer:
-            o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, blk.freq, threads, blk.codec, blk.pair)
+        for off, rr, c, S in layers:
+            o.decode_dequant_layer_mt(payload, off, cs, rr, c, S, freq, threads, blk.codec, pair)
 
-    t = time.time()
-    one_pass()
-    once = max(time.time() - t, 1e-4)
-    reps = max(1, int(min(3.0, 180.0 / max(1, args.steps + args.warmup)) / once))
-    bytes_pass = blk.n_params * 2 + len(blk.payload) + 4 * (blk.n_chunks + 1) + 2 * sum(r for r, _ in blk.layer_shapes) + 512
+    bytes_pass = blk.compressed_bytes() + 2 * blk.n_params
     for _ in range(args.warmup):
-        for _ in range(reps):
-            one_pass()
+        one_pass()
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        for _ in range(reps):
-            one_pass()
+        one_pass()
         times.append(time.perf_counter() - t)
     tot = sum(times)
-    gbs = bytes_pass * reps * args.steps / tot / 1e9
-    sample = (f"oracle decode+dequant (eqo_decode_chunk + bf16 RNE dequant) of {rows_per} rows of each of the 7 "
-              f"{args.model} block-0 matrices ({blk.n_params} params, {blk.n_chunks} chunks, λ={lam}, "
-              f"{blk.effective_bits():.3f} eff. bits/param), x{reps} per step")
+    gbs = bytes_pass * args.steps / tot / 1e9
+    sample = (f"oracle decode + bf16 dequant (eqo_decode_chunk_* per chunk, POSIX threads) of block 0: all 7 whole "
+              f"{args.model} layers ({blk.n_params} params, {blk.n_chunks} chunks of {cs} symbols, "
+              f"{8 * blk.compressed_bytes() / blk.n_params:.4f} eff. bits/param), one block per step")
     line = {
-        "metric": METRIC, "value": gbs, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+        "metric": METRIC, "value": gbs, "unit": "GB/s", "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": workload_config(args, n_params_full, lam),
+        "data": "synthetic (eqsynth: Student-t nu=4, sigma=0.02, per-row log-normal spread; Llama shapes)",
+        "config": workload_config(args, len(ids), n_params, cs, g),
+        "lambda": lam,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "bits_per_param": blk.effective_bits(), "encode_s_sample": enc_s,
+        "bits_per_param": 8 * blk.compressed_bytes() / blk.n_params, "encode_s_sample": enc_s,
     }
     print(json.dumps(line), flush=True)
-
-
-def workload_config(args, n_params, lam):
-    return {
-        "workload": f"config3: {args.model}-shaped layer set, {args.blocks or 'all'} blocks x 7 linear layers per rank, "
-                    f"~{args.target_bits} effective bits/param, chunk-parallel rANS decode + fused dequant to bf16",
-        "model_shapes": args.model, "blocks_per_rank": args.blocks, "params_per_rank": n_params,
-        "chunk_symbols": 4096, "codec": args.codec, "lambda": lam, "target_bits": args.target_bits,
-        "l2": "inputs larger than L2 (compressed in + decoded out per step >> 126 MB); no flush",
-        "parallelism": f"block-sharded x{args.gpus} ({args.scaling})",
-    }
 
 
 # ---------------------------------------------------------------- our arm
@@ -268,43 +375,23 @@ def main():
 
     import eqsynth
     import paper_2601_22787_b200 as eq
+    from paper_2601_22787_b200 import shard
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    L = eqsynth.LLAMA[args.model]["layers"]
     if args.blocks <= 0:
-        args.blocks = L
-    from paper_2601_22787_b200 import shard
-    layer_ids = shard.layer_ids(rank, world, args.blocks, args.scaling)
+        args.blocks = eqsynth.LLAMA[args.model]["layers"]
+    layer_ids, (sim_rank, sim_world) = share_ids(args, rank, world)
+    lanes = eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, local)
+    cs = choose_chunk(args, layer_ids, lanes)
 
     # ---- encode side (once): λ calibration (global) then Alg. 1 per block
-    t0 = time.time()
-    lam = args.lam
-    est = None
-    if lam is None:
-        calib = eqsynth.block_weights(args.model, 0, device=dev)
-        lam, est = eq.calibrate_lambda(calib, args.target_bits, row_stride=args.calib_stride)
-        del calib
-    if world > 1:
-        t = torch.tensor([lam], dtype=torch.float64, device=dev)
-        dist.broadcast(t, 0)
-        lam = float(t.item())
-    blocks = []
-    scratch = None
-    for lid in layer_ids:
-        Ws = eqsynth.block_weights(args.model, lid, device=dev)
-        if scratch is None:
-            _, _, sb = eq.encode_bounds(Ws)
-            scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch, codec=CODECS[args.codec]))
-        del Ws
-    del scratch
-    torch.cuda.synchronize()
-    enc_s = time.time() - t0
+    blocks, lam, est, enc_s = encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist if world > 1 else None)
     torch.cuda.empty_cache()
 
     n_params = sum(b.n_params for b in blocks)
+    n_chunks = sum(b.n_chunks for b in blocks)
     comp_bytes = sum(b.compressed_bytes() for b in blocks)
     payload_bytes = sum(b.payload_bytes for b in blocks)
     bytes_bf16 = comp_bytes + 2 * n_params
@@ -336,7 +423,7 @@ def main():
         total = shard.max_over_ranks(total, dist if world > 1 else None, dev)
         return total, per
 
-    # ---- main metric: bf16-out decode of the whole layer set
+    # ---- main metric: bf16-out decode of the rank's share
     dec = eq.Decoder(blocks, eq.EQ_OUT_BF16)
     clocks = ClockSampler(local) if not args.profile else None
     total_ms, per = time_decoder(dec, args.steps, args.warmup, clocks)
@@ -344,21 +431,24 @@ def main():
     launch_ms = statistics.mean(per)
     achieved = bytes_bf16 / (launch_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
+    traffic, traffic_src = traffic_from_profiles(args.codec, "bf16", len(blocks), cs)
 
-    fp8 = None
+    fp8, dec8 = None, None
     if not args.no_fp8:
-        del dec
-        torch.cuda.empty_cache()
         dec8 = eq.Decoder(blocks, eq.EQ_OUT_FP8)
         t8, per8 = time_decoder(dec8, args.steps, args.warmup)
         l8 = statistics.mean(per8)
+        tr8, _ = traffic_from_profiles(args.codec, "fp8", len(blocks), cs)
         fp8 = {"value": shard.aggregate_gbs(bytes_fp8, world, args.steps, t8), "unit": "GB/s",
-               "ms_per_step": t8 / args.steps, "frac": bytes_fp8 / (l8 / 1e3) / 1e9 / peak,
-               "traffic": traffic_from_profiles(args.codec, "fp8")}
+               "ms_per_step": t8 / args.steps, "frac": bytes_fp8 / (l8 / 1e3) / 1e9 / peak, "traffic": tr8}
+
+    # ---- rate statistics of the encoded share (Eq. 2)
+    stats = None
+    if not args.no_stats and not args.profile:
+        stats = rate_stats(args, eq, eqsynth, blocks, layer_ids, dec, dec8, dev, dist if world > 1 else None)
+    if dec8 is not None:
         del dec8
         torch.cuda.empty_cache()
-    else:
-        del dec
 
     # ---- e2e through the public C-ABI with host buffers (H2D + decode + D2H per step)
     e2e = None
@@ -384,30 +474,42 @@ def main():
                "ms_per_step": ms / k_e2e}
         del hb
 
-    # ---- CPU baseline: the oracle on the host cores, rank 0, N=1, bounded sample
-    cpu = None
+    # ---- CPU baseline: the oracle on the host cores, rank 0, N=1, bounded sample; every
+    #      layer it decodes is compared with the GPU arena bit for bit
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cpu = cpu_baseline(blocks, args.cpu_seconds)
+        cpu, parity = cpu_baseline(blocks, dec, args.cpu_seconds)
+    del dec
 
     if rank == 0:
-        cs = clocks.summary() if clocks is not None else None
+        cs_clk = clocks.summary() if clocks is not None else None
+        per_rank = {"rank": sim_rank, "of": sim_world, "blocks": layer_ids[0] if len(layer_ids) == 1 else
+                    [layer_ids[0], layer_ids[-1]], "chunks": n_chunks, "decoder_lanes": lanes,
+                    "rounds": n_chunks / lanes} if args.as_rank else None
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "out_dtype": "bf16",
             "data": "synthetic (eqsynth: Student-t nu=4, sigma=0.02, per-row log-normal spread; Llama shapes)",
-            "config": workload_config(args, n_params, lam),
+            "config": workload_config(args, len(layer_ids), n_params, cs, sim_world),
+            "lambda": lam,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic_from_profiles(args.codec, "bf16"),
-                         "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": bytes_bf16, "launch_ms": launch_ms},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps, "clocks": cs,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src, "kernel": f"k_decode_{'p' if args.codec == 'pair' else 'w' if args.codec == 'word' else ''}",
+                         "kernel_sha": decoder_source_sha(),
+                         "algorithmic_bytes_per_launch": bytes_bf16, "launch_ms": launch_ms,
+                         "chunks": n_chunks, "decoder_lanes": lanes},
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "gpu_launches": args.steps, "clocks": cs_clk,
             "bits_per_param": 8.0 * comp_bytes / n_params,
             "payload_bits_per_param": 8.0 * payload_bytes / n_params,
-            "calib_est_bits": est, "symbols_per_s": n_params * world * args.steps / (total_ms / 1e3),
-            "fp8_out": fp8, "encode_s": enc_s,
+            "rate": stats, "calib_est_bits": est,
+            "symbols_per_s": n_params * world * args.steps / (total_ms / 1e3),
+            "fp8_out": fp8, "encode_s": enc_s, "per_rank_share": per_rank,
         }
         print(json.dumps(line), flush=True)
+    if parity is not None and not parity["ok"]:
+        print(f"PARITY FAILURE: {parity}", file=sys.stderr, flush=True)
+        sys.exit(3)
     if world > 1:
         dist.destroy_process_group()
 
@@ -420,64 +522,119 @@ class _Null:
         return False
 
 
-def cpu_baseline(blocks, seconds: float):
-    """The oracle, as it stands, decoding+dequantising a bounded sample of the same
+def rate_stats(args, eq, eqsynth, blocks, layer_ids, dec, dec8, dev, dist=None):
+    """Rate and distortion of the encoded share: Ĥ of each block's joint histogram (Eq. 2,
+    P:160-168) and of each layer alone (the block-table penalty), coded size
+    (payload + offsets) over n·Ĥ (the north star's ≤ 1.02), unique codes, p(0), and the
+    relative ℓ1 distortion Σ|W − Ŵ| / Σ|W| of Eq. 4 (weights regenerated by eqsynth).
+    Codes come from the FP8-out arena (else from the bf16 one is not possible: requires dec8)."""
+    import torch
+    if dec8 is None:
+        return None
+    v8, v16 = dec8.views(), dec.views()
+    H_blocks, ratios, uniq, per_layer_gap = [], [], [], []
+    hist_all = torch.zeros(256, dtype=torch.float64, device=dev)
+    err_l1 = torch.zeros((), dtype=torch.float64, device=dev)
+    w_l1 = torch.zeros((), dtype=torch.float64, device=dev)
+
+    def ent(h):
+        p = h[h > 0] / h.sum()
+        return float(-(p * torch.log2(p)).sum())
+
+    for blk, lid, l8, l16 in zip(blocks, layer_ids, v8, v16):
+        hb = torch.zeros(256, dtype=torch.float64, device=dev)
+        nh = 0.0
+        for v in l8:
+            h = torch.bincount(v.view(torch.uint8).reshape(-1), minlength=256).double()
+            nh += float(h.sum()) * ent(h)
+            hb += h
+        Hb = ent(hb)
+        H_blocks.append(Hb)
+        per_layer_gap.append(Hb - nh / float(hb.sum()))
+        coded = blk.payload_bytes + 4 * (blk.n_chunks + 1)
+        ratios.append(8.0 * coded / (float(hb.sum()) * Hb))
+        uniq.append(int((hb > 0).sum()))
+        hist_all += hb
+        Ws = eqsynth.block_weights(args.model, lid, device=dev)
+        for W, What in zip(Ws, l16):
+            err_l1 += (W.double() - What.double()).abs().sum()
+            w_l1 += W.double().abs().sum()
+        del Ws
+    n = float(hist_all.sum())
+    coded_all = float(sum(b.payload_bytes + 4 * (b.n_chunks + 1) for b in blocks))
+    payload_all = float(sum(b.payload_bytes for b in blocks))
+    nH = float(sum(float(b.n_params) * H for b, H in zip(blocks, H_blocks)))
+    if dist is not None:                       # whole-job figures over all ranks
+        t = torch.tensor([n, coded_all, payload_all, nH, float(err_l1), float(w_l1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        dist.all_reduce(hist_all)
+        n, coded_all, payload_all, nH, e1, w1 = t.tolist()
+        mx = torch.tensor([max(ratios)], dtype=torch.float64, device=dev)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        ratio_max = float(mx.item())
+    else:
+        e1, w1 = float(err_l1), float(w_l1)
+        ratio_max = max(ratios)
+    return {
+        "H_block_bits": {"min": min(H_blocks), "mean": sum(H_blocks) / len(H_blocks), "max": max(H_blocks)},
+        "H_layer_set_bits": ent(hist_all),
+        "block_table_penalty_bits": {"max": max(per_layer_gap), "mean": sum(per_layer_gap) / len(per_layer_gap)},
+        "coded_over_nH": coded_all * 8.0 / nH, "coded_over_nH_max_block": ratio_max,
+        "coded_def": "payload (incl. 4-byte chunk states) + 4-byte chunk offsets, over n x H-hat of each block's histogram",
+        "payload_bits_per_symbol": 8.0 * payload_all / n,
+        "unique_codes": {"min": min(uniq), "max": max(uniq)},
+        "p0": float(hist_all[0] / hist_all.sum()),
+        "rel_l1": e1 / w1,
+        "symbols": n,
+    }
+
+
+def cpu_baseline(blocks, dec, seconds: float):
+    """The oracle, as it stands, decoding + dequantising a bounded sample of the same
     workload (whole layers of the leading blocks, until ~``seconds`` of host work) on all
-    host cores.  Timing only — not a parity check."""
+    host cores, timed; and every layer it decodes compared with the GPU's bf16 arena bit for
+    bit (the full-size parity leg: a mismatch fails the run)."""
     import numpy as np
     import torch
 
     import oracle as o
     threads = os.cpu_count() or 1
-    done_bytes, done_syms, wall, layers = 0, 0, 0.0, 0
-    for blk in blocks:
-        cs = blk.chunk_symbols
-        off_all = blk.chunk_off.cpu().numpy().astype(np.uint32)
-        payload = blk.payload.cpu().numpy()
-        table = blk.freq.cpu().numpy().view(np.uint16)
-        freq = table[:256]
-        pair = None
-        if blk.codec == CODECS["pair"]:                    # the table buffer layout of include/entquant.h
-            pair = o.PairTable(table.view(np.uint8)[968:984].copy(), int(table[482]), table[256:481].copy(),
-                               int(table[481]))
-        scales = blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)
-        k0, r0 = 0, 0
-        for (r, c) in blk.shapes:
-            nk = (r * c + cs - 1) // cs
-            off = off_all[k0:k0 + nk + 1]
+    views = dec.views()
+    done_bytes, done_syms, wall, layers, mism = 0, 0, 0.0, 0, 0
+    for blk, vb in zip(blocks, views):
+        payload, freq, pair, lay = oracle_layers(blk, o)
+        for (off, r, c, S), v in zip(lay, vb):
+            nk = off.size - 1
             t = time.perf_counter()
-            o.decode_dequant_layer_mt(payload, off, cs, r, c, scales[r0:r0 + r], freq, threads, blk.codec, pair)
+            out = o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, freq, threads, blk.codec, pair)
             wall += time.perf_counter() - t
+            gpu = v.contiguous().view(torch.int16).cpu().numpy().view(np.uint16).reshape(r, c)
+            mism += int(np.count_nonzero(np.asarray(out).reshape(r, c) != gpu))
             done_bytes += int(off[-1] - off[0]) + 4 * (nk + 1) + 2 * r + 2 * r * c
             done_syms += r * c
             layers += 1
-            k0 += nk
-            r0 += r
             if wall >= seconds:
                 break
-        done_bytes += 512
+        done_bytes += 2 * blk.freq.numel()
         if wall >= seconds:
             break
     # the same oracle on ONE host thread (SURVEY §8(d)), on the first layer of block 0
     blk = blocks[0]
-    r, c = blk.shapes[0]
-    nk = (r * c + blk.chunk_symbols - 1) // blk.chunk_symbols
-    off = blk.chunk_off.cpu().numpy().astype(np.uint32)[:nk + 1]
+    payload, freq, pair, lay = oracle_layers(blk, o)
+    off, r, c, S = lay[0]
     t = time.perf_counter()
-    table = blk.freq.cpu().numpy().view(np.uint16)
-    pair = None
-    if blk.codec == CODECS["pair"]:
-        pair = o.PairTable(table.view(np.uint8)[968:984].copy(), int(table[482]), table[256:481].copy(), int(table[481]))
-    o.decode_dequant_layer_mt(blk.payload.cpu().numpy(), off, blk.chunk_symbols, r, c,
-                              blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)[:r],
-                              table[:256], 1, blk.codec, pair)
+    o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, freq, 1, blk.codec, pair)
     w1 = time.perf_counter() - t
-    b1 = int(off[-1] - off[0]) + 4 * (nk + 1) + 2 * r + 2 * r * c
-    return {"value": done_bytes / wall / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
-            "sample": f"{layers} whole layers ({done_syms} symbols) of the leading blocks, decode+dequant to bf16 "
-                      f"with eqo_decode_chunk on {threads} threads, {wall:.1f} s wall",
-            "value_1_thread": b1 / w1 / 1e9,
-            "sample_1_thread": f"layer 0 of block 0 ({r * c} symbols) on 1 thread, {w1:.1f} s wall"}
+    b1 = int(off[-1] - off[0]) + 4 * off.size + 2 * r + 2 * r * c
+    cpu = {"value": done_bytes / wall / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
+           "sample": f"{layers} whole layers ({done_syms} symbols) of the leading blocks, decode+dequant to bf16 "
+                     f"with the oracle's per-chunk decoder on {threads} threads, {wall:.1f} s wall",
+           "value_1_thread": b1 / w1 / 1e9,
+           "sample_1_thread": f"layer 0 of block 0 ({r * c} symbols) on 1 thread, {w1:.1f} s wall"}
+    parity = {"layers": layers, "symbols": done_syms, "mismatches": mism, "ok": mism == 0,
+              "what": "oracle decode+dequant of the GPU-encoded streams vs the GPU bf16 arena of the timed launch, "
+                      "element by element"}
+    return cpu, parity
 
 
 if __name__ == "__main__":

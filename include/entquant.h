@@ -67,6 +67,13 @@ typedef enum {
                                     /* by ra*15+rb, [481] escape, [482] K, [484,492) rank   */
                                     /* codes as bytes                                        */
 
+/* Chunking of a block's symbol stream (R10). */
+#define EQ_CHUNK_LAYER 0u           /* chunks of chunk_symbols restart at every layer start */
+#define EQ_CHUNK_ROW   1u           /* ... and at every row start: a row of K columns is    */
+                                    /* ceil(K/cs) chunks (4096+4096+4096+2048 for K=14336),  */
+                                    /* independent K slices for eq_qmatmul (§8(f) row 1);    */
+                                    /* identical bytes to EQ_CHUNK_LAYER when K % cs == 0    */
+
 #define EQ_SCALES_SEARCH 0u         /* exhaustive per-row Eq. 4 minimisation (R5)          */
 #define EQ_SCALES_ABSMAX 1u         /* AbsMax scales, Eq. 1 (the λ = 0 lossless-FP8 rate)  */
 #define EQ_SCALES_GIVEN  2u         /* caller supplies eq_block.scales                     */
@@ -93,6 +100,7 @@ typedef struct {
     uint32_t exclude_mask;          /* bit l: layer l keeps AbsMax scales (λ = 0) — the    */
                                     /* super-weight exclusion of P:393-396          */
     uint32_t codec;                 /* EQ_CODEC_BYTE (0, default) | _WORD | _PAIR          */
+    uint32_t chunk_mode;            /* EQ_CHUNK_LAYER (0, default) | EQ_CHUNK_ROW          */
 } eq_params;
 
 /* One compressed transformer block: all its layers in one bitstream with one table
@@ -113,7 +121,7 @@ typedef struct {
     int64_t   layer_rows[EQ_MAX_LAYERS];
     int64_t   layer_cols[EQ_MAX_LAYERS];
     uint32_t  codec;                /* EQ_CODEC_* of the streams (set by eq_quantize_encode) */
-    uint32_t  reserved;             /* 0                                                   */
+    uint32_t  chunk_mode;           /* EQ_CHUNK_* of the streams (set by eq_quantize_encode) */
 } eq_block;
 
 /* ---------------------------------------------------------------- library info */

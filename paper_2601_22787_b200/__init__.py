@@ -26,6 +26,7 @@ EQ_ERR_CORRUPT, EQ_ERR_TRUNCATED, EQ_ERR_UNKNOWN_SYMBOL, EQ_ERR_UNREACHABLE_TARG
 EQ_FMT_E4M3, EQ_FMT_INT8 = 0, 1
 EQ_CODEC_BYTE, EQ_CODEC_WORD, EQ_CODEC_PAIR = 0, 1, 2
 EQ_OUT_FP8, EQ_OUT_BF16 = 0, 1
+EQ_CHUNK_LAYER, EQ_CHUNK_ROW = 0, 1
 EQ_SCALES_SEARCH, EQ_SCALES_ABSMAX, EQ_SCALES_GIVEN = 0, 1, 2
 EQ_MAX_LAYERS = 8
 EQ_DEFAULT_CHUNK = 4096
@@ -63,7 +64,7 @@ class eq_params(ctypes.Structure):
     _fields_ = [("format", ctypes.c_uint32), ("chunk_symbols", ctypes.c_uint32),
                 ("prob_bits", ctypes.c_uint32), ("scale_mode", ctypes.c_uint32),
                 ("lambda_", ctypes.c_double), ("oct_lo", ctypes.c_int32), ("oct_hi", ctypes.c_int32),
-                ("exclude_mask", ctypes.c_uint32), ("codec", ctypes.c_uint32)]
+                ("exclude_mask", ctypes.c_uint32), ("codec", ctypes.c_uint32), ("chunk_mode", ctypes.c_uint32)]
 
 
 class eq_lbfgs_params(ctypes.Structure):
@@ -79,7 +80,7 @@ class eq_block(ctypes.Structure):
                 ("freq", ctypes.c_void_p), ("scales", ctypes.c_void_p), ("n_layers", ctypes.c_uint32),
                 ("format", ctypes.c_uint32),
                 ("layer_rows", ctypes.c_int64 * EQ_MAX_LAYERS), ("layer_cols", ctypes.c_int64 * EQ_MAX_LAYERS),
-                ("codec", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("codec", ctypes.c_uint32), ("chunk_mode", ctypes.c_uint32)]
 
 
 _lib = None
@@ -167,11 +168,11 @@ def _tensor(W: torch.Tensor) -> eq_tensor:
 
 
 def _params(chunk_symbols=EQ_DEFAULT_CHUNK, scale_mode=EQ_SCALES_SEARCH, lam=0.0, oct_lo=-1, oct_hi=20,
-            fmt=EQ_FMT_E4M3, exclude=(), codec=EQ_CODEC_BYTE) -> eq_params:
+            fmt=EQ_FMT_E4M3, exclude=(), codec=EQ_CODEC_BYTE, chunk_mode=EQ_CHUNK_LAYER) -> eq_params:
     mask = 0
     for i in exclude:
         mask |= 1 << int(i)
-    return eq_params(fmt, chunk_symbols, EQ_PROB_BITS, scale_mode, float(lam), oct_lo, oct_hi, mask, codec)
+    return eq_params(fmt, chunk_symbols, EQ_PROB_BITS, scale_mode, float(lam), oct_lo, oct_hi, mask, codec, chunk_mode)
 
 
 # ---------------------------------------------------------------- compressed block
@@ -188,6 +189,7 @@ class Block:
     meta: dict = field(default_factory=dict)
     format: int = EQ_FMT_E4M3
     codec: int = EQ_CODEC_BYTE
+    chunk_mode: int = EQ_CHUNK_LAYER
 
     @property
     def n_chunks(self) -> int:
@@ -210,6 +212,7 @@ class Block:
         b.n_layers = len(self.shapes)
         b.format = self.format
         b.codec = self.codec
+        b.chunk_mode = self.chunk_mode
         for i, (r, c) in enumerate(self.shapes):
             b.layer_rows[i] = r
             b.layer_cols[i] = c
@@ -229,11 +232,11 @@ class Block:
         return self.compressed_bytes()
 
 
-def encode_bounds(layers, chunk_symbols=EQ_DEFAULT_CHUNK):
+def encode_bounds(layers, chunk_symbols=EQ_DEFAULT_CHUNK, codec: int = EQ_CODEC_BYTE, chunk_mode: int = EQ_CHUNK_LAYER):
     ts = (eq_tensor * len(layers))(*[eq_tensor(0 if not W.is_cuda else W.data_ptr(), W.shape[0], W.shape[1]) for W in layers])
     for i, W in enumerate(layers):
         ts[i].w = 1 if ts[i].w == 0 else ts[i].w       # sizing does not dereference
-    p = _params(chunk_symbols)
+    p = _params(chunk_symbols, codec=codec, chunk_mode=chunk_mode)
     cap, nc, sb = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint64()
     _ck(lib().eq_encode_bounds(ts, len(layers), ctypes.byref(p), ctypes.byref(cap), ctypes.byref(nc), ctypes.byref(sb)),
         "eq_encode_bounds")
@@ -243,15 +246,17 @@ def encode_bounds(layers, chunk_symbols=EQ_DEFAULT_CHUNK):
 def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH, scales: torch.Tensor | None = None,
                     chunk_symbols: int = EQ_DEFAULT_CHUNK, oct_lo: int = -1, oct_hi: int = 20,
                     stream=None, scratch: torch.Tensor | None = None, shrink: bool = True,
-                    format: int = EQ_FMT_E4M3, exclude=(), codec: int = EQ_CODEC_BYTE) -> Block:
+                    format: int = EQ_FMT_E4M3, exclude=(), codec: int = EQ_CODEC_BYTE,
+                    chunk_mode: int = EQ_CHUNK_LAYER) -> Block:
     """Alg. 1 for one block of bf16 CUDA matrices.  Synchronous (reads payload size).
     ``exclude``: layer indices kept at AbsMax scales (λ = 0); ``codec``: rANS
-    renormalisation (EQ_CODEC_BYTE, R9 / EQ_CODEC_WORD, R14)."""
+    renormalisation (EQ_CODEC_BYTE, R9 / EQ_CODEC_WORD, R14 / EQ_CODEC_PAIR, R15);
+    ``chunk_mode``: EQ_CHUNK_LAYER or EQ_CHUNK_ROW (chunks also restart at row starts)."""
     if scales is not None:
         scale_mode = EQ_SCALES_GIVEN
     dev = layers[0].device
     ts = (eq_tensor * len(layers))(*[_tensor(W) for W in layers])
-    p = _params(chunk_symbols, scale_mode, lam, oct_lo, oct_hi, format, exclude, codec)
+    p = _params(chunk_symbols, scale_mode, lam, oct_lo, oct_hi, format, exclude, codec, chunk_mode)
     cap, nc, sb = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint64()
     _ck(lib().eq_encode_bounds(ts, len(layers), ctypes.byref(p), ctypes.byref(cap), ctypes.byref(nc), ctypes.byref(sb)),
         "eq_encode_bounds")
@@ -276,7 +281,7 @@ def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH
         keep = (nbytes + EQ_PAYLOAD_SLACK + 255) // 256 * 256
         payload = payload[:keep].clone()
     return Block(payload, nbytes, off, freq, scales, [tuple(W.shape) for W in layers], chunk_symbols,
-                 {"lambda": lam, "scale_mode": scale_mode, "exclude": tuple(exclude)}, format, codec)
+                 {"lambda": lam, "scale_mode": scale_mode, "exclude": tuple(exclude)}, format, codec, chunk_mode)
 
 
 def arena_layout(blocks, out_dtype=EQ_OUT_BF16):
@@ -445,16 +450,20 @@ def build_pair_table(hist: torch.Tensor, stream=None):
 
 
 def rans_encode(codes: torch.Tensor, shapes, freq: torch.Tensor, scales: torch.Tensor | None = None,
-                chunk_symbols: int = EQ_DEFAULT_CHUNK, stream=None, codec: int = EQ_CODEC_BYTE) -> Block:
+                chunk_symbols: int = EQ_DEFAULT_CHUNK, stream=None, codec: int = EQ_CODEC_BYTE,
+                chunk_mode: int = EQ_CHUNK_LAYER) -> Block:
     """a6 alone: encode a concatenated symbol stream (uint8 CUDA) with a given table."""
     _require_cuda(codes, freq)
     n = sum(r * c for r, c in shapes)
-    nc = sum((r * c + chunk_symbols - 1) // chunk_symbols for r, c in shapes)
+    if chunk_mode == EQ_CHUNK_ROW:
+        nc = sum(r * ((c + chunk_symbols - 1) // chunk_symbols) for r, c in shapes)
+    else:
+        nc = sum((r * c + chunk_symbols - 1) // chunk_symbols for r, c in shapes)
     cap = (4 * nc + (3 if codec == EQ_CODEC_PAIR else 2) * n + EQ_PAYLOAD_SLACK + 255) // 256 * 256
     dev = codes.device
     blk = Block(torch.empty(cap, dtype=torch.uint8, device=dev), 0, torch.empty(nc + 1, dtype=torch.int32, device=dev),
                 freq, scales if scales is not None else torch.ones(sum(r for r, _ in shapes), dtype=torch.bfloat16, device=dev),
-                list(shapes), chunk_symbols, codec=codec)
+                list(shapes), chunk_symbols, codec=codec, chunk_mode=chunk_mode)
     sizes = torch.empty(max(nc, 1), dtype=torch.int32, device=dev)
     tot = torch.zeros(1, dtype=torch.int64, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)

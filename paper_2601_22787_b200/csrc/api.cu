@@ -33,6 +33,7 @@ eq_status check_params(const eq_params* p) {
     if (p->chunk_symbols == 0 || p->chunk_symbols > 262144u) return EQ_ERR_ARG;
     if (p->scale_mode > EQ_SCALES_GIVEN) return EQ_ERR_ARG;
     if (p->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
+    if (p->chunk_mode > EQ_CHUNK_ROW) return EQ_ERR_ARG;
     if (p->scale_mode == EQ_SCALES_SEARCH && !(p->lambda >= 0.0)) return EQ_ERR_ARG;
     return EQ_OK;
 }
@@ -72,11 +73,10 @@ EncodeScratch carve(const eq_tensor* layers, uint32_t n_layers, uint32_t n_chunk
     return s;
 }
 
-uint32_t count_chunks(const eq_tensor* layers, uint32_t n_layers, uint32_t cs) {
+uint64_t count_chunks(const eq_tensor* layers, uint32_t n_layers, uint32_t cs, uint32_t mode) {
     uint64_t n = 0;
-    for (uint32_t l = 0; l < n_layers; ++l)
-        n += ((uint64_t)layers[l].rows * (uint64_t)layers[l].cols + cs - 1) / cs;
-    return (uint32_t)n;
+    for (uint32_t l = 0; l < n_layers; ++l) n += layer_chunks(mode, layers[l].rows, layers[l].cols, cs);
+    return n;
 }
 
 eq_status err_to_status(uint32_t e) {
@@ -114,7 +114,7 @@ extern "C" eq_status eq_encode_bounds(const eq_tensor* layers, uint32_t n_layers
     EQ_TRY(check_params(p));
     uint64_t syms = 0;
     for (uint32_t l = 0; l < n_layers; ++l) syms += (uint64_t)layers[l].rows * (uint64_t)layers[l].cols;
-    const uint64_t nc = count_chunks(layers, n_layers, p->chunk_symbols);
+    const uint64_t nc = count_chunks(layers, n_layers, p->chunk_symbols, p->chunk_mode);
     // worst case per chunk: 4-byte state + at most 2 renormalisation bytes per symbol
     // (two bytes, EQ_CODEC_BYTE, or one 16-bit word, EQ_CODEC_WORD)
     // (EQ_CODEC_PAIR: an escaped pair is three words for two symbols)
@@ -150,7 +150,7 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
     out->n_layers = n_layers;
     out->format = p->format;
     out->codec = p->codec;
-    out->reserved = 0;
+    out->chunk_mode = p->chunk_mode;
     out->n_chunks = nc;
     out->chunk_symbols = p->chunk_symbols;
     for (uint32_t l = 0; l < EQ_MAX_LAYERS; ++l) {
@@ -381,7 +381,7 @@ extern "C" eq_status eq_calibrate_lambda(const eq_tensor* layers, uint32_t n_lay
         const double sz = (double)layers[l].rows * (double)layers[l].cols;
         params += sz;
         rows_total += (double)layers[l].rows;
-        chunks += std::ceil(sz / p->chunk_symbols);
+        chunks += (double)layer_chunks(p->chunk_mode, layers[l].rows, layers[l].cols, p->chunk_symbols);
     }
     const double side = (8.0 * (4.0 * chunks + 4.0 * chunks + 2.0 * rows_total) + (p->codec == EQ_CODEC_PAIR ? 8192.0 : 4096.0) * std::ceil(n_layers / 7.0)) / params;
 

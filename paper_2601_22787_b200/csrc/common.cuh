@@ -29,6 +29,29 @@ constexpr float kQmax = 448.0f;              // E4M3 Q_max
         if (_s != EQ_OK) return _s;                         \
     } while (0)
 
+// Chunk geometry of one layer: chunking restarts every `seg` symbols — the
+// whole layer (EQ_CHUNK_LAYER) or one row (EQ_CHUNK_ROW) — so a segment holds cps =
+// ceil(seg / cs) chunks, all of cs symbols but the last.
+struct ChunkGeom {
+    uint64_t seg;          // segment length in symbols
+    uint32_t cps;          // chunks per segment
+};
+__host__ __device__ __forceinline__ ChunkGeom chunk_geom(uint32_t mode, uint64_t rows, uint64_t cols, uint32_t cs) {
+    const uint64_t seg = mode == EQ_CHUNK_ROW ? cols : rows * cols;
+    return ChunkGeom{seg, (uint32_t)((seg + cs - 1) / cs)};
+}
+__host__ __device__ __forceinline__ uint64_t layer_chunks(uint32_t mode, uint64_t rows, uint64_t cols, uint32_t cs) {
+    const ChunkGeom g = chunk_geom(mode, rows, cols, cs);
+    return (rows * cols / g.seg) * g.cps;
+}
+// first symbol (within the layer) and length of the layer's local chunk k
+__host__ __device__ __forceinline__ uint64_t chunk_start(const ChunkGeom& g, uint32_t cs, uint32_t k, uint32_t& n) {
+    const uint32_t s = k / g.cps, j = k - s * g.cps;
+    const uint64_t a = (uint64_t)j * cs;
+    n = (uint32_t)(g.seg - a < cs ? g.seg - a : cs);
+    return (uint64_t)s * g.seg + a;
+}
+
 __device__ __forceinline__ float bf16_bits_to_float(uint32_t b) {
     return __uint_as_float(b << 16);
 }

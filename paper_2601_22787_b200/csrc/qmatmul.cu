@@ -142,9 +142,9 @@ __device__ __forceinline__ void decode_step(ChainW& c, const DecTable& T, const 
     c.i += kQK;
 }
 
-__device__ __forceinline__ bool chunk_begin(ChainW& c, const QmmParams& P, uint32_t chunk, uint32_t ring) {
+__device__ __forceinline__ bool chunk_begin(ChainW& c, const QmmParams& P, uint32_t chunk, uint32_t ring, uint32_t len) {
     c.i = 0;
-    c.n = P.cs;
+    c.n = len;
     c.runaway = false;
     const uint32_t a = __ldg(P.off + chunk), e = __ldg(P.off + chunk + 1);
     if (e < a || (uint64_t)e > P.payload_bytes || e - a < 4) {
@@ -179,9 +179,9 @@ __device__ __forceinline__ bool runaway_q(const ChainW& c) { return c.r.Q > c.e 
 __device__ __forceinline__ bool runaway_q(const Chain& c) { return c.br.wi4 > c.wlimit4; }
 
 // start decoding chunk `chunk` (payload bytes, ring staging, first state) for this lane
-__device__ __forceinline__ bool chunk_begin(Chain& c, const QmmParams& P, uint32_t chunk, uint32_t ring) {
+__device__ __forceinline__ bool chunk_begin(Chain& c, const QmmParams& P, uint32_t chunk, uint32_t ring, uint32_t len) {
     c.i = 0;
-    c.n = P.cs;
+    c.n = len;
     c.runaway = false;
     const uint32_t a = __ldg(P.off + chunk), e = __ldg(P.off + chunk + 1);
     if (e < a || (uint64_t)e > P.payload_bytes || e - a < 4) {
@@ -310,6 +310,9 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
     __syncthreads();                                 // cum (in the A tiles) read by everyone
 
     // ---- this lane's row and chunk
+    const uint32_t kbase = jcol * P.cs;
+    const uint32_t clen = min(P.cs, J.K - kbase);    // the last chunk of a row may be shorter (EQ_CHUNK_ROW)
+    const uint32_t steps = clen / kQK;
     const uint32_t grow = (kTiles * pair + h) * kTileRows + r;
     const uint32_t ring = smem_u32(rings + t * kRingWords);
     typename std::conditional<WORD, ChainW, Chain>::type c;
@@ -322,10 +325,8 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
     if (my_on) {
         c.s = bf16_bits_to_float(J.scales[grow]);
         c.s16 = c.i8 ? 0 : scale_f16(c.s);
-        if (table_ok) chunk_begin(c, P, J.chunk0 + grow * J.cpr + jcol, ring);
+        if (table_ok) chunk_begin(c, P, J.chunk0 + grow * J.cpr + jcol, ring, clen);
     }
-    const uint32_t steps = P.cs / kQK;
-    const uint32_t kbase = jcol * P.cs;
     uint8_t* a_tile = a_tiles + h * kATile;
     uint8_t* arow = a_tile + (r >> 3) * kAtom + (r & 7) * kRowB;
     const uint32_t bar = smem_u32(&bars[0]);
@@ -440,20 +441,24 @@ static eq_status qmm_validate(const eq_block* blk, uint32_t n_jobs, const uint32
     if ((reinterpret_cast<uintptr_t>(blk->payload) & 15) != 0) return EQ_ERR_ARG;
     if (blk->payload_cap < blk->payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;
     const uint32_t cs = blk->chunk_symbols;
+    if (blk->chunk_mode > EQ_CHUNK_ROW) return EQ_ERR_ARG;
     if (batch < 1 || batch > 256 || cs == 0 || cs % kQK != 0) return EQ_ERR_SHAPE;
     uint32_t chunk0 = 0;
     uint64_t srow = 0;
     for (uint32_t l = 0; l < blk->n_layers; ++l) {
         plan->chunk0[l] = chunk0;
         plan->srow[l] = srow;
-        chunk0 += (uint32_t)(((uint64_t)blk->layer_rows[l] * blk->layer_cols[l] + cs - 1) / cs);
+        chunk0 += (uint32_t)layer_chunks(blk->chunk_mode, blk->layer_rows[l], blk->layer_cols[l], cs);
         srow += (uint64_t)blk->layer_rows[l];
     }
     for (uint32_t q = 0; q < n_jobs; ++q) {
         const uint32_t l = layers[q];
         if (l >= blk->n_layers) return EQ_ERR_ARG;
         const uint64_t rows = blk->layer_rows[l], K = blk->layer_cols[l];
-        if (rows == 0 || rows % kTileRows != 0 || K == 0 || K % cs != 0) return EQ_ERR_SHAPE;
+        // a row's chunks must be independent K slices: row chunking (any K, multiple of the K
+        // step), or layer chunking with rows made of whole chunks
+        const bool row_aligned = blk->chunk_mode == EQ_CHUNK_ROW ? K % kQK == 0 : K % cs == 0;
+        if (rows == 0 || rows % kTileRows != 0 || K == 0 || !row_aligned) return EQ_ERR_SHAPE;
     }
     return EQ_OK;
 }
@@ -473,7 +478,7 @@ extern "C" uint64_t eq_qmatmul_workspace_bytes(const eq_block* blk, uint32_t n_j
     uint64_t total = 0;
     for (uint32_t q = 0; q < n_jobs; ++q) {
         const uint32_t l = layers[q];
-        total += qmm_part_bytes(blk->layer_cols[l] / blk->chunk_symbols, batch, blk->layer_rows[l]);
+        total += qmm_part_bytes((blk->layer_cols[l] + blk->chunk_symbols - 1) / blk->chunk_symbols, batch, blk->layer_rows[l]);
     }
     return total;
 }
@@ -507,7 +512,7 @@ extern "C" eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, cons
         J.chunk0 = plan.chunk0[l];
         J.rows = blk->layer_rows[l];
         J.K = blk->layer_cols[l];
-        J.cpr = J.K / cs;
+        J.cpr = (J.K + cs - 1) / cs;
         J.tile_begin = tiles;
         tiles += (J.rows / kTileRows + kTiles - 1) / kTiles * J.cpr;
         if (J.cpr == 1) {

@@ -31,7 +31,7 @@ constexpr int kMaxDecBlocks = 48;
 
 struct DecLayer {
     uint64_t out_off;      // byte offset of the layer in the arena
-    uint64_t size;         // rows * cols symbols
+    ChunkGeom geom;        // chunking segment (layer or row, EQ_CHUNK_*) and chunks per segment
     uint32_t chunk0;       // first chunk index of the layer within its block
     uint32_t cols;
     uint32_t scale_off;    // first row's index into the block's scale array
@@ -162,8 +162,7 @@ __device__ __forceinline__ void chain_setup(Chain& c, const DecBlock& B, uint32_
     uint32_t l = 0;
     while (l + 1 < B.n_layers && chunk >= B.layer[l + 1].chunk0) ++l;
     const DecLayer& Ly = B.layer[l];
-    const uint64_t sym0 = (uint64_t)(chunk - Ly.chunk0) * B.cs;
-    c.n = (uint32_t)min((uint64_t)B.cs, Ly.size - sym0);
+    const uint64_t sym0 = chunk_start(Ly.geom, B.cs, chunk - Ly.chunk0, c.n);
     const uint32_t a = __ldg(B.off + chunk), e = __ldg(B.off + chunk + 1);
     if (e < a || (uint64_t)e > B.payload_bytes || e - a < 4) {
         atomicOr(err, EQ_EF_TRUNCATED);
@@ -405,8 +404,7 @@ __device__ __forceinline__ void chain_setup_w(ChainW& c, const DecBlock& B, uint
     uint32_t l = 0;
     while (l + 1 < B.n_layers && chunk >= B.layer[l + 1].chunk0) ++l;
     const DecLayer& Ly = B.layer[l];
-    const uint64_t sym0 = (uint64_t)(chunk - Ly.chunk0) * B.cs;
-    c.n = (uint32_t)min((uint64_t)B.cs, Ly.size - sym0);
+    const uint64_t sym0 = chunk_start(Ly.geom, B.cs, chunk - Ly.chunk0, c.n);
     const uint32_t a = __ldg(B.off + chunk), e = __ldg(B.off + chunk + 1);
     if (e < a || (uint64_t)e > B.payload_bytes || e - a < 4) {
         atomicOr(err, EQ_EF_TRUNCATED);
@@ -698,11 +696,13 @@ __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, cons
 #define EQ_PAIR_WALK 1   // LUT fills: one binary search per 16 slots + a forward walk (else one per slot)
 #endif
 // lut[slot] = entry(slot, s) for the s with cm[s] <= slot < cm[s + 1] (cm[0..NS], cm[NS] = kM),
-// 256 threads: thread t fills slots [16t, 16t + 16), one binary search then a forward walk
-// over the symbol boundaries (zero-width symbols are stepped over), 4 × 16-byte stores
-template <int NS, class F>
-__device__ __forceinline__ void lut_walk256(uint32_t* lut, const uint32_t* cm, F entry) {
-    const uint32_t s0 = 16u * (uint32_t)threadIdx.x;
+// NT threads: thread t fills slots [S·t, S·t + S), S = kM / NT, one binary search then a forward
+// walk over the symbol boundaries (zero-width symbols are stepped over), 16-byte stores
+template <int NS, int NT, class F>
+__device__ __forceinline__ void lut_walk(uint32_t* lut, const uint32_t* cm, F entry) {
+    constexpr uint32_t S = kM / NT;
+    static_assert(S >= 4 && S * NT == kM, "slots per thread");
+    const uint32_t s0 = S * (uint32_t)threadIdx.x;
     int lo = 0, hi = NS - 1;                       // largest s with cm[s] <= s0
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -710,7 +710,7 @@ __device__ __forceinline__ void lut_walk256(uint32_t* lut, const uint32_t* cm, F
     }
     uint4* dst = reinterpret_cast<uint4*>(lut + s0);
     #pragma unroll 1
-    for (int k = 0; k < 16; k += 4) {
+    for (uint32_t k = 0; k < S; k += 4) {
         uint32_t v[4];
         #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -774,8 +774,8 @@ __device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut,
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
         return false;
     }
-    if constexpr (NT == 256 && EQ_PAIR_WALK) {
-        lut_walk256<226>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
+    if constexpr (EQ_PAIR_WALK) {
+        lut_walk<226, NT>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
             const uint32_t f = pcum[q + 1] - pcum[q];
             const uint32_t nib = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : 0xFFu;
             return nib | ((slot - pcum[q]) << 8) | ((f - 1) << 20);
@@ -839,13 +839,18 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
     }
 }
 
+#ifndef EQ_PTHREADS
+#define EQ_PTHREADS 256             // chunks (= threads) per CTA of k_decode_p
+#endif
 #ifndef EQ_DECP_MIN_CTAS
 #define EQ_DECP_MIN_CTAS 5          // shared memory (40 KB: pair LUT, byte single LUT, rings) allows 5 CTAs/SM: 48 registers
 #endif
+constexpr int kPThreads = EQ_PTHREADS;
+constexpr uint32_t kDecPSmem = kPThreads * kWRing;          // dynamic: the staging rings
 template <bool BF16>
-__global__ void __launch_bounds__(kWThreads, EQ_DECP_MIN_CTAS)
+__global__ void __launch_bounds__(kPThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
-    extern __shared__ __align__(128) uint8_t rings[];      // kWThreads × kWRing
+    extern __shared__ __align__(128) uint8_t rings[];      // kPThreads × kWRing
     __shared__ __align__(16) uint32_t lut[kM + 128];       // pair LUT, then the 256 × u16 codes table
     __shared__ uint32_t cum[257];
     __shared__ uint32_t pcum[227];
@@ -865,16 +870,16 @@ k_decode_p(const __grid_constant__ DecParams P) {
     const DecBlock& B = P.b[bi];
     const int t = threadIdx.x;
     ChainW c;
-    chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kWThreads + t,
+    chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kPThreads + t,
                         (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
     stage_commit();
-    if (!build_pair_lut<kWThreads>(B, lut, cum, pcum, P.err)) {
+    if (!build_pair_lut<kPThreads>(B, lut, cum, pcum, P.err)) {
         stage_wait_all();
         return;
     }
 #if EQ_PAIR_LUT1 == 3
     {                                              // bucket t (slots [16t, 16t + 16)): its first symbol
-        static_assert(kWThreads == 256, "bucket fill assumes 256 threads");
+        static_assert(kPThreads == 256, "bucket fill assumes 256 threads");
         const uint32_t s0 = 16u * (uint32_t)t;
         int lo = 0, hi = 255;
         while (lo < hi) {
@@ -884,22 +889,25 @@ k_decode_p(const __grid_constant__ DecParams P) {
         lut1[t] = (uint8_t)lo;
     }
 #elif EQ_PAIR_LUT1 == 2
-    {                                              // symbol per slot: thread t fills [16t, 16t + 16)
-        static_assert(kWThreads == 256, "byte single LUT fill assumes 256 threads");
-        const uint32_t s0 = 16u * (uint32_t)t;
+    {                                              // symbol per slot: thread t fills [S·t, S·t + S)
+        constexpr uint32_t S = kM / kPThreads;
+        static_assert(S % 4 == 0 && S * kPThreads == kM, "byte single LUT fill");
+        const uint32_t s0 = S * (uint32_t)t;
         int lo = 0, hi = 255;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
         }
-        uint32_t w[4];
         #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            while (cum[lo + 1] <= s0 + k) ++lo;
-            if ((k & 3) == 0) w[k >> 2] = 0;
-            w[k >> 2] |= (uint32_t)lo << (8 * (k & 3));
+        for (uint32_t k4 = 0; k4 < S; k4 += 4) {
+            uint32_t w = 0;
+            #pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                while (cum[lo + 1] <= s0 + k4 + k) ++lo;
+                w |= (uint32_t)lo << (8 * k);
+            }
+            *reinterpret_cast<uint32_t*>(lut1 + s0 + k4) = w;
         }
-        *reinterpret_cast<uint4*>(lut1 + s0) = make_uint4(w[0], w[1], w[2], w[3]);
     }
 #elif EQ_PAIR_LUT1
     {                                              // single LUT in decode_one_w's entry layout
@@ -907,10 +915,10 @@ k_decode_p(const __grid_constant__ DecParams P) {
             const uint32_t fs = cum[sym + 1] - cum[sym];
             return (uint32_t)sym | ((slot - cum[sym]) << 8) | ((fs - 1) << 20);
         };
-        if constexpr (kWThreads == 256 && EQ_PAIR_WALK) {
-            lut_walk256<256>(lut1, cum, entry);
+        if constexpr (EQ_PAIR_WALK) {
+            lut_walk<256, kPThreads>(lut1, cum, entry);
         } else {
-            for (int slot = t; slot < (int)kM; slot += kWThreads) {
+            for (int slot = t; slot < (int)kM; slot += kPThreads) {
                 int lo = 0, hi = 255;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
@@ -924,7 +932,7 @@ k_decode_p(const __grid_constant__ DecParams P) {
 #if EQ_PAIR_CODETAB
     {                                              // pair id of (ra, rb) -> code(ra) | code(rb) << 8
         const uint8_t* rcb = reinterpret_cast<const uint8_t*>(B.freq + kRankIdx);
-        for (int q = t; q < 225; q += kWThreads)
+        for (int q = t; q < 225; q += kPThreads)
             ctab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = (uint16_t)(rcb[q / 15] | (rcb[q % 15] << 8));
     }
 #endif
@@ -996,7 +1004,7 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     d.scales = blk.scales;
     d.payload_bytes = blk.payload_bytes;
     if (blk.format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if (blk.codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
+    if (blk.codec > EQ_CODEC_PAIR || blk.chunk_mode > EQ_CHUNK_ROW) return EQ_ERR_ARG;
     d.format = blk.format;
     d.codec = blk.codec;
     d.cs = blk.chunk_symbols;
@@ -1006,16 +1014,15 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     for (uint32_t l = 0; l < EQ_MAX_LAYERS; ++l) {
         DecLayer& L = d.layer[l];
         if (l < blk.n_layers) {
-            uint64_t size = (uint64_t)blk.layer_rows[l] * (uint64_t)blk.layer_cols[l];
             L.out_off = offs[l];
-            L.size = size;
+            L.geom = chunk_geom(blk.chunk_mode, blk.layer_rows[l], blk.layer_cols[l], blk.chunk_symbols);
             L.chunk0 = chunk;
             L.cols = (uint32_t)blk.layer_cols[l];
             L.scale_off = srow;
-            chunk += (uint32_t)((size + blk.chunk_symbols - 1) / blk.chunk_symbols);
+            chunk += (uint32_t)layer_chunks(blk.chunk_mode, blk.layer_rows[l], blk.layer_cols[l], blk.chunk_symbols);
             srow += (uint32_t)blk.layer_rows[l];
         } else {
-            L = DecLayer{0, 0, chunk, 1, srow, 0};
+            L = DecLayer{0, ChunkGeom{1, 1}, chunk, 1, srow, 0};
         }
     }
     if (chunk != blk.n_chunks) return EQ_ERR_SHAPE;
@@ -1031,7 +1038,7 @@ extern "C" eq_status eq_decode_lanes(uint32_t codec, uint32_t out_dtype, int dev
     size_t dyn;
     if (codec == EQ_CODEC_PAIR) {
         fn = bf ? (const void*)k_decode_p<true> : (const void*)k_decode_p<false>;
-        threads = kWThreads, per = kWChunksPerCta, dyn = kDecWSmem;
+        threads = kPThreads, per = kPThreads, dyn = kDecPSmem;
     } else if (codec == EQ_CODEC_WORD) {
         fn = bf ? (const void*)k_decode_w<true> : (const void*)k_decode_w<false>;
         threads = kWThreads, per = kWChunksPerCta, dyn = kDecWSmem;
@@ -1076,19 +1083,20 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
         uint32_t ctas = 0;
         for (uint32_t k = 0; k < nb; ++k) {
             EQ_TRY(fill_desc(blocks[b0 + k], all.get() + (size_t)(b0 + k) * EQ_MAX_LAYERS, P.b[k], ctas));
-            const uint32_t per = codec != EQ_CODEC_BYTE ? (uint32_t)kWChunksPerCta : (uint32_t)kChunksPerCta;
+            const uint32_t per = codec == EQ_CODEC_PAIR ? (uint32_t)kPThreads
+                               : codec == EQ_CODEC_WORD ? (uint32_t)kWChunksPerCta : (uint32_t)kChunksPerCta;
             ctas += (P.b[k].n_chunks + per - 1) / per;
         }
         // blocks with zero chunks cannot exist (layers are non-empty); ctas > 0
         if (codec == EQ_CODEC_PAIR) {
             const int bi = out_dtype == EQ_OUT_BF16 ? 1 : 0;
-            const uint32_t dyn = kDecWSmem;
+            const uint32_t dyn = kDecPSmem;
             EQ_CUDA_TRY(cudaFuncSetAttribute(bi ? (const void*)k_decode_p<true> : (const void*)k_decode_p<false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
             if (bi)
-                k_decode_p<true><<<ctas, kWThreads, dyn, st>>>(P);
+                k_decode_p<true><<<ctas, kPThreads, dyn, st>>>(P);
             else
-                k_decode_p<false><<<ctas, kWThreads, dyn, st>>>(P);
+                k_decode_p<false><<<ctas, kPThreads, dyn, st>>>(P);
         } else if (codec == EQ_CODEC_WORD) {
             const int bi = out_dtype == EQ_OUT_BF16 ? 1 : 0;
             // (6 CTAs/SM: for the 8B layer set 7.5 waves; forcing 5 CTAs/SM for exactly 9 waves

@@ -4,7 +4,8 @@
 // in reverse from x = L, units of b emitted while x ≥ ((L>>12)·b)·f; the final state is
 // stored first (little-endian), followed by the units in decode order.
 //   EQ_CODEC_BYTE (R9):  L = 2^23, b = 2^8;   EQ_CODEC_WORD (R14): L = 2^16, b = 2^16 (LE).
-// Chunks of cs symbols restart at each layer start (R10).
+// Chunks of cs symbols restart at each layer start (R10), and at each row start under
+// EQ_CHUNK_ROW.
 //
 // Two passes, one thread per chunk: (1) exact byte count per chunk, (2) exclusive scan
 // into chunk offsets, (3) encode again writing back-to-front straight into the final
@@ -31,15 +32,13 @@ struct EncParams {
     uint32_t n_layers;
     uint32_t chunk0[EQ_MAX_LAYERS + 1];
     uint64_t sym_base[EQ_MAX_LAYERS];
-    uint64_t size[EQ_MAX_LAYERS];
+    ChunkGeom geom[EQ_MAX_LAYERS];
 };
 
 __device__ __forceinline__ void chunk_range(const EncParams& P, uint32_t c, uint64_t& base, uint32_t& n) {
     uint32_t l = 0;
     while (l + 1 < P.n_layers && c >= P.chunk0[l + 1]) ++l;
-    const uint64_t a = (uint64_t)(c - P.chunk0[l]) * P.cs;
-    base = P.sym_base[l] + a;
-    n = (uint32_t)min((uint64_t)P.cs, P.size[l] - a);
+    base = P.sym_base[l] + chunk_start(P.geom[l], P.cs, c - P.chunk0[l], n);
 }
 
 __device__ __forceinline__ void load_table(const EncParams& P, uint32_t* sf, uint32_t* scum) {
@@ -269,7 +268,7 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     if (!blk->payload || !blk->chunk_off || !blk->freq) return EQ_ERR_ARG;
     if (blk->n_layers == 0 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (blk->chunk_symbols == 0 || blk->chunk_symbols > 262144u) return EQ_ERR_ARG;
-    if (blk->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
+    if (blk->codec > EQ_CODEC_PAIR || blk->chunk_mode > EQ_CHUNK_ROW) return EQ_ERR_ARG;
     EncParams P;
     memset(&P, 0, sizeof(P));
     P.codes = codes;
@@ -289,8 +288,8 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
         const uint64_t sz = (uint64_t)blk->layer_rows[l] * (uint64_t)blk->layer_cols[l];
         P.chunk0[l] = chunk;
         P.sym_base[l] = base;
-        P.size[l] = sz;
-        chunk += (uint32_t)((sz + P.cs - 1) / P.cs);
+        P.geom[l] = chunk_geom(blk->chunk_mode, blk->layer_rows[l], blk->layer_cols[l], P.cs);
+        chunk += (uint32_t)layer_chunks(blk->chunk_mode, blk->layer_rows[l], blk->layer_cols[l], P.cs);
         base += sz;
     }
     P.chunk0[blk->n_layers] = chunk;

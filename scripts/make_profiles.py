@@ -34,6 +34,9 @@ def main(ev, rnd):
     summ = json.load(open(sp)) if os.path.exists(sp) else {}
     if "bf16" in summ:                       # old flat layout (byte codec only)
         summ = {"byte": {k: summ.pop(k) for k in ("bf16", "fp8", "source") if k in summ}}
+    sha_f = os.path.join(ev, "kernel_sha.txt")
+    sha = open(sha_f).read().strip() if os.path.exists(sha_f) else None
+    when = open(os.path.join(ev, "when.txt")).read().strip() if os.path.exists(os.path.join(ev, "when.txt")) else None
     for d in full:
         k = d["kernel"]
         codec = "word" if "k_decode_w" in k else "pair" if "k_decode_p" in k else "byte" if "k_decode" in k else None
@@ -44,6 +47,10 @@ def main(ev, rnd):
         summ.setdefault(codec, {})["source"] = (
             f"profiles/{rnd}/ncu_decode_full.json (ncu --set full --clock-control none, bench.py --profile "
             f"--steps 1 --warmup 1 --codec {codec}: 32 blocks, lambda 230.2)")
+        summ[codec]["kernel_sha"] = sha
+        summ[codec]["when"] = when
+        summ[codec]["blocks"] = 32
+        summ[codec]["chunk_symbols"] = 4096
         summ[codec][kind] = {"kernel": k, "duration_ms_under_ncu": _num(d["gpu__time_duration.sum"]),
                              "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                              "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")}

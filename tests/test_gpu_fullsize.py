@@ -6,9 +6,16 @@ eq_decode_dequant launch into the bf16 arena.  The oracle
 recomputes sampled rows one by one from the INPUT weights (its own search, quantiser and
 dequantiser) and must equal the decoded rows bit for bit (rows whose GPU scale is a
 documented near-tie of the oracle's objective are checked for optimality instead).
-Properties checked at full size: lossless FP8 decode of every block, coded size ≤ 1.02×
-the histogram entropy, effective rate near the target.
+Every symbol: the oracle's own decoder (threaded, the bench's CPU-baseline helper) decodes
+every chunk of all 32 blocks and its bf16 output must equal the GPU arena of the bench's
+launch bit for bit (~7.0 G symbols per codec).  Encode at full size: for blocks 0, 15 and 31
+the oracle re-runs Alg. 1 l.3-5 from the INPUT weights with the GPU's scales (the search is
+checked separately on sampled rows) and must reproduce the GPU's table, offsets and payload
+byte for byte.  Properties checked at full size: coded size ≤ 1.02× the histogram entropy,
+Shannon's bound, effective rate near the target.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -45,12 +52,75 @@ def layer_set(request):
         if scratch is None:
             scratch = torch.empty(eq.encode_bounds(Ws)[2], dtype=torch.uint8, device=dev)
         blocks.append(eq.quantize_encode(Ws, lam=LAM, scratch=scratch, codec=request.param))
-        if lid in (0, 31):
+        if lid in (0, 15, 31):
             kept[lid] = [W.cpu() for W in Ws]          # the INPUT weights, for the oracle
         del Ws
     del scratch
     torch.cuda.empty_cache()
     return blocks, kept
+
+
+def _host_block(b):
+    """Host copies of a GPU block for the oracle: payload, offsets, table, scales."""
+    payload = b.payload.cpu().numpy()
+    off = b.chunk_off.cpu().numpy().astype(np.uint32)
+    table = b.freq.cpu().numpy().view(np.uint16)
+    pair = None
+    if b.codec == eq.EQ_CODEC_PAIR:
+        pair = o.PairTable(table.view(np.uint8)[968:984].copy(), int(table[482]), table[256:481].copy(),
+                           int(table[481]))
+    return payload, off, table, pair, u16(b.scales)
+
+
+def test_config3_every_symbol_matches_oracle_decode(layer_set):
+    """All 32 blocks, every chunk: the oracle's decoder on the host cores vs the GPU arena of
+    the bench's single launch, bf16 bit for bit (Alg. 2 l.1-2)."""
+    blocks, _ = layer_set
+    dec = eq.Decoder(blocks, eq.EQ_OUT_BF16)
+    dec()
+    dec.check()
+    views = dec.views()
+    threads = os.cpu_count() or 1
+    total = 0
+    for b, vb in zip(blocks, views):
+        payload, off, table, pair, scales = _host_block(b)
+        k0 = r0 = 0
+        for (r, c), v in zip(b.shapes, vb):
+            nk = (r * c + b.chunk_symbols - 1) // b.chunk_symbols
+            ref = o.decode_dequant_layer_mt(payload, off[k0:k0 + nk + 1], b.chunk_symbols, r, c, scales[r0:r0 + r],
+                                            table[:256], threads, b.codec, pair)
+            got = u16(v).reshape(r, c)
+            assert np.array_equal(ref, got), (b.codec, r, c, int(np.count_nonzero(ref != got)))
+            total += r * c
+            k0 += nk
+            r0 += r
+    assert total == 32 * 218103808
+
+
+def test_config3_full_block_encode_matches_oracle(layer_set):
+    """Blocks 0, 15, 31 at full size: the oracle quantises the INPUT weights with the GPU's
+    scales and entropy-codes them (its own table rules R8/R15 and coder): table, offsets and
+    payload equal the GPU's byte for byte (Alg. 1 l.3-5)."""
+    blocks, kept = layer_set
+    for lid, Ws in kept.items():
+        b = blocks[lid]
+        _, off, table, _, scales = _host_block(b)
+        S, r0 = [], 0
+        for (r, _) in b.shapes:
+            S.append(scales[r0:r0 + r])
+            r0 += r
+        ref = o.quantize_encode(Ws, scales=S, cs=b.chunk_symbols, codec=b.codec)
+        want = np.zeros_like(table)
+        want[:256] = ref.freq
+        if b.codec == eq.EQ_CODEC_PAIR:
+            want[256:481] = ref.pair.pf
+            want[481] = ref.pair.fesc
+            want[482] = ref.pair.K
+            want.view(np.uint8)[968:984] = ref.pair.rank_code
+        assert np.array_equal(table, want), lid
+        assert np.array_equal(off, np.asarray(ref.chunk_off, dtype=np.uint32)), lid
+        assert b.payload_bytes == len(ref.payload), lid
+        assert b.payload[:b.payload_bytes].cpu().numpy().tobytes() == ref.payload, lid
 
 
 def test_config3_decode_sampled_rows_match_oracle(layer_set):

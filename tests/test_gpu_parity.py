@@ -48,7 +48,7 @@ def oracle_block_to_gpu(blk: o.OracleBlock) -> eq.Block:
     freq = torch.from_numpy(table_u16(blk).view(np.int16).copy())
     scales = to_bf16(np.concatenate(blk.scales))
     return eq.Block(payload.to(DEV), len(blk.payload), off.to(DEV), freq.to(DEV), scales, list(blk.layer_shapes),
-                    blk.chunk_symbols, format=blk.fmt, codec=blk.codec)
+                    blk.chunk_symbols, format=blk.fmt, codec=blk.codec, chunk_mode=blk.chunk_mode)
 
 
 RAGGED = [(37, 53), (1, 1), (64, 64), (5, 4097), (16, 4096)]

@@ -20,7 +20,7 @@ def to_gpu_block(blk):
     sc = torch.from_numpy(np.concatenate(blk.scales).view(np.int16)).view(torch.bfloat16)
     return eq.Block(payload.to(DEV), len(blk.payload), torch.from_numpy(blk.chunk_off.astype(np.int64).astype(np.int32)).to(DEV),
                     torch.from_numpy(blk.freq.view(np.int16).copy()).to(DEV), sc.to(DEV), list(blk.layer_shapes),
-                    blk.chunk_symbols, format=blk.fmt, codec=blk.codec)
+                    blk.chunk_symbols, format=blk.fmt, codec=blk.codec, chunk_mode=blk.chunk_mode)
 
 
 @pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
