@@ -323,7 +323,7 @@ def run_reference(args, rank, world):
     if args.blocks <= 0:
         args.blocks = eqsynth.LLAMA[args.model]["layers"]
     ids, (r, g) = share_ids(args, rank, world)
-    cs = choose_chunk(args, ids, eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, 0))
+    cs = choose_chunk(args, ids, max(1, eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, 0)))
     n_params = len(ids) * sum(a * b for a, b in eqsynth.block_shapes(args.model))
     blocks, lam, est, enc_s = encode_share(args, eq, eqsynth, dev, [0], cs)
     blk = blocks[0]
@@ -383,7 +383,7 @@ def main():
     if args.blocks <= 0:
         args.blocks = eqsynth.LLAMA[args.model]["layers"]
     layer_ids, (sim_rank, sim_world) = share_ids(args, rank, world)
-    lanes = eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, local)
+    lanes = max(1, eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, local))
     cs = choose_chunk(args, layer_ids, lanes)
 
     # ---- encode side (once): λ calibration (global) then Alg. 1 per block

@@ -1,0 +1,241 @@
+// pair_core.cuh — device side of the EQ_CODEC_PAIR decoder (reading R15), shared by
+// the stand-alone decoder (rans_dec.cu, k_decode_p: §8(a) rows a7 + a8) and the decode-fused
+// GEMM (qmatmul.cu, §8(f) row 1).
+//
+// The pair codec is the word codec's rANS (R14: L = 2^16, 16-bit words, M = 2^12) over PAIRS
+// of consecutive symbols of a chunk for the block's 15 most frequent codes, with an escape
+// (the top slots of the pair table) followed by the two codes coded with the single table.
+// Per decoded pair: one pair-LUT lookup, one codes-table lookup, at most one word.
+//
+// Table buffer of a block (u16[512], include/entquant.h): [0,256) single frequencies,
+// [256,481) pair frequencies by ra·15 + rb, [481] escape frequency, [482] K, [484,492) the 16
+// rank codes as bytes.  Per CTA the decoder builds in shared memory (kPairSmemBytes):
+//   lut[4096]   pair LUT, entry id(ra, rb) | (slot − c) << 8 | (f − 1) << 20 (escape id 0xFF),
+//   lut[4096..] the 256 × u16 codes table id -> code(ra) | code(rb) << 8 (right after the LUT:
+//               its address is the LUT's uniform base + a constant — a separate array's address
+//               was rematerialised with four uniform instructions per pair step),
+//   lut1[4096]  the single table's symbol per slot (escapes), cum[257] its cumulative
+//               frequencies, pcum[227] the pair table's.
+#pragma once
+#include "decode_core.cuh"
+
+namespace eq {
+
+constexpr int kPairOff = 256, kFescIdx = 481, kKIdx = 482, kRankIdx = 484;
+constexpr int kPairLutWords = kM + 128;
+
+constexpr uint32_t kPairSmemBytes = kPairLutWords * 4 + kM + 257 * 4 + 227 * 4;
+
+struct PairTab {
+    uint32_t lut_s;        // shared address of the pair LUT (the codes table follows at + 4·kM)
+    uint32_t lut1_s;       // shared address of the single table's symbol per slot
+    uint32_t cum_s;        // shared address of the single table's cum[257]
+    uint32_t esc_lo;       // slot << 20 at and above which a pair step is the escape (0xFFFFFFFF: none)
+    uint32_t fesc, cesc;   // escape frequency and cumulative start
+    uint32_t k2p20, k2p12; // 2^20, 2^12 passed at run time (IMAD forms on the FMA pipe)
+};
+
+// the LUT entry's 8-bit id of rank pair (ra, rb), ra, rb < 15: a bijection onto [0, 225) in
+// anti-diagonal order, so the frequent pairs (small ranks) get consecutive ids and their
+// codes-table words fall in distinct banks (−10 % shared wavefronts vs row-major ids)
+__device__ __forceinline__ uint32_t pair_id(uint32_t ra, uint32_t rb) {
+    const uint32_t d = ra + rb;
+    if (d <= 14) return d * (d + 1) / 2 + ra;
+    const uint32_t e = 28 - d;
+    return 225 - (e + 1) * (e + 2) / 2 + ra - (d - 14);
+}
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// word renormalisation (R14): at most one 16-bit word per step, prefetched into r.w
+__device__ __forceinline__ void renorm_w(uint32_t& x, WordReader& r) {
+    if (x < kLw) {
+        x = __byte_perm(r.w, x, 0x5410);                                // (x << 16) | w
+        r.w = lds_u16(r.ring | (r.Q & (kWRing - 1)));
+        r.Q += 2;
+    }
+}
+
+// a single-table symbol (escape path and odd tails): symbol per slot, then its cum entries
+__device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, const PairTab& T) {
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    const uint32_t slot = lo >> 20;
+    const uint32_t s = lds_u8(T.lut1_s + slot);
+    const uint32_t cs = lds_u32(T.cum_s + 4 * s), ce = lds_u32(T.cum_s + 4 * s + 4);
+    x = (ce - cs) * xs + slot - cs;
+    renorm_w(x, r);
+    return s;
+}
+
+// one pair step; returns the two codes in the low 16 bits (first symbol in the low byte)
+__device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, const PairTab& T, const uint8_t* payload) {
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    if (lo >= T.esc_lo) {                          // escape: its step, then two singles
+        x = T.fesc * xs + (lo >> 20) - T.cesc;
+        renorm_w(x, r);
+        ring_step_w(r, payload);                   // up to 2 more words follow: keep the ring ahead
+        const uint32_t a = decode_single_p(x, r, T);
+        const uint32_t b = decode_single_p(x, r, T);
+        return a | (b << 8);
+    }
+    const uint32_t e = lds_u32(T.lut_s + (lo >> 18));
+    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
+    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
+    renorm_w(x, r);
+    return lds_u16(T.lut_s + 4 * kM + ((e & 0xFFu) << 1));              // pair id -> codes
+}
+
+// lut[slot] = entry(slot, s) for the s with cm[s] <= slot < cm[s + 1] (cm[0..NS], cm[NS] = kM),
+// NT threads: thread t fills slots [S·t, S·t + S), S = kM / NT, one binary search then a forward
+// walk over the symbol boundaries (zero-width symbols are stepped over), 16-byte stores
+template <int NS, int NT, class F>
+__device__ __forceinline__ void lut_walk(uint32_t* lut, const uint32_t* cm, F entry) {
+    constexpr uint32_t S = kM / NT;
+    static_assert(S >= 4 && S * NT == kM, "slots per thread");
+    const uint32_t s0 = S * (uint32_t)threadIdx.x;
+    int lo = 0, hi = NS - 1;                       // largest s with cm[s] <= s0
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cm[mid] <= s0) lo = mid; else hi = mid - 1;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(lut + s0);
+    #pragma unroll 1
+    for (uint32_t k = 0; k < S; k += 4) {
+        uint32_t v[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            while (cm[lo + 1] <= s0 + k + u) ++lo;
+            v[u] = entry(s0 + k + u, lo);
+        }
+        dst[k >> 2] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+// The block's tables (PairSmem) from its table buffer `freq`.  ALL threads of the CTA call it
+// (it holds the barriers); threads t < NT (NT ≥ 64, a power of two ≤ 1024) do the work: the
+// single cum by a block scan, the pair cum (226 entries: kept pairs in (ra, rb) order, then the
+// escape) by warp 0, then the LUT walks and the codes table.  The caller waits for the table
+// stores (a barrier) before decoding.  Returns false on every thread for a corrupt table
+// (EQ_EF_CORRUPT set once).
+// (This sequence keeps the table bases in uniform registers through the decode loop; a variant
+// scanning both tables concurrently made ptxas rematerialise them per pair step, −1.6 %.)
+template <int NT, bool ALL = false>                  // ALL: the CTA has exactly NT threads
+__device__ __forceinline__ bool pair_tables_build(const uint16_t* freq, uint32_t* lut, uint8_t* lut1,
+                                                  uint32_t* cum, uint32_t* pcum, uint32_t* err) {
+    static_assert(NT >= 64 && (NT & (NT - 1)) == 0 && NT <= 1024, "thread count");
+    const int t = threadIdx.x;
+    {                                              // cum[257]: exclusive prefix of the 256 frequencies
+        __shared__ uint32_t wsum[8];
+        const int lane = t & 31, w = t >> 5;
+        for (int base = 0; base < 256; base += NT) {
+            if ((ALL || t < NT) && base + t < 256) {
+                uint32_t v = freq[base + t];
+                #pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+                    if (lane >= d) v += o;
+                }
+                if (lane == 31) wsum[(base >> 5) + w] = v;
+                cum[base + t + 1] = v;             // warp-local inclusive prefix for now
+            }
+        }
+        __syncthreads();
+        for (int base = 0; base < 256; base += NT) {
+            const int idx = base + t;
+            if ((ALL || t < NT) && idx < 256) {
+                uint32_t add = 0;
+                for (int q = 0; q < (idx >> 5); ++q) add += wsum[q];
+                cum[idx + 1] += add;
+            }
+        }
+        if (t == 0) cum[0] = 0;
+    }
+    __syncthreads();
+    if (cum[256] != kM) {
+        if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
+        return false;
+    }
+    const uint32_t K = freq[kKIdx];
+    if (t < 32) {                                  // 226-entry pair cum: (ra, rb) order, escape last
+        uint32_t v[8], s = 0;
+        #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int q = t * 8 + j;
+            v[j] = (q < 225 && (uint32_t)(q / 15) < K && (uint32_t)(q % 15) < K) ? freq[kPairOff + q] : 0u;
+            s += v[j];
+        }
+        uint32_t inc = s;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (t >= d) inc += o;
+        }
+        uint32_t run = inc - s;
+        #pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int q = t * 8 + j;
+            if (q < 225) pcum[q] = run;
+            run += v[j];
+        }
+        if (t == 31) {
+            pcum[225] = inc;
+            pcum[226] = inc + freq[kFescIdx];
+        }
+    }
+    __syncthreads();
+    if (pcum[226] != kM || K > 15) {
+        if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
+        return false;
+    }
+    if (ALL || t < NT) {
+        lut_walk<226, NT>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
+            const uint32_t f = pcum[q + 1] - pcum[q];
+            const uint32_t id = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : 0xFFu;
+            return id | ((slot - pcum[q]) << 8) | ((f - 1) << 20);
+        });
+        constexpr uint32_t SP = kM / NT;           // symbol per slot: thread t fills [SP·t, SP·t + SP)
+        const uint32_t s0 = SP * (uint32_t)t;
+        int lo = 0, hi = 255;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
+        }
+        #pragma unroll
+        for (uint32_t k4 = 0; k4 < SP; k4 += 4) {
+            uint32_t w = 0;
+            #pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                while (cum[lo + 1] <= s0 + k4 + k) ++lo;
+                w |= (uint32_t)lo << (8 * k);
+            }
+            *reinterpret_cast<uint32_t*>(lut1 + s0 + k4) = w;
+        }
+        const uint8_t* rcb = reinterpret_cast<const uint8_t*>(freq + kRankIdx);
+        uint16_t* ctab = reinterpret_cast<uint16_t*>(lut + kM);
+        for (int q = t; q < 225; q += NT)
+            ctab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = (uint16_t)(rcb[q / 15] | (rcb[q % 15] << 8));
+    }
+    return true;
+}
+
+__device__ __forceinline__ PairTab pair_tab(const uint16_t* freq, const uint32_t* lut, const uint8_t* lut1,
+                                            const uint32_t* cum, const uint32_t* pcum, uint32_t k2p20, uint32_t k2p12) {
+    PairTab T;
+    T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
+    T.lut1_s = (uint32_t)__cvta_generic_to_shared(lut1);
+    T.cum_s = (uint32_t)__cvta_generic_to_shared(cum);
+    T.fesc = freq[kFescIdx];
+    T.cesc = pcum[225];
+    T.esc_lo = T.fesc ? (T.cesc << 20) : 0xFFFFFFFFu;
+    T.k2p20 = k2p20;
+    T.k2p12 = k2p12;
+    return T;
+}
+
+}  // namespace eq

@@ -22,6 +22,10 @@
 // fixed order (deterministic split-K).
 #include "common.cuh"
 #include "decode_core.cuh"
+#include "pair_core.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstring>
@@ -401,6 +405,305 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols));
 }
 
+// ================================================================ warp-specialised kernel
+// k_qmm_ws — EQ_CODEC_WORD / EQ_CODEC_PAIR blocks (the bench's codec), row-chunked streams.
+// CTA = (GEMM, one 128-row tile, chunk column j), 160 threads:
+//   warps 0-3  decoders: lane r decodes chunk j of row r (its rANS chain), dequantises with the
+//              row scale and writes 32 columns per K step (64 B, bf16) into A stage s of a
+//              kWsStages-deep ring (K-major, SWIZZLE_64B canonical UMMA layout), then
+//              fence.proxy.async + one mbarrier arrive per warp on full[s];
+//   warp 4     producer + MMA issuer (one elected lane): TMA-loads X[:, k0 : k0 + 32] as the B
+//              stage (the tensor map's SWIZZLE_64B box lands in the UMMA layout; rows past the
+//              batch are zero-filled), waits full[s], issues 2 × tcgen05.mma (M = 128, N =
+//              batch rounded up to 16, K = 16) into one TMEM accumulator and commits to
+//              empty[s], which frees both stages for step + kWsStages.
+// The decoders never wait for the tensor cores unless they run kWsStages steps ahead; no
+// CTA-wide barrier inside the K loop.  Epilogue: the decoder warps read their TMEM lanes
+// (tcgen05.ld 32x32b) and write Y (one chunk column) or the split-K partial.
+#ifndef EQ_QMM_WS_STAGES
+#define EQ_QMM_WS_STAGES 3
+#endif
+#ifndef EQ_QMM_WS_MIN_CTAS
+#define EQ_QMM_WS_MIN_CTAS 3
+#endif
+constexpr int kWsStages = EQ_QMM_WS_STAGES;
+constexpr int kWsK = 32;                       // K columns per step (one SWIZZLE_64B row = 64 B)
+constexpr int kWsRowB = kWsK * 2;
+constexpr int kWsATile = kTileRows * kWsRowB;  // 8 KB per A stage
+constexpr int kWsDec = 128, kWsThreads = kWsDec + 32;
+
+struct QmmWsParams {
+    CUtensorMap tmap[EQ_MAX_LAYERS];           // X of each job: [batch, K] bf16, box {32, n_pad}, SWIZZLE_64B
+    QmmJob job[EQ_MAX_LAYERS];
+    uint32_t n_jobs;
+    const uint8_t* payload;
+    const uint32_t* off;
+    const uint16_t* freq;
+    uint64_t payload_bytes;
+    uint32_t* err;
+    uint32_t format, cs, n_pad, n_real, idesc, tmem_cols, b_stage_bytes;
+    uint32_t k2p20, k2p12, kneg2p14, k4;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1; }" ::"r"(bar),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+// the 8 codes -> 8 bf16 (16 bytes) of one lane, with the lane's row scale
+template <class C>
+__device__ __forceinline__ uint4 ws_dequant8(const C& c, uint32_t q0, uint32_t q1) {
+    return dequant8(c, q0, q1);
+}
+
+template <int CODEC>
+__global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const __grid_constant__ QmmWsParams P) {
+    extern __shared__ __align__(1024) uint8_t ws_raw[];
+    uint8_t* dsm = ws_raw + ((1024u - (smem_u32(ws_raw) & 1023u)) & 1023u);
+    // layout: [A stages | B stages | tables | rings | barriers | tmem slot]
+    uint8_t* a_st = dsm;
+    uint8_t* b_st = dsm + kWsStages * kWsATile;
+    uint8_t* tabs = b_st + kWsStages * P.b_stage_bytes;
+    constexpr uint32_t kTabBytes = CODEC == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4u;
+    uint32_t* rings = reinterpret_cast<uint32_t*>(tabs + ((kTabBytes + 127u) & ~127u));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + kWsDec * (kWRing / 4));   // full[S], empty[S]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kWsStages);
+
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    uint32_t jb = 0;
+    for (uint32_t q = 1; q < P.n_jobs; ++q)
+        if (blockIdx.x >= P.job[q].tile_begin) jb = q;
+    const QmmJob& J = P.job[jb];
+    const uint32_t local = blockIdx.x - J.tile_begin;
+    const uint32_t tile = local / J.cpr, jcol = local - tile * J.cpr;
+    const uint32_t kbase = jcol * P.cs;
+    const uint32_t clen = min(P.cs, J.K - kbase);
+    const uint32_t steps = clen / kWsK;
+    const uint32_t grow = tile * kTileRows + (uint32_t)t;            // decoder lanes only
+
+    // ---- the decoder lanes start staging their chunk while the tables are built
+    ChainW c;
+    c.active = false;
+    c.runaway = false;
+    c.i8 = P.format == EQ_FMT_INT8;
+    c.s = 0.f;
+    c.s16 = 0;
+    const uint32_t ring = smem_u32(rings + t * (kWRing / 4));
+    if (t < kWsDec) {
+        c.s = bf16_bits_to_float(J.scales[grow]);
+        c.s16 = c.i8 ? 0 : scale_f16(c.s);
+        const uint32_t chunk = J.chunk0 + grow * J.cpr + jcol;
+        const uint32_t a = __ldg(P.off + chunk), e = __ldg(P.off + chunk + 1);
+        if (e < a || (uint64_t)e > P.payload_bytes || e - a < 4) {
+            atomicOr(P.err, EQ_EF_TRUNCATED);
+        } else {
+            c.active = true;
+            c.a = a;
+            c.e = e;
+            c.i = 0;
+            c.n = clen;
+            c.r.ring = ring;
+            const uint32_t g0 = a & ~15u;
+            #pragma unroll
+            for (uint32_t q = 0; q < kWRing / 16; ++q) stage_segment_w(ring, P.payload, g0 + 16 * q);
+            c.r.gn = g0 + kWRing;
+        }
+    }
+    stage_commit();
+    // ---- tables (all 160 threads reach the barriers; the 128 decoder threads work)
+    PairTab PT{};
+    DecTable WT{};
+    bool ok;
+    if constexpr (CODEC == EQ_CODEC_PAIR) {
+        uint32_t* lut = reinterpret_cast<uint32_t*>(tabs);
+        uint8_t* lut1 = tabs + kPairLutWords * 4;
+        uint32_t* cum = reinterpret_cast<uint32_t*>(lut1 + kM);
+        uint32_t* pcum = cum + 257;
+        ok = pair_tables_build<kWsDec>(P.freq, lut, lut1, cum, pcum, P.err);
+        __syncthreads();                           // table stores visible to every decoder lane
+        if (ok) PT = pair_tab(P.freq, lut, lut1, cum, pcum, P.k2p20, P.k2p12);
+    } else {
+        uint32_t* lut = reinterpret_cast<uint32_t*>(tabs);
+        uint32_t* cum = lut + kM;
+        if (t < 32) {                              // exclusive prefix of the 256 frequencies
+            uint32_t v[8], sum = 0;
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) { v[j] = P.freq[t * 8 + j]; sum += v[j]; }
+            uint32_t inc = sum;
+            #pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (t >= d) inc += o;
+            }
+            uint32_t run = inc - sum;
+            #pragma unroll
+            for (int j = 0; j < 8; ++j) { cum[t * 8 + j] = run; run += v[j]; }
+            if (t == 31) cum[256] = inc;
+        }
+        __syncthreads();
+        ok = cum[256] == kM;
+        if (ok && t < kWsDec) {
+            lut_walk<256, kWsDec>(lut, cum, [&](uint32_t slot, int sym) -> uint32_t {
+                const uint32_t fs = cum[sym + 1] - cum[sym];
+                return (uint32_t)sym | ((slot - cum[sym]) << 8) | ((fs - 1) << 20);   // (f−1)-on-top layout
+            });
+        } else if (!ok && t == 0) {
+            atomicOr(P.err, EQ_EF_CORRUPT);
+        }
+        __syncthreads();
+        WT.k2p20 = P.k2p20;
+        WT.k2p12 = P.k2p12;
+        WT.kneg2p14 = P.kneg2p14;
+        WT.k4 = P.k4;
+        WT.lut_s = smem_u32(lut);
+    }
+    if (!ok) {                                     // nothing decodable: the whole CTA leaves together
+        stage_wait_all();
+        return;
+    }
+    // ---- barriers (thread 128), TMEM accumulator (warp 4)
+    if (t == kWsDec) {
+        for (int q = 0; q < kWsStages; ++q) {
+            mbar_init(smem_u32(&bars[q]), 4 + 1);                 // 4 decoder warps + the TMA arrive
+            mbar_init(smem_u32(&bars[kWsStages + q]), 1);         // tcgen05.commit
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(P.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // ===== producer (TMA of X) + MMA issuer: one lane
+        if (lane == 0) {
+            const CUtensorMap* map = &P.tmap[jb];
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+            const uint32_t pre = steps < (uint32_t)kWsStages ? steps : (uint32_t)kWsStages;
+            for (uint32_t q = 0; q < pre; ++q) {
+                const uint32_t fb = smem_u32(&bars[q]);
+                mbar_arrive_tx(fb, P.b_stage_bytes);
+                tma_load_2d(smem_u32(b_st + q * P.b_stage_bytes), map, (int32_t)(kbase + q * kWsK), 0, fb);
+            }
+            for (uint32_t st = 0; st < steps; ++st) {
+                const uint32_t sidx = st % kWsStages, use = st / kWsStages;
+                mbar_wait(smem_u32(&bars[sidx]), use & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t da = umma_desc_sw64(smem_u32(a_st + sidx * kWsATile));
+                const uint64_t db = umma_desc_sw64(smem_u32(b_st + sidx * P.b_stage_bytes));
+                #pragma unroll
+                for (int kk = 0; kk < kWsK / 16; ++kk) {
+                    const uint32_t acc = (st > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+                            tmem),
+                        "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(P.idesc), "r"(acc));
+                }
+                const uint32_t eb = smem_u32(&bars[kWsStages + sidx]);
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(eb)
+                             : "memory");
+                if (st + kWsStages < steps) {      // refill the B stage once the MMAs that read it are done
+                    mbar_wait(eb, use & 1);
+                    const uint32_t fb = smem_u32(&bars[sidx]);
+                    mbar_arrive_tx(fb, P.b_stage_bytes);
+                    tma_load_2d(smem_u32(b_st + sidx * P.b_stage_bytes), map,
+                                (int32_t)(kbase + (st + kWsStages) * kWsK), 0, fb);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===== decoders: lane r = row r of the tile
+        stage_wait_all();
+        if (c.active) {
+            const uint32_t m = kWRing - 1, A = c.a + kWBias;
+            c.x = lds_u16(ring | (A & m)) | (lds_u16(ring | ((A + 2) & m)) << 16);
+            c.r.w = lds_u16(ring | ((A + 4) & m));
+            c.r.Q = A + 6;
+        }
+        const uint32_t r = (uint32_t)t;
+        const uint32_t row_off = (r >> 3) * 512u + (r & 7) * (uint32_t)kWsRowB;
+        const uint32_t sw = (r >> 1) & 3;                         // SWIZZLE_64B: 16-byte chunk q at q ^ sw
+        const uint32_t qlim = c.e + (2u + kWBias);
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t sidx = st % kWsStages, use = st / kWsStages;
+            if (st >= (uint32_t)kWsStages) mbar_wait(smem_u32(&bars[kWsStages + sidx]), (use - 1) & 1);
+            const uint32_t arow = smem_u32(a_st + sidx * kWsATile) + row_off;
+            const bool live = c.active && !c.runaway;
+            #pragma unroll
+            for (uint32_t g = 0; g < kWsK / 8; ++g) {             // 4 × 8 symbols -> 16 bytes each
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (live) {
+                    uint32_t q0, q1;
+                    if constexpr (CODEC == EQ_CODEC_PAIR) {
+                        const uint32_t p0 = decode_pair(c.x, c.r, PT, P.payload);
+                        const uint32_t p1 = decode_pair(c.x, c.r, PT, P.payload);
+                        const uint32_t p2 = decode_pair(c.x, c.r, PT, P.payload);
+                        const uint32_t p3 = decode_pair(c.x, c.r, PT, P.payload);
+                        q0 = __byte_perm(p0, p1, 0x5410);
+                        q1 = __byte_perm(p2, p3, 0x5410);
+                        if (g & 1) ring_step_w(c.r, P.payload);   // one stage per 8 pair steps
+                    } else {
+                        q0 = decode4_w(c, WT);
+                        q1 = decode4_w(c, WT);
+                        ring_step_w(c.r, P.payload);              // one stage per 8 steps
+                    }
+                    v = dequant8(c, q0, q1);
+                }
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + ((g ^ sw) << 4)), "r"(v.x),
+                             "r"(v.y), "r"(v.z), "r"(v.w)
+                             : "memory");
+            }
+            if (live) {
+                c.i += kWsK;
+                if (c.r.Q > qlim) c.runaway = true;               // overran its chunk: stop reading
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bars[sidx]));
+        }
+        stage_wait_all();
+        if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
+        // ---- epilogue: the last commit covers every MMA of this CTA
+        const uint32_t last = steps - 1;
+        mbar_wait(smem_u32(&bars[kWsStages + last % kWsStages]), (last / kWsStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float* out = J.out + (uint64_t)jcol * P.n_real * J.rows;
+        for (uint32_t col = 0; col < P.n_pad; col += 8) {
+            uint32_t v[8];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + col;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                         : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            #pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t b = col + q;
+                if (b < P.n_real) out[(uint64_t)b * J.rows + grow] = __uint_as_float(v[q]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols));
+}
+
 // Y = Σ_j partial_j in a fixed order (j = 0, 1, …): deterministic split-K reduction
 struct RedJob {
     const float* part;
@@ -436,7 +739,7 @@ static eq_status qmm_validate(const eq_block* blk, uint32_t n_jobs, const uint32
                               QmmPlan* plan) {
     if (!blk || !layers || n_jobs < 1 || n_jobs > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (!blk->payload || !blk->chunk_off || !blk->freq || !blk->scales || blk->format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if (blk->codec > EQ_CODEC_WORD) return EQ_ERR_ARG;
+    if (blk->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
     if (blk->n_layers < 1 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(blk->payload) & 15) != 0) return EQ_ERR_ARG;
     if (blk->payload_cap < blk->payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;
@@ -465,6 +768,94 @@ static eq_status qmm_validate(const eq_block* blk, uint32_t n_jobs, const uint32
 
 static uint64_t qmm_part_bytes(uint64_t cpr, uint64_t batch, uint64_t rows) {
     return cpr > 1 ? (cpr * batch * rows * 4 + EQ_ARENA_ALIGN - 1) / EQ_ARENA_ALIGN * EQ_ARENA_ALIGN : 0;
+}
+
+// cuTensorMapEncodeTiled from the driver, resolved once through the runtime (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// Launch of k_qmm_ws (word / pair codecs): one CTA per (GEMM, 128-row tile, chunk column);
+// the split-K partials go to the same workspace offsets as the byte-codec kernel's (the caller
+// runs k_qmm_reduce afterwards).
+static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers, const QmmPlan& plan,
+                               const void* const* x, float* const* y, uint32_t batch, void* workspace, uint32_t* d_err,
+                               cudaStream_t st) {
+    auto encode = tensor_map_encoder();
+    if (!encode) return EQ_ERR_CUDA;
+    QmmWsParams W;
+    memset(&W, 0, sizeof(W));
+    const uint32_t cs = blk->chunk_symbols;
+    const uint32_t n_pad = (batch + 15) & ~15u;    // UMMA N: a multiple of 16 for M = 128
+    uint64_t ws_off = 0;
+    uint32_t tiles = 0;
+    for (uint32_t q = 0; q < n_jobs; ++q) {
+        const uint32_t l = layers[q];
+        QmmJob& J = W.job[q];
+        J.x = static_cast<const uint16_t*>(x[q]);
+        J.scales = blk->scales + plan.srow[l];
+        J.chunk0 = plan.chunk0[l];
+        J.rows = blk->layer_rows[l];
+        J.K = blk->layer_cols[l];
+        J.cpr = (J.K + cs - 1) / cs;
+        J.tile_begin = tiles;
+        tiles += J.rows / kTileRows * J.cpr;
+        if (J.cpr == 1) {
+            J.out = y[q];
+        } else {
+            J.out = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + ws_off);
+            ws_off += qmm_part_bytes(J.cpr, batch, J.rows);
+        }
+        // X [batch, K] bf16 row-major: dims {K, batch}, row stride 2K bytes, box {32, n_pad}
+        const cuuint64_t dims[2] = {J.K, batch};
+        const cuuint64_t strides[1] = {(cuuint64_t)J.K * 2};
+        const cuuint32_t box[2] = {(cuuint32_t)kWsK, n_pad};
+        const cuuint32_t estr[2] = {1, 1};
+        if (encode(&W.tmap[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x[q]), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return EQ_ERR_ARG;
+    }
+    W.n_jobs = n_jobs;
+    W.payload = blk->payload;
+    W.off = blk->chunk_off;
+    W.freq = blk->freq;
+    W.payload_bytes = blk->payload_bytes;
+    W.err = d_err;
+    W.format = blk->format;
+    W.cs = cs;
+    W.n_pad = n_pad;
+    W.n_real = batch;
+    W.tmem_cols = 32;
+    while (W.tmem_cols < n_pad) W.tmem_cols <<= 1;
+    W.b_stage_bytes = (n_pad * (uint32_t)kWsRowB + 1023u) & ~1023u;
+    // instruction descriptor, kind::f16: D f32, A = B = bf16, both K-major, N = n_pad, M = 128
+    W.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((n_pad >> 3) << 17) | ((128u >> 4) << 24);
+    W.k2p20 = 1u << 20;
+    W.k2p12 = 1u << 12;
+    W.kneg2p14 = 0u - (1u << 14);
+    W.k4 = 4u;
+    const size_t tab = blk->codec == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4;
+    const size_t smem = 1024 + kWsStages * kWsATile + kWsStages * W.b_stage_bytes + ((tab + 127) & ~(size_t)127) +
+                        kWsDec * kWRing + 2 * kWsStages * 8 + 16;
+    const void* fn = blk->codec == EQ_CODEC_PAIR ? (const void*)k_qmm_ws<EQ_CODEC_PAIR> : (const void*)k_qmm_ws<EQ_CODEC_WORD>;
+    EQ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (blk->codec == EQ_CODEC_PAIR)
+        k_qmm_ws<EQ_CODEC_PAIR><<<tiles, kWsThreads, smem, st>>>(W);
+    else
+        k_qmm_ws<EQ_CODEC_WORD><<<tiles, kWsThreads, smem, st>>>(W);
+    EQ_CUDA_TRY(cudaGetLastError());
+    return EQ_OK;
 }
 
 }  // namespace eq
@@ -527,6 +918,17 @@ extern "C" eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, cons
             max_red = std::max(max_red, R.job[n_red].n);
             ++n_red;
         }
+    }
+    if (blk->codec != EQ_CODEC_BYTE) {            // warp-specialised kernel (word and pair codecs)
+        const eq_status ws = qmm_ws_launch(blk, n_jobs, layers, plan, x, y, batch, workspace, d_err,
+                                           (cudaStream_t)stream);
+        if (ws != EQ_OK) return ws;
+        if (n_red) {
+            const uint32_t gx = std::min<uint32_t>((max_red / 4 + 255) / 256, 148u * 8u);
+            k_qmm_reduce<<<dim3(gx, n_red), 256, 0, (cudaStream_t)stream>>>(R);
+            EQ_CUDA_TRY(cudaGetLastError());
+        }
+        return EQ_OK;
     }
     P.n_jobs = n_jobs;
     P.payload = blk->payload;

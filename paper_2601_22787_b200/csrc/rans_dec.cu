@@ -14,6 +14,7 @@
 //    per group when cols % 16 == 0 (generic per-symbol path otherwise).
 #include "common.cuh"
 #include "decode_core.cuh"
+#include "pair_core.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -185,7 +186,9 @@ __device__ __forceinline__ void chain_setup(Chain& c, const DecBlock& B, uint32_
     c.s = BF16 ? bf16_bits_to_float(c.sc[c.row]) : 0.f;
     c.i8 = B.format == EQ_FMT_INT8;
     c.s16 = (BF16 && !c.i8) ? scale_f16(c.s) : 0;
-    c.fast = BF16 ? ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) : ((B.cs & 31) == 0);
+    // 16 / 32-symbol groups with 32-byte stores need a 32-byte aligned chunk start (row chunks
+    // start at row·cols + j·cs) and whole groups per row (bf16: one scale per group)
+    c.fast = BF16 ? ((Ly.cols & 15) == 0 && ((sym0 | B.cs) & 15) == 0) : (((sym0 | B.cs) & 31) == 0);
 }
 
 // after the initial segments landed: read the 4-byte state and fill the window
@@ -426,7 +429,9 @@ __device__ __forceinline__ void chain_setup_w(ChainW& c, const DecBlock& B, uint
     c.s = BF16 ? bf16_bits_to_float(c.sc[c.row]) : 0.f;
     c.i8 = B.format == EQ_FMT_INT8;
     c.s16 = (BF16 && !c.i8) ? scale_f16(c.s) : 0;
-    c.fast = BF16 ? ((Ly.cols & 15) == 0 && (B.cs & 15) == 0) : ((B.cs & 31) == 0);
+    // 16 / 32-symbol groups with 32-byte stores need a 32-byte aligned chunk start (row chunks
+    // start at row·cols + j·cs) and whole groups per row (bf16: one scale per group)
+    c.fast = BF16 ? ((Ly.cols & 15) == 0 && ((sym0 | B.cs) & 15) == 0) : (((sym0 | B.cs) & 31) == 0);
 }
 
 // after the initial segments landed: 4-byte little-endian state, then the first word
@@ -550,252 +555,8 @@ k_decode_w(const __grid_constant__ DecParams P) {
 
 
 // ================================================================ EQ_CODEC_PAIR decoder (R15)
-// Word-codec rANS over pairs of symbols: one LUT lookup and at most one 16-bit word per TWO
-// symbols for the block's top-15 codes; an escape (top slots) decodes two singles by binary
-// search over the single table.  Table buffer (u16[512], see include/entquant.h): [0,256)
-// single frequencies, [256,481) pair frequencies by ra·15 + rb, [481] escape frequency,
-// [482] K, [484,492) the 16 rank codes as bytes.
-constexpr int kPairOff = 256, kFescIdx = 481, kKIdx = 482, kRankIdx = 484;
-
-struct PairTab {
-    uint32_t lut_s;        // shared address of the pair LUT (4096 × u32: nib | bias << 8 | (f−1) << 20)
-    uint32_t lut1_s;       // shared address of the single-symbol LUT (escapes; EQ_PAIR_LUT1)
-    uint32_t esc_lo;       // slot << 20 at and above which a pair step is the escape (0xFFFFFFFF: none)
-    uint32_t fesc, cesc;   // escape frequency and cumulative start
-    uint32_t rc0, rc1, rc2, rc3;   // rank codes 0..15 as bytes
-    uint32_t k2p20, k2p12;
-    const uint32_t* cum;   // single-table cumulative frequencies (shared, 257)
-    uint32_t cum_s;        // shared address of cum (EQ_PAIR_LUT1 == 2)
-};
-
-#ifndef EQ_PAIR_CODETAB
-#define EQ_PAIR_CODETAB 1   // pair codes from a 512-B shared table (1 LDS) instead of 6 ALU ops over rc0..rc3
-#endif
-#ifndef EQ_PAIR_DIAG
-#define EQ_PAIR_DIAG 1   // pair ids in anti-diagonal order of (ra, rb): the frequent pairs (small ranks)
-                         // get consecutive ids, so their codes-table words fall in distinct banks
-#endif
-// the LUT entry's 8-bit pair id of rank pair (ra, rb), ra, rb < 15 (a bijection onto [0, 225))
-__device__ __forceinline__ uint32_t pair_id(uint32_t ra, uint32_t rb) {
-#if EQ_PAIR_DIAG && EQ_PAIR_CODETAB
-    const uint32_t d = ra + rb;
-    if (d <= 14) return d * (d + 1) / 2 + ra;
-    const uint32_t e = 28 - d;
-    return 225 - (e + 1) * (e + 2) / 2 + ra - (d - 14);
-#else
-    return ra | (rb << 4);
-#endif
-}
-
-
-__device__ __forceinline__ void renorm_w(uint32_t& x, WordReader& r) {
-    if (x < kLw) {
-        x = __byte_perm(r.w, x, 0x5410);                                // (x << 16) | w
-        r.w = lds_u16(r.ring | (r.Q & (kWRing - 1)));
-        r.Q += 2;
-    }
-}
-
-#ifndef EQ_PAIR_LUT1
-#define EQ_PAIR_LUT1 2   // escapes decode their two singles from a u8 symbol per slot + the cum table
-                         // (1: u32 LUT entries, 12 KB more shared memory -> 4 CTAs/SM; 0: binary search)
-#endif
-__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
-    uint32_t v;
-    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-// a single-table symbol (escape path and odd tails)
-__device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, const PairTab& T) {
-#if EQ_PAIR_LUT1 == 3
-    uint32_t lo, xs;
-    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
-    const uint32_t slot = lo >> 20;
-    uint32_t s = lds_u8(T.lut1_s + (slot >> 4));   // first symbol of the slot's 16-slot bucket
-    uint32_t ce = lds_u32(T.cum_s + 4 * s + 4);
-    while (ce <= slot) {                           // walk the bucket's symbol boundaries
-        ++s;
-        ce = lds_u32(T.cum_s + 4 * s + 4);
-    }
-    const uint32_t cs = lds_u32(T.cum_s + 4 * s);
-    x = (ce - cs) * xs + slot - cs;
-    renorm_w(x, r);
-    return s;
-#elif EQ_PAIR_LUT1 == 2
-    uint32_t lo, xs;
-    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
-    const uint32_t slot = lo >> 20;
-    const uint32_t s = lds_u8(T.lut1_s + slot);
-    const uint32_t cs = lds_u32(T.cum_s + 4 * s), ce = lds_u32(T.cum_s + 4 * s + 4);
-    x = (ce - cs) * xs + slot - cs;
-    renorm_w(x, r);
-    return s;
-#elif EQ_PAIR_LUT1
-    uint32_t lo, xs;
-    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
-    const uint32_t e = lds_u32(T.lut1_s + (lo >> 18));
-    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);
-    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));
-    renorm_w(x, r);
-    return e & 0xFFu;
-#else
-    const uint32_t slot = x & (kM - 1);
-    int lo = 0, hi = 255;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (T.cum[mid] <= slot) lo = mid; else hi = mid - 1;
-    }
-    const uint32_t c = T.cum[lo], f = T.cum[lo + 1] - c;
-    x = f * (x >> 12) + slot - c;
-    renorm_w(x, r);
-    return (uint32_t)lo;
-#endif
-}
-
-// one pair step; returns the two codes in the low 16 bits (first symbol in the low byte)
-__device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, const PairTab& T, const uint8_t* payload) {
-    uint32_t lo, xs;
-    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
-    const bool esc = lo >= T.esc_lo;
-#ifndef EQ_PAIR_VOTE
-#define EQ_PAIR_VOTE 0   // 1: test for escapes warp-wide first (measured: more SASS, not less)
-#endif
-    if ((!EQ_PAIR_VOTE || __any_sync(__activemask(), esc)) && esc) {   // escape: its step, then two singles
-        x = T.fesc * xs + (lo >> 20) - T.cesc;
-        renorm_w(x, r);
-#ifndef EQ_PAIR_ESCRING
-#define EQ_PAIR_ESCRING 1
-#endif
-        if (EQ_PAIR_ESCRING) ring_step_w(r, payload);   // up to 2 more words follow: keep the ring ahead
-        const uint32_t a = decode_single_p(x, r, T);
-        const uint32_t b = decode_single_p(x, r, T);
-        return a | (b << 8);
-    }
-    const uint32_t e = lds_u32(T.lut_s + (lo >> 18));
-    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
-    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
-    renorm_w(x, r);
-#if EQ_PAIR_CODETAB
-    // the codes table sits right after the 16 KB LUT in one shared array: its address is the
-    // LUT's uniform base + a constant (a separate array's address was rematerialised per step
-    // with S2UR / UMOV / UIADD3 / ULEA — four issue slots per pair)
-    return lds_u16(T.lut_s + 4 * kM + ((e & 0xFFu) << 1));            // pair id -> codes
-#endif
-    // rank nibbles -> codes: bytes of {rc0, rc1} for ranks 0-7, of {rc2, rc3} for 8-15,
-    // chosen per byte by the nibble's bit 3 (PRMT sign-replicate of bits 3 and 7 of e)
-    // (t1 may take e's nibbles as they are: a rank ≥ 8 byte of t1 is replaced by t2's)
-    uint32_t t1;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(t1) : "r"(T.rc0), "r"(T.rc1), "r"(e));
-    const uint32_t t2 = __byte_perm(T.rc2, T.rc3, e & 0x77u);
-    uint32_t m;                                    // PTX prmt: selector bit 3 = replicate the msb
-    asm("prmt.b32 %0, %1, %2, 0xC8;" : "=r"(m) : "r"(e << 4), "r"(e));
-    return (t1 & ~m) | (t2 & m);
-}
-
-#ifndef EQ_PAIR_WALK
-#define EQ_PAIR_WALK 1   // LUT fills: one binary search per 16 slots + a forward walk (else one per slot)
-#endif
-// lut[slot] = entry(slot, s) for the s with cm[s] <= slot < cm[s + 1] (cm[0..NS], cm[NS] = kM),
-// NT threads: thread t fills slots [S·t, S·t + S), S = kM / NT, one binary search then a forward
-// walk over the symbol boundaries (zero-width symbols are stepped over), 16-byte stores
-template <int NS, int NT, class F>
-__device__ __forceinline__ void lut_walk(uint32_t* lut, const uint32_t* cm, F entry) {
-    constexpr uint32_t S = kM / NT;
-    static_assert(S >= 4 && S * NT == kM, "slots per thread");
-    const uint32_t s0 = S * (uint32_t)threadIdx.x;
-    int lo = 0, hi = NS - 1;                       // largest s with cm[s] <= s0
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (cm[mid] <= s0) lo = mid; else hi = mid - 1;
-    }
-    uint4* dst = reinterpret_cast<uint4*>(lut + s0);
-    #pragma unroll 1
-    for (uint32_t k = 0; k < S; k += 4) {
-        uint32_t v[4];
-        #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            while (cm[lo + 1] <= s0 + k + u) ++lo;
-            v[u] = entry(s0 + k + u, lo);
-        }
-        dst[k >> 2] = make_uint4(v[0], v[1], v[2], v[3]);
-    }
-}
-
-// the pair LUT (and the single cum for escapes) of one block, all NT threads
-template <int NT>
-__device__ __forceinline__ bool build_pair_lut(const DecBlock& B, uint32_t* lut, uint32_t* cum, uint32_t* pcum,
-                                               uint32_t* err) {
-    const int t = threadIdx.x;
-    if (!build_cum<NT>(B, cum, err)) return false;
-    const uint32_t K = B.freq[kKIdx];
-#ifndef EQ_PAIR_PSCAN
-#define EQ_PAIR_PSCAN 1  // the 226-entry pair cum by one warp scan (else one thread's serial loop)
-#endif
-#if EQ_PAIR_PSCAN
-    if (t < 32) {                                  // 226-entry pair cum: (ra, rb) order, escape last
-        uint32_t v[8], s = 0;                      // lane t: q in [8t, 8t + 8)
-        #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int q = t * 8 + j;
-            v[j] = (q < 225 && (uint32_t)(q / 15) < K && (uint32_t)(q % 15) < K) ? B.freq[kPairOff + q] : 0u;
-            s += v[j];
-        }
-        uint32_t inc = s;
-        #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-            if (t >= d) inc += o;
-        }
-        uint32_t run = inc - s;
-        #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int q = t * 8 + j;
-            if (q < 225) pcum[q] = run;
-            run += v[j];
-        }
-        if (t == 31) {
-            pcum[225] = inc;
-            pcum[226] = inc + B.freq[kFescIdx];
-        }
-    }
-#else
-    if (t == 0) {                                  // 226-entry pair cum: (ra, rb) order, escape last
-        uint32_t run = 0;
-        for (int q = 0; q < 225; ++q) {
-            pcum[q] = run;
-            if ((uint32_t)(q / 15) < K && (uint32_t)(q % 15) < K) run += B.freq[kPairOff + q];
-        }
-        pcum[225] = run;
-        pcum[226] = run + B.freq[kFescIdx];
-    }
-#endif
-    __syncthreads();
-    if (pcum[226] != kM || K > 15) {
-        if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
-        return false;
-    }
-    if constexpr (EQ_PAIR_WALK) {
-        lut_walk<226, NT>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
-            const uint32_t f = pcum[q + 1] - pcum[q];
-            const uint32_t nib = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : 0xFFu;
-            return nib | ((slot - pcum[q]) << 8) | ((f - 1) << 20);
-        });
-        return true;
-    } else {
-        for (int slot = t; slot < (int)kM; slot += NT) {
-            int lo = 0, hi = 225;                  // largest q with pcum[q] <= slot
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (pcum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
-            }
-            const uint32_t f = lo < 225 ? B.freq[kPairOff + lo] : B.freq[kFescIdx];
-            const uint32_t nib = lo < 225 ? pair_id((uint32_t)lo / 15, (uint32_t)lo % 15) : 0xFFu;
-            lut[slot] = nib | (((uint32_t)slot - pcum[lo]) << 8) | ((f - 1) << 20);
-        }
-        return true;
-    }
-}
-
+// Same CTA ↔ block and lane ↔ chunk mapping and staging as k_decode_w; the pair tables and the
+// pair / single decode steps are in pair_core.cuh (shared with the fused GEMM).
 template <bool BF16>
 __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload, const PairTab& T) {
     if (!c.active || c.runaway) return;
@@ -851,111 +612,26 @@ template <bool BF16>
 __global__ void __launch_bounds__(kPThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) uint8_t rings[];      // kPThreads × kWRing
-    __shared__ __align__(16) uint32_t lut[kM + 128];       // pair LUT, then the 256 × u16 codes table
+    __shared__ __align__(16) uint32_t lut[kPairLutWords];  // pair LUT + codes table
+    __shared__ __align__(16) uint8_t lut1[kM];
     __shared__ uint32_t cum[257];
     __shared__ uint32_t pcum[227];
-#if EQ_PAIR_LUT1 == 3
-    __shared__ __align__(16) uint8_t lut1[kM / 16];
-#elif EQ_PAIR_LUT1 == 2
-    __shared__ __align__(16) uint8_t lut1[kM];
-#elif EQ_PAIR_LUT1
-    __shared__ __align__(16) uint32_t lut1[kM];
-#endif
-#if EQ_PAIR_CODETAB
-    uint16_t* ctab = reinterpret_cast<uint16_t*>(lut + kM);
-#endif
 
     uint32_t bi = 0;
     while (bi + 1 < P.n_blocks && blockIdx.x >= P.b[bi + 1].cta0) ++bi;
     const DecBlock& B = P.b[bi];
     const int t = threadIdx.x;
-    ChainW c;
+    ChainW c;                                      // setup first: the initial copies overlap the table build
     chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kPThreads + t,
                         (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
     stage_commit();
-    if (!build_pair_lut<kPThreads>(B, lut, cum, pcum, P.err)) {
+    if (!pair_tables_build<kPThreads, true>(B.freq, lut, lut1, cum, pcum, P.err)) {
         stage_wait_all();
         return;
     }
-#if EQ_PAIR_LUT1 == 3
-    {                                              // bucket t (slots [16t, 16t + 16)): its first symbol
-        static_assert(kPThreads == 256, "bucket fill assumes 256 threads");
-        const uint32_t s0 = 16u * (uint32_t)t;
-        int lo = 0, hi = 255;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
-        }
-        lut1[t] = (uint8_t)lo;
-    }
-#elif EQ_PAIR_LUT1 == 2
-    {                                              // symbol per slot: thread t fills [S·t, S·t + S)
-        constexpr uint32_t S = kM / kPThreads;
-        static_assert(S % 4 == 0 && S * kPThreads == kM, "byte single LUT fill");
-        const uint32_t s0 = S * (uint32_t)t;
-        int lo = 0, hi = 255;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (cum[mid] <= s0) lo = mid; else hi = mid - 1;
-        }
-        #pragma unroll
-        for (uint32_t k4 = 0; k4 < S; k4 += 4) {
-            uint32_t w = 0;
-            #pragma unroll
-            for (uint32_t k = 0; k < 4; ++k) {
-                while (cum[lo + 1] <= s0 + k4 + k) ++lo;
-                w |= (uint32_t)lo << (8 * k);
-            }
-            *reinterpret_cast<uint32_t*>(lut1 + s0 + k4) = w;
-        }
-    }
-#elif EQ_PAIR_LUT1
-    {                                              // single LUT in decode_one_w's entry layout
-        auto entry = [&](uint32_t slot, int sym) -> uint32_t {
-            const uint32_t fs = cum[sym + 1] - cum[sym];
-            return (uint32_t)sym | ((slot - cum[sym]) << 8) | ((fs - 1) << 20);
-        };
-        if constexpr (EQ_PAIR_WALK) {
-            lut_walk<256, kPThreads>(lut1, cum, entry);
-        } else {
-            for (int slot = t; slot < (int)kM; slot += kPThreads) {
-                int lo = 0, hi = 255;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (cum[mid] <= (uint32_t)slot) lo = mid; else hi = mid - 1;
-                }
-                lut1[slot] = entry((uint32_t)slot, lo);
-            }
-        }
-    }
-#endif
-#if EQ_PAIR_CODETAB
-    {                                              // pair id of (ra, rb) -> code(ra) | code(rb) << 8
-        const uint8_t* rcb = reinterpret_cast<const uint8_t*>(B.freq + kRankIdx);
-        for (int q = t; q < 225; q += kPThreads)
-            ctab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = (uint16_t)(rcb[q / 15] | (rcb[q % 15] << 8));
-    }
-#endif
     stage_wait_all();
     __syncthreads();
-    PairTab T;
-    T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
-#if EQ_PAIR_LUT1
-    T.lut1_s = (uint32_t)__cvta_generic_to_shared(lut1);
-#endif
-    T.fesc = B.freq[kFescIdx];
-    T.cesc = pcum[225];
-    T.esc_lo = T.fesc ? (T.cesc << 20) : 0xFFFFFFFFu;
-    const uint32_t* rk = reinterpret_cast<const uint32_t*>(B.freq + kRankIdx);
-    T.rc0 = rk[0]; T.rc1 = rk[1]; T.rc2 = rk[2]; T.rc3 = rk[3];
-    T.k2p20 = P.k2p20;
-    T.k2p12 = P.k2p12;
-    T.cum = cum;
-    T.cum_s = (uint32_t)__cvta_generic_to_shared(cum);
-#ifdef EQ_PAIR_PROLOGUE_ONLY
-    stage_wait_all();
-    return;                                        // timing experiment: table builds only
-#endif
+    const PairTab T = pair_tab(B.freq, lut, lut1, cum, pcum, P.k2p20, P.k2p12);
     chain_start_w(c);
     chain_finish_p<BF16>(c, B.payload, T);
     stage_wait_all();
@@ -1048,6 +724,7 @@ extern "C" eq_status eq_decode_lanes(uint32_t codec, uint32_t out_dtype, int dev
     }
     int sms = 0, ctas = 0;
     EQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (dyn) EQ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     EQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, threads, dyn));
     *lanes = (uint64_t)sms * (uint64_t)ctas * (uint64_t)per;
     return EQ_OK;

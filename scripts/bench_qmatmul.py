@@ -1,5 +1,7 @@
-"""Config 4: one Llama-3-8B decoder block (7 linears, chunk_symbols 2048 so every K is a
-multiple) — fused decode→tcgen05 GEMM (eq_qmatmul) vs decode-then-cuBLAS, batch 1 and 64."""
+"""Config 4: one Llama-3-8B decoder block (7 linears) — fused decode→tcgen05 GEMM
+(eq_qmatmul_group) vs decode-then-cuBLAS, batch 1 and 64.  Default: the bench's pair codec with
+ROW chunking at 4096 symbols (4096+4096+4096+2048 per down_proj row), i.e. the same encoding
+as config 3; reports the fused launch's decode rate (symbols / s)."""
 import json
 import os
 import sys
@@ -28,18 +30,20 @@ def timed(fn, reps=20, warm=3):
 def main():
     import argparse
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cs", type=int, default=2048)
+    ap.add_argument("--cs", type=int, default=4096)
+    ap.add_argument("--chunk-mode", default="row", choices=["row", "layer"])
     ap.add_argument("--profile", action="store_true", help="one grouped launch per batch (for ncu)")
-    ap.add_argument("--codec", default="word", choices=["byte", "word"])
+    ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"])
     args = ap.parse_args()
-    codec = {"byte": eq.EQ_CODEC_BYTE, "word": eq.EQ_CODEC_WORD}[args.codec]
+    codec = {"byte": eq.EQ_CODEC_BYTE, "word": eq.EQ_CODEC_WORD, "pair": eq.EQ_CODEC_PAIR}[args.codec]
+    mode = {"row": eq.EQ_CHUNK_ROW, "layer": eq.EQ_CHUNK_LAYER}[args.chunk_mode]
     dev = torch.device("cuda")
     Ws = eqsynth.block_weights("llama-3-8b", 0, device=dev)
-    blk = eq.quantize_encode(Ws, lam=230.2, chunk_symbols=args.cs, codec=codec)
+    blk = eq.quantize_encode(Ws, lam=230.2, chunk_symbols=args.cs, codec=codec, chunk_mode=mode)
     dec = eq.Decoder([blk])
-    out = {"workload": f"config4: Llama-3-8B decoder block (q,k,v,o,gate,up,down), chunk {args.cs}, ~2 bits, "
-                       f"{args.codec} codec",
-           "effective_bits": blk.effective_bits()}
+    out = {"workload": f"config4: Llama-3-8B decoder block (q,k,v,o,gate,up,down), chunk {args.cs} "
+                       f"({args.chunk_mode} chunking), ~2 bits, {args.codec} codec",
+           "effective_bits": blk.effective_bits(), "params": blk.n_params, "chunks": blk.n_chunks}
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     for batch in (1, 64):
         xs = [torch.randn(batch, c, device=dev, dtype=torch.bfloat16) * 0.1 for _, c in blk.shapes]
@@ -77,6 +81,8 @@ def main():
         out[f"batch{batch}"] = {"fused_group_ms": timed(fused_group), "fused_chain4_ms": timed(fused_chain),
                                 "fused_per_layer_ms": timed(fused), "decode_then_cublas_ms": timed(unfused),
                                 "dense_bf16_cublas_ms": timed(dense)}
+        out[f"batch{batch}"]["fused_group_decode_Tsym_per_s"] = blk.n_params / out[f"batch{batch}"]["fused_group_ms"] / 1e9
+        out[f"batch{batch}"]["decode_only_ms"] = timed(dec)
         eq.check(err)
         # correctness vs decode + fp32 matmul
         dec()

@@ -49,7 +49,7 @@ def test_rowchunk_encode_byte_identical(codec, cs):
         assert (u16(v) == r).all()
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
 @pytest.mark.parametrize("batch", [1, 64])
 def test_rowchunk_qmatmul_ragged_k(codec, batch):
     """Fused GEMM on a row-chunked layer whose K is not a multiple of the chunk length:
