@@ -72,6 +72,11 @@ __device__ __forceinline__ uint32_t e4m3x2_from_float2(float a, float b) {
     return u;
 }
 
+// Two E4M3 codes as cvt.rn.satfinite.e4m3x2.f32 gives them (−0 kept as 0x80)
+__device__ __forceinline__ uint32_t e4m3x2_sat(float a, float b) {
+    return (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+}
+
 // Two E4M3 codes (packed lo/hi byte) to two exact floats via the f16 path (exact).
 __device__ __forceinline__ float2 e4m3x2_to_float2(uint32_t pair) {
     __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(pair & 0xFFFFu), __NV_E4M3);

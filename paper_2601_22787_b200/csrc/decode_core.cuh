@@ -342,11 +342,21 @@ __device__ __forceinline__ void store16_bf16_at(C& c, const uint32_t q[4], uint8
 // (Measured alternatives: a 128-byte ring with 3 groups in flight — 4 instead of 6 CTAs/SM,
 // −4 %; whole 32-byte sectors every 16 steps — the 2-slot ring then has to wait for the
 // sector it just issued, −10 %.)
-constexpr uint32_t kWRing = 64;
+#ifndef EQ_WRING
+#define EQ_WRING 64      // bytes per lane (64 for the throughput-bound stand-alone decoders; the fused
+                         // GEMM, latency-bound with few resident chains, stages further ahead)
+#endif
+constexpr uint32_t kWRing = EQ_WRING;
+static_assert(kWRing == 64 || kWRing == 128 || kWRing == 256, "ring size");
 // Ring addressing: payload byte p lives at ring | ((p + kWBias) & 63), and the reader keeps
 // Q = (payload offset of the next word) + kWBias, so a word address is one LOP3 and the test
 // "slot of segment gn is free" (all bytes < gn − 48 consumed: gn ≤ q + 48) is gn ≤ Q.
 constexpr uint32_t kWBias = kWRing - 16;
+// A segment issued at a boundary starts > (read offset) + kWRing − 32 (the stage front keeps pace:
+// ≤ 16 bytes consumed and ≤ one segment staged per boundary) and the steps after a boundary
+// read < 18 bytes ahead, so it is first needed kWRing/16 − 3 boundaries later: that many newer
+// groups may stay in flight (64-byte ring: 1, 128: 5).
+constexpr int kWWaitGroups = (int)(kWRing / 16) - 3;
 
 struct WordReader {
     uint32_t Q;            // payload byte offset of the next word to load into w, + kWBias
@@ -381,8 +391,9 @@ __device__ __forceinline__ void ring_step_w(WordReader& r, const uint8_t* payloa
                  "@p cp.async.cg.shared.global.L2::128B [%2], [%3], 16;\n\t"
                  "@p add.u32 %0, %0, 16; }\n\t"
                  "cp.async.commit_group;\n\t"
-                 "cp.async.wait_group 1;"
-                 : "+r"(r.gn) : "r"(r.Q), "r"(r.ring | ((r.gn + kWBias) & (kWRing - 1))), "l"(payload + r.gn)
+                 "cp.async.wait_group %4;"
+                 : "+r"(r.gn) : "r"(r.Q), "r"(r.ring | ((r.gn + kWBias) & (kWRing - 1))), "l"(payload + r.gn),
+                   "n"(kWWaitGroups)
                  : "memory");
 #else
     asm volatile("cp.async.wait_all;\n\t"

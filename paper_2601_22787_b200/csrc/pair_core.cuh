@@ -72,7 +72,11 @@ __device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, 
     return s;
 }
 
-// one pair step; returns the two codes in the low 16 bits (first symbol in the low byte)
+// one pair step; returns the two codes in the low 16 bits (first symbol in the low byte).
+// NARROW: the LUT entry holds 2·id | (slot − c) << 9 | (f − 1) << 20 (every kept pair has f ≤ 2048,
+// pair_tables_build decides per block), so the codes-table offset is one LOP3 (e & 0x1FE)
+// instead of an add and a mask; otherwise id | (slot − c) << 8 | (f − 1) << 20.
+template <bool NARROW = false>
 __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, const PairTab& T, const uint8_t* payload) {
     uint32_t lo, xs;
     asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
@@ -86,6 +90,11 @@ __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, cons
     }
     const uint32_t e = lds_u32(T.lut_s + (lo >> 18));
     const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
+    if (NARROW) {
+        x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 21));       // f·⌊x/M⌋ + slot − c
+        renorm_w(x, r);
+        return lds_u16(T.lut_s + 4 * kM + (e & 0x1FEu));                // 2·id -> codes
+    }
     x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));           // f·⌊x/M⌋ + slot − c
     renorm_w(x, r);
     return lds_u16(T.lut_s + 4 * kM + ((e & 0xFFu) << 1));              // pair id -> codes
@@ -121,12 +130,14 @@ __device__ __forceinline__ void lut_walk(uint32_t* lut, const uint32_t* cm, F en
 // (it holds the barriers); threads t < NT (NT ≥ 64, a power of two ≤ 1024) do the work: the
 // single cum by a block scan, the pair cum (226 entries: kept pairs in (ra, rb) order, then the
 // escape) by warp 0, then the LUT walks and the codes table.  The caller waits for the table
-// stores (a barrier) before decoding.  Returns false on every thread for a corrupt table
-// (EQ_EF_CORRUPT set once).
+// stores (a barrier) before decoding.  Returns 0 on every thread for a corrupt table
+// (EQ_EF_CORRUPT set once), else 1 (LUT entries id | (slot − c) << 8 | (f − 1) << 20) or, with
+// NARROW_OK and every kept pair's f ≤ 2048, 2 (entries 2·id | (slot − c) << 9 | (f − 1) << 20).
+// (Only the rank-(0,0) pair can exceed 2048 slots, when p(rank 0)² > ½.)
 // (This sequence keeps the table bases in uniform registers through the decode loop; a variant
 // scanning both tables concurrently made ptxas rematerialise them per pair step, −1.6 %.)
-template <int NT, bool ALL = false>                  // ALL: the CTA has exactly NT threads
-__device__ __forceinline__ bool pair_tables_build(const uint16_t* freq, uint32_t* lut, uint8_t* lut1,
+template <int NT, bool ALL = false, bool NARROW_OK = false>   // ALL: the CTA has exactly NT threads
+__device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint32_t* lut, uint8_t* lut1,
                                                   uint32_t* cum, uint32_t* pcum, uint32_t* err) {
     static_assert(NT >= 64 && (NT & (NT - 1)) == 0 && NT <= 1024, "thread count");
     const int t = threadIdx.x;
@@ -159,17 +170,21 @@ __device__ __forceinline__ bool pair_tables_build(const uint16_t* freq, uint32_t
     __syncthreads();
     if (cum[256] != kM) {
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
-        return false;
+        return 0;
     }
     const uint32_t K = freq[kKIdx];
+    __shared__ uint32_t s_fmax;
     if (t < 32) {                                  // 226-entry pair cum: (ra, rb) order, escape last
-        uint32_t v[8], s = 0;
+        uint32_t v[8], s = 0, fmax = 0;
         #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int q = t * 8 + j;
             v[j] = (q < 225 && (uint32_t)(q / 15) < K && (uint32_t)(q % 15) < K) ? freq[kPairOff + q] : 0u;
             s += v[j];
+            fmax = max(fmax, v[j]);
         }
+        fmax = __reduce_max_sync(0xFFFFFFFFu, fmax);
+        if (t == 0) s_fmax = fmax;
         uint32_t inc = s;
         #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -191,13 +206,16 @@ __device__ __forceinline__ bool pair_tables_build(const uint16_t* freq, uint32_t
     __syncthreads();
     if (pcum[226] != kM || K > 15) {
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
-        return false;
+        return 0;
     }
+    const bool narrow = NARROW_OK && s_fmax <= 2048u;
     if (ALL || t < NT) {
+        // (escape slots keep id 0xFF; their entries are never read: the escape test precedes the lookup)
+        const uint32_t idsh = narrow ? 1u : 0u, scsh = narrow ? 9u : 8u;
         lut_walk<226, NT>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
             const uint32_t f = pcum[q + 1] - pcum[q];
             const uint32_t id = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : 0xFFu;
-            return id | ((slot - pcum[q]) << 8) | ((f - 1) << 20);
+            return (id << idsh) | ((slot - pcum[q]) << scsh) | ((f - 1) << 20);
         });
         constexpr uint32_t SP = kM / NT;           // symbol per slot: thread t fills [SP·t, SP·t + SP)
         const uint32_t s0 = SP * (uint32_t)t;
@@ -221,7 +239,7 @@ __device__ __forceinline__ bool pair_tables_build(const uint16_t* freq, uint32_t
         for (int q = t; q < 225; q += NT)
             ctab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = (uint16_t)(rcb[q / 15] | (rcb[q % 15] << 8));
     }
-    return true;
+    return narrow ? 2u : 1u;
 }
 
 __device__ __forceinline__ PairTab pair_tab(const uint16_t* freq, const uint32_t* lut, const uint8_t* lut1,

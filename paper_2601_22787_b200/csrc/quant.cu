@@ -96,6 +96,28 @@ __device__ __forceinline__ void term2(float w0, float w1, float s, double& D, ui
     R += (uint32_t)__fmul_rn(fabsf(v.x), 512.f) + (uint32_t)__fmul_rn(fabsf(v.y), 512.f);
 }
 
+#ifndef EQ_SEARCH_FAST
+#define EQ_SEARCH_FAST 1
+#endif
+// Division-free E4M3 term pair (same codes as term2).  For bf16 w and s the
+// exact quotient w/s is never within 2^-13 (relative) of an E4M3 rounding midpoint unless it
+// equals one (§8c.3; pinned by the oracle tests).  q± = w·fl(fl(1/s)·(1 ± 2^-18)) lie within
+// 2^-18 ± 3·2^-24 of w/s, strictly above / below it: off a midpoint both round like w/s; on a
+// midpoint they round to the two neighbours and RNE takes the even one (the code with LSB 0).
+// (The sign of a zero code does not matter here: ±0 give the same |w − s·v| and |v|.)
+// R accumulates |v|·512 + 2^23 as f32 bits (exact integers < 2^23): the caller subtracts
+// 0x4B000000 per term once.
+__device__ __forceinline__ void term2_fast(float w0, float w1, float s, float rp, float rm, double& D, uint32_t& R) {
+    const uint32_t cp = e4m3x2_sat(__fmul_rn(w0, rp), __fmul_rn(w1, rp));
+    const uint32_t cm = e4m3x2_sat(__fmul_rn(w0, rm), __fmul_rn(w1, rm));
+    const uint32_t odd = (cp & 0x0101u) * 0xFFu;                  // bytes of cp with LSB 1
+    const uint32_t q = cp ^ ((cp ^ cm) & odd);                    // a tie byte takes the even code
+    const float2 v = e4m3x2_to_float2(q);
+    D += (double)fabsf(__fsub_rn(w0, __fmul_rn(s, v.x)));
+    D += (double)fabsf(__fsub_rn(w1, __fmul_rn(s, v.y)));
+    R += __float_as_uint(__fmaf_rn(fabsf(v.x), 512.f, 8388608.f)) + __float_as_uint(__fmaf_rn(fabsf(v.y), 512.f, 8388608.f));
+}
+
 __device__ __forceinline__ bool better(double f, uint32_t k, double bf, uint32_t bk) {
     return f < bf || (f == bf && k < bk);
 }
@@ -159,9 +181,22 @@ k_search(const __grid_constant__ SearchParams P) {
         const float s = bf16_bits_to_float((uint32_t)(lo + (int)k));
         double D = 0.0;
         uint32_t R = 0;
-        for (int64_t p = lane; p < npair; p += 32) {
-            const float2 w = reinterpret_cast<const float2*>(srow)[p];
-            term2<FMT>(w.x, w.y, s, D, R);
+        // fast path: E4M3 and fl(1/s) normal with margin (uniform per warp: one candidate)
+        if (EQ_SEARCH_FAST && FMT == EQ_FMT_E4M3 && s >= 0x1p-124f && s <= 0x1p124f) {
+            const float r = __frcp_rn(s);
+            const float rp = __fmul_rn(r, 1.0f + 0x1p-18f), rm = __fmul_rn(r, 1.0f - 0x1p-18f);
+            uint32_t nt = 0;
+            for (int64_t p = lane; p < npair; p += 32) {
+                const float2 w = reinterpret_cast<const float2*>(srow)[p];
+                term2_fast(w.x, w.y, s, rp, rm, D, R);
+                nt += 2;
+            }
+            R -= nt * 0x4B000000u;                                // modulo 2^32: the exact Σ|v|·512
+        } else {
+            for (int64_t p = lane; p < npair; p += 32) {
+                const float2 w = reinterpret_cast<const float2*>(srow)[p];
+                term2<FMT>(w.x, w.y, s, D, R);
+            }
         }
         unsigned long long R64 = R;                 // a 28672-wide row overflows u32
         #pragma unroll

@@ -555,20 +555,79 @@ k_decode_w(const __grid_constant__ DecParams P) {
 
 
 // ================================================================ EQ_CODEC_PAIR decoder (R15)
+#ifndef EQ_PAIR_LOOP2
+#define EQ_PAIR_LOOP2 1
+#endif
 // Same CTA ↔ block and lane ↔ chunk mapping and staging as k_decode_w; the pair tables and the
 // pair / single decode steps are in pair_core.cuh (shared with the fused GEMM).
-template <bool BF16>
+template <bool BF16, bool NARROW>
 __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload, const PairTab& T) {
     if (!c.active || c.runaway) return;
     const uint32_t qlim = c.e + (2 + kWBias);
+#if EQ_PAIR_LOOP2
+    if (c.fast) {
+        // group loop with a down-counter and a running 32-byte output pointer; the runaway test
+        // shares the loop test; the f16-scale dequant (the usual case) is tested first
+        constexpr uint32_t G = BF16 ? 16 : 32;
+        const uint32_t ng0 = (c.n - c.i) / G;
+        const bool tail = c.i + ng0 * G < c.n;     // symbols after the groups (they need the row's scale)
+        uint32_t ng = ng0;
+        uint8_t* o = c.out + (uint64_t)c.i * (BF16 ? 2 : 1);
+        uint32_t s16 = c.i8 ? 0u : (uint32_t)c.s16;
+        while (ng != 0 && c.r.Q <= qlim) {
+            uint32_t q[8];
+            #pragma unroll
+            for (int k = 0; k < (BF16 ? 4 : 8); ++k) {
+                const uint32_t a = decode_pair<NARROW>(c.x, c.r, T, payload);
+                const uint32_t b = decode_pair<NARROW>(c.x, c.r, T, payload);
+                q[k] = __byte_perm(a, b, 0x5410);
+                if ((k & 3) == 3) ring_step_w(c.r, payload);
+            }
+            if (BF16) {
+                uint4 lo, hi;
+                if (s16) {
+                    const uint16_t h = (uint16_t)s16;
+                    lo = make_uint4(dequant2_h(q[0], h), dequant2_h(q[0] >> 16, h), dequant2_h(q[1], h), dequant2_h(q[1] >> 16, h));
+                    hi = make_uint4(dequant2_h(q[2], h), dequant2_h(q[2] >> 16, h), dequant2_h(q[3], h), dequant2_h(q[3] >> 16, h));
+                } else if (c.i8) {
+                    lo = make_uint4(dequant2_i8(q[0], c.s), dequant2_i8(q[0] >> 16, c.s), dequant2_i8(q[1], c.s),
+                                    dequant2_i8(q[1] >> 16, c.s));
+                    hi = make_uint4(dequant2_i8(q[2], c.s), dequant2_i8(q[2] >> 16, c.s), dequant2_i8(q[3], c.s),
+                                    dequant2_i8(q[3] >> 16, c.s));
+                } else {
+                    lo = make_uint4(dequant2(q[0], c.s), dequant2(q[0] >> 16, c.s), dequant2(q[1], c.s), dequant2(q[1] >> 16, c.s));
+                    hi = make_uint4(dequant2(q[2], c.s), dequant2(q[2] >> 16, c.s), dequant2(q[3], c.s), dequant2(q[3] >> 16, c.s));
+                }
+                st_out32(o, lo, hi);
+                c.col += 16;
+                if (c.col >= c.cols) {                 // next row: its scale (unless this was the last group)
+                    c.col -= c.cols;
+                    ++c.row;
+                    if (ng > 1 || tail) {
+                        c.s = bf16_bits_to_float(c.sc[c.row]);
+                        s16 = c.i8 ? 0u : (uint32_t)scale_f16(c.s);
+                    }
+                }
+            } else {
+                st_out32(o, make_uint4(q[0], q[1], q[2], q[3]), make_uint4(q[4], q[5], q[6], q[7]));
+            }
+            o += 32;
+            --ng;
+        }
+        c.i += (ng0 - ng) * G;
+        if (ng != 0) { c.runaway = true; return; }
+        c.s16 = (uint16_t)s16;
+        if (c.r.Q > qlim) { c.runaway = true; return; }
+    }
+#else
     if (c.fast) {
         const uint32_t G = BF16 ? 16 : 32;
         while (c.i + G <= c.n) {
             uint32_t q[8];
             #pragma unroll
             for (int k = 0; k < (BF16 ? 4 : 8); ++k) {
-                const uint32_t a = decode_pair(c.x, c.r, T, payload);
-                const uint32_t b = decode_pair(c.x, c.r, T, payload);
+                const uint32_t a = decode_pair<NARROW>(c.x, c.r, T, payload);
+                const uint32_t b = decode_pair<NARROW>(c.x, c.r, T, payload);
                 q[k] = __byte_perm(a, b, 0x5410);
                 if ((k & 3) == 3) ring_step_w(c.r, payload);
             }
@@ -578,9 +637,10 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
             if (c.r.Q > qlim) { c.runaway = true; return; }
         }
     }
+#endif
     uint32_t k = 0;                                // generic / ragged tail
     for (; c.i + 2 <= c.n; c.i += 2) {
-        const uint32_t ab = decode_pair(c.x, c.r, T, payload);
+        const uint32_t ab = decode_pair<NARROW>(c.x, c.r, T, payload);
         if ((++k & 7) == 0) ring_step_w(c.r, payload);
         #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -600,6 +660,9 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
     }
 }
 
+#ifndef EQ_PAIR_NARROW
+#define EQ_PAIR_NARROW 1            // 2·id LUT entries when every kept pair has f ≤ 2048 (one add fewer per pair)
+#endif
 #ifndef EQ_PTHREADS
 #define EQ_PTHREADS 256             // chunks (= threads) per CTA of k_decode_p
 #endif
@@ -625,7 +688,8 @@ k_decode_p(const __grid_constant__ DecParams P) {
     chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kPThreads + t,
                         (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
     stage_commit();
-    if (!pair_tables_build<kPThreads, true>(B.freq, lut, lut1, cum, pcum, P.err)) {
+    const uint32_t mode = pair_tables_build<kPThreads, true, EQ_PAIR_NARROW>(B.freq, lut, lut1, cum, pcum, P.err);
+    if (!mode) {
         stage_wait_all();
         return;
     }
@@ -633,7 +697,8 @@ k_decode_p(const __grid_constant__ DecParams P) {
     __syncthreads();
     const PairTab T = pair_tab(B.freq, lut, lut1, cum, pcum, P.k2p20, P.k2p12);
     chain_start_w(c);
-    chain_finish_p<BF16>(c, B.payload, T);
+    if (EQ_PAIR_NARROW && mode == 2) chain_finish_p<BF16, true>(c, B.payload, T);    // CTA-uniform
+    else chain_finish_p<BF16, false>(c, B.payload, T);
     stage_wait_all();
     if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
 }

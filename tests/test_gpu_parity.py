@@ -208,6 +208,27 @@ def test_search_vs_oracle(lam):
     assert np.mean(S == S_or) > 0.95
 
 
+@pytest.mark.parametrize("lam", [0.0, 100.0])
+def test_search_exact_midpoint_ties(lam):
+    """Rows whose quotients w/s are EXACT E4M3 rounding midpoints (ties, §8c.3: RNE takes the
+    even code) at the single candidate s = s0 = 2^k (bracket [0, 0]): the GPU objective of that
+    candidate — the division-free search decides ties by two perturbed products — equals the
+    oracle's exact-quotient objective.  A tie rounded away from even changes R = Σ|v|."""
+    vals = sorted({o.e4m3_value(c) for c in range(0x7F)})            # 0 .. 448
+    mids = [(a + b) / 2 for a, b in zip(vals[:-1], vals[1:])]         # 126 midpoints, exact in bf16
+    rows = []
+    for k in (-6, -2, 0, 3):
+        r = [448.0] + mids + [-m for m in mids] + [3.0, -0.5, 100.0]
+        rows.append(np.array(r[:256] + [0.0] * (256 - len(r)), dtype=np.float64) * 2.0 ** k)
+    W = torch.from_numpy(np.stack(rows)).to(torch.bfloat16)
+    assert torch.equal(W.double(), torch.from_numpy(np.stack(rows)))  # exact in bf16
+    _, ob = eq.search_scales(W.to(DEV), [lam], oct_lo=0, oct_hi=0, with_obj=True)
+    for r in range(4):
+        first, f = o.row_objectives(W, r, lam, 0, 0)
+        assert f.size == 1
+        assert float(ob[0, r]) == pytest.approx(f[0], rel=1e-12), r
+
+
 def test_search_multi_lambda_and_row_subset():
     W = eqsynth.weights(40, 256, seed=7, dist="mix")
     lams = [0.0, 10.0, 100.0, 400.0]
