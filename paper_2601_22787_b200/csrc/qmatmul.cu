@@ -21,6 +21,8 @@
 // [j][b][row] (or Y directly when a row is one chunk); k_qmm_reduce sums the partials in a
 // fixed order (deterministic split-K).
 #include "common.cuh"
+// (EQ_WRING = 128, five segments in flight per decoder lane, measured: same time at batch 1, and
+// at batch 64 the extra 8 KB per CTA leaves 2 CTAs/SM, 0.29 -> 0.45 ms; profiles/r2/s1qmm)
 #include "decode_core.cuh"
 #include "pair_core.cuh"
 
@@ -426,6 +428,9 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 #ifndef EQ_QMM_WS_MIN_CTAS
 #define EQ_QMM_WS_MIN_CTAS 3
 #endif
+#ifndef EQ_QMM_NARROW
+#define EQ_QMM_NARROW 1                        // pair codec: 2·id LUT entries when every kept pair has f ≤ 2048
+#endif
 constexpr int kWsStages = EQ_QMM_WS_STAGES;
 constexpr int kWsK = 32;                       // K columns per step (one SWIZZLE_64B row = 64 B)
 constexpr int kWsRowB = kWsK * 2;
@@ -525,12 +530,14 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
     PairTab PT{};
     DecTable WT{};
     bool ok;
+    uint32_t mode = 1;                             // pair codec: 2 = narrow LUT entries (2·id)
     if constexpr (CODEC == EQ_CODEC_PAIR) {
         uint32_t* lut = reinterpret_cast<uint32_t*>(tabs);
         uint8_t* lut1 = tabs + kPairLutWords * 4;
         uint32_t* cum = reinterpret_cast<uint32_t*>(lut1 + kM);
         uint32_t* pcum = cum + 257;
-        ok = pair_tables_build<kWsDec>(P.freq, lut, lut1, cum, pcum, P.err);
+        mode = pair_tables_build<kWsDec, false, EQ_QMM_NARROW>(P.freq, lut, lut1, cum, pcum, P.err);
+        ok = mode != 0;
         __syncthreads();                           // table stores visible to every decoder lane
         if (ok) PT = pair_tab(P.freq, lut, lut1, cum, pcum, P.k2p20, P.k2p12);
     } else {
@@ -641,42 +648,68 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
         const uint32_t row_off = (r >> 3) * 512u + (r & 7) * (uint32_t)kWsRowB;
         const uint32_t sw = (r >> 1) & 3;                         // SWIZZLE_64B: 16-byte chunk q at q ^ sw
         const uint32_t qlim = c.e + (2u + kWBias);
-        for (uint32_t st = 0; st < steps; ++st) {
-            const uint32_t sidx = st % kWsStages, use = st / kWsStages;
-            if (st >= (uint32_t)kWsStages) mbar_wait(smem_u32(&bars[kWsStages + sidx]), (use - 1) & 1);
-            const uint32_t arow = smem_u32(a_st + sidx * kWsATile) + row_off;
-            const bool live = c.active && !c.runaway;
-            #pragma unroll
-            for (uint32_t g = 0; g < kWsK / 8; ++g) {             // 4 × 8 symbols -> 16 bytes each
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (live) {
-                    uint32_t q0, q1;
-                    if constexpr (CODEC == EQ_CODEC_PAIR) {
-                        const uint32_t p0 = decode_pair(c.x, c.r, PT, P.payload);
-                        const uint32_t p1 = decode_pair(c.x, c.r, PT, P.payload);
-                        const uint32_t p2 = decode_pair(c.x, c.r, PT, P.payload);
-                        const uint32_t p3 = decode_pair(c.x, c.r, PT, P.payload);
-                        q0 = __byte_perm(p0, p1, 0x5410);
-                        q1 = __byte_perm(p2, p3, 0x5410);
-                        if (g & 1) ring_step_w(c.r, P.payload);   // one stage per 8 pair steps
-                    } else {
-                        q0 = decode4_w(c, WT);
-                        q1 = decode4_w(c, WT);
-                        ring_step_w(c.r, P.payload);              // one stage per 8 steps
+        const uint32_t a0 = smem_u32(a_st) + row_off;
+        // one K step = 32 symbols of the lane's chain into 4 × 16 bytes of its A row; branches
+        // once per step (live chain, scale mode), stage index / phase by counters
+        auto run = [&](auto narrow_c) {
+            constexpr bool NARROW = decltype(narrow_c)::value;
+            static_assert(CODEC == EQ_CODEC_PAIR || !NARROW, "narrow entries are a pair-codec layout");
+            const uint32_t s16 = c.i8 ? 0u : (uint32_t)c.s16;
+            uint32_t sidx = 0, use = 0;
+            for (uint32_t st = 0; st < steps; ++st) {
+                if (st >= (uint32_t)kWsStages) mbar_wait(smem_u32(&bars[kWsStages + sidx]), (use & 1) ^ 1);
+                const uint32_t arow = a0 + sidx * kWsATile;
+                uint4 v[kWsK / 8];
+                if (c.active && !c.runaway) {
+                    uint32_t q[kWsK / 4];
+                    #pragma unroll
+                    for (uint32_t g = 0; g < kWsK / 8; ++g) {
+                        if constexpr (CODEC == EQ_CODEC_PAIR) {
+                            const uint32_t p0 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                            const uint32_t p1 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                            const uint32_t p2 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                            const uint32_t p3 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                            q[2 * g] = __byte_perm(p0, p1, 0x5410);
+                            q[2 * g + 1] = __byte_perm(p2, p3, 0x5410);
+                            if (g & 1) ring_step_w(c.r, P.payload);   // one stage per 8 pair steps
+                        } else {
+                            q[2 * g] = decode4_w(c, WT);
+                            q[2 * g + 1] = decode4_w(c, WT);
+                            ring_step_w(c.r, P.payload);              // one stage per 8 steps
+                        }
                     }
-                    v = dequant8(c, q0, q1);
+                    if (s16) {
+                        const uint16_t h = (uint16_t)s16;
+                        #pragma unroll
+                        for (uint32_t g = 0; g < kWsK / 8; ++g)
+                            v[g] = make_uint4(dequant2_h(q[2 * g], h), dequant2_h(q[2 * g] >> 16, h),
+                                              dequant2_h(q[2 * g + 1], h), dequant2_h(q[2 * g + 1] >> 16, h));
+                    } else {
+                        #pragma unroll
+                        for (uint32_t g = 0; g < kWsK / 8; ++g) v[g] = dequant8(c, q[2 * g], q[2 * g + 1]);
+                    }
+                    c.i += kWsK;
+                    if (c.r.Q > qlim) c.runaway = true;           // overran its chunk: stop reading
+                } else {
+                    #pragma unroll
+                    for (uint32_t g = 0; g < kWsK / 8; ++g) v[g] = make_uint4(0, 0, 0, 0);
                 }
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + ((g ^ sw) << 4)), "r"(v.x),
-                             "r"(v.y), "r"(v.z), "r"(v.w)
-                             : "memory");
+                #pragma unroll
+                for (uint32_t g = 0; g < kWsK / 8; ++g)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + ((g ^ sw) << 4)), "r"(v[g].x),
+                                 "r"(v[g].y), "r"(v[g].z), "r"(v[g].w)
+                                 : "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bars[sidx]));
+                if (++sidx == (uint32_t)kWsStages) { sidx = 0; ++use; }
             }
-            if (live) {
-                c.i += kWsK;
-                if (c.r.Q > qlim) c.runaway = true;               // overran its chunk: stop reading
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bars[sidx]));
+        };
+        if constexpr (CODEC == EQ_CODEC_PAIR && EQ_QMM_NARROW) {
+            if (mode == 2) run(std::true_type{});                 // CTA-uniform
+            else run(std::false_type{});
+        } else {
+            run(std::false_type{});
         }
         stage_wait_all();
         if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
