@@ -42,6 +42,7 @@ DEFAULT_LAMBDA = 230.2               # reference arm only: the GPU calibration o
 
 
 CODECS = {"byte": 0, "word": 1, "pair": 2}     # EQ_CODEC_* (include/entquant.h)
+CHUNK_MODES = {"layer": 0, "row": 1}            # EQ_CHUNK_* (include/entquant.h, R16)
 
 
 def parse():
@@ -66,6 +67,9 @@ def parse():
     ap.add_argument("--no-stats", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
+    ap.add_argument("--chunk-mode", default="row", choices=["layer", "row"],
+                    help="chunk restarts (R16): row (default; every row start too, so the same streams feed "
+                         "the decode-fused GEMM of config 4) or layer (R10)")
     ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"],
                     help="wire format: byte rANS (SPEC S:355, R9), 16-bit-word rANS (R14), or the word "
                          "rANS over symbol pairs with escapes (R15, default: fastest, smallest)")
@@ -218,21 +222,27 @@ def share_ids(args, rank: int, world: int):
 
 
 def choose_chunk(args, layer_ids, lanes: int) -> int:
-    """Chunk length for the rank's share: a launch runs ceil(chunks / lanes)
+    """Chunk length for the rank's share: a launch runs about chunks / lanes
     rounds of one serial chunk-length chain, so a share of 1.1 rounds at 4096 symbols wastes
-    almost half the GPU.  Among 4096 / 2048 / 1024 take the one with the shortest
-    rounds × (length + per-chunk overhead); 4096 (the smallest rate) wins ties."""
+    almost half the GPU.  Measured rule: 4096 (the smallest rate) when the share is ≥ 4 rounds
+    of it; one round at 4608 when that fits (the 4-block share at G = 8: 0.549 vs 0.543 at
+    1024; other non-power-of-two lengths measured slower); otherwise 2048 or 1024, whichever
+    gives the shorter ceil(rounds) × (length + per-chunk overhead)."""
     import eqsynth
     if args.chunk_symbols:
         return args.chunk_symbols
-    sizes = [r * c for r, c in eqsynth.block_shapes(args.model)] * len(layer_ids)
-    best, best_t = 4096, None
-    for cs in (4096, 2048, 1024):
-        n = sum((x + cs - 1) // cs for x in sizes)
-        t = -(-n // lanes) * (cs + CHUNK_OVERHEAD_SYMBOLS)
-        if best_t is None or t < best_t:
-            best, best_t = cs, t
-    return best
+    shapes = list(eqsynth.block_shapes(args.model)) * len(layer_ids)
+
+    def n_chunks(cs):
+        if args.chunk_mode == "row":
+            return sum(r * ((c + cs - 1) // cs) for r, c in shapes)
+        return sum((r * c + cs - 1) // cs for r, c in shapes)
+    r4096 = n_chunks(4096) / lanes
+    if r4096 >= 4:
+        return 4096
+    if r4096 <= 1.25 and n_chunks(4608) <= lanes:
+        return 4608
+    return min((2048, 1024), key=lambda cs: -(-n_chunks(cs) // lanes) * (cs + CHUNK_OVERHEAD_SYMBOLS))
 
 
 CHUNK_OVERHEAD_SYMBOLS = 256        # per-chunk setup (staging, table-build share, stores) in symbol-steps
@@ -247,7 +257,7 @@ def encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist=None):
     if lam is None:
         calib = eqsynth.block_weights(args.model, 0, device=dev)
         lam, est = eq.calibrate_lambda(calib, args.target_bits, row_stride=args.calib_stride, chunk_symbols=cs,
-                                       codec=CODECS[args.codec])
+                                       codec=CODECS[args.codec], chunk_mode=CHUNK_MODES[args.chunk_mode])
         del calib
     if dist is not None:
         t = torch.tensor([lam], dtype=torch.float64, device=dev)
@@ -257,9 +267,11 @@ def encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist=None):
     for lid in layer_ids:
         Ws = eqsynth.block_weights(args.model, lid, device=dev)
         if scratch is None:
-            _, _, sb = eq.encode_bounds(Ws, chunk_symbols=cs)
+            _, _, sb = eq.encode_bounds(Ws, chunk_symbols=cs, codec=CODECS[args.codec],
+                                        chunk_mode=CHUNK_MODES[args.chunk_mode])
             scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch, chunk_symbols=cs, codec=CODECS[args.codec]))
+        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch, chunk_symbols=cs, codec=CODECS[args.codec],
+                                         chunk_mode=CHUNK_MODES[args.chunk_mode]))
         del Ws
     del scratch
     torch.cuda.synchronize()
@@ -272,7 +284,7 @@ def workload_config(args, n_blocks, n_params, cs, world):
                     f"{n_blocks} blocks per rank, ~{args.target_bits} effective bits/param, chunk-parallel rANS "
                     f"decode + fused dequant to bf16",
         "model_shapes": args.model, "blocks_per_rank": n_blocks, "params_per_rank": n_params,
-        "chunk_symbols": cs, "codec": args.codec, "target_bits": args.target_bits,
+        "chunk_symbols": cs, "chunk_mode": args.chunk_mode, "codec": args.codec, "target_bits": args.target_bits,
         "l2": "inputs larger than L2 (compressed in + decoded out per step >> 126 MB); no flush",
         "parallelism": f"block-sharded x{world} ({args.scaling}, contiguous ranges)" if args.scaling == "strong"
                        else f"block-sharded x{world} (weak)",
@@ -296,8 +308,9 @@ def oracle_layers(blk, o):
     pair = oracle_pair_table(table, o) if blk.codec == CODECS["pair"] else None
     scales = blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)
     out, k0, r0 = [], 0, 0
+    row = getattr(blk, "chunk_mode", 0) == CHUNK_MODES["row"]
     for (r, c) in blk.shapes:
-        nk = (r * c + cs - 1) // cs
+        nk = r * ((c + cs - 1) // cs) if row else (r * c + cs - 1) // cs
         out.append((off_all[k0:k0 + nk + 1], r, c, scales[r0:r0 + r]))
         k0 += nk
         r0 += r
@@ -332,7 +345,7 @@ def run_reference(args, rank, world):
 
     def one_pass():
         for off, rr, c, S in layers:
-            o.decode_dequant_layer_mt(payload, off, cs, rr, c, S, freq, threads, blk.codec, pair)
+            o.decode_dequant_layer_mt(payload, off, cs, rr, c, S, freq, threads, blk.codec, pair, blk.chunk_mode)
 
     bytes_pass = blk.compressed_bytes() + 2 * blk.n_params
     for _ in range(args.warmup):
@@ -606,7 +619,8 @@ def cpu_baseline(blocks, dec, seconds: float):
         for (off, r, c, S), v in zip(lay, vb):
             nk = off.size - 1
             t = time.perf_counter()
-            out = o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, freq, threads, blk.codec, pair)
+            out = o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, freq, threads, blk.codec, pair,
+                                            blk.chunk_mode)
             wall += time.perf_counter() - t
             gpu = v.contiguous().view(torch.int16).cpu().numpy().view(np.uint16).reshape(r, c)
             mism += int(np.count_nonzero(np.asarray(out).reshape(r, c) != gpu))
@@ -623,7 +637,7 @@ def cpu_baseline(blocks, dec, seconds: float):
     payload, freq, pair, lay = oracle_layers(blk, o)
     off, r, c, S = lay[0]
     t = time.perf_counter()
-    o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, freq, 1, blk.codec, pair)
+    o.decode_dequant_layer_mt(payload, off, blk.chunk_symbols, r, c, S, freq, 1, blk.codec, pair, blk.chunk_mode)
     w1 = time.perf_counter() - t
     b1 = int(off[-1] - off[0]) + 4 * off.size + 2 * r + 2 * r * c
     cpu = {"value": done_bytes / wall / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",

@@ -25,6 +25,9 @@ EQ_OK, EQ_ERR_ARG, EQ_ERR_SHAPE, EQ_ERR_EMPTY, EQ_ERR_BUFFER = 0, 1, 2, 3, 4
 EQ_ERR_CORRUPT, EQ_ERR_TRUNCATED, EQ_ERR_UNKNOWN_SYMBOL, EQ_ERR_UNREACHABLE_TARGET, EQ_ERR_CUDA = 5, 6, 7, 8, 9
 EQ_FMT_E4M3, EQ_FMT_INT8 = 0, 1
 EQ_CODEC_BYTE, EQ_CODEC_WORD, EQ_CODEC_PAIR = 0, 1, 2
+# The binding's default codec: the pair codec (R15), the fastest decoder and the lowest rate.
+# The C ABI's zero-initialised eq_params keep SPEC's byte codec (R9); pass codec= for it here.
+EQ_DEFAULT_CODEC = EQ_CODEC_PAIR
 EQ_OUT_FP8, EQ_OUT_BF16 = 0, 1
 EQ_CHUNK_LAYER, EQ_CHUNK_ROW = 0, 1
 EQ_SCALES_SEARCH, EQ_SCALES_ABSMAX, EQ_SCALES_GIVEN = 0, 1, 2
@@ -232,7 +235,7 @@ class Block:
         return self.compressed_bytes()
 
 
-def encode_bounds(layers, chunk_symbols=EQ_DEFAULT_CHUNK, codec: int = EQ_CODEC_BYTE, chunk_mode: int = EQ_CHUNK_LAYER):
+def encode_bounds(layers, chunk_symbols=EQ_DEFAULT_CHUNK, codec: int = EQ_DEFAULT_CODEC, chunk_mode: int = EQ_CHUNK_LAYER):
     ts = (eq_tensor * len(layers))(*[eq_tensor(0 if not W.is_cuda else W.data_ptr(), W.shape[0], W.shape[1]) for W in layers])
     for i, W in enumerate(layers):
         ts[i].w = 1 if ts[i].w == 0 else ts[i].w       # sizing does not dereference
@@ -246,7 +249,7 @@ def encode_bounds(layers, chunk_symbols=EQ_DEFAULT_CHUNK, codec: int = EQ_CODEC_
 def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH, scales: torch.Tensor | None = None,
                     chunk_symbols: int = EQ_DEFAULT_CHUNK, oct_lo: int = -1, oct_hi: int = 20,
                     stream=None, scratch: torch.Tensor | None = None, shrink: bool = True,
-                    format: int = EQ_FMT_E4M3, exclude=(), codec: int = EQ_CODEC_BYTE,
+                    format: int = EQ_FMT_E4M3, exclude=(), codec: int = EQ_DEFAULT_CODEC,
                     chunk_mode: int = EQ_CHUNK_LAYER) -> Block:
     """Alg. 1 for one block of bf16 CUDA matrices.  Synchronous (reads payload size).
     ``exclude``: layer indices kept at AbsMax scales (λ = 0); ``codec``: rANS
@@ -450,7 +453,7 @@ def build_pair_table(hist: torch.Tensor, stream=None):
 
 
 def rans_encode(codes: torch.Tensor, shapes, freq: torch.Tensor, scales: torch.Tensor | None = None,
-                chunk_symbols: int = EQ_DEFAULT_CHUNK, stream=None, codec: int = EQ_CODEC_BYTE,
+                chunk_symbols: int = EQ_DEFAULT_CHUNK, stream=None, codec: int = EQ_DEFAULT_CODEC,
                 chunk_mode: int = EQ_CHUNK_LAYER) -> Block:
     """a6 alone: encode a concatenated symbol stream (uint8 CUDA) with a given table."""
     _require_cuda(codes, freq)
@@ -477,11 +480,11 @@ def rans_encode(codes: torch.Tensor, shapes, freq: torch.Tensor, scales: torch.T
 
 def calibrate_lambda(layers, target_bits: float, row_stride: int = 8, chunk_symbols: int = EQ_DEFAULT_CHUNK,
                      oct_lo: int = -1, oct_hi: int = 20, stream=None, format: int = EQ_FMT_E4M3,
-                     codec: int = EQ_CODEC_BYTE):
+                     codec: int = EQ_DEFAULT_CODEC, chunk_mode: int = EQ_CHUNK_LAYER):
     """Global λ for a target effective rate (P:192, P:507).  Returns (λ, estimated bits);
-    ``codec`` sizes the per-block table in the side information."""
+    ``codec`` sizes the per-block table and ``chunk_mode`` the chunk count in the side information."""
     ts = (eq_tensor * len(layers))(*[_tensor(W) for W in layers])
-    p = _params(chunk_symbols, EQ_SCALES_SEARCH, 0.0, oct_lo, oct_hi, format, codec=codec)
+    p = _params(chunk_symbols, EQ_SCALES_SEARCH, 0.0, oct_lo, oct_hi, format, codec=codec, chunk_mode=chunk_mode)
     sb = lib().eq_calibrate_scratch_bytes(ts, len(layers), row_stride)
     scratch = torch.empty(sb, dtype=torch.uint8, device=layers[0].device)
     lam, est = ctypes.c_double(), ctypes.c_double()

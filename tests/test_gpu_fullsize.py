@@ -50,7 +50,7 @@ def layer_set(request):
     for lid in range(32):
         Ws = eqsynth.block_weights("llama-3-8b", lid, device=dev)
         if scratch is None:
-            scratch = torch.empty(eq.encode_bounds(Ws)[2], dtype=torch.uint8, device=dev)
+            scratch = torch.empty(eq.encode_bounds(Ws, codec=eq.EQ_CODEC_BYTE)[2], dtype=torch.uint8, device=dev)
         blocks.append(eq.quantize_encode(Ws, lam=LAM, scratch=scratch, codec=request.param))
         if lid in (0, 15, 31):
             kept[lid] = [W.cpu() for W in Ws]          # the INPUT weights, for the oracle

@@ -172,7 +172,7 @@ def test_rans_encode_byte_identical(cs):
     scales = [(o.absmax_scales(W).astype(np.int32) + 1500).astype(np.uint16) for W in layers]
     blk = o.quantize_encode(layers, scales=scales, cs=cs)
     g = eq.rans_encode(torch.from_numpy(blk.codes).to(DEV), blk.layer_shapes,
-                       torch.from_numpy(blk.freq.view(np.int16).copy()).to(DEV), chunk_symbols=cs)
+                       torch.from_numpy(blk.freq.view(np.int16).copy()).to(DEV), chunk_symbols=cs, codec=eq.EQ_CODEC_BYTE)
     assert g.payload_bytes == len(blk.payload)
     assert (g.chunk_off.cpu().numpy().astype(np.uint32) == blk.chunk_off).all()
     assert g.payload[:g.payload_bytes].cpu().numpy().tobytes() == blk.payload
@@ -247,14 +247,14 @@ def test_config1_full_pipeline_vs_oracle():
     chunks; GPU search+quantise+table+encode vs the full oracle pipeline."""
     W = eqsynth.weights(256, 256, seed=0)
     lam = 150.0
-    g = eq.quantize_encode([W.to(DEV)], lam=lam)
+    g = eq.quantize_encode([W.to(DEV)], lam=lam, codec=eq.EQ_CODEC_BYTE)
     S_gpu = u16(g.scales)
     S_or, f_or = o.search(W, lam)
     _, ob = eq.search_scales(W.to(DEV), [lam], with_obj=True)
     diff = np.nonzero(S_gpu != S_or)[0]
     check_search_rows(W, lam, S_gpu, ob[0].cpu().numpy(), list(diff) + [0, 1, 2])
     # with the oracle's own scales the GPU stream is the oracle's bit for bit
-    g2 = eq.quantize_encode([W.to(DEV)], scales=to_bf16(S_or))
+    g2 = eq.quantize_encode([W.to(DEV)], scales=to_bf16(S_or), codec=eq.EQ_CODEC_BYTE)
     ref2 = o.quantize_encode([W], scales=[S_or])
     assert (g2.freq.cpu().numpy().view(np.uint16) == ref2.freq).all()
     assert (g2.chunk_off.cpu().numpy().astype(np.uint32) == ref2.chunk_off).all()
@@ -271,7 +271,7 @@ def test_config1_full_pipeline_vs_oracle():
 def test_quantize_encode_absmax_and_ragged():
     layers = small_layers(seed=3)
     for cs in [4096, 100]:
-        g = eq.quantize_encode([W.to(DEV) for W in layers], scale_mode=eq.EQ_SCALES_ABSMAX, chunk_symbols=cs)
+        g = eq.quantize_encode([W.to(DEV) for W in layers], scale_mode=eq.EQ_SCALES_ABSMAX, chunk_symbols=cs, codec=eq.EQ_CODEC_BYTE)
         ref = o.quantize_encode(layers, lam=None, cs=cs)
         assert g.payload[:g.payload_bytes].cpu().numpy().tobytes() == ref.payload
         for v, r in zip(eq.decode_dequant([g], eq.EQ_OUT_BF16)[0], o.decode_dequant(ref)):
@@ -280,7 +280,7 @@ def test_quantize_encode_absmax_and_ragged():
 
 def test_host_buffer_e2e_decode():
     layers = small_layers(seed=8, shapes=[(64, 256), (32, 512)])
-    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=80.0)
+    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=80.0, codec=eq.EQ_CODEC_BYTE)
     hb = eq.HostBlocks([g], eq.EQ_OUT_BF16)
     arena = hb.decode()
     dev = eq.Decoder([g], eq.EQ_OUT_BF16)
@@ -292,13 +292,25 @@ def test_host_buffer_e2e_decode():
 def test_calibrate_lambda_reaches_target():
     layers = [eqsynth.weights(r, c, seed=2, layer=0, matrix=m) for m, (r, c) in enumerate([(128, 512), (256, 512)])]
     dl = [W.to(DEV) for W in layers]
-    lam, est = eq.calibrate_lambda(dl, 2.5, row_stride=2)
+    lam, est = eq.calibrate_lambda(dl, 2.5, row_stride=2, codec=eq.EQ_CODEC_BYTE)
     assert abs(est - 2.5) < 0.1
-    g = eq.quantize_encode(dl, lam=lam)
+    g = eq.quantize_encode(dl, lam=lam, codec=eq.EQ_CODEC_BYTE)
     assert abs(g.effective_bits() - 2.5) < 0.35
     with pytest.raises(eq.EqError) as ei:
-        eq.calibrate_lambda(dl, 9.5, row_stride=4)
+        eq.calibrate_lambda(dl, 9.5, row_stride=4, codec=eq.EQ_CODEC_BYTE)
     assert ei.value.status == eq.EQ_ERR_UNREACHABLE_TARGET
+
+
+def test_calibrate_lambda_full_block_within_005_bits():
+    """λ for a target rate within ±0.05 effective bits, at the bench's scale (one
+    Llama-3-8B-shaped block, pair codec, row chunks of 4096): calibrate on sampled rows, then
+    encode the whole block."""
+    Ws = eqsynth.block_weights("llama-3-8b", 3, device=DEV)
+    for target in (2.0, 3.0):
+        lam, est = eq.calibrate_lambda(Ws, target, row_stride=16, codec=eq.EQ_CODEC_PAIR, chunk_mode=eq.EQ_CHUNK_ROW)
+        assert abs(est - target) < 0.05, (target, est)
+        g = eq.quantize_encode(Ws, lam=lam, codec=eq.EQ_CODEC_PAIR, chunk_mode=eq.EQ_CHUNK_ROW)
+        assert abs(g.effective_bits() - target) < 0.05, (target, g.effective_bits())
 
 
 def test_dequant_all_codes_all_scale_ranges():
@@ -376,12 +388,12 @@ def test_int8_decode_oracle_streams(out):
 def test_quantize_encode_format_and_exclusion(fmt):
     layers = [eqsynth.weights(r, c, seed=22, layer=1, matrix=m) for m, (r, c) in enumerate([(48, 256), (32, 512), (8, 4096)])]
     lam = 150.0
-    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=lam, format=fmt, exclude=(2,))
+    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=lam, format=fmt, exclude=(2,), codec=eq.EQ_CODEC_BYTE)
     S_gpu = u16(g.scales)
     assert (S_gpu[80:88] == o.absmax_scales(layers[2], fmt)).all()              # excluded layer: λ = 0
     S_or = [o.search(W, lam, fmt=fmt)[0] for W in layers[:2]] + [o.absmax_scales(layers[2], fmt)]
     sc = to_bf16(np.concatenate(S_or))
-    g2 = eq.quantize_encode([W.to(DEV) for W in layers], scales=sc, format=fmt)
+    g2 = eq.quantize_encode([W.to(DEV) for W in layers], scales=sc, format=fmt, codec=eq.EQ_CODEC_BYTE)
     ref = o.quantize_encode(layers, scales=S_or, fmt=fmt)
     assert g2.payload[:g2.payload_bytes].cpu().numpy().tobytes() == ref.payload
     for v, r in zip(eq.decode_dequant([g2], eq.EQ_OUT_BF16)[0], o.decode_dequant(ref)):

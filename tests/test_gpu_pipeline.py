@@ -23,7 +23,7 @@ def test_pipeline_matches_oracle_weights():
         ob = o.quantize_encode(Ws, scales=S)
         ref_blocks.append([torch.from_numpy(d.view(np.int16)).view(torch.bfloat16).to(dev) for d in o.decode_dequant(ob)])
         sc = torch.from_numpy(np.concatenate(S).view(np.int16)).view(torch.bfloat16).to(dev)
-        blocks.append(eq.quantize_encode([W.to(dev) for W in Ws], scales=sc))
+        blocks.append(eq.quantize_encode([W.to(dev) for W in Ws], scales=sc, codec=eq.EQ_CODEC_BYTE))
     x0 = (torch.arange(4 * 256, device=dev, dtype=torch.float32).reshape(4, 256).sin() * 0.1).to(torch.bfloat16)
     ref = x0
     for views in ref_blocks:

@@ -144,7 +144,7 @@ def test_word_rate_vs_byte_codec_at_two_bits():
     offsets (north_star) and within 0.5 % of the byte codec's."""
     W = eqsynth.weights(512, 4096, seed=6)
     gw = eq.quantize_encode([W.to(DEV)], lam=230.0, codec=W16)
-    gb = eq.quantize_encode([W.to(DEV)], scales=gw.scales)
+    gb = eq.quantize_encode([W.to(DEV)], scales=gw.scales, codec=eq.EQ_CODEC_BYTE)
     codes, hist = eq.quantize_hist(W.to(DEV), gw.scales)
     H = o.entropy(hist.cpu().numpy().astype(np.uint64))
     assert gw.payload_bytes + 4 * (gw.n_chunks + 1) <= 1.02 * W.numel() * H / 8
