@@ -180,7 +180,7 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
-DECODER_SOURCES = ("rans_dec.cu", "decode_core.cuh", "common.cuh")
+DECODER_SOURCES = ("rans_dec.cu", "decode_core.cuh", "pair_core.cuh", "common.cuh")
 
 
 def decoder_source_sha() -> str:

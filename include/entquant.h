@@ -241,8 +241,8 @@ eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks,
                                  void* arena_host, uint64_t arena_bytes, void* workspace,
                                  uint64_t workspace_bytes, eq_stream_t stream);
 
-/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4; EQ_CODEC_BYTE or EQ_CODEC_WORD
- * blocks — EQ_CODEC_PAIR blocks return EQ_ERR_ARG): Y_q = X_q · Ŵ_qᵀ for
+/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4; all three codecs — the word
+ * and pair codecs run the warp-specialised kernel): Y_q = X_q · Ŵ_qᵀ for
  * n_jobs layers `layers[q]` of block `blk` in ONE launch, Ŵ = the layer's decoded +
  * dequantised bf16 weights (never written to memory): each chunk is decoded straight into
  * tcgen05 shared-memory tiles and multiplied on the 5th-gen tensor cores (bf16 × bf16 →
@@ -253,9 +253,11 @@ eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks,
  * y: HOST array of n_jobs DEVICE pointers, fp32 [batch, rows_q], 16-byte aligned, disjoint.
  * workspace: device, ≥ eq_qmatmul_workspace_bytes (0 when every row is one chunk), 16-byte
  * aligned; caller-owned, reused freely after the stream passes the call.
- * Requires row-aligned chunks (cols % chunk_symbols == 0), rows % 128 == 0,
- * chunk_symbols % 64 == 0, 1 ≤ batch ≤ 256 (else EQ_ERR_SHAPE); EQ_ERR_BUFFER for a short
- * workspace.  Stream integrity checks as eq_decode_dequant (d_err).  Asynchronous. */
+ * Requires row-independent chunks — EQ_CHUNK_ROW (R16: any cols that are a multiple of 64; a
+ * ragged last chunk per row is fine) or EQ_CHUNK_LAYER with cols % chunk_symbols == 0 —
+ * rows % 128 == 0, chunk_symbols % 64 == 0, 1 ≤ batch ≤ 256 (else EQ_ERR_SHAPE);
+ * EQ_ERR_BUFFER for a short workspace.  Stream integrity checks as eq_decode_dequant (d_err).
+ * Asynchronous. */
 uint64_t eq_qmatmul_workspace_bytes(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers,
                                     uint32_t batch);
 eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, const uint32_t* layers,

@@ -14,22 +14,23 @@
 //   lut[4096..] the 256 × u16 codes table id -> code(ra) | code(rb) << 8 (right after the LUT:
 //               its address is the LUT's uniform base + a constant — a separate array's address
 //               was rematerialised with four uniform instructions per pair step),
-//   lut1[4096]  the single table's symbol per slot (escapes), cum[257] its cumulative
-//               frequencies, pcum[227] the pair table's.
+//   lut1[4096]  the single table's symbol per slot (escapes); while the tables are built it
+//               first holds pcum[227], the pair table's cumulative frequencies;
+//   cum[257]    u16, the single table's cumulative frequencies.
 #pragma once
 #include "decode_core.cuh"
 
 namespace eq {
 
 constexpr int kPairOff = 256, kFescIdx = 481, kKIdx = 482, kRankIdx = 484;
-constexpr int kPairLutWords = kM + 128;
+constexpr int kPairLutWords = kM + 113;           // + the 225 × u16 codes table
 
-constexpr uint32_t kPairSmemBytes = kPairLutWords * 4 + kM + 257 * 4 + 227 * 4;
+constexpr uint32_t kPairSmemBytes = kPairLutWords * 4 + kM + 258 * 2;
 
 struct PairTab {
     uint32_t lut_s;        // shared address of the pair LUT (the codes table follows at + 4·kM)
     uint32_t lut1_s;       // shared address of the single table's symbol per slot
-    uint32_t cum_s;        // shared address of the single table's cum[257]
+    uint32_t cum_s;        // shared address of the single table's cum[257] (u16)
     uint32_t esc_lo;       // slot << 20 at and above which a pair step is the escape (0xFFFFFFFF: none)
     uint32_t fesc, cesc;   // escape frequency and cumulative start
     uint32_t k2p20, k2p12; // 2^20, 2^12 passed at run time (IMAD forms on the FMA pipe)
@@ -66,7 +67,7 @@ __device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, 
     asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
     const uint32_t slot = lo >> 20;
     const uint32_t s = lds_u8(T.lut1_s + slot);
-    const uint32_t cs = lds_u32(T.cum_s + 4 * s), ce = lds_u32(T.cum_s + 4 * s + 4);
+    const uint32_t cs = lds_u16(T.cum_s + 2 * s), ce = lds_u16(T.cum_s + 2 * s + 2);
     x = (ce - cs) * xs + slot - cs;
     renorm_w(x, r);
     return s;
@@ -136,9 +137,12 @@ __device__ __forceinline__ void lut_walk(uint32_t* lut, const uint32_t* cm, F en
 // (Only the rank-(0,0) pair can exceed 2048 slots, when p(rank 0)² > ½.)
 // (This sequence keeps the table bases in uniform registers through the decode loop; a variant
 // scanning both tables concurrently made ptxas rematerialise them per pair step, −1.6 %.)
+// pcum lives in lut1's space (the pair LUT walk is done, behind a barrier of the NT threads,
+// before lut1 is filled); cesc returns the escape's cumulative start pcum[225].
 template <int NT, bool ALL = false, bool NARROW_OK = false>   // ALL: the CTA has exactly NT threads
 __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint32_t* lut, uint8_t* lut1,
-                                                  uint32_t* cum, uint32_t* pcum, uint32_t* err) {
+                                                      uint16_t* cum, uint32_t& cesc, uint32_t* err) {
+    uint32_t* pcum = reinterpret_cast<uint32_t*>(lut1);
     static_assert(NT >= 64 && (NT & (NT - 1)) == 0 && NT <= 1024, "thread count");
     const int t = threadIdx.x;
     {                                              // cum[257]: exclusive prefix of the 256 frequencies
@@ -173,7 +177,7 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
         return 0;
     }
     const uint32_t K = freq[kKIdx];
-    __shared__ uint32_t s_fmax;
+    __shared__ uint32_t s_fmax, s_cesc;
     if (t < 32) {                                  // 226-entry pair cum: (ra, rb) order, escape last
         uint32_t v[8], s = 0, fmax = 0;
         #pragma unroll
@@ -201,6 +205,7 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
         if (t == 31) {
             pcum[225] = inc;
             pcum[226] = inc + freq[kFescIdx];
+            s_cesc = inc;
         }
     }
     __syncthreads();
@@ -209,6 +214,7 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
         return 0;
     }
     const bool narrow = NARROW_OK && s_fmax <= 2048u;
+    cesc = s_cesc;
     if (ALL || t < NT) {
         // (escape slots keep id 0xFF; their entries are never read: the escape test precedes the lookup)
         const uint32_t idsh = narrow ? 1u : 0u, scsh = narrow ? 9u : 8u;
@@ -217,6 +223,7 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
             const uint32_t id = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : 0xFFu;
             return (id << idsh) | ((slot - pcum[q]) << scsh) | ((f - 1) << 20);
         });
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");     // pcum read by all: lut1 may be written
         constexpr uint32_t SP = kM / NT;           // symbol per slot: thread t fills [SP·t, SP·t + SP)
         const uint32_t s0 = SP * (uint32_t)t;
         int lo = 0, hi = 255;
@@ -243,13 +250,13 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
 }
 
 __device__ __forceinline__ PairTab pair_tab(const uint16_t* freq, const uint32_t* lut, const uint8_t* lut1,
-                                            const uint32_t* cum, const uint32_t* pcum, uint32_t k2p20, uint32_t k2p12) {
+                                            const uint16_t* cum, uint32_t cesc, uint32_t k2p20, uint32_t k2p12) {
     PairTab T;
     T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
     T.lut1_s = (uint32_t)__cvta_generic_to_shared(lut1);
     T.cum_s = (uint32_t)__cvta_generic_to_shared(cum);
     T.fesc = freq[kFescIdx];
-    T.cesc = pcum[225];
+    T.cesc = cesc;
     T.esc_lo = T.fesc ? (T.cesc << 20) : 0xFFFFFFFFu;
     T.k2p20 = k2p20;
     T.k2p12 = k2p12;

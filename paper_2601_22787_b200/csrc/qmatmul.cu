@@ -534,12 +534,12 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
     if constexpr (CODEC == EQ_CODEC_PAIR) {
         uint32_t* lut = reinterpret_cast<uint32_t*>(tabs);
         uint8_t* lut1 = tabs + kPairLutWords * 4;
-        uint32_t* cum = reinterpret_cast<uint32_t*>(lut1 + kM);
-        uint32_t* pcum = cum + 257;
-        mode = pair_tables_build<kWsDec, false, EQ_QMM_NARROW>(P.freq, lut, lut1, cum, pcum, P.err);
+        uint16_t* cum = reinterpret_cast<uint16_t*>(lut1 + kM);
+        uint32_t cesc = 0;
+        mode = pair_tables_build<kWsDec, false, EQ_QMM_NARROW>(P.freq, lut, lut1, cum, cesc, P.err);
         ok = mode != 0;
         __syncthreads();                           // table stores visible to every decoder lane
-        if (ok) PT = pair_tab(P.freq, lut, lut1, cum, pcum, P.k2p20, P.k2p12);
+        if (ok) PT = pair_tab(P.freq, lut, lut1, cum, cesc, P.k2p20, P.k2p12);
     } else {
         uint32_t* lut = reinterpret_cast<uint32_t*>(tabs);
         uint32_t* cum = lut + kM;
@@ -971,7 +971,7 @@ extern "C" eq_status eq_qmatmul_group(const eq_block* blk, uint32_t n_jobs, cons
     P.err = d_err;
     P.format = blk->format;
     P.cs = cs;
-    P.n_pad = (batch + 7) & ~7u;
+    P.n_pad = (batch + 15) & ~15u;             // UMMA N for M = 128: a multiple of 16 (PTX ISA)
     P.n_real = batch;
     P.acc_cols = P.n_pad;                      // half h accumulates in columns [h·n_pad, (h+1)·n_pad)
     P.tmem_cols = 32;

@@ -676,9 +676,8 @@ __global__ void __launch_bounds__(kPThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) uint8_t rings[];      // kPThreads × kWRing
     __shared__ __align__(16) uint32_t lut[kPairLutWords];  // pair LUT + codes table
-    __shared__ __align__(16) uint8_t lut1[kM];
-    __shared__ uint32_t cum[257];
-    __shared__ uint32_t pcum[227];
+    __shared__ __align__(16) uint8_t lut1[kM];             // (first the pair cum, see pair_tables_build)
+    __shared__ uint16_t cum[258];
 
     uint32_t bi = 0;
     while (bi + 1 < P.n_blocks && blockIdx.x >= P.b[bi + 1].cta0) ++bi;
@@ -688,14 +687,15 @@ k_decode_p(const __grid_constant__ DecParams P) {
     chain_setup_w<BF16>(c, B, (blockIdx.x - B.cta0) * kPThreads + t,
                         (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
     stage_commit();
-    const uint32_t mode = pair_tables_build<kPThreads, true, EQ_PAIR_NARROW>(B.freq, lut, lut1, cum, pcum, P.err);
+    uint32_t cesc;
+    const uint32_t mode = pair_tables_build<kPThreads, true, EQ_PAIR_NARROW>(B.freq, lut, lut1, cum, cesc, P.err);
     if (!mode) {
         stage_wait_all();
         return;
     }
     stage_wait_all();
     __syncthreads();
-    const PairTab T = pair_tab(B.freq, lut, lut1, cum, pcum, P.k2p20, P.k2p12);
+    const PairTab T = pair_tab(B.freq, lut, lut1, cum, cesc, P.k2p20, P.k2p12);
     chain_start_w(c);
     if (EQ_PAIR_NARROW && mode == 2) chain_finish_p<BF16, true>(c, B.payload, T);    // CTA-uniform
     else chain_finish_p<BF16, false>(c, B.payload, T);
