@@ -33,13 +33,21 @@ def test_pair_decode_oracle_streams(cs, out):
             assert (u16(v) == o.dequant(codes, S)).all()
 
 
+@pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16], ids=["fp8", "bf16"])
 @pytest.mark.parametrize("kind", ["uniform", "subset2", "single", "skewed", "subset40"])
-def test_pair_decode_extreme_streams(kind):
-    """Escape-heavy (uniform bytes: 15 of 256 codes ranked), single-code and two-code tables."""
+def test_pair_decode_extreme_streams(kind, out):
+    """Escape-heavy (uniform bytes: 15 of 256 codes ranked), single-code and two-code tables.
+    The single-code table's (0,0) pair has f > 2048, so it also runs the decoder's wide LUT
+    entries (the narrow 2·id layout needs every kept pair at f ≤ 2048)."""
     s = eqsynth.random_codes_stream(64 * 4096, 3, kind)
-    blk = o.encode_codes([s.reshape(64, 4096)], [(64, 4096)], [np.full(64, 0x3F80, np.uint16)], 4096, codec=PAIR)
-    v = eq.decode_dequant([oracle_block_to_gpu(blk)], eq.EQ_OUT_FP8)[0][0]
-    assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == s).all()
+    s = np.where((s & 0x7F) == 0x7F, s ^ 1, s).astype(np.uint8)       # no NaN codes (never produced, R1)
+    S = (np.arange(64, dtype=np.uint16) * 37 + 0x3C00).astype(np.uint16)
+    blk = o.encode_codes([s.reshape(64, 4096)], [(64, 4096)], [S], 4096, codec=PAIR)
+    v = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0][0]
+    if out == eq.EQ_OUT_FP8:
+        assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == s).all()
+    else:
+        assert (u16(v) == o.dequant(s.reshape(64, 4096), S)).all()
 
 
 def _pair_hists():
