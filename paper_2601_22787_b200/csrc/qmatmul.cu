@@ -422,8 +422,11 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 // The decoders never wait for the tensor cores unless they run kWsStages steps ahead; no
 // CTA-wide barrier inside the K loop.  Epilogue: the decoder warps read their TMEM lanes
 // (tcgen05.ld 32x32b) and write Y (one chunk column) or the split-K partial.
+#ifndef EQ_QMM_NTILE
+#define EQ_QMM_NTILE 2                         // 128-row tiles (4 decoder warps each) per CTA
+#endif
 #ifndef EQ_QMM_WS_STAGES
-#define EQ_QMM_WS_STAGES 3
+#define EQ_QMM_WS_STAGES (EQ_QMM_NTILE > 1 ? 2 : 3)   // (2 vs 3 stages measured equal; 2 keeps 3 CTAs/SM at NTILE 2)
 #endif
 #ifndef EQ_QMM_WS_MIN_CTAS
 #define EQ_QMM_WS_MIN_CTAS 3
@@ -431,6 +434,7 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 #ifndef EQ_QMM_NARROW
 #define EQ_QMM_NARROW 1                        // pair codec: 2·id LUT entries when every kept pair has f ≤ 2048
 #endif
+constexpr int kQmmNTile = EQ_QMM_NTILE;
 constexpr int kWsStages = EQ_QMM_WS_STAGES;
 constexpr int kWsK = 32;                       // K columns per step (one SWIZZLE_64B row = 64 B)
 constexpr int kWsRowB = kWsK * 2;
@@ -472,17 +476,22 @@ __device__ __forceinline__ uint4 ws_dequant8(const C& c, uint32_t q0, uint32_t q
     return dequant8(c, q0, q1);
 }
 
-template <int CODEC>
-__global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const __grid_constant__ QmmWsParams P) {
+// NTILE = 128-row tiles per CTA: 4·NTILE decoder warps (one row per lane) share one copy of the
+// tables and one X stage; NTILE A sub-tiles per stage feed NTILE TMEM accumulators (columns
+// h·n_pad).  NTILE = 2 holds twice the chains per CTA for the same table memory.
+template <int CODEC, int NTILE>
+__global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const __grid_constant__ QmmWsParams P) {
+    constexpr int kDec = kWsDec * NTILE;           // decoder lanes
+    constexpr uint32_t kAStage = NTILE * kWsATile;
     extern __shared__ __align__(1024) uint8_t ws_raw[];
     uint8_t* dsm = ws_raw + ((1024u - (smem_u32(ws_raw) & 1023u)) & 1023u);
-    // layout: [A stages | B stages | tables | rings | barriers | tmem slot]
+    // layout: [A stages (NTILE sub-tiles each) | B stages | tables | rings | barriers | tmem slot]
     uint8_t* a_st = dsm;
-    uint8_t* b_st = dsm + kWsStages * kWsATile;
+    uint8_t* b_st = dsm + kWsStages * kAStage;
     uint8_t* tabs = b_st + kWsStages * P.b_stage_bytes;
     constexpr uint32_t kTabBytes = CODEC == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4u;
     uint32_t* rings = reinterpret_cast<uint32_t*>(tabs + ((kTabBytes + 127u) & ~127u));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + kWsDec * (kWRing / 4));   // full[S], empty[S]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + kDec * (kWRing / 4));     // full[S], empty[S]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kWsStages);
 
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -495,7 +504,7 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
     const uint32_t kbase = jcol * P.cs;
     const uint32_t clen = min(P.cs, J.K - kbase);
     const uint32_t steps = clen / kWsK;
-    const uint32_t grow = tile * kTileRows + (uint32_t)t;            // decoder lanes only
+    const uint32_t grow = tile * (NTILE * kTileRows) + (uint32_t)t;  // decoder lanes only
 
     // ---- the decoder lanes start staging their chunk while the tables are built
     ChainW c;
@@ -505,7 +514,7 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
     c.s = 0.f;
     c.s16 = 0;
     const uint32_t ring = smem_u32(rings + t * (kWRing / 4));
-    if (t < kWsDec) {
+    if (t < kDec && grow < J.rows) {
         c.s = bf16_bits_to_float(J.scales[grow]);
         c.s16 = c.i8 ? 0 : scale_f16(c.s);
         const uint32_t chunk = J.chunk0 + grow * J.cpr + jcol;
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
         uint8_t* lut1 = tabs + kPairLutWords * 4;
         uint16_t* cum = reinterpret_cast<uint16_t*>(lut1 + kM);
         uint32_t cesc = 0;
-        mode = pair_tables_build<kWsDec, false, EQ_QMM_NARROW>(P.freq, lut, lut1, cum, cesc, P.err);
+        mode = pair_tables_build<kDec, false, EQ_QMM_NARROW>(P.freq, lut, lut1, cum, cesc, P.err);
         ok = mode != 0;
         __syncthreads();                           // table stores visible to every decoder lane
         if (ok) PT = pair_tab(P.freq, lut, lut1, cum, cesc, P.k2p20, P.k2p12);
@@ -560,8 +569,8 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
         }
         __syncthreads();
         ok = cum[256] == kM;
-        if (ok && t < kWsDec) {
-            lut_walk<256, kWsDec>(lut, cum, [&](uint32_t slot, int sym) -> uint32_t {
+        if (ok && t < kDec) {
+            lut_walk<256, kDec>(lut, cum, [&](uint32_t slot, int sym) -> uint32_t {
                 const uint32_t fs = cum[sym + 1] - cum[sym];
                 return (uint32_t)sym | ((slot - cum[sym]) << 8) | ((fs - 1) << 20);   // (f−1)-on-top layout
             });
@@ -579,15 +588,16 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
         stage_wait_all();
         return;
     }
-    // ---- barriers (thread 128), TMEM accumulator (warp 4)
-    if (t == kWsDec) {
+    // ---- barriers (first thread of the MMA warp), TMEM accumulators (the MMA warp)
+    constexpr int kMmaWarp = 4 * NTILE;
+    if (t == kDec) {
         for (int q = 0; q < kWsStages; ++q) {
-            mbar_init(smem_u32(&bars[q]), 4 + 1);                 // 4 decoder warps + the TMA arrive
+            mbar_init(smem_u32(&bars[q]), 4 * NTILE + 1);         // the decoder warps + the TMA arrive
             mbar_init(smem_u32(&bars[kWsStages + q]), 1);         // tcgen05.commit
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(P.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -597,7 +607,7 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 4) {
+    if (warp == kMmaWarp) {
         // ===== producer (TMA of X) + MMA issuer: one lane
         if (lane == 0) {
             const CUtensorMap* map = &P.tmap[jb];
@@ -612,15 +622,18 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
                 const uint32_t sidx = st % kWsStages, use = st / kWsStages;
                 mbar_wait(smem_u32(&bars[sidx]), use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t da = umma_desc_sw64(smem_u32(a_st + sidx * kWsATile));
                 const uint64_t db = umma_desc_sw64(smem_u32(b_st + sidx * P.b_stage_bytes));
                 #pragma unroll
-                for (int kk = 0; kk < kWsK / 16; ++kk) {
-                    const uint32_t acc = (st > 0 || kk > 0) ? 1u : 0u;
-                    asm volatile(
-                        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
-                            tmem),
-                        "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(P.idesc), "r"(acc));
+                for (int h = 0; h < NTILE; ++h) {
+                    const uint64_t da = umma_desc_sw64(smem_u32(a_st + sidx * kAStage + h * kWsATile));
+                    #pragma unroll
+                    for (int kk = 0; kk < kWsK / 16; ++kk) {
+                        const uint32_t acc = (st > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(
+                                tmem + (uint32_t)h * P.n_pad),
+                            "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(P.idesc), "r"(acc));
+                    }
                 }
                 const uint32_t eb = smem_u32(&bars[kWsStages + sidx]);
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(eb)
@@ -644,11 +657,11 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
             c.r.w = lds_u16(ring | ((A + 4) & m));
             c.r.Q = A + 6;
         }
-        const uint32_t r = (uint32_t)t;
+        const uint32_t r = (uint32_t)t & (kTileRows - 1);          // row within the lane's 128-row sub-tile
         const uint32_t row_off = (r >> 3) * 512u + (r & 7) * (uint32_t)kWsRowB;
         const uint32_t sw = (r >> 1) & 3;                         // SWIZZLE_64B: 16-byte chunk q at q ^ sw
         const uint32_t qlim = c.e + (2u + kWBias);
-        const uint32_t a0 = smem_u32(a_st) + row_off;
+        const uint32_t a0 = smem_u32(a_st) + ((uint32_t)t / kTileRows) * kWsATile + row_off;
         // one K step = 32 symbols of the lane's chain into 4 × 16 bytes of its A row; branches
         // once per step (live chain, scale mode), stage index / phase by counters
         auto run = [&](auto narrow_c) {
@@ -658,7 +671,7 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
             uint32_t sidx = 0, use = 0;
             for (uint32_t st = 0; st < steps; ++st) {
                 if (st >= (uint32_t)kWsStages) mbar_wait(smem_u32(&bars[kWsStages + sidx]), (use & 1) ^ 1);
-                const uint32_t arow = a0 + sidx * kWsATile;
+                const uint32_t arow = a0 + sidx * kAStage;
                 uint4 v[kWsK / 8];
                 if (c.active && !c.runaway) {
                     uint32_t q[kWsK / 4];
@@ -720,7 +733,7 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
         float* out = J.out + (uint64_t)jcol * P.n_real * J.rows;
         for (uint32_t col = 0; col < P.n_pad; col += 8) {
             uint32_t v[8];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + col;
+            const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * P.n_pad + col;
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                          : "r"(taddr));
@@ -728,13 +741,13 @@ __global__ void __launch_bounds__(kWsThreads, EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const
             #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const uint32_t b = col + q;
-                if (b < P.n_real) out[(uint64_t)b * J.rows + grow] = __uint_as_float(v[q]);
+                if (b < P.n_real && grow < J.rows) out[(uint64_t)b * J.rows + grow] = __uint_as_float(v[q]);
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols));
+    if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols));
 }
 
 // Y = Σ_j partial_j in a fixed order (j = 0, 1, …): deterministic split-K reduction
@@ -842,7 +855,7 @@ static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint3
         J.K = blk->layer_cols[l];
         J.cpr = (J.K + cs - 1) / cs;
         J.tile_begin = tiles;
-        tiles += J.rows / kTileRows * J.cpr;
+        tiles += (J.rows + kQmmNTile * kTileRows - 1) / (kQmmNTile * kTileRows) * J.cpr;
         if (J.cpr == 1) {
             J.out = y[q];
         } else {
@@ -870,7 +883,7 @@ static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint3
     W.n_pad = n_pad;
     W.n_real = batch;
     W.tmem_cols = 32;
-    while (W.tmem_cols < n_pad) W.tmem_cols <<= 1;
+    while (W.tmem_cols < kQmmNTile * n_pad) W.tmem_cols <<= 1;
     W.b_stage_bytes = (n_pad * (uint32_t)kWsRowB + 1023u) & ~1023u;
     // instruction descriptor, kind::f16: D f32, A = B = bf16, both K-major, N = n_pad, M = 128
     W.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((n_pad >> 3) << 17) | ((128u >> 4) << 24);
@@ -879,14 +892,16 @@ static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint3
     W.kneg2p14 = 0u - (1u << 14);
     W.k4 = 4u;
     const size_t tab = blk->codec == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4;
-    const size_t smem = 1024 + kWsStages * kWsATile + kWsStages * W.b_stage_bytes + ((tab + 127) & ~(size_t)127) +
-                        kWsDec * kWRing + 2 * kWsStages * 8 + 16;
-    const void* fn = blk->codec == EQ_CODEC_PAIR ? (const void*)k_qmm_ws<EQ_CODEC_PAIR> : (const void*)k_qmm_ws<EQ_CODEC_WORD>;
+    const size_t smem = 1024 + kWsStages * kQmmNTile * kWsATile + kWsStages * W.b_stage_bytes + ((tab + 127) & ~(size_t)127) +
+                        kQmmNTile * kWsDec * kWRing + 2 * kWsStages * 8 + 16;
+    const void* fn = blk->codec == EQ_CODEC_PAIR ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile>
+                                                 : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile>;
     EQ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int threads = 32 * (4 * kQmmNTile + 1);
     if (blk->codec == EQ_CODEC_PAIR)
-        k_qmm_ws<EQ_CODEC_PAIR><<<tiles, kWsThreads, smem, st>>>(W);
+        k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile><<<tiles, threads, smem, st>>>(W);
     else
-        k_qmm_ws<EQ_CODEC_WORD><<<tiles, kWsThreads, smem, st>>>(W);
+        k_qmm_ws<EQ_CODEC_WORD, kQmmNTile><<<tiles, threads, smem, st>>>(W);
     EQ_CUDA_TRY(cudaGetLastError());
     return EQ_OK;
 }
