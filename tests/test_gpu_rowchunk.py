@@ -70,3 +70,25 @@ def test_rowchunk_qmatmul_ragged_k(codec, batch):
             bound = 1e-4 * (np.abs(X64) @ np.abs(W64).T) + 1e-30
             y = eq.qmatmul(g, layer, x.to(DEV)).cpu().double().numpy()
             assert (np.abs(y - ref) <= bound).all(), (cs, layer, float(np.max(np.abs(y - ref) / bound)))
+
+
+@pytest.mark.parametrize("batch", [1, 64])
+def test_qmatmul_escape_heavy_pair_stream(batch):
+    """Pair codec with escapes on most steps (uniform bytes: only 15 of the codes are ranked):
+    the fused GEMM's escape singles — from the 4 KB symbol table at small batches, by a binary
+    search over the cumulative frequencies when the table does not fit 3 CTAs/SM (batch 64) —
+    must reproduce the fp64 product of the oracle's dequantised weights."""
+    rows, cols = 256, 4096
+    s = eqsynth.random_codes_stream(rows * cols, 11, "uniform")
+    s = np.where((s & 0x7F) == 0x7F, s ^ 1, s).astype(np.uint8)        # no NaN codes (never produced, R1)
+    S = (np.arange(rows, dtype=np.uint16) % 97 + 0x3A00).astype(np.uint16)
+    blk = o.encode_codes([s.reshape(rows, cols)], [(rows, cols)], [S], 2048, codec=o.CODEC_PAIR,
+                         chunk_mode=o.CHUNK_ROW)
+    g = oracle_block_to_gpu(blk)
+    W64 = torch.from_numpy(o.dequant(s.reshape(rows, cols), S).view(np.int16)).view(torch.bfloat16).double().numpy()
+    x = (torch.randn(batch, cols, generator=torch.Generator().manual_seed(batch)) * 0.5).to(torch.bfloat16)
+    X64 = x.double().numpy()
+    ref = X64 @ W64.T
+    bound = 1e-4 * (np.abs(X64) @ np.abs(W64).T) + 1e-30
+    y = eq.qmatmul(g, 0, x.to(DEV)).cpu().double().numpy()
+    assert (np.abs(y - ref) <= bound).all(), float(np.max(np.abs(y - ref) / bound))
