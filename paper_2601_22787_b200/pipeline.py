@@ -104,3 +104,16 @@ def llama_block_forward(views, x: torch.Tensor) -> torch.Tensor:
     h = x + q @ wo.t()
     m = torch.nn.functional.silu(h @ wg.t()) * (h @ wu.t())
     return h + m @ wd.t()
+
+
+def llama_block_forward_fused(block: Block, x: torch.Tensor, err: torch.Tensor, workspace: torch.Tensor) -> torch.Tensor:
+    """``llama_block_forward`` with every GEMM fused with the block's decode
+    (``eq_qmatmul_group``, §8(f) row 1): the weights are never materialised.  The dataflow
+    needs four dependent launches: {q, k, v} → o → {gate, up} → down; activations between them
+    are rounded to bf16 as in the dense forward."""
+    from . import qmatmul_group
+    q, _, _ = qmatmul_group(block, [0, 1, 2], [x, x, x], err=err, check=False, workspace=workspace)
+    h = x + qmatmul_group(block, [3], [q.to(torch.bfloat16)], err=err, check=False, workspace=workspace)[0].to(torch.bfloat16)
+    g, u = qmatmul_group(block, [4, 5], [h, h], err=err, check=False, workspace=workspace)
+    m = (torch.nn.functional.silu(g) * u).to(torch.bfloat16)
+    return h + qmatmul_group(block, [6], [m], err=err, check=False, workspace=workspace)[0].to(torch.bfloat16)
