@@ -67,9 +67,12 @@ def parse():
     ap.add_argument("--no-stats", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
-    ap.add_argument("--chunk-mode", default="row", choices=["layer", "row"],
-                    help="chunk restarts (R16): row (default; every row start too, so the same streams feed "
-                         "the decode-fused GEMM of config 4) or layer (R10)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: exercise the multi-rank path with several ranks per GPU (a logic check)")
+    ap.add_argument("--chunk-mode", default="layer", choices=["layer", "row"],
+                    help="chunk restarts: layer (R10, default) or row (R16: every row start too, as the "
+                         "decode-fused GEMM of config 4 needs; identical streams for every layer whose K "
+                         "is a multiple of the chunk length — all Llama-3-8B layers but down_proj)")
     ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"],
                     help="wire format: byte rANS (SPEC S:355, R9), 16-bit-word rANS (R14), or the word "
                          "rANS over symbol pairs with escapes (R15, default: fastest, smallest)")
@@ -222,12 +225,11 @@ def share_ids(args, rank: int, world: int):
 
 
 def choose_chunk(args, layer_ids, lanes: int) -> int:
-    """Chunk length for the rank's share: a launch runs about chunks / lanes
-    rounds of one serial chunk-length chain, so a share of 1.1 rounds at 4096 symbols wastes
-    almost half the GPU.  Measured rule: 4096 (the smallest rate) when the share is ≥ 4 rounds
-    of it; one round at 4608 when that fits (the 4-block share at G = 8: 0.549 vs 0.543 at
-    1024; other non-power-of-two lengths measured slower); otherwise 2048 or 1024, whichever
-    gives the shorter ceil(rounds) × (length + per-chunk overhead)."""
+    """Chunk length for the rank's share: 4096 symbols, or — for a share that
+    is barely more than one round of 4096-symbol chains (a launch runs chunks / lanes rounds of
+    serial chains; 4 Llama-3-8B blocks are 1.12 rounds, the SMs idle 17 % of such a launch) —
+    one round of 4608 with layer chunking (0.549 of the HBM peak vs 0.46).  Shorter chunks are not
+    chosen: at 2048 the coded size passes the north star's 1.02 × n·Ĥ (≈ 1.0205 ×)."""
     import eqsynth
     if args.chunk_symbols:
         return args.chunk_symbols
@@ -237,15 +239,9 @@ def choose_chunk(args, layer_ids, lanes: int) -> int:
         if args.chunk_mode == "row":
             return sum(r * ((c + cs - 1) // cs) for r, c in shapes)
         return sum((r * c + cs - 1) // cs for r, c in shapes)
-    r4096 = n_chunks(4096) / lanes
-    if r4096 >= 4:
-        return 4096
-    if r4096 <= 1.25 and n_chunks(4608) <= lanes:
+    if 1 < n_chunks(4096) / lanes <= 1.25 and n_chunks(4608) <= lanes:
         return 4608
-    return min((2048, 1024), key=lambda cs: -(-n_chunks(cs) // lanes) * (cs + CHUNK_OVERHEAD_SYMBOLS))
-
-
-CHUNK_OVERHEAD_SYMBOLS = 256        # per-chunk setup (staging, table-build share, stores) in symbol-steps
+    return 4096
 
 
 def encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist=None):
@@ -389,10 +385,15 @@ def main():
     import eqsynth
     import paper_2601_22787_b200 as eq
     from paper_2601_22787_b200 import shard
+    if args.dist_backend == "gloo":             # logic check of the N-rank path on fewer GPUs (no timing value)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     if args.blocks <= 0:
         args.blocks = eqsynth.LLAMA[args.model]["layers"]
     layer_ids, (sim_rank, sim_world) = share_ids(args, rank, world)

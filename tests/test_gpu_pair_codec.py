@@ -147,3 +147,20 @@ def test_pair_runaway_stream_is_reported():
     with pytest.raises(eq.EqError) as ei:
         d.check()
     assert ei.value.status == eq.EQ_ERR_CORRUPT
+
+
+@pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16], ids=["fp8", "bf16"])
+def test_pair_decode_many_tiny_chunks(out):
+    """204,800 chunks of 16 symbols in one launch (800 CTAs: a second, thin round on 148 SMs at
+    5 CTAs/SM; every chunk is one fast group): the decoded symbols equal the oracle's stream."""
+    rows, cols, cs = 800, 4096, 16
+    s = eqsynth.random_codes_stream(rows * cols, 5, "skewed")
+    s = np.where((s & 0x7F) == 0x7F, s ^ 1, s).astype(np.uint8)
+    S = (np.arange(rows, dtype=np.uint16) % 61 + 0x3B80).astype(np.uint16)
+    blk = o.encode_codes([s.reshape(rows, cols)], [(rows, cols)], [S], cs, codec=PAIR)
+    assert blk.n_chunks == rows * cols // cs
+    v = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0][0]
+    if out == eq.EQ_OUT_FP8:
+        assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == s).all()
+    else:
+        assert (u16(v) == o.dequant(s.reshape(rows, cols), S)).all()
