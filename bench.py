@@ -213,6 +213,18 @@ def traffic_from_profiles(codec: str, kind: str, blocks: int, chunk_symbols: int
     return e["dram_bytes_per_launch"], f"{e.get('source', p)} (kernel sha {e['kernel_sha']}, {e.get('when', '?')})"
 
 
+def inst_from_profiles(codec: str, kind: str, blocks: int, chunk_symbols: int):
+    """Warp-level SASS instructions per launch from the same sha-matched ncu capture, or None."""
+    tr, _ = traffic_from_profiles(codec, kind, blocks, chunk_symbols)
+    if tr is None:
+        return None
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_decode_summary.json")))[codec][kind].get(
+            "warp_inst_per_launch")
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- shared: the workload
 def share_ids(args, rank: int, world: int):
     """(block ids of this process, simulated (rank, world)) — --as-rank R/G runs rank R's share
@@ -446,6 +458,7 @@ def main():
     achieved = bytes_bf16 / (launch_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
     traffic, traffic_src = traffic_from_profiles(args.codec, "bf16", len(blocks), cs)
+    inst = inst_from_profiles(args.codec, "bf16", len(blocks), cs)
 
     fp8, dec8 = None, None
     if not args.no_fp8:
@@ -512,7 +525,8 @@ def main():
                          "peak_source": peak_src, "kernel": f"k_decode_{'p' if args.codec == 'pair' else 'w' if args.codec == 'word' else ''}",
                          "kernel_sha": decoder_source_sha(),
                          "algorithmic_bytes_per_launch": bytes_bf16, "launch_ms": launch_ms,
-                         "chunks": n_chunks, "decoder_lanes": lanes},
+                         "chunks": n_chunks, "decoder_lanes": lanes,
+                         "warp_inst_per_32_symbols": (None if inst is None else inst / n_params * 32)},
             "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "gpu_launches": args.steps, "clocks": cs_clk,
             "bits_per_param": 8.0 * comp_bytes / n_params,
             "payload_bits_per_param": 8.0 * payload_bytes / n_params,

@@ -40,7 +40,9 @@ def main(ev, rnd):
     for d in full:
         k = d["kernel"]
         codec = "word" if "k_decode_w" in k else "pair" if "k_decode_p" in k else "byte" if "k_decode" in k else None
-        kind = "bf16" if "<1>" in k or "<(bool)1>" in k else "fp8" if "<0>" in k or "<(bool)0>" in k else None
+        import re
+        kind = ("bf16" if re.search(r"<(\(bool\))?1[,>]", k) else
+                "fp8" if re.search(r"<(\(bool\))?0[,>]", k) else None)
         if codec is None or kind is None:
             continue
         rd, wr = _num(d["dram__bytes_read.sum"]), _num(d["dram__bytes_write.sum"])
@@ -54,6 +56,8 @@ def main(ev, rnd):
         summ[codec][kind] = {"kernel": k, "duration_ms_under_ncu": _num(d["gpu__time_duration.sum"]),
                              "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                              "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")}
+        if d.get("smsp__inst_executed.sum"):
+            summ[codec][kind]["warp_inst_per_launch"] = float(d["smsp__inst_executed.sum"].split()[0].replace(",", ""))
     json.dump(summ, open(sp, "w"), indent=1)
 
     # launch list: "ID",...,"Kernel Name",...,"Metric Value"
@@ -72,7 +76,7 @@ def main(ev, rnd):
         w.writerow(["kernel", "launches", "total_us", "share_of_command", "mean_us"])
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
             w.writerow([k, len(v), round(sum(v), 1), round(sum(v) / tot, 5), round(sum(v) / len(v), 1)])
-    dec = {k: v for k, v in per.items() if "k_decode" in k and "<1>" in k}
+    dec = {k: v for k, v in per.items() if "k_decode" in k and ("<1>" in k or "<1," in k)}
     json.dump({"command": "python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --lam 230.2 "
                           "(ncu --metrics gpu__time_duration.sum --clock-control none)",
                "timed_step_kernels": {k: {"launches": len(v), "mean_us": sum(v) / len(v)} for k, v in dec.items()},
