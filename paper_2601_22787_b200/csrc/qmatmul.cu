@@ -409,19 +409,20 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 
 // ================================================================ warp-specialised kernel
 // k_qmm_ws — EQ_CODEC_WORD / EQ_CODEC_PAIR blocks (the bench's codec), row-chunked streams.
-// CTA = (GEMM, one 128-row tile, chunk column j), 160 threads:
-//   warps 0-3  decoders: lane r decodes chunk j of row r (its rANS chain), dequantises with the
-//              row scale and writes 32 columns per K step (64 B, bf16) into A stage s of a
+// CTA = (GEMM, NTILE 128-row tiles, chunk column j), 32·(4·NTILE + 1) threads (NTILE = 2: 288):
+//   warps 0 .. 4·NTILE−1  decoders (4 per tile, one copy of the tables for all): lane r decodes
+//              chunk j of its row (its rANS chain), dequantises with the row scale and writes 32
+//              columns per K step (64 B, bf16) into its tile's sub-tile of A stage s of a
 //              kWsStages-deep ring (K-major, SWIZZLE_64B canonical UMMA layout), then
 //              fence.proxy.async + one mbarrier arrive per warp on full[s];
-//   warp 4     producer + MMA issuer (one elected lane): TMA-loads X[:, k0 : k0 + 32] as the B
+//   warp 4·NTILE  producer + MMA issuer (one elected lane): TMA-loads X[:, k0 : k0 + 32] as the B
 //              stage (the tensor map's SWIZZLE_64B box lands in the UMMA layout; rows past the
-//              batch are zero-filled), waits full[s], issues 2 × tcgen05.mma (M = 128, N =
-//              batch rounded up to 16, K = 16) into one TMEM accumulator and commits to
-//              empty[s], which frees both stages for step + kWsStages.
+//              batch are zero-filled), waits full[s], issues per tile 2 × tcgen05.mma (M = 128,
+//              N = batch rounded up to 16, K = 16) into that tile's TMEM accumulator (columns
+//              h·N) and commits to empty[s], which frees both stages for step + kWsStages.
 // The decoders never wait for the tensor cores unless they run kWsStages steps ahead; no
-// CTA-wide barrier inside the K loop.  Epilogue: the decoder warps read their TMEM lanes
-// (tcgen05.ld 32x32b) and write Y (one chunk column) or the split-K partial.
+// CTA-wide barrier inside the K loop.  Epilogue: decoder warp w reads TMEM lanes 32·(w % 4) of
+// accumulator w / 4 (tcgen05.ld 32x32b) and writes Y (one chunk column) or the split-K partial.
 #ifndef EQ_QMM_NTILE
 #define EQ_QMM_NTILE 2                         // 128-row tiles (4 decoder warps each) per CTA
 #endif
@@ -439,7 +440,7 @@ constexpr int kWsStages = EQ_QMM_WS_STAGES;
 constexpr int kWsK = 32;                       // K columns per step (one SWIZZLE_64B row = 64 B)
 constexpr int kWsRowB = kWsK * 2;
 constexpr int kWsATile = kTileRows * kWsRowB;  // 8 KB per A stage
-constexpr int kWsDec = 128, kWsThreads = kWsDec + 32;
+constexpr int kWsDec = 128;                   // decoder lanes (rows) per 128-row tile
 
 struct QmmWsParams {
     CUtensorMap tmap[EQ_MAX_LAYERS];           // X of each job: [batch, K] bf16, box {32, n_pad}, SWIZZLE_64B
