@@ -168,6 +168,14 @@ k_search(const __grid_constant__ SearchParams P) {
     lo = max(lo, 1);
     hi = min(hi, 0x7F7F);
     if (hi < lo) hi = lo;
+    {   // every candidate from the first s with max|w|/s ≤ the first rounding midpoint (2^-10 for
+        // E4M3, ½ for Int8; a tie rounds to the even code 0) quantises the whole row to 0: equal
+        // objectives, and the smallest of them wins ties, so the rest need no evaluation
+        const float z = __fmul_rn(bf16_bits_to_float(m), FMT == EQ_FMT_INT8 ? 2.0f : 1024.0f);
+        const uint32_t zb = __float_as_uint(z);
+        const int hz = (int)((zb >> 16) + ((zb & 0xFFFFu) ? 1u : 0u));   // smallest bf16 ≥ z
+        if (isfinite(z) && hz >= lo && hz < hi) hi = hz;
+    }
     const uint32_t nc = (uint32_t)(hi - lo + 1);
 
     const double l1 = *P.l1;
