@@ -13,6 +13,8 @@ the oracle re-runs Alg. 1 l.3-5 from the INPUT weights with the GPU's scales (th
 checked separately on sampled rows) and must reproduce the GPU's table, offsets and payload
 byte for byte.  Properties checked at full size: coded size ≤ 1.02× the histogram entropy,
 Shannon's bound, effective rate near the target.
+Configs 2 and 5: every symbol of the 16-block Llama-3.2-1B set and of one whole Llama-3-70B block
+against the oracle's decoder, and a sampled block's encode against the oracle's.
 """
 import os
 
@@ -174,3 +176,76 @@ def test_config3_lossless_and_rate_properties(layer_set):
         n += b.n_params
         comp += b.compressed_bytes()
     assert 1.9 < 8 * comp / n < 2.1
+
+
+def _decode_all_vs_oracle(blocks):
+    """Every symbol of one eq_decode_dequant launch over ``blocks`` against the oracle's
+    threaded decoder, bf16 bit for bit; returns the number of symbols checked."""
+    dec = eq.Decoder(blocks, eq.EQ_OUT_BF16)
+    dec()
+    dec.check()
+    views = dec.views()
+    threads = os.cpu_count() or 1
+    total = 0
+    for b, vb in zip(blocks, views):
+        payload, off, table, pair, scales = _host_block(b)
+        k0 = r0 = 0
+        for (r, c), v in zip(b.shapes, vb):
+            nk = (r * c + b.chunk_symbols - 1) // b.chunk_symbols
+            ref = o.decode_dequant_layer_mt(payload, off[k0:k0 + nk + 1], b.chunk_symbols, r, c, scales[r0:r0 + r],
+                                            table[:256], threads, b.codec, pair)
+            assert np.array_equal(ref, u16(v).reshape(r, c)), (b.codec, r, c)
+            total += r * c
+            k0 += nk
+            r0 += r
+    return total
+
+
+def _encode_matches_oracle(b, Ws):
+    """Alg. 1 l.3-5 of the oracle on the INPUT weights with the GPU's scales reproduces the GPU's
+    table, offsets and payload byte for byte."""
+    _, off, table, _, scales = _host_block(b)
+    S, r0 = [], 0
+    for (r, _) in b.shapes:
+        S.append(scales[r0:r0 + r])
+        r0 += r
+    ref = o.quantize_encode(Ws, scales=S, cs=b.chunk_symbols, codec=b.codec)
+    assert np.array_equal(off, np.asarray(ref.chunk_off, dtype=np.uint32))
+    assert b.payload_bytes == len(ref.payload)
+    assert b.payload[:b.payload_bytes].cpu().numpy().tobytes() == ref.payload
+
+
+def test_config2_llama_1b_every_symbol_and_sampled_encode():
+    """BASELINE config 2 (Llama-3.2-1B shapes, 16 blocks, 0.97 G parameters), the bench's pair
+    codec: λ calibrated for 2 bits on the GPU, Alg. 1 for every block, one decode launch; every
+    symbol against the oracle's decoder, block 7's encode against the oracle's."""
+    dev = torch.device("cuda")
+    calib = eqsynth.block_weights("llama-3.2-1b", 0, device=dev)
+    lam, _ = eq.calibrate_lambda(calib, 2.0, row_stride=16, codec=eq.EQ_CODEC_PAIR)
+    del calib
+    blocks, kept = [], None
+    for lid in range(16):
+        Ws = eqsynth.block_weights("llama-3.2-1b", lid, device=dev)
+        blocks.append(eq.quantize_encode(Ws, lam=lam, codec=eq.EQ_CODEC_PAIR))
+        if lid == 7:
+            kept = [W.cpu() for W in Ws]
+        del Ws
+    n = _decode_all_vs_oracle(blocks)
+    assert n == 16 * 60817408
+    _encode_matches_oracle(blocks[7], kept)
+    bits = 8 * sum(b.compressed_bytes() for b in blocks) / n
+    assert abs(bits - 2.0) < 0.05
+
+
+def test_config5_llama_70b_block_every_symbol_and_encode():
+    """BASELINE config 5 (Llama-3-70B shapes; the per-rank parity of §8(d) is on sampled
+    blocks): one whole 70B block (856 M parameters) with the bench's pair codec — every symbol
+    of its decode against the oracle's decoder, and its encode against the oracle's."""
+    dev = torch.device("cuda")
+    Ws = eqsynth.block_weights("llama-3-70b", 3, device=dev)
+    b = eq.quantize_encode(Ws, lam=LAM, codec=eq.EQ_CODEC_PAIR)
+    Wc = [W.cpu() for W in Ws]
+    del Ws
+    torch.cuda.empty_cache()
+    assert _decode_all_vs_oracle([b]) == 855638016
+    _encode_matches_oracle(b, Wc)
