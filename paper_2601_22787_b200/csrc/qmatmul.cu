@@ -432,6 +432,9 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 #ifndef EQ_QMM_WS_MIN_CTAS
 #define EQ_QMM_WS_MIN_CTAS 3
 #endif
+#ifndef EQ_QMM_HALF
+#define EQ_QMM_HALF 1                          // decoder K step as a loop over two 16-symbol halves
+#endif
 #ifndef EQ_QMM_NARROW
 #define EQ_QMM_NARROW 1                        // pair codec: 2·id LUT entries when every kept pair has f ≤ 2048
 #endif
@@ -673,6 +676,57 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
             for (uint32_t st = 0; st < steps; ++st) {
                 if (st >= (uint32_t)kWsStages) mbar_wait(smem_u32(&bars[kWsStages + sidx]), (use & 1) ^ 1);
                 const uint32_t arow = a0 + sidx * kAStage;
+#if EQ_QMM_HALF
+                // the step as a (not unrolled) loop over two halves of 16 symbols: half the code
+                // of the fully unrolled step (the decoder loop then fits the instruction cache)
+                if (c.active && !c.runaway) {
+                    const uint16_t h16 = (uint16_t)s16;
+                    #pragma unroll 1
+                    for (uint32_t hs = 0; hs < 2; ++hs) {
+                        uint32_t q[4];
+                        if constexpr (CODEC == EQ_CODEC_PAIR) {
+                            #pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const uint32_t p0 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                                const uint32_t p1 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                                const uint32_t p2 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                                const uint32_t p3 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
+                                q[2 * u] = __byte_perm(p0, p1, 0x5410);
+                                q[2 * u + 1] = __byte_perm(p2, p3, 0x5410);
+                            }
+                            ring_step_w(c.r, P.payload);              // one stage per 8 pair steps
+                        } else {
+                            q[0] = decode4_w(c, WT);
+                            q[1] = decode4_w(c, WT);
+                            ring_step_w(c.r, P.payload);
+                            q[2] = decode4_w(c, WT);
+                            q[3] = decode4_w(c, WT);
+                            ring_step_w(c.r, P.payload);
+                        }
+                        uint4 v0, v1;
+                        if (s16) {
+                            v0 = make_uint4(dequant2_h(q[0], h16), dequant2_h(q[0] >> 16, h16), dequant2_h(q[1], h16),
+                                            dequant2_h(q[1] >> 16, h16));
+                            v1 = make_uint4(dequant2_h(q[2], h16), dequant2_h(q[2] >> 16, h16), dequant2_h(q[3], h16),
+                                            dequant2_h(q[3] >> 16, h16));
+                        } else {
+                            v0 = dequant8(c, q[0], q[1]);
+                            v1 = dequant8(c, q[2], q[3]);
+                        }
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + (((2 * hs) ^ sw) << 4)),
+                                     "r"(v0.x), "r"(v0.y), "r"(v0.z), "r"(v0.w) : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + (((2 * hs + 1) ^ sw) << 4)),
+                                     "r"(v1.x), "r"(v1.y), "r"(v1.z), "r"(v1.w) : "memory");
+                    }
+                    c.i += kWsK;
+                    if (c.r.Q > qlim) c.runaway = true;           // overran its chunk: stop reading
+                } else {
+                    #pragma unroll
+                    for (uint32_t g = 0; g < kWsK / 8; ++g)
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + ((g ^ sw) << 4)), "r"(0u),
+                                     "r"(0u), "r"(0u), "r"(0u) : "memory");
+                }
+#else
                 uint4 v[kWsK / 8];
                 if (c.active && !c.runaway) {
                     uint32_t q[kWsK / 4];
@@ -713,6 +767,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + ((g ^ sw) << 4)), "r"(v[g].x),
                                  "r"(v[g].y), "r"(v[g].z), "r"(v[g].w)
                                  : "memory");
+#endif
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bars[sidx]));
