@@ -164,3 +164,23 @@ def test_pair_decode_many_tiny_chunks(out):
         assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == s).all()
     else:
         assert (u16(v) == o.dequant(s.reshape(rows, cols), S)).all()
+
+
+def test_gpu_pair_codec_reproduces_hand_derived_streams():
+    """The device path against the hand-derived pair-codec chunks (tests/golden/
+    rans_pair_worked.json, no code involved): k_build_pair_table from the counts, the GPU
+    encoder on the symbols -> exactly the golden bytes; the GPU decoder on the golden bytes ->
+    the symbols (FP8 output = the codes)."""
+    import json, os
+    from test_oracle_codec import _expand, hist_of
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rans_pair_worked.json")))
+    for case in g["cases"]:
+        h = hist_of(_expand(case["counts"]))
+        tab, err = eq.build_pair_table(torch.from_numpy(h.astype(np.int64)).to(DEV))
+        eq.check(err)
+        sym = np.array(case["symbols"], dtype=np.uint8)
+        n = sym.size
+        blk = eq.rans_encode(torch.from_numpy(sym).to(DEV), [(1, n)], tab, chunk_symbols=4096, codec=eq.EQ_CODEC_PAIR)
+        assert blk.payload[:blk.payload_bytes].cpu().numpy().tobytes().hex() == case["bytes_hex"], case["name"]
+        v = eq.decode_dequant([blk], eq.EQ_OUT_FP8)[0][0]
+        assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == sym).all(), case["name"]
