@@ -439,7 +439,8 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 #define EQ_QMM_NARROW 1                        // pair codec: 2·id LUT entries when every kept pair has f ≤ 2048
 #endif
 constexpr int kQmmNTile = EQ_QMM_NTILE;
-constexpr int kWsStages = EQ_QMM_WS_STAGES;
+constexpr int kWsStages = EQ_QMM_WS_STAGES;   // the default; a launch that would lose its one-wave
+                                              // fit at kWsStages CTAs/SM may take 1 stage (below)
 constexpr int kWsK = 32;                       // K columns per step (one SWIZZLE_64B row = 64 B)
 constexpr int kWsRowB = kWsK * 2;
 constexpr int kWsATile = kTileRows * kWsRowB;  // 8 KB per A stage
@@ -483,7 +484,7 @@ __device__ __forceinline__ uint4 ws_dequant8(const C& c, uint32_t q0, uint32_t q
 // NTILE = 128-row tiles per CTA: 4·NTILE decoder warps (one row per lane) share one copy of the
 // tables and one X stage; NTILE A sub-tiles per stage feed NTILE TMEM accumulators (columns
 // h·n_pad).  NTILE = 2 holds twice the chains per CTA for the same table memory.
-template <int CODEC, int NTILE>
+template <int CODEC, int NTILE, int STAGES>
 __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qmm_ws(const __grid_constant__ QmmWsParams P) {
     constexpr int kDec = kWsDec * NTILE;           // decoder lanes
     constexpr uint32_t kAStage = NTILE * kWsATile;
@@ -491,12 +492,12 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
     uint8_t* dsm = ws_raw + ((1024u - (smem_u32(ws_raw) & 1023u)) & 1023u);
     // layout: [A stages (NTILE sub-tiles each) | B stages | tables | rings | barriers | tmem slot]
     uint8_t* a_st = dsm;
-    uint8_t* b_st = dsm + kWsStages * kAStage;
-    uint8_t* tabs = b_st + kWsStages * P.b_stage_bytes;
+    uint8_t* b_st = dsm + STAGES * kAStage;
+    uint8_t* tabs = b_st + STAGES * P.b_stage_bytes;
     constexpr uint32_t kTabBytes = CODEC == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4u;
     uint32_t* rings = reinterpret_cast<uint32_t*>(tabs + ((kTabBytes + 127u) & ~127u));
     uint64_t* bars = reinterpret_cast<uint64_t*>(rings + kDec * (kWRing / 4));     // full[S], empty[S]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kWsStages);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES);
 
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     uint32_t jb = 0;
@@ -595,9 +596,9 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
     // ---- barriers (first thread of the MMA warp), TMEM accumulators (the MMA warp)
     constexpr int kMmaWarp = 4 * NTILE;
     if (t == kDec) {
-        for (int q = 0; q < kWsStages; ++q) {
+        for (int q = 0; q < STAGES; ++q) {
             mbar_init(smem_u32(&bars[q]), 4 * NTILE + 1);         // the decoder warps + the TMA arrive
-            mbar_init(smem_u32(&bars[kWsStages + q]), 1);         // tcgen05.commit
+            mbar_init(smem_u32(&bars[STAGES + q]), 1);         // tcgen05.commit
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -616,14 +617,14 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
         if (lane == 0) {
             const CUtensorMap* map = &P.tmap[jb];
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-            const uint32_t pre = steps < (uint32_t)kWsStages ? steps : (uint32_t)kWsStages;
+            const uint32_t pre = steps < (uint32_t)STAGES ? steps : (uint32_t)STAGES;
             for (uint32_t q = 0; q < pre; ++q) {
                 const uint32_t fb = smem_u32(&bars[q]);
                 mbar_arrive_tx(fb, P.b_stage_bytes);
                 tma_load_2d(smem_u32(b_st + q * P.b_stage_bytes), map, (int32_t)(kbase + q * kWsK), 0, fb);
             }
             for (uint32_t st = 0; st < steps; ++st) {
-                const uint32_t sidx = st % kWsStages, use = st / kWsStages;
+                const uint32_t sidx = st % STAGES, use = st / STAGES;
                 mbar_wait(smem_u32(&bars[sidx]), use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint64_t db = umma_desc_sw64(smem_u32(b_st + sidx * P.b_stage_bytes));
@@ -639,15 +640,15 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                             "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(P.idesc), "r"(acc));
                     }
                 }
-                const uint32_t eb = smem_u32(&bars[kWsStages + sidx]);
+                const uint32_t eb = smem_u32(&bars[STAGES + sidx]);
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(eb)
                              : "memory");
-                if (st + kWsStages < steps) {      // refill the B stage once the MMAs that read it are done
+                if (st + STAGES < steps) {      // refill the B stage once the MMAs that read it are done
                     mbar_wait(eb, use & 1);
                     const uint32_t fb = smem_u32(&bars[sidx]);
                     mbar_arrive_tx(fb, P.b_stage_bytes);
                     tma_load_2d(smem_u32(b_st + sidx * P.b_stage_bytes), map,
-                                (int32_t)(kbase + (st + kWsStages) * kWsK), 0, fb);
+                                (int32_t)(kbase + (st + STAGES) * kWsK), 0, fb);
                 }
             }
         }
@@ -674,7 +675,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
             const uint32_t s16 = c.i8 ? 0u : (uint32_t)c.s16;
             uint32_t sidx = 0, use = 0;
             for (uint32_t st = 0; st < steps; ++st) {
-                if (st >= (uint32_t)kWsStages) mbar_wait(smem_u32(&bars[kWsStages + sidx]), (use & 1) ^ 1);
+                if (st >= (uint32_t)STAGES) mbar_wait(smem_u32(&bars[STAGES + sidx]), (use & 1) ^ 1);
                 const uint32_t arow = a0 + sidx * kAStage;
 #if EQ_QMM_HALF
                 // the step as a (not unrolled) loop over two halves of 16 symbols: half the code
@@ -771,7 +772,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bars[sidx]));
-                if (++sidx == (uint32_t)kWsStages) { sidx = 0; ++use; }
+                if (++sidx == (uint32_t)STAGES) { sidx = 0; ++use; }
             }
         };
         if constexpr (CODEC == EQ_CODEC_PAIR && EQ_QMM_NARROW) {
@@ -784,7 +785,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
         if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
         // ---- epilogue: the last commit covers every MMA of this CTA
         const uint32_t last = steps - 1;
-        mbar_wait(smem_u32(&bars[kWsStages + last % kWsStages]), (last / kWsStages) & 1);
+        mbar_wait(smem_u32(&bars[STAGES + last % STAGES]), (last / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float* out = J.out + (uint64_t)jcol * P.n_real * J.rows;
         for (uint32_t col = 0; col < P.n_pad; col += 8) {
@@ -948,16 +949,51 @@ static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint3
     W.kneg2p14 = 0u - (1u << 14);
     W.k4 = 4u;
     const size_t tab = blk->codec == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4;
-    const size_t smem = 1024 + kWsStages * kQmmNTile * kWsATile + kWsStages * W.b_stage_bytes + ((tab + 127) & ~(size_t)127) +
-                        kQmmNTile * kWsDec * kWRing + 2 * kWsStages * 8 + 16;
-    const void* fn = blk->codec == EQ_CODEC_PAIR ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile>
-                                                 : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile>;
-    EQ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto smem_for = [&](int stages) {
+        return (size_t)1024 + stages * kQmmNTile * kWsATile + stages * W.b_stage_bytes + ((tab + 127) & ~(size_t)127) +
+               kQmmNTile * kWsDec * kWRing + 2 * stages * 8 + 16;
+    };
+    const bool pair = blk->codec == EQ_CODEC_PAIR;
+    const void* fS = pair ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, kWsStages>
+                          : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, kWsStages>;
+    const void* f1 = pair ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, 1>
+                          : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, 1>;
     const int threads = 32 * (4 * kQmmNTile + 1);
-    if (blk->codec == EQ_CODEC_PAIR)
-        k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile><<<tiles, threads, smem, st>>>(W);
-    else
-        k_qmm_ws<EQ_CODEC_WORD, kQmmNTile><<<tiles, threads, smem, st>>>(W);
+    // resident CTAs per SM with kWsStages stages and with 1: one stage (the decoders then wait for
+    // each step's MMAs: ~6 % slower per CTA) only when it turns two waves into one — e.g. a
+    // Llama-3-8B block at chunk 2048 and batch 64, where the 4 KB X stages cost the third CTA/SM
+    int dev = 0, sms = 0, cS = 0, c1 = 0;
+    EQ_CUDA_TRY(cudaGetDevice(&dev));
+    EQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    EQ_CUDA_TRY(cudaFuncSetAttribute(fS, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kWsStages)));
+    EQ_CUDA_TRY(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(1)));
+    // resident CTAs from the kernels' own resource use (cudaOccupancyMaxActiveBlocksPerMultiprocessor
+    // reports 1 for these tcgen05 kernels, while 3 run per SM: ncu launch__occupancy_limit_*)
+    int smem_sm = 0, reserved = 0;
+    EQ_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    EQ_CUDA_TRY(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+    auto ctas_per_sm = [&](const void* f, size_t dyn, int* out) -> cudaError_t {
+        cudaFuncAttributes a;
+        cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+        const size_t per = a.sharedSizeBytes + dyn + (size_t)reserved;
+        const int by_smem = (int)((size_t)smem_sm / per);
+        const int regs = ((a.numRegs * 32 + 255) / 256) * 256 * (threads / 32);   // per-warp allocation granularity
+        const int by_regs = regs > 0 ? 65536 / regs : 32;
+        *out = std::min(std::min(by_smem, by_regs), 2048 / threads);
+        return cudaSuccess;
+    };
+    EQ_CUDA_TRY(ctas_per_sm(fS, smem_for(kWsStages), &cS));
+    EQ_CUDA_TRY(ctas_per_sm(f1, smem_for(1), &c1));
+    const bool one = (uint64_t)tiles > (uint64_t)cS * sms && (uint64_t)tiles <= (uint64_t)c1 * sms;
+    const size_t smem = smem_for(one ? 1 : kWsStages);
+    if (pair) {
+        if (one) k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, 1><<<tiles, threads, smem, st>>>(W);
+        else k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, kWsStages><<<tiles, threads, smem, st>>>(W);
+    } else {
+        if (one) k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, 1><<<tiles, threads, smem, st>>>(W);
+        else k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, kWsStages><<<tiles, threads, smem, st>>>(W);
+    }
     EQ_CUDA_TRY(cudaGetLastError());
     return EQ_OK;
 }
