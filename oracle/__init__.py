@@ -32,6 +32,8 @@ FMT_E4M3, FMT_INT8 = 0, 1
 CODEC_BYTE, CODEC_WORD = 0, 1      # rANS renormalisation: bytes (R9) / 16-bit words (R14)
 CODEC_PAIR = 2                      # word rANS over pairs of symbols with escapes (R15)
 CHUNK_LAYER, CHUNK_ROW = 0, 1       # chunks restart at every layer start / also at every row start (§8c.10)
+CHUNK_INTERLEAVED = 2                # R17: layer chunking over 16-symbol groups dealt to 32 chunks in turn
+IL_GROUP, IL_WAYS = 16, 32
 PAIR_K = 15
 
 
@@ -377,12 +379,33 @@ class OracleBlock:
         return 8.0 * b / self.n_params
 
 
+def interleave_order(size: int, cs: int) -> np.ndarray:
+    """R17: the layer positions in chunk order under CHUNK_INTERLEAVED.  A layer
+    of `size` symbols is cut into super-chunks of 32·cs symbols; chunk j (0 ≤ j < 32) of a
+    super-chunk holds its 16-symbol groups j, j + 32, j + 64, … (cs / 16 groups), so symbol i
+    of that chunk is layer symbol  s·32·cs + (⌊i/16⌋·32 + j)·16 + i mod 16.  The symbols after
+    the last whole super-chunk form plain contiguous chunks of cs (the last one ragged), as
+    under CHUNK_LAYER.  Returns src with src[q] = the layer position of the q-th symbol in chunk
+    order (chunk k is src[k·cs : k·cs + n_k]).  The four nested loops of that definition as one
+    broadcast (a loop transcription is checked against it in tests/test_oracle_codec.py)."""
+    if cs % IL_GROUP:
+        raise ValueError("CHUNK_INTERLEAVED needs chunk_symbols % 16 == 0")
+    sc = IL_WAYS * cs
+    full = size // sc
+    s = np.arange(full, dtype=np.int64)[:, None, None, None]            # super-chunk
+    j = np.arange(IL_WAYS, dtype=np.int64)[None, :, None, None]         # chunk within it
+    g = np.arange(cs // IL_GROUP, dtype=np.int64)[None, None, :, None]  # group within the chunk
+    r = np.arange(IL_GROUP, dtype=np.int64)[None, None, None, :]        # symbol within the group
+    head = (s * sc + (g * IL_WAYS + j) * IL_GROUP + r).reshape(-1)      # loop order s, j, g, r
+    return np.concatenate([head, np.arange(full * sc, size, dtype=np.int64)])
+
+
 def segment_sizes(layer_shapes, chunk_mode: int = CHUNK_LAYER) -> np.ndarray:
     """Lengths of the stream segments at whose starts chunking restarts: one per layer
     (CHUNK_LAYER), or one per row (CHUNK_ROW: every row of a layer with K
     columns is split into ⌈K/cs⌉ chunks, e.g. 4096 + 4096 + 4096 + 2048 for K = 14336, so a
     row's chunks are independent K slices of the fused GEMM, §8(f) row 1)."""
-    if chunk_mode == CHUNK_LAYER:
+    if chunk_mode in (CHUNK_LAYER, CHUNK_INTERLEAVED):
         return np.array([r * c for r, c in layer_shapes], dtype=np.int64)
     if chunk_mode == CHUNK_ROW:
         return np.concatenate([np.full(r, c, dtype=np.int64) for r, c in layer_shapes])
@@ -394,6 +417,12 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt:
     """Alg. 1 l.4-5 + App. A.1: concatenate vec(W_q) of the block's layers, one table,
     chunked rANS (chunks restart at every segment of ``segment_sizes``)."""
     stream = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1) for c in codes_list])
+    if chunk_mode == CHUNK_INTERLEAVED:          # the layers' symbols in chunk order (R17)
+        for (r, c) in layer_shapes:
+            if c % IL_GROUP:
+                raise ValueError("CHUNK_INTERLEAVED needs cols % 16 == 0")
+        stream = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1)[interleave_order(c.size, cs)]
+                                 for c in codes_list])
     hist = histogram(stream)
     freq = normalize(hist)
     sizes = segment_sizes(layer_shapes, chunk_mode)
@@ -452,6 +481,12 @@ def decode_block(blk: OracleBlock) -> np.ndarray:
                                           blk.chunk_symbols, _p(blk.freq), _p(out))
     if st:
         raise ValueError({1: "corrupt", 2: "truncated"}[st])
+    if blk.chunk_mode == CHUNK_INTERLEAVED:      # back from chunk order to layer order (R17)
+        res, a = np.empty_like(out), 0
+        for (r, c) in blk.layer_shapes:
+            res[a + interleave_order(r * c, blk.chunk_symbols)] = out[a:a + r * c]
+            a += r * c
+        out = res
     return out
 
 
@@ -489,6 +524,16 @@ def decode_dequant_layer_mt(payload: np.ndarray, chunk_off: np.ndarray, cs: int,
                             scales: np.ndarray, freq: np.ndarray, threads: int, codec: int = CODEC_BYTE,
                             pair: PairTable | None = None, chunk_mode: int = CHUNK_LAYER) -> np.ndarray:
     """Alg. 2 l.1-2 for one layer's chunks on ``threads`` host threads (CPU baseline)."""
+    if chunk_mode == CHUNK_INTERLEAVED:
+        # decode in chunk order with one "row" per 16-symbol group (its row's scale), then put
+        # every symbol back at its layer position (R17)
+        src = interleave_order(rows * cols, cs)
+        gscale = np.asarray(scales, dtype=np.uint16)[src[::IL_GROUP] // cols]
+        flat = decode_dequant_layer_mt(payload, chunk_off, cs, rows * cols // IL_GROUP, IL_GROUP, gscale, freq,
+                                       threads, codec, pair, CHUNK_LAYER).reshape(-1)
+        out = np.empty(rows * cols, dtype=np.uint16)
+        out[src] = flat
+        return out.reshape(rows, cols)
     seg = rows * cols if chunk_mode == CHUNK_LAYER else cols
     payload = np.ascontiguousarray(payload, dtype=np.uint8)
     off = np.ascontiguousarray(chunk_off, dtype=np.uint32)

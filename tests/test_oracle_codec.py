@@ -469,3 +469,82 @@ def test_row_chunking_threaded_dequant_helper(codec):
     out = o.decode_dequant_layer_mt(payload, blk.chunk_off, 256, 40, 700, S, blk.freq, 3, codec, blk.pair,
                                     chunk_mode=o.CHUNK_ROW)
     assert (out == o.decode_dequant(blk)[0]).all()
+
+
+# ------------------------------------------------------------------ CHUNK_INTERLEAVED (R17)
+def _interleave_literal(size: int, cs: int) -> list:
+    """R17 read literally: for each whole super-chunk of 32·cs symbols, chunk j holds the
+    super-chunk's 16-symbol groups j, j + 32, j + 64, …; the rest of the layer is plain
+    chunks.  Returns, per chunk, the list of layer positions of its symbols in order."""
+    chunks, sc = [], 32 * cs
+    full = size // sc
+    for s in range(full):
+        for j in range(32):
+            pos = []
+            for g in range(j, cs // 16 * 32, 32):            # groups j, j + 32, … of the super-chunk
+                pos.extend(range(s * sc + g * 16, s * sc + g * 16 + 16))
+            chunks.append(pos)
+    for a in range(full * sc, size, cs):
+        chunks.append(list(range(a, min(size, a + cs))))
+    return chunks
+
+
+@pytest.mark.parametrize("size,cs", [(3 * 32 * 32 + 100, 32), (32 * 64, 64), (1000, 48), (2 * 32 * 48 + 48, 48)])
+def test_interleave_order_matches_the_literal_definition(size, cs):
+    lit = _interleave_literal(size, cs)
+    src = o.interleave_order(size, cs)
+    assert np.array_equal(np.sort(src), np.arange(size))                 # a permutation
+    assert np.array_equal(src, np.concatenate([np.array(c, dtype=np.int64) for c in lit]))
+    assert len(lit) == (size + cs - 1) // cs                            # as many chunks as layer chunking
+
+
+@pytest.mark.parametrize("codec", ALL_CODECS)
+def test_interleaved_chunking_layout_by_brute_force(codec):
+    """Each chunk, decoded ALONE from its byte range, is exactly the codes at its R17 positions
+    (whole super-chunks interleaved, then a ragged tail of plain chunks); the block round trips."""
+    rng = np.random.default_rng(10 + codec)
+    shapes = [(8, 272), (3, 80), (5, 16)]                               # cs 32: 2176 = 2·1024 + 128, 240, 80
+    codes = [eqsynth.random_codes_stream(r * c, int(rng.integers(1 << 30)), "skewed").reshape(r, c) for r, c in shapes]
+    S = [np.full(r, 0x3F80, np.uint16) for r, _ in shapes]
+    blk = o.encode_codes(codes, shapes, S, 32, codec=codec, chunk_mode=o.CHUNK_INTERLEAVED)
+    k = 0
+    for C, (r, c) in zip(codes, shapes):
+        flat = C.reshape(-1)
+        for pos in _interleave_literal(r * c, 32):
+            want = flat[np.array(pos)]
+            assert (_chunk_alone(blk, k, want.size) == want).all(), (k, pos[:3])
+            k += 1
+    assert k == blk.n_chunks
+    assert (o.decode_block(blk) == np.concatenate([C.reshape(-1) for C in codes])).all()
+
+
+@pytest.mark.parametrize("codec", ALL_CODECS)
+def test_interleaved_chunking_degenerate_cases(codec):
+    """A layer shorter than one super-chunk is plain layer chunking; with cs = 16 every chunk is
+    one group, so R17 is layer chunking too — the same bytes in both cases.  A layer of whole
+    super-chunks has the same chunk count and, for i.i.d. symbols, the same rate up to rANS state
+    effects (the symbols of each chunk differ, the table does not)."""
+    W = eqsynth.weights(24, 512, seed=13)
+    S = (o.absmax_scales(W).astype(np.int32) + 1700).astype(np.uint16)
+    for cs in (1024, 16):                                                # 24·512 < 32·1024; cs 16: groups = chunks
+        a = o.quantize_encode([W], scales=[S], cs=cs, codec=codec)
+        b = o.quantize_encode([W], scales=[S], cs=cs, codec=codec, chunk_mode=o.CHUNK_INTERLEAVED)
+        assert a.payload == b.payload and (a.chunk_off == b.chunk_off).all(), cs
+    a = o.quantize_encode([W], scales=[S], cs=128, codec=codec)
+    b = o.quantize_encode([W], scales=[S], cs=128, codec=codec, chunk_mode=o.CHUNK_INTERLEAVED)
+    assert a.n_chunks == b.n_chunks and a.payload != b.payload
+    assert abs(len(a.payload) - len(b.payload)) <= 0.01 * len(a.payload)
+    assert (o.decode_block(b) == o.decode_block(a)).all()
+
+
+@pytest.mark.parametrize("codec", ALL_CODECS)
+def test_interleaved_chunking_threaded_dequant_helper(codec):
+    """The threaded decode + dequant helper follows R17: equal to decode_dequant (per-row scales
+    spread over the interleaved groups)."""
+    W = eqsynth.weights(40, 704, seed=15)
+    S = (o.absmax_scales(W).astype(np.int32) + 1600).astype(np.uint16)
+    blk = o.quantize_encode([W], scales=[S], cs=256, codec=codec, chunk_mode=o.CHUNK_INTERLEAVED)
+    payload = np.frombuffer(blk.payload + b"\0" * 16, dtype=np.uint8)
+    out = o.decode_dequant_layer_mt(payload, blk.chunk_off, 256, 40, 704, S, blk.freq, 3, codec, blk.pair,
+                                    chunk_mode=o.CHUNK_INTERLEAVED)
+    assert (out == o.decode_dequant(blk)[0]).all()
