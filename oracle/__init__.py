@@ -358,7 +358,7 @@ class OracleBlock:
     payload: bytes
     chunk_off: np.ndarray            # uint32[n_chunks+1]
     chunk_symbols: int = CHUNK_SYMBOLS
-    codes: np.ndarray = field(default=None, repr=False)   # concatenated symbol stream
+    codes: np.ndarray = field(default=None, repr=False)   # vec(W_q) of the layers, concatenated (layer order)
     fmt: int = FMT_E4M3
     codec: int = CODEC_BYTE
     pair: object = None              # PairTable (codec CODEC_PAIR)
@@ -416,7 +416,8 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt:
                  codec: int = CODEC_BYTE, chunk_mode: int = CHUNK_LAYER) -> OracleBlock:
     """Alg. 1 l.4-5 + App. A.1: concatenate vec(W_q) of the block's layers, one table,
     chunked rANS (chunks restart at every segment of ``segment_sizes``)."""
-    stream = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1) for c in codes_list])
+    codes = np.concatenate([np.ascontiguousarray(c, dtype=np.uint8).reshape(-1) for c in codes_list])
+    stream = codes
     if chunk_mode == CHUNK_INTERLEAVED:          # the layers' symbols in chunk order (R17)
         for (r, c) in layer_shapes:
             if c % IL_GROUP:
@@ -443,7 +444,7 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt:
     if n < 0:
         raise ValueError("encode failed %d" % n)
     return OracleBlock(list(layer_shapes), [np.asarray(s, dtype=np.uint16) for s in scales], freq, hist,
-                       payload[:n].tobytes(), off, cs, stream, fmt, codec, pt, chunk_mode)
+                       payload[:n].tobytes(), off, cs, codes, fmt, codec, pt, chunk_mode)
 
 
 def quantize_encode(layers, lam: float | None = None, scales=None, oct_lo: int = -1, oct_hi: int = 20,

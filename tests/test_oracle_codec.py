@@ -444,6 +444,7 @@ def test_row_chunking_layout_by_brute_force(codec):
                 k += 1
     assert k == blk.n_chunks
     assert (o.decode_block(blk) == np.concatenate([C.reshape(-1) for C in codes])).all()
+    assert (blk.codes == np.concatenate([C.reshape(-1) for C in codes])).all()      # layer order
 
 
 @pytest.mark.parametrize("codec", ALL_CODECS)
@@ -516,6 +517,7 @@ def test_interleaved_chunking_layout_by_brute_force(codec):
             k += 1
     assert k == blk.n_chunks
     assert (o.decode_block(blk) == np.concatenate([C.reshape(-1) for C in codes])).all()
+    assert (blk.codes == np.concatenate([C.reshape(-1) for C in codes])).all()      # layer order
 
 
 @pytest.mark.parametrize("codec", ALL_CODECS)
