@@ -42,7 +42,7 @@ DEFAULT_LAMBDA = 230.2               # reference arm only: the GPU calibration o
 
 
 CODECS = {"byte": 0, "word": 1, "pair": 2}     # EQ_CODEC_* (include/entquant.h)
-CHUNK_MODES = {"layer": 0, "row": 1}            # EQ_CHUNK_* (include/entquant.h, R16)
+CHUNK_MODES = {"layer": 0, "row": 1, "interleaved": 2}   # EQ_CHUNK_* (include/entquant.h, R16, R17)
 
 
 def parse():
@@ -69,14 +69,19 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: exercise the multi-rank path with several ranks per GPU (a logic check)")
-    ap.add_argument("--chunk-mode", default="layer", choices=["layer", "row"],
-                    help="chunk restarts: layer (R10, default) or row (R16: every row start too, as the "
-                         "decode-fused GEMM of config 4 needs; identical streams for every layer whose K "
-                         "is a multiple of the chunk length — all Llama-3-8B layers but down_proj)")
+    ap.add_argument("--chunk-mode", default="auto", choices=["auto", "layer", "row", "interleaved"],
+                    help="chunk layout: layer (R10: chunks restart at every layer), row (R16: at every row "
+                         "start too, as the decode-fused GEMM of config 4 needs), interleaved (R17: the "
+                         "16-symbol groups of 32 consecutive chunks dealt round-robin, so a warp's 32 "
+                         "lanes store 1 KB contiguously; pair codec only).  auto: interleaved for the "
+                         "pair codec, layer for the others")
     ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"],
                     help="wire format: byte rANS (SPEC S:355, R9), 16-bit-word rANS (R14), or the word "
                          "rANS over symbol pairs with escapes (R15, default: fastest, smallest)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.chunk_mode == "auto":
+        args.chunk_mode = "interleaved" if args.codec == "pair" else "layer"
+    return args
 
 
 def peak_hbm():
@@ -240,7 +245,7 @@ def choose_chunk(args, layer_ids, lanes: int) -> int:
     """Chunk length for the rank's share: 4096 symbols, or — for a share that
     is barely more than one round of 4096-symbol chains (a launch runs chunks / lanes rounds of
     serial chains; 4 Llama-3-8B blocks are 1.12 rounds, the SMs idle 17 % of such a launch) —
-    one round of 4608 with layer chunking (0.549 of the HBM peak vs 0.46).  Shorter chunks are not
+    one round of 4608 with layer or interleaved chunking (0.549 of the HBM peak vs 0.46).  Shorter chunks are not
     chosen: at 2048 the coded size passes the north star's 1.02 × n·Ĥ (≈ 1.0205 ×)."""
     import eqsynth
     if args.chunk_symbols:

@@ -73,6 +73,13 @@ typedef enum {
                                     /* ceil(K/cs) chunks (4096+4096+4096+2048 for K=14336),  */
                                     /* independent K slices for eq_qmatmul (§8(f) row 1);    */
                                     /* identical bytes to EQ_CHUNK_LAYER when K % cs == 0    */
+#define EQ_CHUNK_INTERLEAVED 2u     /* R17: layer chunking over super-chunks of 32*cs        */
+                                    /* symbols whose 16-symbol groups are dealt to their 32  */
+                                    /* chunks in turn (chunk j: groups j, j+32, ...); the    */
+                                    /* rest of the layer is plain chunks.  A decoder warp's  */
+                                    /* stores are then contiguous.  Pair codec only; needs   */
+                                    /* chunk_symbols % 32 == 0 and cols % 16 == 0 (else      */
+                                    /* EQ_ERR_ARG / EQ_ERR_SHAPE); not for eq_qmatmul        */
 
 #define EQ_SCALES_SEARCH 0u         /* exhaustive per-row Eq. 4 minimisation (R5)          */
 #define EQ_SCALES_ABSMAX 1u         /* AbsMax scales, Eq. 1 (the λ = 0 lossless-FP8 rate)  */
@@ -100,7 +107,7 @@ typedef struct {
     uint32_t exclude_mask;          /* bit l: layer l keeps AbsMax scales (λ = 0) — the    */
                                     /* super-weight exclusion of P:393-396          */
     uint32_t codec;                 /* EQ_CODEC_BYTE (0, default) | _WORD | _PAIR          */
-    uint32_t chunk_mode;            /* EQ_CHUNK_LAYER (0, default) | EQ_CHUNK_ROW          */
+    uint32_t chunk_mode;            /* EQ_CHUNK_LAYER (0, default) | _ROW | _INTERLEAVED     */
 } eq_params;
 
 /* One compressed transformer block: all its layers in one bitstream with one table

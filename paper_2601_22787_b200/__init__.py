@@ -29,7 +29,7 @@ EQ_CODEC_BYTE, EQ_CODEC_WORD, EQ_CODEC_PAIR = 0, 1, 2
 # The C ABI's zero-initialised eq_params keep SPEC's byte codec (R9); pass codec= for it here.
 EQ_DEFAULT_CODEC = EQ_CODEC_PAIR
 EQ_OUT_FP8, EQ_OUT_BF16 = 0, 1
-EQ_CHUNK_LAYER, EQ_CHUNK_ROW = 0, 1
+EQ_CHUNK_LAYER, EQ_CHUNK_ROW, EQ_CHUNK_INTERLEAVED = 0, 1, 2
 EQ_SCALES_SEARCH, EQ_SCALES_ABSMAX, EQ_SCALES_GIVEN = 0, 1, 2
 EQ_MAX_LAYERS = 8
 EQ_DEFAULT_CHUNK = 4096
@@ -254,7 +254,8 @@ def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH
     """Alg. 1 for one block of bf16 CUDA matrices.  Synchronous (reads payload size).
     ``exclude``: layer indices kept at AbsMax scales (λ = 0); ``codec``: rANS
     renormalisation (EQ_CODEC_BYTE, R9 / EQ_CODEC_WORD, R14 / EQ_CODEC_PAIR, R15);
-    ``chunk_mode``: EQ_CHUNK_LAYER or EQ_CHUNK_ROW (chunks also restart at row starts)."""
+    ``chunk_mode``: EQ_CHUNK_LAYER, EQ_CHUNK_ROW (chunks also restart at row starts) or
+    EQ_CHUNK_INTERLEAVED (R17: 16-symbol groups dealt to 32 chunks in turn; pair codec)."""
     if scales is not None:
         scale_mode = EQ_SCALES_GIVEN
     dev = layers[0].device

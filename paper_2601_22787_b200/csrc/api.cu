@@ -33,7 +33,9 @@ eq_status check_params(const eq_params* p) {
     if (p->chunk_symbols == 0 || p->chunk_symbols > 262144u) return EQ_ERR_ARG;
     if (p->scale_mode > EQ_SCALES_GIVEN) return EQ_ERR_ARG;
     if (p->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
-    if (p->chunk_mode > EQ_CHUNK_ROW) return EQ_ERR_ARG;
+    if (p->chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
+    if (p->chunk_mode == EQ_CHUNK_INTERLEAVED && (p->codec != EQ_CODEC_PAIR || p->chunk_symbols % 32 != 0))
+        return EQ_ERR_ARG;
     if (p->scale_mode == EQ_SCALES_SEARCH && !(p->lambda >= 0.0)) return EQ_ERR_ARG;
     return EQ_OK;
 }
@@ -112,6 +114,9 @@ extern "C" eq_status eq_encode_bounds(const eq_tensor* layers, uint32_t n_layers
                                       uint64_t* payload_cap, uint32_t* n_chunks, uint64_t* scratch_bytes) {
     EQ_TRY(check_layers(layers, n_layers));
     EQ_TRY(check_params(p));
+    if (p->chunk_mode == EQ_CHUNK_INTERLEAVED)        // R17: 16-symbol groups must not straddle rows
+        for (uint32_t l = 0; l < n_layers; ++l)
+            if (layers[l].cols % 16 != 0) return EQ_ERR_SHAPE;
     uint64_t syms = 0;
     for (uint32_t l = 0; l < n_layers; ++l) syms += (uint64_t)layers[l].rows * (uint64_t)layers[l].cols;
     const uint64_t nc = count_chunks(layers, n_layers, p->chunk_symbols, p->chunk_mode);

@@ -30,22 +30,36 @@ constexpr float kQmax = 448.0f;              // E4M3 Q_max
     } while (0)
 
 // Chunk geometry of one layer: chunking restarts every `seg` symbols — the
-// whole layer (EQ_CHUNK_LAYER) or one row (EQ_CHUNK_ROW) — so a segment holds cps =
-// ceil(seg / cs) chunks, all of cs symbols but the last.
+// whole layer (EQ_CHUNK_LAYER, EQ_CHUNK_INTERLEAVED) or one row (EQ_CHUNK_ROW) — so a segment
+// holds cps = ceil(seg / cs) chunks, all of cs symbols but the last.  Under EQ_CHUNK_INTERLEAVED
+// (R17) the first nil = 32·⌊seg / 32cs⌋ chunks of the layer are interleaved: chunk k < nil is
+// chunk j = k mod 32 of super-chunk s = ⌊k / 32⌋ and holds the super-chunk's 16-symbol groups
+// j, j + 32, …, i.e. symbol i sits at s·32cs + (⌊i/16⌋·32 + j)·16 + i mod 16.
+constexpr uint32_t kIlWays = 32, kIlGroup = 16;
 struct ChunkGeom {
     uint64_t seg;          // segment length in symbols
     uint32_t cps;          // chunks per segment
+    uint32_t nil;          // leading interleaved chunks of the layer (EQ_CHUNK_INTERLEAVED), else 0
 };
 __host__ __device__ __forceinline__ ChunkGeom chunk_geom(uint32_t mode, uint64_t rows, uint64_t cols, uint32_t cs) {
     const uint64_t seg = mode == EQ_CHUNK_ROW ? cols : rows * cols;
-    return ChunkGeom{seg, (uint32_t)((seg + cs - 1) / cs)};
+    const uint32_t nil = mode == EQ_CHUNK_INTERLEAVED ? (uint32_t)(seg / ((uint64_t)kIlWays * cs)) * kIlWays : 0u;
+    return ChunkGeom{seg, (uint32_t)((seg + cs - 1) / cs), nil};
 }
 __host__ __device__ __forceinline__ uint64_t layer_chunks(uint32_t mode, uint64_t rows, uint64_t cols, uint32_t cs) {
     const ChunkGeom g = chunk_geom(mode, rows, cols, cs);
     return (rows * cols / g.seg) * g.cps;
 }
-// first symbol (within the layer) and length of the layer's local chunk k
-__host__ __device__ __forceinline__ uint64_t chunk_start(const ChunkGeom& g, uint32_t cs, uint32_t k, uint32_t& n) {
+// first symbol (within the layer) and length of the layer's local chunk k; *gstride = layer
+// positions between consecutive 16-symbol groups of the chunk (16: contiguous; 512: R17)
+__host__ __device__ __forceinline__ uint64_t chunk_start(const ChunkGeom& g, uint32_t cs, uint32_t k, uint32_t& n,
+                                                         uint32_t* gstride = nullptr) {
+    if (k < g.nil) {
+        if (gstride) *gstride = kIlWays * kIlGroup;
+        n = cs;
+        return (uint64_t)(k / kIlWays) * kIlWays * cs + (uint64_t)(k % kIlWays) * kIlGroup;
+    }
+    if (gstride) *gstride = kIlGroup;
     const uint32_t s = k / g.cps, j = k - s * g.cps;
     const uint64_t a = (uint64_t)j * cs;
     n = (uint32_t)(g.seg - a < cs ? g.seg - a : cs);

@@ -472,6 +472,7 @@ struct ChainW {
     bool i8;
     uint32_t n, i;
     uint32_t a, e;         // chunk payload byte range [a, e)
+    uint32_t gs;           // layer positions between the chunk's 16-symbol groups: 16, or 512 (R17)
     bool active, runaway, fast;
 };
 

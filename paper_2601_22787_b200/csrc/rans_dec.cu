@@ -407,7 +407,7 @@ __device__ __forceinline__ void chain_setup_w(ChainW& c, const DecBlock& B, uint
     uint32_t l = 0;
     while (l + 1 < B.n_layers && chunk >= B.layer[l + 1].chunk0) ++l;
     const DecLayer& Ly = B.layer[l];
-    const uint64_t sym0 = chunk_start(Ly.geom, B.cs, chunk - Ly.chunk0, c.n);
+    const uint64_t sym0 = chunk_start(Ly.geom, B.cs, chunk - Ly.chunk0, c.n, &c.gs);
     const uint32_t a = __ldg(B.off + chunk), e = __ldg(B.off + chunk + 1);
     if (e < a || (uint64_t)e > B.payload_bytes || e - a < 4) {
         atomicOr(err, EQ_EF_TRUNCATED);
@@ -432,6 +432,7 @@ __device__ __forceinline__ void chain_setup_w(ChainW& c, const DecBlock& B, uint
     // 16 / 32-symbol groups with 32-byte stores need a 32-byte aligned chunk start (row chunks
     // start at row·cols + j·cs) and whole groups per row (bf16: one scale per group)
     c.fast = BF16 ? ((Ly.cols & 15) == 0 && ((sym0 | B.cs) & 15) == 0) : (((sym0 | B.cs) & 31) == 0);
+    if (c.gs != kIlGroup) c.fast = true;           // R17 chunk: cs % 32 == 0, cols % 16 == 0 (validated)
 }
 
 // after the initial segments landed: 4-byte little-endian state, then the first word
@@ -555,16 +556,12 @@ k_decode_w(const __grid_constant__ DecParams P) {
 
 
 // ================================================================ EQ_CODEC_PAIR decoder (R15)
-#ifndef EQ_PAIR_LOOP2
-#define EQ_PAIR_LOOP2 1
-#endif
 // Same CTA ↔ block and lane ↔ chunk mapping and staging as k_decode_w; the pair tables and the
 // pair / single decode steps are in pair_core.cuh (shared with the fused GEMM).
 template <bool BF16, bool NARROW>
 __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload, const PairTab& T) {
     if (!c.active || c.runaway) return;
     const uint32_t qlim = c.e + (2 + kWBias);
-#if EQ_PAIR_LOOP2
     if (c.fast) {
         // group loop with a down-counter and a running 32-byte output pointer; the runaway test
         // shares the loop test; the f16-scale dequant (the usual case) is tested first
@@ -599,19 +596,24 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
                     hi = make_uint4(dequant2(q[2], c.s), dequant2(q[2] >> 16, c.s), dequant2(q[3], c.s), dequant2(q[3] >> 16, c.s));
                 }
                 st_out32(o, lo, hi);
-                c.col += 16;
+                c.col += c.gs;                         // the next group: 16 symbols on, or 512 (R17)
                 if (c.col >= c.cols) {                 // next row: its scale (unless this was the last group)
-                    c.col -= c.cols;
-                    ++c.row;
+                    do {
+                        c.col -= c.cols;
+                        ++c.row;
+                    } while (c.col >= c.cols);
                     if (ng > 1 || tail) {
                         c.s = bf16_bits_to_float(c.sc[c.row]);
                         s16 = c.i8 ? 0u : (uint32_t)scale_f16(c.s);
                     }
                 }
-            } else {
+            } else if (c.gs == kIlGroup) {
                 st_out32(o, make_uint4(q[0], q[1], q[2], q[3]), make_uint4(q[4], q[5], q[6], q[7]));
+            } else {                                   // R17: the two groups are 512 positions apart
+                st_out(reinterpret_cast<uint4*>(o), make_uint4(q[0], q[1], q[2], q[3]));
+                st_out(reinterpret_cast<uint4*>(o + c.gs), make_uint4(q[4], q[5], q[6], q[7]));
             }
-            o += 32;
+            o += 2 * c.gs;                             // 16 bf16 / 32 FP8 symbols on (32 B if contiguous)
             --ng;
         }
         c.i += (ng0 - ng) * G;
@@ -619,25 +621,6 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
         c.s16 = (uint16_t)s16;
         if (c.r.Q > qlim) { c.runaway = true; return; }
     }
-#else
-    if (c.fast) {
-        const uint32_t G = BF16 ? 16 : 32;
-        while (c.i + G <= c.n) {
-            uint32_t q[8];
-            #pragma unroll
-            for (int k = 0; k < (BF16 ? 4 : 8); ++k) {
-                const uint32_t a = decode_pair<NARROW>(c.x, c.r, T, payload);
-                const uint32_t b = decode_pair<NARROW>(c.x, c.r, T, payload);
-                q[k] = __byte_perm(a, b, 0x5410);
-                if ((k & 3) == 3) ring_step_w(c.r, payload);
-            }
-            if (BF16) store16_bf16(c, q);
-            else st_out32(c.out + c.i, make_uint4(q[0], q[1], q[2], q[3]), make_uint4(q[4], q[5], q[6], q[7]));
-            c.i += G;
-            if (c.r.Q > qlim) { c.runaway = true; return; }
-        }
-    }
-#endif
     uint32_t k = 0;                                // generic / ragged tail
     for (; c.i + 2 <= c.n; c.i += 2) {
         const uint32_t ab = decode_pair<NARROW>(c.x, c.r, T, payload);
@@ -745,7 +728,12 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     d.scales = blk.scales;
     d.payload_bytes = blk.payload_bytes;
     if (blk.format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if (blk.codec > EQ_CODEC_PAIR || blk.chunk_mode > EQ_CHUNK_ROW) return EQ_ERR_ARG;
+    if (blk.codec > EQ_CODEC_PAIR || blk.chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
+    if (blk.chunk_mode == EQ_CHUNK_INTERLEAVED && (blk.codec != EQ_CODEC_PAIR || blk.chunk_symbols % 32 != 0))
+        return EQ_ERR_ARG;                         // R17 is decoded by k_decode_p only
+    if (blk.chunk_mode == EQ_CHUNK_INTERLEAVED)    // R17: whole 16-symbol groups per row
+        for (uint32_t l = 0; l < blk.n_layers && l < EQ_MAX_LAYERS; ++l)
+            if (blk.layer_cols[l] % 16 != 0) return EQ_ERR_SHAPE;
     d.format = blk.format;
     d.codec = blk.codec;
     d.cs = blk.chunk_symbols;

@@ -35,11 +35,21 @@ struct EncParams {
     ChunkGeom geom[EQ_MAX_LAYERS];
 };
 
-__device__ __forceinline__ void chunk_range(const EncParams& P, uint32_t c, uint64_t& base, uint32_t& n) {
+__device__ __forceinline__ void chunk_range(const EncParams& P, uint32_t c, uint64_t& base, uint32_t& n,
+                                            uint32_t& gstride) {
     uint32_t l = 0;
     while (l + 1 < P.n_layers && c >= P.chunk0[l + 1]) ++l;
-    base = P.sym_base[l] + chunk_start(P.geom[l], P.cs, c - P.chunk0[l], n);
+    base = P.sym_base[l] + chunk_start(P.geom[l], P.cs, c - P.chunk0[l], n, &gstride);
 }
+
+// symbol i of a chunk: contiguous (gstride 16) or R17-interleaved (gstride 512) 16-symbol groups
+struct ChunkSyms {
+    const uint8_t* p;
+    uint32_t gstride;
+    __device__ __forceinline__ uint32_t operator[](int64_t i) const {
+        return p[(uint64_t)(i >> 4) * gstride + (uint64_t)(i & 15)];
+    }
+};
 
 __device__ __forceinline__ void load_table(const EncParams& P, uint32_t* sf, uint32_t* scum) {
     // sf[s] = freq, scum[s] = cumulative (code order); one warp scans, others wait
@@ -68,8 +78,9 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
     if (c >= P.n_chunks) return;
     uint64_t base;
     uint32_t n;
-    chunk_range(P, c, base, n);
-    const uint8_t* sym = P.codes + base;
+    uint32_t gstride;
+    chunk_range(P, c, base, n, gstride);
+    const ChunkSyms sym{P.codes + base, gstride};
     uint8_t* dst = nullptr;
     uint64_t end = 0, beg = 0;
     if (WRITE) {
@@ -175,8 +186,9 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_pair(const __grid_consta
     if (c >= P.n_chunks) return;
     uint64_t base;
     uint32_t n;
-    chunk_range(P, c, base, n);
-    const uint8_t* sym = P.codes + base;
+    uint32_t gstride;
+    chunk_range(P, c, base, n, gstride);
+    const ChunkSyms sym{P.codes + base, gstride};
     uint64_t end = 0, beg = 0;
     WordEmitter E{kLw, 0, nullptr};
     if (WRITE) {
@@ -268,7 +280,9 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     if (!blk->payload || !blk->chunk_off || !blk->freq) return EQ_ERR_ARG;
     if (blk->n_layers == 0 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (blk->chunk_symbols == 0 || blk->chunk_symbols > 262144u) return EQ_ERR_ARG;
-    if (blk->codec > EQ_CODEC_PAIR || blk->chunk_mode > EQ_CHUNK_ROW) return EQ_ERR_ARG;
+    if (blk->codec > EQ_CODEC_PAIR || blk->chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
+    if (blk->chunk_mode == EQ_CHUNK_INTERLEAVED && (blk->codec != EQ_CODEC_PAIR || blk->chunk_symbols % 32 != 0))
+        return EQ_ERR_ARG;
     EncParams P;
     memset(&P, 0, sizeof(P));
     P.codes = codes;
@@ -285,6 +299,7 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     uint32_t chunk = 0;
     for (uint32_t l = 0; l < blk->n_layers; ++l) {
         if (blk->layer_rows[l] < 1 || blk->layer_cols[l] < 1) return EQ_ERR_SHAPE;
+        if (blk->chunk_mode == EQ_CHUNK_INTERLEAVED && blk->layer_cols[l] % 16 != 0) return EQ_ERR_SHAPE;
         const uint64_t sz = (uint64_t)blk->layer_rows[l] * (uint64_t)blk->layer_cols[l];
         P.chunk0[l] = chunk;
         P.sym_base[l] = base;
