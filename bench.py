@@ -201,26 +201,28 @@ def decoder_source_sha() -> str:
     return h.hexdigest()[:16]
 
 
-def traffic_from_profiles(codec: str, kind: str, blocks: int, chunk_symbols: int):
+def traffic_from_profiles(codec: str, kind: str, blocks: int, chunk_symbols: int, chunk_mode: str = "layer"):
     """DRAM bytes per launch of the decode kernel from the committed ncu --set full summary —
     only if it was captured on THIS kernel source (sha) and launch (blocks, chunk size);
     otherwise None (a stale figure is never reported)."""
     p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
     try:
         c = json.load(open(p))[codec]
-        e = dict(c[kind], **{k: c.get(k) for k in ("kernel_sha", "blocks", "chunk_symbols", "when", "source")})
+        e = dict(c[kind], **{k: c.get(k) for k in ("kernel_sha", "blocks", "chunk_symbols", "chunk_mode", "when",
+                                                    "source")})
     except Exception:
         return None, "no ncu capture"
     if e.get("kernel_sha") != decoder_source_sha():
         return None, f"ncu capture stale (kernel sha {e.get('kernel_sha')} != {decoder_source_sha()})"
-    if e.get("blocks") != blocks or e.get("chunk_symbols") != chunk_symbols:
+    if (e.get("blocks") != blocks or e.get("chunk_symbols") != chunk_symbols
+            or e.get("chunk_mode", "layer") != chunk_mode):
         return None, "ncu capture of another launch"
     return e["dram_bytes_per_launch"], f"{e.get('source', p)} (kernel sha {e['kernel_sha']}, {e.get('when', '?')})"
 
 
-def inst_from_profiles(codec: str, kind: str, blocks: int, chunk_symbols: int):
+def inst_from_profiles(codec: str, kind: str, blocks: int, chunk_symbols: int, chunk_mode: str = "layer"):
     """Warp-level SASS instructions per launch from the same sha-matched ncu capture, or None."""
-    tr, _ = traffic_from_profiles(codec, kind, blocks, chunk_symbols)
+    tr, _ = traffic_from_profiles(codec, kind, blocks, chunk_symbols, chunk_mode)
     if tr is None:
         return None
     try:
@@ -462,15 +464,15 @@ def main():
     launch_ms = statistics.mean(per)
     achieved = bytes_bf16 / (launch_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
-    traffic, traffic_src = traffic_from_profiles(args.codec, "bf16", len(blocks), cs)
-    inst = inst_from_profiles(args.codec, "bf16", len(blocks), cs)
+    traffic, traffic_src = traffic_from_profiles(args.codec, "bf16", len(blocks), cs, args.chunk_mode)
+    inst = inst_from_profiles(args.codec, "bf16", len(blocks), cs, args.chunk_mode)
 
     fp8, dec8 = None, None
     if not args.no_fp8:
         dec8 = eq.Decoder(blocks, eq.EQ_OUT_FP8)
         t8, per8 = time_decoder(dec8, args.steps, args.warmup)
         l8 = statistics.mean(per8)
-        tr8, _ = traffic_from_profiles(args.codec, "fp8", len(blocks), cs)
+        tr8, _ = traffic_from_profiles(args.codec, "fp8", len(blocks), cs, args.chunk_mode)
         fp8 = {"value": shard.aggregate_gbs(bytes_fp8, world, args.steps, t8), "unit": "GB/s",
                "ms_per_step": t8 / args.steps, "frac": bytes_fp8 / (l8 / 1e3) / 1e9 / peak, "traffic": tr8}
 

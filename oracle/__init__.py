@@ -31,6 +31,8 @@ CHUNK_SYMBOLS = 4096
 FMT_E4M3, FMT_INT8 = 0, 1
 CODEC_BYTE, CODEC_WORD = 0, 1      # rANS renormalisation: bytes (R9) / 16-bit words (R14)
 CODEC_PAIR = 2                      # word rANS over pairs of symbols with escapes (R15)
+CODEC_PAIR_G = 3                    # the same with each 16-symbol group's escaped codes after its pairs (R18)
+PAIR_CODECS = (CODEC_PAIR, CODEC_PAIR_G)
 CHUNK_LAYER, CHUNK_ROW = 0, 1       # chunks restart at every layer start / also at every row start (§8c.10)
 CHUNK_INTERLEAVED = 2                # R17: layer chunking over 16-symbol groups dealt to 32 chunks in turn
 IL_GROUP, IL_WAYS = 16, 32
@@ -112,6 +114,12 @@ def lib():
                                                                      P, ctypes.c_int]),
             "eqo_decode_dequant_layer_mt_pair_seg": (ctypes.c_int, [P, P, i64, i64, i64, i64, i64, P, P, P, i32, P, u16,
                                                                     P, ctypes.c_int]),
+            "eqo_encode_chunk_pairg": (i64, [P, i64, P, P, i32, P, u16, P, i64]),
+            "eqo_decode_chunk_pairg": (ctypes.c_int, [P, i64, P, P, i32, P, u16, P, i64]),
+            "eqo_encode_block_pairx": (i64, [P, P, i32, i64, P, P, i32, P, u16, P, i64, P, i32]),
+            "eqo_decode_block_pairx": (ctypes.c_int, [P, P, P, i32, i64, P, P, i32, P, u16, P, i32]),
+            "eqo_decode_dequant_layer_mt_pairx_seg": (ctypes.c_int, [P, P, i64, i64, i64, i64, i64, P, P, P, i32, P,
+                                                                     u16, P, ctypes.c_int, i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -322,13 +330,14 @@ def pair_table(hist: np.ndarray) -> PairTable:
     return PairTable(rc, K.value, pf, fe.value)
 
 
-def encode_chunk_pair(sym: np.ndarray, freq: np.ndarray, pt: PairTable) -> bytes:
+def encode_chunk_pair(sym: np.ndarray, freq: np.ndarray, pt: PairTable, grouped: bool = False) -> bytes:
+    """One chunk of the pair codec: R15 order, or R18 (grouped escapes) when ``grouped``."""
     sym = np.ascontiguousarray(sym, dtype=np.uint8).reshape(-1)
     freq = np.ascontiguousarray(freq, dtype=np.uint16)
     cap = 4 + 4 * sym.size + 8
     out = np.zeros(cap, dtype=np.uint8)
-    n = lib().eqo_encode_chunk_pair(_p(sym), sym.size, _p(freq), _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc,
-                                    _p(out), cap)
+    fn = lib().eqo_encode_chunk_pairg if grouped else lib().eqo_encode_chunk_pair
+    n = fn(_p(sym), sym.size, _p(freq), _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc, _p(out), cap)
     if n == -2:
         raise ValueError("unknown-symbol")
     if n < 0:
@@ -336,11 +345,12 @@ def encode_chunk_pair(sym: np.ndarray, freq: np.ndarray, pt: PairTable) -> bytes
     return out[:n].tobytes()
 
 
-def decode_chunk_pair(data: bytes, freq: np.ndarray, pt: PairTable, n: int) -> np.ndarray:
+def decode_chunk_pair(data: bytes, freq: np.ndarray, pt: PairTable, n: int, grouped: bool = False) -> np.ndarray:
     buf = np.frombuffer(data, dtype=np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
     out = np.zeros(max(n, 1), dtype=np.uint8)
-    st = lib().eqo_decode_chunk_pair(_p(buf), len(data), _p(np.ascontiguousarray(freq, dtype=np.uint16)),
-                                     _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc, _p(out), n)
+    fn = lib().eqo_decode_chunk_pairg if grouped else lib().eqo_decode_chunk_pair
+    st = fn(_p(buf), len(data), _p(np.ascontiguousarray(freq, dtype=np.uint16)), _p(pt.rank_code), pt.K, _p(pt.pf),
+            pt.fesc, _p(out), n)
     if st == 1:
         raise ValueError("corrupt")
     if st == 2:
@@ -361,7 +371,7 @@ class OracleBlock:
     codes: np.ndarray = field(default=None, repr=False)   # vec(W_q) of the layers, concatenated (layer order)
     fmt: int = FMT_E4M3
     codec: int = CODEC_BYTE
-    pair: object = None              # PairTable (codec CODEC_PAIR)
+    pair: object = None              # PairTable (codecs CODEC_PAIR, CODEC_PAIR_G)
     chunk_mode: int = CHUNK_LAYER
 
     @property
@@ -432,12 +442,12 @@ def encode_codes(codes_list, layer_shapes, scales, cs: int = CHUNK_SYMBOLS, fmt:
     payload = np.zeros(cap, dtype=np.uint8)
     off = np.zeros(n_chunks + 1, dtype=np.uint32)
     pt = None
-    if codec == CODEC_PAIR:
+    if codec in PAIR_CODECS:
         pt = pair_table(hist)
         cap = 4 * n_chunks + 4 * stream.size + 64
         payload = np.zeros(cap, dtype=np.uint8)
-        n = lib().eqo_encode_block_pair(_p(stream), _p(sizes), sizes.size, cs, _p(freq), _p(pt.rank_code),
-                                        pt.K, _p(pt.pf), pt.fesc, _p(payload), cap, _p(off))
+        n = lib().eqo_encode_block_pairx(_p(stream), _p(sizes), sizes.size, cs, _p(freq), _p(pt.rank_code),
+                                         pt.K, _p(pt.pf), pt.fesc, _p(payload), cap, _p(off), int(codec == CODEC_PAIR_G))
     else:
         n = lib().eqo_encode_block_codec(codec, _p(stream), _p(sizes), sizes.size, cs, _p(freq), _p(payload),
                                          cap, _p(off))
@@ -473,10 +483,11 @@ def decode_block(blk: OracleBlock) -> np.ndarray:
     out = np.zeros(int(sizes.sum()), dtype=np.uint8)
     payload = np.frombuffer(blk.payload, dtype=np.uint8).copy()
     off = np.ascontiguousarray(blk.chunk_off, dtype=np.uint32)
-    if blk.codec == CODEC_PAIR:
+    if blk.codec in PAIR_CODECS:
         pt = blk.pair
-        st = lib().eqo_decode_block_pair(_p(payload), _p(off), _p(sizes), sizes.size, blk.chunk_symbols,
-                                         _p(blk.freq), _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc, _p(out))
+        st = lib().eqo_decode_block_pairx(_p(payload), _p(off), _p(sizes), sizes.size, blk.chunk_symbols,
+                                          _p(blk.freq), _p(pt.rank_code), pt.K, _p(pt.pf), pt.fesc, _p(out),
+                                          int(blk.codec == CODEC_PAIR_G))
     else:
         st = lib().eqo_decode_block_codec(blk.codec, _p(payload), _p(off), _p(sizes), sizes.size,
                                           blk.chunk_symbols, _p(blk.freq), _p(out))
@@ -539,11 +550,12 @@ def decode_dequant_layer_mt(payload: np.ndarray, chunk_off: np.ndarray, cs: int,
     payload = np.ascontiguousarray(payload, dtype=np.uint8)
     off = np.ascontiguousarray(chunk_off, dtype=np.uint32)
     out = np.zeros(rows * cols, dtype=np.uint16)
-    if codec == CODEC_PAIR:
-        st = lib().eqo_decode_dequant_layer_mt_pair_seg(_p(payload), _p(off), off.size - 1, cs, rows * cols, cols, seg,
-                                                    _p(np.ascontiguousarray(scales, dtype=np.uint16)),
-                                                    _p(np.ascontiguousarray(freq, dtype=np.uint16)),
-                                                    _p(pair.rank_code), pair.K, _p(pair.pf), pair.fesc, _p(out), threads)
+    if codec in PAIR_CODECS:
+        st = lib().eqo_decode_dequant_layer_mt_pairx_seg(_p(payload), _p(off), off.size - 1, cs, rows * cols, cols,
+                                                         seg, _p(np.ascontiguousarray(scales, dtype=np.uint16)),
+                                                         _p(np.ascontiguousarray(freq, dtype=np.uint16)),
+                                                         _p(pair.rank_code), pair.K, _p(pair.pf), pair.fesc, _p(out),
+                                                         threads, int(codec == CODEC_PAIR_G))
         if st:
             raise ValueError({1: "corrupt", 2: "truncated"}[st])
         return out.reshape(rows, cols)

@@ -1014,18 +1014,149 @@ int eqo_decode_chunk_pair(const uint8_t* in, int64_t nbytes, const uint16_t freq
     return 0;
 }
 
+/* ------------------------------------------------------------------------------------
+ * Pair codec with grouped escapes (codec 3, EQO_CODEC_PAIRG; reading R18).  The
+ * same tables and the same coded symbols as codec 2 (R15) — only their ORDER in the rANS
+ * stream differs, so the coded size is the same up to the state's end effects.  The chunk's
+ * n symbols are cut into groups of 16 (the last one may be shorter, length g).  In decode
+ * order, a group is:
+ *   (1) its ⌊g/2⌋ pair positions in order, each a kept pair or the escape (pair table);
+ *   (2) for every escaped position, in increasing order, its two codes a then b (single table);
+ *   (3) if g is odd (the chunk's last group only), its last symbol (single table).
+ * The encoder writes the group sequence (1)(2)(3) of every group, first group first, into a
+ * list of (frequency, cumulative) steps and codes the list in reverse.
+ * ---------------------------------------------------------------------------------- */
+#define EQO_CODEC_PAIRG 3
+#define EQO_GROUP 16
+
+int64_t eqo_encode_chunk_pairg(const uint8_t* sym, int64_t n, const uint16_t freq[256], const uint8_t rank_code[16],
+                               int32_t K, const uint16_t pf[225], uint16_t fesc, uint8_t* out, int64_t cap)
+{
+    uint32_t cum[257], pcum[225], cesc;
+    eqo_cum(freq, cum);
+    eqo_pair_cum(pf, K, pcum, &cesc);
+    int rank[256];
+    for (int c = 0; c < 256; c++) rank[c] = -1;
+    for (int r = 0; r < K; r++) rank[rank_code[r]] = r;
+    /* the decode-order list of steps: at most 3 per pair position + 1 */
+    uint32_t* sf = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(3 * n / 2 + 2));
+    uint32_t* sc = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(3 * n / 2 + 2));
+    int64_t m = 0;
+    for (int64_t g0 = 0; g0 < n; g0 += EQO_GROUP) {
+        int64_t g = n - g0 < EQO_GROUP ? n - g0 : EQO_GROUP;
+        int esc[EQO_GROUP / 2];
+        for (int64_t i = 0; i < g / 2; i++) {                         /* (1) */
+            uint8_t a = sym[g0 + 2 * i], b = sym[g0 + 2 * i + 1];
+            if (freq[a] == 0 || freq[b] == 0) { free(sf); free(sc); return -2; }
+            int ra = rank[a], rb = rank[b];
+            esc[i] = !(ra >= 0 && rb >= 0 && pf[ra * EQO_PAIR_K + rb] > 0);
+            if (esc[i]) {
+                if (fesc == 0) { free(sf); free(sc); return -2; }
+                sf[m] = fesc; sc[m] = cesc; m++;
+            } else {
+                sf[m] = pf[ra * EQO_PAIR_K + rb]; sc[m] = pcum[ra * EQO_PAIR_K + rb]; m++;
+            }
+        }
+        for (int64_t i = 0; i < g / 2; i++) {                         /* (2) */
+            if (!esc[i]) continue;
+            uint8_t a = sym[g0 + 2 * i], b = sym[g0 + 2 * i + 1];
+            sf[m] = freq[a]; sc[m] = cum[a]; m++;
+            sf[m] = freq[b]; sc[m] = cum[b]; m++;
+        }
+        if (g & 1) {                                                  /* (3) */
+            uint8_t s = sym[g0 + g - 1];
+            if (freq[s] == 0) { free(sf); free(sc); return -2; }
+            sf[m] = freq[s]; sc[m] = cum[s]; m++;
+        }
+    }
+    int64_t tcap = 4 + 4 * n + 8;
+    uint8_t* tmp = (uint8_t*)malloc((size_t)tcap);
+    int64_t pos = tcap;
+    uint64_t x = 1u << 16;
+    for (int64_t k = m - 1; k >= 0; k--) eqo_w_put(&x, sf[k], sc[k], tmp, &pos);
+    free(sf);
+    free(sc);
+    pos -= 4;
+    for (int k = 0; k < 4; k++) tmp[pos + k] = (uint8_t)((x >> (8 * k)) & 0xFF);
+    int64_t len = tcap - pos;
+    if (len > cap) { free(tmp); return -1; }
+    memcpy(out, tmp + pos, (size_t)len);
+    free(tmp);
+    return len;
+}
+
+/* the single-table symbol owning slot sl, then its decode step */
+static int eqo_w_single(uint64_t* x, const uint16_t freq[256], const uint32_t cum[257], const uint8_t* in,
+                        int64_t nbytes, int64_t* p, uint8_t* s_out)
+{
+    uint32_t sl = (uint32_t)(*x % EQO_M);
+    int s = 0;
+    while (!(cum[s] <= sl && sl < cum[s + 1])) s++;
+    *s_out = (uint8_t)s;
+    return eqo_w_get(x, freq[s], cum[s], sl, in, nbytes, p);
+}
+
+int eqo_decode_chunk_pairg(const uint8_t* in, int64_t nbytes, const uint16_t freq[256], const uint8_t rank_code[16],
+                           int32_t K, const uint16_t pf[225], uint16_t fesc, uint8_t* sym, int64_t n)
+{
+    uint32_t cum[257], pcum[225], cesc;
+    eqo_cum(freq, cum);
+    eqo_pair_cum(pf, K, pcum, &cesc);
+    if (nbytes < 4) return 2;
+    uint64_t x = (uint64_t)in[0] | ((uint64_t)in[1] << 8) | ((uint64_t)in[2] << 16) | ((uint64_t)in[3] << 24);
+    int64_t p = 4;
+    for (int64_t g0 = 0; g0 < n; g0 += EQO_GROUP) {
+        int64_t g = n - g0 < EQO_GROUP ? n - g0 : EQO_GROUP;
+        int esc[EQO_GROUP / 2];
+        for (int64_t i = 0; i < g / 2; i++) {                         /* (1) */
+            uint32_t slot = (uint32_t)(x % EQO_M);
+            esc[i] = slot >= cesc;
+            if (esc[i]) {
+                if (eqo_w_get(&x, fesc, cesc, slot, in, nbytes, &p)) return 2;
+                continue;
+            }
+            int j = -1;                                              /* the kept pair owning slot */
+            for (int q = 0; q < 225 && j < 0; q++) {
+                int ra = q / EQO_PAIR_K, rb = q % EQO_PAIR_K;
+                if (ra < K && rb < K && pf[q] && pcum[q] <= slot && slot < pcum[q] + pf[q]) j = q;
+            }
+            if (j < 0) return 1;
+            sym[g0 + 2 * i] = rank_code[j / EQO_PAIR_K];
+            sym[g0 + 2 * i + 1] = rank_code[j % EQO_PAIR_K];
+            if (eqo_w_get(&x, pf[j], pcum[j], slot, in, nbytes, &p)) return 2;
+        }
+        for (int64_t i = 0; i < g / 2; i++) {                         /* (2) */
+            if (!esc[i]) continue;
+            if (eqo_w_single(&x, freq, cum, in, nbytes, &p, &sym[g0 + 2 * i])) return 2;
+            if (eqo_w_single(&x, freq, cum, in, nbytes, &p, &sym[g0 + 2 * i + 1])) return 2;
+        }
+        if (g & 1)                                                    /* (3) */
+            if (eqo_w_single(&x, freq, cum, in, nbytes, &p, &sym[g0 + g - 1])) return 2;
+    }
+    if (x != (1u << 16) || p != nbytes) return 1;
+    return 0;
+}
+
+typedef int64_t (*eqo_penc_fn)(const uint8_t*, int64_t, const uint16_t*, const uint8_t*, int32_t, const uint16_t*,
+                               uint16_t, uint8_t*, int64_t);
+typedef int (*eqo_pdec_fn)(const uint8_t*, int64_t, const uint16_t*, const uint8_t*, int32_t, const uint16_t*,
+                           uint16_t, uint8_t*, int64_t);
+/* the chunk coder of a pair codec: grouped = 0 -> R15 (codec 2), 1 -> R18 (codec 3) */
+static eqo_penc_fn eqo_penc(int32_t grouped) { return grouped ? eqo_encode_chunk_pairg : eqo_encode_chunk_pair; }
+static eqo_pdec_fn eqo_pdec(int32_t grouped) { return grouped ? eqo_decode_chunk_pairg : eqo_decode_chunk_pair; }
+
 /* block stream of the pair codec (same chunking as eqo_encode_block) */
-int64_t eqo_encode_block_pair(const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers, int64_t cs,
-                              const uint16_t freq[256], const uint8_t rank_code[16], int32_t K, const uint16_t pf[225],
-                              uint16_t fesc, uint8_t* payload, int64_t cap, uint32_t* chunk_off)
+int64_t eqo_encode_block_pairx(const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers, int64_t cs,
+                               const uint16_t freq[256], const uint8_t rank_code[16], int32_t K, const uint16_t pf[225],
+                               uint16_t fesc, uint8_t* payload, int64_t cap, uint32_t* chunk_off, int32_t grouped)
 {
     int64_t pos = 0, k = 0, sbase = 0;
     for (int32_t l = 0; l < n_layers; l++) {
         for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
             int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
             chunk_off[k++] = (uint32_t)pos;
-            int64_t len = eqo_encode_chunk_pair(codes + sbase + a, n, freq, rank_code, K, pf, fesc, payload + pos,
-                                                cap - pos);
+            int64_t len = eqo_penc(grouped)(codes + sbase + a, n, freq, rank_code, K, pf, fesc, payload + pos,
+                                            cap - pos);
             if (len < 0) return len;
             pos += len;
         }
@@ -1035,16 +1166,16 @@ int64_t eqo_encode_block_pair(const uint8_t* codes, const int64_t* layer_sizes, 
     return pos;
 }
 
-int eqo_decode_block_pair(const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
-                          int32_t n_layers, int64_t cs, const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
-                          const uint16_t pf[225], uint16_t fesc, uint8_t* codes)
+int eqo_decode_block_pairx(const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
+                           int32_t n_layers, int64_t cs, const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
+                           const uint16_t pf[225], uint16_t fesc, uint8_t* codes, int32_t grouped)
 {
     int64_t k = 0, sbase = 0;
     for (int32_t l = 0; l < n_layers; l++) {
         for (int64_t a = 0; a < layer_sizes[l]; a += cs) {
             int64_t n = layer_sizes[l] - a < cs ? layer_sizes[l] - a : cs;
-            int st = eqo_decode_chunk_pair(payload + chunk_off[k], (int64_t)chunk_off[k + 1] - chunk_off[k], freq,
-                                           rank_code, K, pf, fesc, codes + sbase + a, n);
+            int st = eqo_pdec(grouped)(payload + chunk_off[k], (int64_t)chunk_off[k + 1] - chunk_off[k], freq,
+                                       rank_code, K, pf, fesc, codes + sbase + a, n);
             if (st) return st;
             k++;
         }
@@ -1058,7 +1189,7 @@ int eqo_decode_block_pair(const uint8_t* payload, const uint32_t* chunk_off, con
 typedef struct {
     const uint8_t* payload; const uint32_t* chunk_off; int64_t cs, size, cols;
     const uint16_t* scales; const uint16_t* freq; const uint8_t* rank_code; int32_t K; const uint16_t* pf;
-    uint16_t fesc; uint16_t* out; int64_t k0, k1; int status; int64_t seg;
+    uint16_t fesc; uint16_t* out; int64_t k0, k1; int status; int64_t seg; int32_t grouped;
 } eqo_pjob;
 
 static void* eqo_pworker(void* p)
@@ -1068,7 +1199,7 @@ static void* eqo_pworker(void* p)
     j->status = 0;
     for (int64_t k = j->k0; k < j->k1; k++) {
         int64_t n, a = eqo_chunk_start(k, j->cs, j->seg, &n);
-        int st = eqo_decode_chunk_pair(j->payload + j->chunk_off[k], (int64_t)j->chunk_off[k + 1] - j->chunk_off[k],
+        int st = eqo_pdec(j->grouped)(j->payload + j->chunk_off[k], (int64_t)j->chunk_off[k + 1] - j->chunk_off[k],
                                        j->freq, j->rank_code, j->K, j->pf, j->fesc, sym, n);
         if (st && !j->status) j->status = st;
         for (int64_t i = 0; i < n; i++) {
@@ -1080,17 +1211,18 @@ static void* eqo_pworker(void* p)
     return NULL;
 }
 
-int eqo_decode_dequant_layer_mt_pair_seg(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks,
-                                         int64_t cs, int64_t size, int64_t cols, int64_t seg, const uint16_t* scales,
-                                         const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
-                                         const uint16_t pf[225], uint16_t fesc, uint16_t* out, int threads)
+int eqo_decode_dequant_layer_mt_pairx_seg(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks,
+                                          int64_t cs, int64_t size, int64_t cols, int64_t seg, const uint16_t* scales,
+                                          const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
+                                          const uint16_t pf[225], uint16_t fesc, uint16_t* out, int threads,
+                                          int32_t grouped)
 {
     if (threads < 1) threads = 1;
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
     eqo_pjob* jobs = (eqo_pjob*)malloc(sizeof(eqo_pjob) * (size_t)threads);
     for (int t = 0; t < threads; t++) {
         jobs[t] = (eqo_pjob){payload, chunk_off, cs, size, cols, scales, freq, rank_code, K, pf, fesc, out,
-                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0, seg};
+                             n_chunks * t / threads, n_chunks * (t + 1) / threads, 0, seg, grouped};
         pthread_create(&th[t], NULL, eqo_pworker, &jobs[t]);
     }
     int st = 0;
@@ -1108,6 +1240,31 @@ int eqo_decode_dequant_layer_mt_pair(const uint8_t* payload, const uint32_t* chu
                                      const uint8_t rank_code[16], int32_t K, const uint16_t pf[225], uint16_t fesc,
                                      uint16_t* out, int threads)
 {
-    return eqo_decode_dequant_layer_mt_pair_seg(payload, chunk_off, n_chunks, cs, size, cols, size, scales, freq,
-                                                rank_code, K, pf, fesc, out, threads);
+    return eqo_decode_dequant_layer_mt_pairx_seg(payload, chunk_off, n_chunks, cs, size, cols, size, scales, freq,
+                                                rank_code, K, pf, fesc, out, threads, 0);
+}
+
+/* codec 2 (R15) forms of the block and layer helpers */
+int64_t eqo_encode_block_pair(const uint8_t* codes, const int64_t* layer_sizes, int32_t n_layers, int64_t cs,
+                              const uint16_t freq[256], const uint8_t rank_code[16], int32_t K, const uint16_t pf[225],
+                              uint16_t fesc, uint8_t* payload, int64_t cap, uint32_t* chunk_off)
+{
+    return eqo_encode_block_pairx(codes, layer_sizes, n_layers, cs, freq, rank_code, K, pf, fesc, payload, cap,
+                                  chunk_off, 0);
+}
+
+int eqo_decode_block_pair(const uint8_t* payload, const uint32_t* chunk_off, const int64_t* layer_sizes,
+                          int32_t n_layers, int64_t cs, const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
+                          const uint16_t pf[225], uint16_t fesc, uint8_t* codes)
+{
+    return eqo_decode_block_pairx(payload, chunk_off, layer_sizes, n_layers, cs, freq, rank_code, K, pf, fesc, codes, 0);
+}
+
+int eqo_decode_dequant_layer_mt_pair_seg(const uint8_t* payload, const uint32_t* chunk_off, int64_t n_chunks,
+                                         int64_t cs, int64_t size, int64_t cols, int64_t seg, const uint16_t* scales,
+                                         const uint16_t freq[256], const uint8_t rank_code[16], int32_t K,
+                                         const uint16_t pf[225], uint16_t fesc, uint16_t* out, int threads)
+{
+    return eqo_decode_dequant_layer_mt_pairx_seg(payload, chunk_off, n_chunks, cs, size, cols, seg, scales, freq,
+                                                 rank_code, K, pf, fesc, out, threads, 0);
 }

@@ -18,4 +18,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 ncu --set full --clock-control none --import-source on -k regex:k_decode -s 1 -c 2 -o $OUT/decode \
     python bench.py --profile --steps 1 --warmup 1 --no-e2e --no-cpu --lam 230.2 > $OUT/full_bench.log 2>&1; echo full=$?
 python scripts/ncu_summary.py $OUT/decode.ncu-rep > $OUT/summary.json 2>&1
+python -c "import json; d=json.loads(open('$OUT/bench.json').read().strip().splitlines()[-1]); print(d['config'].get('chunk_mode','layer'))" > $OUT/chunk_mode.txt
 tail -c 3000 $OUT/bench.json

@@ -37,6 +37,8 @@ def main(ev, rnd):
     sha_f = os.path.join(ev, "kernel_sha.txt")
     sha = open(sha_f).read().strip() if os.path.exists(sha_f) else None
     when = open(os.path.join(ev, "when.txt")).read().strip() if os.path.exists(os.path.join(ev, "when.txt")) else None
+    cm_f = os.path.join(ev, "chunk_mode.txt")          # the captured launch's chunk layout (R10/R16/R17)
+    chunk_mode = open(cm_f).read().strip() if os.path.exists(cm_f) else "layer"
     for d in full:
         k = d["kernel"]
         codec = "word" if "k_decode_w" in k else "pair" if "k_decode_p" in k else "byte" if "k_decode" in k else None
@@ -53,6 +55,7 @@ def main(ev, rnd):
         summ[codec]["when"] = when
         summ[codec]["blocks"] = 32
         summ[codec]["chunk_symbols"] = 4096
+        summ[codec]["chunk_mode"] = chunk_mode
         summ[codec][kind] = {"kernel": k, "duration_ms_under_ncu": _num(d["gpu__time_duration.sum"]),
                              "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                              "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")}

@@ -406,21 +406,104 @@ def test_cpu_baseline_helpers_match_block_decode():
     three codecs): timing helper, same arithmetic."""
     W = eqsynth.weights(64, 1024, seed=9)
     S = (o.absmax_scales(W).astype(np.int32) + 1600).astype(np.uint16)
-    for codec in (o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR):
+    for codec in (o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G):
         blk = o.quantize_encode([W], scales=[S], cs=512, codec=codec)
         payload = np.frombuffer(blk.payload + b"\0" * 16, dtype=np.uint8)
         out = o.decode_dequant_layer_mt(payload, blk.chunk_off, 512, 64, 1024, S, blk.freq, 3, codec, blk.pair)
         assert (out == o.decode_dequant(blk)[0]).all(), codec
 
 
+# ------------------------------------------------------------------ grouped escapes (DESIGN.md R18)
+def test_pair_grouped_worked_streams(golden):
+    """Hand-derived R18 chunk (tests/golden/rans_pair_worked.json): an escape BEFORE a kept pair
+    of its group, so its two codes come after that pair — bytes differ from the R15 stream."""
+    for case in golden["rans_pair_worked"]["grouped_cases"]:
+        h = hist_of(_expand(case["counts"]))
+        f = o.normalize(h)
+        pt = o.pair_table(h)
+        sym = np.array(case["symbols"], dtype=np.uint8)
+        data = o.encode_chunk_pair(sym, f, pt, grouped=True)
+        assert data.hex() == case["bytes_hex"], case["name"]
+        assert (o.decode_chunk_pair(data, f, pt, sym.size, grouped=True) == sym).all()
+        assert (o.encode_chunk_pair(sym, f, pt).hex() != data.hex()) == case["r15_bytes_hex_differs"]
+
+
+def _escaped(sym, pt):
+    rank = np.full(256, -1)
+    rank[pt.rank_code[:pt.K]] = np.arange(pt.K)
+    a, b = rank[sym[0:sym.size // 2 * 2:2]], rank[sym[1:sym.size // 2 * 2:2]]
+    ok = (a >= 0) & (b >= 0)
+    ok[ok] = pt.pf[a[ok] * 15 + b[ok]] > 0
+    return ~ok
+
+
+@pytest.mark.parametrize("n", [16, 17, 32, 33, 46, 64])
+def test_pair_grouped_equals_r15_when_escapes_end_their_group(n):
+    """When every escaped pair is the LAST pair position of its 16-symbol group, R18's decode
+    order (group pairs, then the escaped codes, then an odd last symbol) is R15's order, so the
+    two streams are byte-identical — a 32-symbol group, or escapes deferred to the chunk's end,
+    would break this for n > 16."""
+    rng = np.random.default_rng(n)
+    h = np.zeros(256, np.uint64)
+    h[0], h[1], h[2], h[3] = 1000, 10, 1, 1            # (2,2), (2,3), (3,2), (3,3) are escapes
+    f, pt = o.normalize(h), o.pair_table(h)
+    for t in range(20):
+        sym = rng.choice(np.array([0, 0, 0, 1], np.uint8), n)
+        for g0 in range(0, n, 16):
+            last = min(g0 + 16, n) // 2 * 2 - 2       # the group's last pair position (symbol index)
+            if last >= g0 and rng.random() < 0.7:
+                sym[last], sym[last + 1] = rng.choice([2, 3]), rng.choice([2, 3])
+        esc = _escaped(sym, pt)
+        assert esc.any() or t > 0 or n < 16
+        data = o.encode_chunk_pair(sym, f, pt, grouped=True)
+        assert data == o.encode_chunk_pair(sym, f, pt)
+        assert (o.decode_chunk_pair(data, f, pt, n, grouped=True) == sym).all()
+
+
+@pytest.mark.parametrize("kind", ["skewed", "uniform", "subset2", "single", "subset40"])
+def test_pair_grouped_round_trip_and_same_rate(kind):
+    """R18 codes the same symbols as R15 with the same (f, c), only reordered: lossless, and
+    the payloads differ by at most one 16-bit word (the final state's end effect); escapes
+    anywhere, every length class (empty groups, odd tails, several groups)."""
+    rng = np.random.default_rng((hash(kind) + 7) & 0xFFFF)
+    for t in range(8):
+        n = int(rng.choice([1, 2, 3, 15, 16, 17, 31, 4095, 4096, 4097, int(rng.integers(1, 12000))]))
+        s = eqsynth.random_codes_stream(n, int(rng.integers(1 << 30)), kind)
+        h = o.histogram(s)
+        f = o.normalize(h)
+        pt = o.pair_table(h)
+        g = o.encode_chunk_pair(s, f, pt, grouped=True)
+        r = o.encode_chunk_pair(s, f, pt)
+        assert (o.decode_chunk_pair(g, f, pt, n, grouped=True) == s).all()
+        assert abs(len(g) - len(r)) <= 2, (n, len(g), len(r))
+    with pytest.raises(ValueError):
+        o.decode_chunk_pair(g[:-2], f, pt, n, grouped=True)
+
+
+def test_pair_grouped_decoder_rejects_the_r15_order():
+    """The hand-derived R15 stream (escape at position 0, kept pair after it) read as R18 is not
+    the same chunk: the integrity check (final state L, every word consumed) or the symbols
+    differ — the two orders are distinguishable."""
+    h = np.zeros(256, np.uint64)
+    h[0], h[1], h[2], h[3] = 1000, 10, 1, 1
+    f, pt = o.normalize(h), o.pair_table(h)
+    sym = np.array([2, 3, 0, 1, 0], np.uint8)
+    r15 = o.encode_chunk_pair(sym, f, pt)
+    try:
+        got = o.decode_chunk_pair(r15, f, pt, 5, grouped=True)
+        assert not (got == sym).all()
+    except ValueError:
+        pass
+
+
 # ------------------------------------------------------------------ EQ_CHUNK_ROW (SURVEY §8c.10, §8(f) row 1)
-ALL_CODECS = [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR]
+ALL_CODECS = [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G]
 
 
 def _chunk_alone(blk, k, n):
     data = blk.payload[int(blk.chunk_off[k]):int(blk.chunk_off[k + 1])]
-    if blk.codec == o.CODEC_PAIR:
-        return o.decode_chunk_pair(data, blk.freq, blk.pair, n)
+    if blk.codec in o.PAIR_CODECS:
+        return o.decode_chunk_pair(data, blk.freq, blk.pair, n, grouped=blk.codec == o.CODEC_PAIR_G)
     return o.decode_chunk(data, blk.freq, n, blk.codec)
 
 
