@@ -41,7 +41,7 @@ FALLBACK_HBM_GBS = 6650.0            # B200_PROFILING.md fallback, used only wit
 DEFAULT_LAMBDA = 230.2               # reference arm only: the GPU calibration of λ for 2.0 bits
 
 
-CODECS = {"byte": 0, "word": 1, "pair": 2}     # EQ_CODEC_* (include/entquant.h)
+CODECS = {"byte": 0, "word": 1, "pair": 2, "pairg": 3}     # EQ_CODEC_* (include/entquant.h)
 CHUNK_MODES = {"layer": 0, "row": 1, "interleaved": 2}   # EQ_CHUNK_* (include/entquant.h, R16, R17)
 
 
@@ -75,12 +75,12 @@ def parse():
                          "16-symbol groups of 32 consecutive chunks dealt round-robin, so a warp's 32 "
                          "lanes store 1 KB contiguously; pair codec only).  auto: interleaved for the "
                          "pair codec, layer for the others")
-    ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"],
+    ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair", "pairg"],
                     help="wire format: byte rANS (SPEC S:355, R9), 16-bit-word rANS (R14), or the word "
                          "rANS over symbol pairs with escapes (R15, default: fastest, smallest)")
     args = ap.parse_args()
     if args.chunk_mode == "auto":
-        args.chunk_mode = "interleaved" if args.codec == "pair" else "layer"
+        args.chunk_mode = "interleaved" if args.codec in ("pair", "pairg") else "layer"
     return args
 
 
@@ -320,7 +320,7 @@ def oracle_layers(blk, o):
     off_all = blk.chunk_off.cpu().numpy().astype(np.uint32)
     payload = blk.payload.cpu().numpy()
     table = blk.freq.cpu().numpy().view(np.uint16)
-    pair = oracle_pair_table(table, o) if blk.codec == CODECS["pair"] else None
+    pair = oracle_pair_table(table, o) if blk.codec in (CODECS["pair"], CODECS["pairg"]) else None
     scales = blk.scales.cpu().view(torch.int16).numpy().view(np.uint16)
     out, k0, r0 = [], 0, 0
     row = getattr(blk, "chunk_mode", 0) == CHUNK_MODES["row"]
@@ -529,7 +529,7 @@ def main():
             "lambda": lam,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_source": peak_src, "kernel": f"k_decode_{'p' if args.codec == 'pair' else 'w' if args.codec == 'word' else ''}",
+                         "peak_source": peak_src, "kernel": f"k_decode_{'p' if args.codec in ('pair', 'pairg') else 'w' if args.codec == 'word' else ''}",
                          "kernel_sha": decoder_source_sha(),
                          "algorithmic_bytes_per_launch": bytes_bf16, "launch_ms": launch_ms,
                          "chunks": n_chunks, "decoder_lanes": lanes,

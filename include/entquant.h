@@ -66,6 +66,11 @@ typedef enum {
                                     /* 512 u16: [0,256) single table, [256,481) pair table  */
                                     /* by ra*15+rb, [481] escape, [482] K, [484,492) rank   */
                                     /* codes as bytes                                        */
+#define EQ_CODEC_PAIR_G 3u          /* R18: EQ_CODEC_PAIR's tables and symbols, reordered:   */
+                                    /* per 16-symbol group of a chunk, the group's pair     */
+                                    /* steps (kept pair or escape), then the two codes of   */
+                                    /* each escaped pair in position order, then an odd     */
+                                    /* last symbol; same table buffer as EQ_CODEC_PAIR      */
 
 /* Chunking of a block's symbol stream (R10). */
 #define EQ_CHUNK_LAYER 0u           /* chunks of chunk_symbols restart at every layer start */
@@ -77,7 +82,7 @@ typedef enum {
                                     /* symbols whose 16-symbol groups are dealt to their 32  */
                                     /* chunks in turn (chunk j: groups j, j+32, ...); the    */
                                     /* rest of the layer is plain chunks.  A decoder warp's  */
-                                    /* stores are then contiguous.  Pair codec only; needs   */
+                                    /* stores are then contiguous.  Pair codecs only; needs  */
                                     /* chunk_symbols % 32 == 0 and cols % 16 == 0 (else      */
                                     /* EQ_ERR_ARG / EQ_ERR_SHAPE); not for eq_qmatmul        */
 

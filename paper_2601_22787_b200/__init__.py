@@ -24,7 +24,8 @@ LIB_PATH = os.environ.get("EQ_LIB") or os.path.join(_HERE, "libentquant.so")
 EQ_OK, EQ_ERR_ARG, EQ_ERR_SHAPE, EQ_ERR_EMPTY, EQ_ERR_BUFFER = 0, 1, 2, 3, 4
 EQ_ERR_CORRUPT, EQ_ERR_TRUNCATED, EQ_ERR_UNKNOWN_SYMBOL, EQ_ERR_UNREACHABLE_TARGET, EQ_ERR_CUDA = 5, 6, 7, 8, 9
 EQ_FMT_E4M3, EQ_FMT_INT8 = 0, 1
-EQ_CODEC_BYTE, EQ_CODEC_WORD, EQ_CODEC_PAIR = 0, 1, 2
+EQ_CODEC_BYTE, EQ_CODEC_WORD, EQ_CODEC_PAIR, EQ_CODEC_PAIR_G = 0, 1, 2, 3
+PAIR_CODECS = (EQ_CODEC_PAIR, EQ_CODEC_PAIR_G)   # R15 and its group-ordered form R18: one table layout
 # The binding's default codec: the pair codec (R15), the fastest decoder and the lowest rate.
 # The C ABI's zero-initialised eq_params keep SPEC's byte codec (R9); pass codec= for it here.
 EQ_DEFAULT_CODEC = EQ_CODEC_PAIR
@@ -253,7 +254,7 @@ def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH
                     chunk_mode: int = EQ_CHUNK_LAYER) -> Block:
     """Alg. 1 for one block of bf16 CUDA matrices.  Synchronous (reads payload size).
     ``exclude``: layer indices kept at AbsMax scales (λ = 0); ``codec``: rANS
-    renormalisation (EQ_CODEC_BYTE, R9 / EQ_CODEC_WORD, R14 / EQ_CODEC_PAIR, R15);
+    renormalisation (EQ_CODEC_BYTE, R9 / EQ_CODEC_WORD, R14 / EQ_CODEC_PAIR, R15 / EQ_CODEC_PAIR_G, R18);
     ``chunk_mode``: EQ_CHUNK_LAYER, EQ_CHUNK_ROW (chunks also restart at row starts) or
     EQ_CHUNK_INTERLEAVED (R17: 16-symbol groups dealt to 32 chunks in turn; pair codec)."""
     if scales is not None:
@@ -267,7 +268,7 @@ def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH
     rows = sum(W.shape[0] for W in layers)
     payload = torch.empty(cap.value, dtype=torch.uint8, device=dev)
     off = torch.empty(nc.value + 1, dtype=torch.int32, device=dev)
-    freq = torch.zeros(512 if codec == EQ_CODEC_PAIR else 256, dtype=torch.int16, device=dev)
+    freq = torch.zeros(512 if codec in PAIR_CODECS else 256, dtype=torch.int16, device=dev)
     if scales is None:
         scales = torch.empty(rows, dtype=torch.bfloat16, device=dev)
     else:
@@ -463,7 +464,7 @@ def rans_encode(codes: torch.Tensor, shapes, freq: torch.Tensor, scales: torch.T
         nc = sum(r * ((c + chunk_symbols - 1) // chunk_symbols) for r, c in shapes)
     else:
         nc = sum((r * c + chunk_symbols - 1) // chunk_symbols for r, c in shapes)
-    cap = (4 * nc + (3 if codec == EQ_CODEC_PAIR else 2) * n + EQ_PAYLOAD_SLACK + 255) // 256 * 256
+    cap = (4 * nc + (3 if codec in PAIR_CODECS else 2) * n + EQ_PAYLOAD_SLACK + 255) // 256 * 256
     dev = codes.device
     blk = Block(torch.empty(cap, dtype=torch.uint8, device=dev), 0, torch.empty(nc + 1, dtype=torch.int32, device=dev),
                 freq, scales if scales is not None else torch.ones(sum(r for r, _ in shapes), dtype=torch.bfloat16, device=dev),

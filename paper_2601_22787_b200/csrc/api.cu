@@ -32,9 +32,9 @@ eq_status check_params(const eq_params* p) {
     if (p->format > EQ_FMT_INT8 || p->prob_bits != EQ_PROB_BITS) return EQ_ERR_ARG;
     if (p->chunk_symbols == 0 || p->chunk_symbols > 262144u) return EQ_ERR_ARG;
     if (p->scale_mode > EQ_SCALES_GIVEN) return EQ_ERR_ARG;
-    if (p->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
+    if (p->codec > EQ_CODEC_PAIR_G) return EQ_ERR_ARG;
     if (p->chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
-    if (p->chunk_mode == EQ_CHUNK_INTERLEAVED && (p->codec != EQ_CODEC_PAIR || p->chunk_symbols % 32 != 0))
+    if (p->chunk_mode == EQ_CHUNK_INTERLEAVED && (!is_pair_codec(p->codec) || p->chunk_symbols % 32 != 0))
         return EQ_ERR_ARG;
     if (p->scale_mode == EQ_SCALES_SEARCH && !(p->lambda >= 0.0)) return EQ_ERR_ARG;
     return EQ_OK;
@@ -123,7 +123,7 @@ extern "C" eq_status eq_encode_bounds(const eq_tensor* layers, uint32_t n_layers
     // worst case per chunk: 4-byte state + at most 2 renormalisation bytes per symbol
     // (two bytes, EQ_CODEC_BYTE, or one 16-bit word, EQ_CODEC_WORD)
     // (EQ_CODEC_PAIR: an escaped pair is three words for two symbols)
-    const uint64_t cap = align_up(4 * nc + (p->codec == EQ_CODEC_PAIR ? 3 : 2) * syms + EQ_PAYLOAD_SLACK, 256);
+    const uint64_t cap = align_up(4 * nc + (is_pair_codec(p->codec) ? 3 : 2) * syms + EQ_PAYLOAD_SLACK, 256);
     if (payload_cap) *payload_cap = cap;
     if (n_chunks) *n_chunks = (uint32_t)nc;
     if (scratch_bytes) *scratch_bytes = carve(layers, n_layers, (uint32_t)nc, nullptr).bytes;
@@ -181,7 +181,7 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
     }
     // metadata ℳ and Alg. 1 l.4-5
     EQ_TRY(eq_build_table(S.hist, out->freq, S.err, stream));
-    if (p->codec == EQ_CODEC_PAIR) EQ_TRY(eq_build_pair_table(S.hist, out->freq, S.err, stream));   // R15
+    if (is_pair_codec(p->codec)) EQ_TRY(eq_build_pair_table(S.hist, out->freq, S.err, stream));   // R15
     EQ_TRY(eq_rans_encode(S.codes, out, S.sizes, S.total, S.err, stream));
     uint64_t total = 0;
     uint32_t e = 0;
@@ -195,8 +195,8 @@ extern "C" eq_status eq_quantize_encode(const eq_tensor* layers, uint32_t n_laye
 }
 
 // ---------------------------------------------------------------- e2e with host buffers
-// bytes of a block's table buffer: 256 u16, or 512 for EQ_CODEC_PAIR (include/entquant.h)
-static uint64_t table_bytes(const eq_block& b) { return b.codec == EQ_CODEC_PAIR ? 1024 : 512; }
+// bytes of a block's table buffer: 256 u16, or 512 for the pair codecs (include/entquant.h)
+static uint64_t table_bytes(const eq_block& b) { return is_pair_codec(b.codec) ? 1024 : 512; }
 extern "C" uint64_t eq_decode_host_workspace_bytes(const eq_block* blocks, uint32_t n_blocks, uint32_t out_dtype) {
     if (!blocks || n_blocks == 0) return 0;
     uint64_t total = 0, pos = 0;
@@ -388,7 +388,7 @@ extern "C" eq_status eq_calibrate_lambda(const eq_tensor* layers, uint32_t n_lay
         rows_total += (double)layers[l].rows;
         chunks += (double)layer_chunks(p->chunk_mode, layers[l].rows, layers[l].cols, p->chunk_symbols);
     }
-    const double side = (8.0 * (4.0 * chunks + 4.0 * chunks + 2.0 * rows_total) + (p->codec == EQ_CODEC_PAIR ? 8192.0 : 4096.0) * std::ceil(n_layers / 7.0)) / params;
+    const double side = (8.0 * (4.0 * chunks + 4.0 * chunks + 2.0 * rows_total) + (is_pair_codec(p->codec) ? 8192.0 : 4096.0) * std::ceil(n_layers / 7.0)) / params;
 
     // sampled row lists
     std::vector<uint32_t> rl;

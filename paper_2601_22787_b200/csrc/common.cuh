@@ -13,6 +13,10 @@ namespace eq {
 
 constexpr uint32_t kL = 1u << 23;            // rANS lower bound, EQ_CODEC_BYTE (R9)
 constexpr uint32_t kLw = 1u << 16;           // rANS lower bound, EQ_CODEC_WORD (R14)
+// the pair codecs share tables and decoder (R15; R18 only reorders a group's steps)
+__host__ __device__ constexpr bool is_pair_codec(uint32_t codec) {
+    return codec == EQ_CODEC_PAIR || codec == EQ_CODEC_PAIR_G;
+}
 constexpr uint32_t kProbBits = 12;
 constexpr uint32_t kM = 1u << kProbBits;
 constexpr float kQmax = 448.0f;              // E4M3 Q_max

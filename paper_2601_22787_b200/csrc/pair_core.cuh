@@ -23,7 +23,12 @@
 namespace eq {
 
 constexpr int kPairOff = 256, kFescIdx = 481, kKIdx = 482, kRankIdx = 484;
+constexpr uint32_t kEscId = 225;                  // LUT id of the escape slots (codes-table word 225)
+constexpr uint32_t kEscCodes = 0xFFFFu;           // ... which holds this sentinel
 constexpr int kPairLutWords = kM + 113;           // + the 225 × u16 codes table
+constexpr int kPairValWords = 226;                // + (bf16 output of R18) the bf16x2 value table
+constexpr uint32_t kValOff = 4 * kM + 4 * 113;    // its byte offset from the LUT base
+constexpr uint32_t kEscVals = 0xFFFFFFFFu;        // the escape's value word (bf16 NaN pair: never a grid value)
 
 constexpr uint32_t kPairSmemBytes = kPairLutWords * 4 + kM + 258 * 2;
 
@@ -34,6 +39,7 @@ struct PairTab {
     uint32_t esc_lo;       // slot << 20 at and above which a pair step is the escape (0xFFFFFFFF: none)
     uint32_t fesc, cesc;   // escape frequency and cumulative start
     uint32_t k2p20, k2p12; // 2^20, 2^12 passed at run time (IMAD forms on the FMA pipe)
+    uint32_t k2p10;        // 2^10 (TOPID entries)
 };
 
 // the LUT entry's 8-bit id of rank pair (ra, rb), ra, rb < 15: a bijection onto [0, 225) in
@@ -44,6 +50,27 @@ __device__ __forceinline__ uint32_t pair_id(uint32_t ra, uint32_t rb) {
     if (d <= 14) return d * (d + 1) / 2 + ra;
     const uint32_t e = 28 - d;
     return 225 - (e + 1) * (e + 2) / 2 + ra - (d - 14);
+}
+
+// the grid value of a code (E4M3, R1; or Int8) as bf16 bits — exact: ≤ 4 / 7 significant bits
+__device__ __forceinline__ uint32_t grid_bf16(uint32_t code, bool i8) {
+    float v;
+    if (i8) {
+        v = (float)(int8_t)code;
+    } else {
+        __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)code, __NV_E4M3);
+        v = __half2float(*reinterpret_cast<__half*>(&h));
+    }
+    return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+
+// two bf16 products in one instruction, each the RNE of the exact product (subnormals kept):
+// s·v has at most 8 + 7 significant bits, so this is the bf16 RNE of P:142's s·Q — the same
+// single rounding as the f32 product followed by one RNE
+__device__ __forceinline__ uint32_t mul_bf16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
 }
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
@@ -101,6 +128,71 @@ __device__ __forceinline__ uint32_t decode_pair(uint32_t& x, WordReader& r, cons
     return lds_u16(T.lut_s + 4 * kM + ((e & 0xFFu) << 1));              // pair id -> codes
 }
 
+// one pair step of EQ_CODEC_PAIR_G (R18): no escape branch — an escape is decoded as the pair
+// table's symbol it is (its LUT entry holds its f and slot − c) and yields the codes sentinel;
+// `esc` accumulates "this group had an escape" (one ISETP with a predicate OR per step)
+// VALS (bf16 output): the pair's two grid values as bf16x2 from the value table instead of the codes.
+// TOPID (narrow tables built with TOPID): entries (f − 1) | (slot − c) << 11 | id << 24, so ONE
+// 64-bit product e·2^10 yields 4·id (high word: the value table offset) and (slot − c) << 21.
+template <bool NARROW = false, bool VALS = false, bool TOPID = false>
+__device__ __forceinline__ uint32_t decode_pair_g(uint32_t& x, WordReader& r, const PairTab& T, bool& esc) {
+    uint32_t lo, xs;
+    asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
+    esc |= lo >= T.esc_lo;
+    const uint32_t e = lds_u32(T.lut_s + (lo >> 18));
+    if (TOPID && NARROW) {
+        uint32_t lo2, id4;
+        asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo2), "=r"(id4) : "r"(e), "r"(T.k2p10));
+        x = mad_lo(e & 0x7FFu, xs, xs + (lo2 >> 21));                  // f·⌊x/M⌋ + slot − c
+        renorm_w(x, r);
+        if (VALS) return lds_u32(T.lut_s + kValOff + id4);
+        return lds_u16(T.lut_s + 4 * kM + (id4 >> 1));
+    }
+    const uint32_t fm1 = mad_hi(e, T.k2p12, 0u);                        // e >> 20
+    if (NARROW) {
+        x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 21));       // f·⌊x/M⌋ + slot − c
+        renorm_w(x, r);
+        if (VALS) return lds_u32(T.lut_s + kValOff + ((e & 0x1FEu) << 1));
+        return lds_u16(T.lut_s + 4 * kM + (e & 0x1FEu));
+    }
+    x = mad_lo(fm1, xs, xs + (mad_lo(e, T.k2p12, 0u) >> 20));
+    renorm_w(x, r);
+    if (VALS) return lds_u32(T.lut_s + kValOff + ((e & 0xFFu) << 2));
+    return lds_u16(T.lut_s + 4 * kM + ((e & 0xFFu) << 1));
+}
+
+// R18 patch for the value words of a group (bf16 output): v[k] is pair position k's bf16x2
+__device__ __forceinline__ void patch_escapes_vals(uint32_t* v, uint32_t& x, WordReader& r, const PairTab& T,
+                                                   const uint8_t* payload, bool i8) {
+    #pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        if (v[k] == kEscVals) {
+            ring_step_w(r, payload);
+            const uint32_t a = decode_single_p(x, r, T);
+            const uint32_t b = decode_single_p(x, r, T);
+            v[k] = grid_bf16(a, i8) | (grid_bf16(b, i8) << 16);
+        }
+    }
+}
+
+// R18, after a group's pair steps: each escaped position (codes sentinel), in position order,
+// is replaced by its two codes (a, then b) decoded with the single table.  q[0..3] hold the
+// group's 8 pair positions, two per word (position k in the half k & 1 of q[k >> 1]); only
+// positions < m are pair positions of the group.
+__device__ __forceinline__ void patch_escapes(uint32_t* q, uint32_t m, uint32_t& x, WordReader& r, const PairTab& T,
+                                              const uint8_t* payload) {
+    #pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t sh = 16 * (k & 1);
+        if (k < m && ((q[k >> 1] >> sh) & 0xFFFFu) == kEscCodes) {
+            ring_step_w(r, payload);               // up to 2 more words: keep the ring ahead
+            const uint32_t a = decode_single_p(x, r, T);
+            const uint32_t b = decode_single_p(x, r, T);
+            q[k >> 1] = (q[k >> 1] & ~(0xFFFFu << sh)) | ((a | (b << 8)) << sh);
+        }
+    }
+}
+
 // lut[slot] = entry(slot, s) for the s with cm[s] <= slot < cm[s + 1] (cm[0..NS], cm[NS] = kM),
 // NT threads: thread t fills slots [S·t, S·t + S), S = kM / NT, one binary search then a forward
 // walk over the symbol boundaries (zero-width symbols are stepped over), 16-byte stores
@@ -139,9 +231,12 @@ __device__ __forceinline__ void lut_walk(uint32_t* lut, const uint32_t* cm, F en
 // scanning both tables concurrently made ptxas rematerialise them per pair step, −1.6 %.)
 // pcum lives in lut1's space (the pair LUT walk is done, behind a barrier of the NT threads,
 // before lut1 is filled); cesc returns the escape's cumulative start pcum[225].
-template <int NT, bool ALL = false, bool NARROW_OK = false>   // ALL: the CTA has exactly NT threads
+// VALS: also the bf16x2 value table (kPairValWords words after the codes table) of format i8;
+// TOPID: narrow entries laid out (f − 1) | (slot − c) << 11 | id << 24 (decode_pair_g).
+template <int NT, bool ALL = false, bool NARROW_OK = false, bool VALS = false, bool TOPID = false>
 __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint32_t* lut, uint8_t* lut1,
-                                                      uint16_t* cum, uint32_t& cesc, uint32_t* err) {
+                                                      uint16_t* cum, uint32_t& cesc, uint32_t* err,
+                                                      bool i8 = false) {
     uint32_t* pcum = reinterpret_cast<uint32_t*>(lut1);
     static_assert(NT >= 64 && (NT & (NT - 1)) == 0 && NT <= 1024, "thread count");
     const int t = threadIdx.x;
@@ -213,14 +308,17 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
         if (t == 0) atomicOr(err, EQ_EF_CORRUPT);
         return 0;
     }
-    const bool narrow = NARROW_OK && s_fmax <= 2048u;
+    const bool narrow = NARROW_OK && s_fmax <= 2048u && pcum[226] - pcum[225] <= 2048u;
     cesc = s_cesc;
     if (ALL || t < NT) {
-        // (escape slots keep id 0xFF; their entries are never read: the escape test precedes the lookup)
+        // escape slots: an ordinary entry (slot − c, f − 1) with id kEscId, whose codes-table
+        // word is the sentinel 0xFFFF (code 0xFF, E4M3 NaN, is never a symbol, R1).  R15 tests
+        // for the escape before the lookup; R18 takes the step like any pair and patches later.
         const uint32_t idsh = narrow ? 1u : 0u, scsh = narrow ? 9u : 8u;
         lut_walk<226, NT>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
             const uint32_t f = pcum[q + 1] - pcum[q];
-            const uint32_t id = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : 0xFFu;
+            const uint32_t id = q < 225 ? pair_id((uint32_t)q / 15, (uint32_t)q % 15) : kEscId;
+            if (TOPID && narrow) return (f - 1) | ((slot - pcum[q]) << 11) | (id << 24);
             return (id << idsh) | ((slot - pcum[q]) << scsh) | ((f - 1) << 20);
         });
         asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");     // pcum read by all: lut1 may be written
@@ -245,6 +343,13 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
         uint16_t* ctab = reinterpret_cast<uint16_t*>(lut + kM);
         for (int q = t; q < 225; q += NT)
             ctab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = (uint16_t)(rcb[q / 15] | (rcb[q % 15] << 8));
+        if (t == 0) ctab[kEscId] = kEscCodes;
+        if (VALS) {
+            uint32_t* vtab = lut + kValOff / 4;
+            for (int q = t; q < 225; q += NT)
+                vtab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = grid_bf16(rcb[q / 15], i8) | (grid_bf16(rcb[q % 15], i8) << 16);
+            if (t == 0) vtab[kEscId] = kEscVals;
+        }
     }
     return narrow ? 2u : 1u;
 }
@@ -260,6 +365,7 @@ __device__ __forceinline__ PairTab pair_tab(const uint16_t* freq, const uint32_t
     T.esc_lo = T.fesc ? (T.cesc << 20) : 0xFFFFFFFFu;
     T.k2p20 = k2p20;
     T.k2p12 = k2p12;
+    T.k2p10 = k2p12 >> 2;
     return T;
 }
 

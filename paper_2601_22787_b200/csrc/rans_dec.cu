@@ -558,7 +558,45 @@ k_decode_w(const __grid_constant__ DecParams P) {
 // ================================================================ EQ_CODEC_PAIR decoder (R15)
 // Same CTA ↔ block and lane ↔ chunk mapping and staging as k_decode_w; the pair tables and the
 // pair / single decode steps are in pair_core.cuh (shared with the fused GEMM).
-template <bool BF16, bool NARROW>
+#ifndef EQ_PAIR_TOPID
+#define EQ_PAIR_TOPID 1             // R18 bf16: narrow entries with the id on top (decode_pair_g)
+#endif
+// R18 (EQ_CODEC_PAIR_G) generic path: one group of len ≤ 16 symbols — its pair steps, the
+// escaped pairs' codes, its odd last symbol — stored one symbol at a time (ragged tails and
+// chunks without the 32-byte group stores; contiguous positions)
+template <bool BF16, bool NARROW, bool TOPID>
+__device__ __forceinline__ void group_generic_g(ChainW& c, const uint8_t* payload, const PairTab& T, uint32_t len) {
+    const uint32_t m = len >> 1;
+    uint32_t q[4] = {0u, 0u, 0u, 0u};
+    bool esc = false;
+    #pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        if (k < m) {
+            q[k >> 1] |= decode_pair_g<NARROW, false, TOPID>(c.x, c.r, T, esc) << (16 * (k & 1));
+            if ((k & 3) == 3) ring_step_w(c.r, payload);
+        }
+    }
+    if (esc) patch_escapes(q, m, c.x, c.r, T, payload);
+    uint32_t last = 0;
+    if (len & 1) {
+        ring_step_w(c.r, payload);
+        last = decode_single_p(c.x, c.r, T);
+    }
+    #pragma unroll
+    for (uint32_t h = 0; h < 16; ++h) {
+        if (h >= len) break;
+        const uint32_t sym = h < 2 * m ? (q[h >> 2] >> (8 * (h & 3))) & 0xFFu : last;
+        store_one<BF16>(c.out, c.i + h, sym, c.s, c.i8);
+        if (BF16 && ++c.col == c.cols) {
+            c.col = 0;
+            ++c.row;
+            if (c.i + h + 1 < c.n) c.s = bf16_bits_to_float(c.sc[c.row]);
+        }
+    }
+    c.i += len;
+}
+
+template <bool BF16, bool NARROW, bool GROUPED>
 __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload, const PairTab& T) {
     if (!c.active || c.runaway) return;
     const uint32_t qlim = c.e + (2 + kWBias);
@@ -571,14 +609,51 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
         uint32_t ng = ng0;
         uint8_t* o = c.out + (uint64_t)c.i * (BF16 ? 2 : 1);
         uint32_t s16 = c.i8 ? 0u : (uint32_t)c.s16;
+        uint32_t s2 = (BF16 && GROUPED) ? c.sc[c.row] * 0x10001u : 0u;     // the row's bf16 scale, twice
         while (ng != 0 && c.r.Q <= qlim) {
+            if (BF16 && GROUPED) {                 // R18 + bf16: value words, one bf16x2 product per pair
+                uint32_t v[8];
+                bool esc = false;
+                #pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = decode_pair_g<NARROW, true, EQ_PAIR_TOPID>(c.x, c.r, T, esc);
+                ring_step_w(c.r, payload);
+                if (esc) patch_escapes_vals(v, c.x, c.r, T, payload, c.i8);
+                st_out32(o, make_uint4(mul_bf16x2(v[0], s2), mul_bf16x2(v[1], s2), mul_bf16x2(v[2], s2),
+                                       mul_bf16x2(v[3], s2)),
+                         make_uint4(mul_bf16x2(v[4], s2), mul_bf16x2(v[5], s2), mul_bf16x2(v[6], s2),
+                                    mul_bf16x2(v[7], s2)));
+                c.col += c.gs;
+                if (c.col >= c.cols) {
+                    do {
+                        c.col -= c.cols;
+                        ++c.row;
+                    } while (c.col >= c.cols);
+                    if (ng > 1 || tail) s2 = c.sc[c.row] * 0x10001u;
+                }
+                o += 2 * c.gs;
+                --ng;
+                continue;
+            }
             uint32_t q[8];
+            bool esc = false;
             #pragma unroll
             for (int k = 0; k < (BF16 ? 4 : 8); ++k) {
-                const uint32_t a = decode_pair<NARROW>(c.x, c.r, T, payload);
-                const uint32_t b = decode_pair<NARROW>(c.x, c.r, T, payload);
+                uint32_t a, b;
+                if (GROUPED) {
+                    a = decode_pair_g<NARROW>(c.x, c.r, T, esc);
+                    b = decode_pair_g<NARROW>(c.x, c.r, T, esc);
+                } else {
+                    a = decode_pair<NARROW>(c.x, c.r, T, payload);
+                    b = decode_pair<NARROW>(c.x, c.r, T, payload);
+                }
                 q[k] = __byte_perm(a, b, 0x5410);
-                if ((k & 3) == 3) ring_step_w(c.r, payload);
+                if ((k & 3) == 3) {
+                    ring_step_w(c.r, payload);
+                    if (GROUPED) {                 // R18: the group's escaped codes follow its pair steps
+                        if (esc) patch_escapes(q + (k - 3), 8, c.x, c.r, T, payload);
+                        esc = false;
+                    }
+                }
             }
             if (BF16) {
                 uint4 lo, hi;
@@ -618,8 +693,19 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
         }
         c.i += (ng0 - ng) * G;
         if (ng != 0) { c.runaway = true; return; }
+        if (BF16 && GROUPED && ng0 != 0 && tail) { // the tail's row scale (s2 tracked the rows)
+            c.s = bf16_bits_to_float(c.sc[c.row]);
+            s16 = c.i8 ? 0u : (uint32_t)scale_f16(c.s);
+        }
         c.s16 = (uint16_t)s16;
         if (c.r.Q > qlim) { c.runaway = true; return; }
+    }
+    if (GROUPED) {                                 // generic / ragged tail, group by group (R18)
+        while (c.i < c.n) {
+            group_generic_g<BF16, NARROW, BF16 && EQ_PAIR_TOPID>(c, payload, T, min(16u, c.n - c.i));
+            if (c.r.Q > qlim) { c.runaway = true; return; }
+        }
+        return;
     }
     uint32_t k = 0;                                // generic / ragged tail
     for (; c.i + 2 <= c.n; c.i += 2) {
@@ -654,11 +740,11 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
 #endif
 constexpr int kPThreads = EQ_PTHREADS;
 constexpr uint32_t kDecPSmem = kPThreads * kWRing;          // dynamic: the staging rings
-template <bool BF16>
+template <bool BF16, bool GROUPED>
 __global__ void __launch_bounds__(kPThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) uint8_t rings[];      // kPThreads × kWRing
-    __shared__ __align__(16) uint32_t lut[kPairLutWords];  // pair LUT + codes table
+    __shared__ __align__(16) uint32_t lut[kPairLutWords + (BF16 && GROUPED ? kPairValWords : 0)];  // pair LUT + codes (+ values)
     __shared__ __align__(16) uint8_t lut1[kM];             // (first the pair cum, see pair_tables_build)
     __shared__ uint16_t cum[258];
 
@@ -671,7 +757,9 @@ k_decode_p(const __grid_constant__ DecParams P) {
                         (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
     stage_commit();
     uint32_t cesc;
-    const uint32_t mode = pair_tables_build<kPThreads, true, EQ_PAIR_NARROW>(B.freq, lut, lut1, cum, cesc, P.err);
+    const uint32_t mode = pair_tables_build<kPThreads, true, EQ_PAIR_NARROW, BF16 && GROUPED,
+                                            BF16 && GROUPED && EQ_PAIR_TOPID>(
+        B.freq, lut, lut1, cum, cesc, P.err, B.format == EQ_FMT_INT8);
     if (!mode) {
         stage_wait_all();
         return;
@@ -680,8 +768,8 @@ k_decode_p(const __grid_constant__ DecParams P) {
     __syncthreads();
     const PairTab T = pair_tab(B.freq, lut, lut1, cum, cesc, P.k2p20, P.k2p12);
     chain_start_w(c);
-    if (EQ_PAIR_NARROW && mode == 2) chain_finish_p<BF16, true>(c, B.payload, T);    // CTA-uniform
-    else chain_finish_p<BF16, false>(c, B.payload, T);
+    if (EQ_PAIR_NARROW && mode == 2) chain_finish_p<BF16, true, GROUPED>(c, B.payload, T);    // CTA-uniform
+    else chain_finish_p<BF16, false, GROUPED>(c, B.payload, T);
     stage_wait_all();
     if (c.active && (c.runaway || c.x != kLw || c.r.Q - (2u + kWBias) != c.e)) atomicOr(P.err, EQ_EF_CORRUPT);
 }
@@ -728,8 +816,8 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     d.scales = blk.scales;
     d.payload_bytes = blk.payload_bytes;
     if (blk.format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if (blk.codec > EQ_CODEC_PAIR || blk.chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
-    if (blk.chunk_mode == EQ_CHUNK_INTERLEAVED && (blk.codec != EQ_CODEC_PAIR || blk.chunk_symbols % 32 != 0))
+    if (blk.codec > EQ_CODEC_PAIR_G || blk.chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
+    if (blk.chunk_mode == EQ_CHUNK_INTERLEAVED && (!is_pair_codec(blk.codec) || blk.chunk_symbols % 32 != 0))
         return EQ_ERR_ARG;                         // R17 is decoded by k_decode_p only
     if (blk.chunk_mode == EQ_CHUNK_INTERLEAVED)    // R17: whole 16-symbol groups per row
         for (uint32_t l = 0; l < blk.n_layers && l < EQ_MAX_LAYERS; ++l)
@@ -759,14 +847,19 @@ static eq_status fill_desc(const eq_block& blk, const uint64_t* offs, DecBlock& 
     return EQ_OK;
 }
 
+static const void* pair_kernel(bool bf16, bool grouped) {
+    return bf16 ? (grouped ? (const void*)k_decode_p<true, true> : (const void*)k_decode_p<true, false>)
+                : (grouped ? (const void*)k_decode_p<false, true> : (const void*)k_decode_p<false, false>);
+}
+
 extern "C" eq_status eq_decode_lanes(uint32_t codec, uint32_t out_dtype, int device, uint64_t* lanes) {
-    if (!lanes || codec > EQ_CODEC_PAIR || (out_dtype != EQ_OUT_FP8 && out_dtype != EQ_OUT_BF16)) return EQ_ERR_ARG;
+    if (!lanes || codec > EQ_CODEC_PAIR_G || (out_dtype != EQ_OUT_FP8 && out_dtype != EQ_OUT_BF16)) return EQ_ERR_ARG;
     const bool bf = out_dtype == EQ_OUT_BF16;
     const void* fn;
     int threads, per;
     size_t dyn;
-    if (codec == EQ_CODEC_PAIR) {
-        fn = bf ? (const void*)k_decode_p<true> : (const void*)k_decode_p<false>;
+    if (is_pair_codec(codec)) {
+        fn = pair_kernel(bf, codec == EQ_CODEC_PAIR_G);
         threads = kPThreads, per = kPThreads, dyn = kDecPSmem;
     } else if (codec == EQ_CODEC_WORD) {
         fn = bf ? (const void*)k_decode_w<true> : (const void*)k_decode_w<false>;
@@ -813,20 +906,19 @@ extern "C" eq_status eq_decode_dequant(const eq_block* blocks, uint32_t n_blocks
         uint32_t ctas = 0;
         for (uint32_t k = 0; k < nb; ++k) {
             EQ_TRY(fill_desc(blocks[b0 + k], all.get() + (size_t)(b0 + k) * EQ_MAX_LAYERS, P.b[k], ctas));
-            const uint32_t per = codec == EQ_CODEC_PAIR ? (uint32_t)kPThreads
+            const uint32_t per = is_pair_codec(codec) ? (uint32_t)kPThreads
                                : codec == EQ_CODEC_WORD ? (uint32_t)kWChunksPerCta : (uint32_t)kChunksPerCta;
             ctas += (P.b[k].n_chunks + per - 1) / per;
         }
         // blocks with zero chunks cannot exist (layers are non-empty); ctas > 0
-        if (codec == EQ_CODEC_PAIR) {
-            const int bi = out_dtype == EQ_OUT_BF16 ? 1 : 0;
+        if (is_pair_codec(codec)) {
+            const bool bi = out_dtype == EQ_OUT_BF16, g = codec == EQ_CODEC_PAIR_G;
             const uint32_t dyn = kDecPSmem;
-            EQ_CUDA_TRY(cudaFuncSetAttribute(bi ? (const void*)k_decode_p<true> : (const void*)k_decode_p<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-            if (bi)
-                k_decode_p<true><<<ctas, kPThreads, dyn, st>>>(P);
-            else
-                k_decode_p<false><<<ctas, kPThreads, dyn, st>>>(P);
+            EQ_CUDA_TRY(cudaFuncSetAttribute(pair_kernel(bi, g), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+            if (bi && g) k_decode_p<true, true><<<ctas, kPThreads, dyn, st>>>(P);
+            else if (bi) k_decode_p<true, false><<<ctas, kPThreads, dyn, st>>>(P);
+            else if (g) k_decode_p<false, true><<<ctas, kPThreads, dyn, st>>>(P);
+            else k_decode_p<false, false><<<ctas, kPThreads, dyn, st>>>(P);
         } else if (codec == EQ_CODEC_WORD) {
             const int bi = out_dtype == EQ_OUT_BF16 ? 1 : 0;
             // (6 CTAs/SM: for the 8B layer set 7.5 waves; forcing 5 CTAs/SM for exactly 9 waves

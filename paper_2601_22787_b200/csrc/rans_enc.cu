@@ -139,6 +139,9 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
 // EQ_CODEC_PAIR (R15): pairs (s[2i], s[2i+1]) of ranked codes whose pair is kept are one
 // pair-table symbol, other pairs the escape followed by the two codes (single table), an
 // odd tail one single; all word-codec rANS steps, in reverse (escaped pair: b, a, escape).
+// EQ_CODEC_PAIR_G (R18): the same steps, per 16-symbol group in the decode order "the group's
+// pair steps, then the codes (a, b) of each escaped pair in position order, then an odd last
+// symbol"; the encoder walks that order backwards, last group first.
 // Table buffer layout as in include/entquant.h (P.freq points at 512 u16).
 struct WordEmitter {
     uint32_t x, bytes;
@@ -158,7 +161,7 @@ struct WordEmitter {
     }
 };
 
-template <bool WRITE>
+template <bool WRITE, bool GROUPED>
 __global__ void __launch_bounds__(kEncThreads) k_encode_pair(const __grid_constant__ EncParams P) {
     __shared__ uint32_t sf[256], scum[256];
     __shared__ uint32_t pf[225], pcum[225];
@@ -201,12 +204,46 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_pair(const __grid_consta
         E.dst = P.payload + end;
     }
     bool bad = false;
-    if (n & 1) {
+    if (GROUPED) {
+        for (int64_t g0 = (int64_t)((n - 1) & ~15u); n > 0 && g0 >= 0 && !bad; g0 -= 16) {
+            const uint32_t len = min(16u, n - (uint32_t)g0), m = len / 2;
+            uint32_t esc = 0;                      // escaped pair positions of the group
+            for (uint32_t k = 0; k < m; ++k) {
+                const uint32_t a = sym[g0 + 2 * k], b = sym[g0 + 2 * k + 1];
+                if (sf[a] == 0 || sf[b] == 0) { bad = true; break; }
+                const int ra = rank[a], rb = rank[b];
+                if (!(ra >= 0 && rb >= 0 && pf[ra * 15 + rb] > 0)) {
+                    if (fesc_s == 0) { bad = true; break; }
+                    esc |= 1u << k;
+                }
+            }
+            if (bad) break;
+            if (len & 1) {                         // the odd last symbol (decoded last)
+                const uint32_t s = sym[g0 + len - 1];
+                if (sf[s] == 0) { bad = true; break; }
+                E.put<WRITE>(sf[s], scum[s]);
+            }
+            for (int k = (int)m - 1; k >= 0; --k)  // the escaped pairs' codes, b then a
+                if (esc >> k & 1) {
+                    const uint32_t a = sym[g0 + 2 * k], b = sym[g0 + 2 * k + 1];
+                    E.put<WRITE>(sf[b], scum[b]);
+                    E.put<WRITE>(sf[a], scum[a]);
+                }
+            for (int k = (int)m - 1; k >= 0; --k) {  // the group's pair steps
+                if (esc >> k & 1) {
+                    E.put<WRITE>(fesc_s, cesc_s);
+                } else {
+                    const int q = rank[sym[g0 + 2 * k]] * 15 + rank[sym[g0 + 2 * k + 1]];
+                    E.put<WRITE>(pf[q], pcum[q]);
+                }
+            }
+        }
+    } else if (n & 1) {
         const uint32_t s = sym[n - 1];
         if (sf[s] == 0) bad = true;
         else E.put<WRITE>(sf[s], scum[s]);
     }
-    for (int64_t i = (int64_t)(n / 2) - 1; i >= 0 && !bad; --i) {
+    for (int64_t i = GROUPED ? -1 : (int64_t)(n / 2) - 1; i >= 0 && !bad; --i) {
         const uint32_t a = sym[2 * i], b = sym[2 * i + 1];
         if (sf[a] == 0 || sf[b] == 0) { bad = true; break; }
         const int ra = rank[a], rb = rank[b];
@@ -280,8 +317,8 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     if (!blk->payload || !blk->chunk_off || !blk->freq) return EQ_ERR_ARG;
     if (blk->n_layers == 0 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (blk->chunk_symbols == 0 || blk->chunk_symbols > 262144u) return EQ_ERR_ARG;
-    if (blk->codec > EQ_CODEC_PAIR || blk->chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
-    if (blk->chunk_mode == EQ_CHUNK_INTERLEAVED && (blk->codec != EQ_CODEC_PAIR || blk->chunk_symbols % 32 != 0))
+    if (blk->codec > EQ_CODEC_PAIR_G || blk->chunk_mode > EQ_CHUNK_INTERLEAVED) return EQ_ERR_ARG;
+    if (blk->chunk_mode == EQ_CHUNK_INTERLEAVED && (!is_pair_codec(blk->codec) || blk->chunk_symbols % 32 != 0))
         return EQ_ERR_ARG;
     EncParams P;
     memset(&P, 0, sizeof(P));
@@ -313,9 +350,13 @@ extern "C" eq_status eq_rans_encode(const uint8_t* codes, const eq_block* blk, u
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g = (chunk + kEncThreads - 1) / kEncThreads;
     if (blk->codec == EQ_CODEC_PAIR) {
-        k_encode_pair<false><<<g, kEncThreads, 0, st>>>(P);
+        k_encode_pair<false, false><<<g, kEncThreads, 0, st>>>(P);
         k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
-        k_encode_pair<true><<<g, kEncThreads, 0, st>>>(P);
+        k_encode_pair<true, false><<<g, kEncThreads, 0, st>>>(P);
+    } else if (blk->codec == EQ_CODEC_PAIR_G) {
+        k_encode_pair<false, true><<<g, kEncThreads, 0, st>>>(P);
+        k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);
+        k_encode_pair<true, true><<<g, kEncThreads, 0, st>>>(P);
     } else if (blk->codec == EQ_CODEC_WORD) {
         k_encode<false, true><<<g, kEncThreads, 0, st>>>(P);
         k_scan<<<1, 1024, 0, st>>>(chunk_sizes, chunk, blk->chunk_off, P.total, d_err);

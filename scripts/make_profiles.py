@@ -9,6 +9,7 @@ profile summaries:
 Usage: python scripts/make_profiles.py gpurun_out/ev1 r1
 """
 import csv
+import re
 import json
 import os
 import shutil
@@ -41,10 +42,14 @@ def main(ev, rnd):
     chunk_mode = open(cm_f).read().strip() if os.path.exists(cm_f) else "layer"
     for d in full:
         k = d["kernel"]
-        codec = "word" if "k_decode_w" in k else "pair" if "k_decode_p" in k else "byte" if "k_decode" in k else None
         import re
-        kind = ("bf16" if re.search(r"<(\(bool\))?1[,>]", k) else
-                "fp8" if re.search(r"<(\(bool\))?0[,>]", k) else None)
+        targs = re.search(r"k_decode\w*<([^>]*)>", k)
+        targs = [a.replace("(bool)", "").strip() for a in targs.group(1).split(",")] if targs else []
+        grouped = "k_decode_p" in k and len(targs) > 1 and targs[1] in ("1", "true")
+        codec = ("word" if "k_decode_w" in k else ("pairg" if grouped else "pair") if "k_decode_p" in k
+                 else "byte" if "k_decode" in k else None)
+        kind = ("bf16" if targs and targs[0] in ("1", "true") else
+                "fp8" if targs and targs[0] in ("0", "false") else None)
         if codec is None or kind is None:
             continue
         rd, wr = _num(d["dram__bytes_read.sum"]), _num(d["dram__bytes_write.sum"])
@@ -79,7 +84,7 @@ def main(ev, rnd):
         w.writerow(["kernel", "launches", "total_us", "share_of_command", "mean_us"])
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
             w.writerow([k, len(v), round(sum(v), 1), round(sum(v) / tot, 5), round(sum(v) / len(v), 1)])
-    dec = {k: v for k, v in per.items() if "k_decode" in k and ("<1>" in k or "<1," in k)}
+    dec = {k: v for k, v in per.items() if "k_decode" in k and re.search(r"<(\(bool\))?(1|true)[,>]", k)}
     json.dump({"command": "python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --lam 230.2 "
                           "(ncu --metrics gpu__time_duration.sum --clock-control none)",
                "timed_step_kernels": {k: {"launches": len(v), "mean_us": sum(v) / len(v)} for k, v in dec.items()},

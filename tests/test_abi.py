@@ -112,5 +112,7 @@ def test_codec_parameter_validated(lib):
     assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == 0
     p.codec = eq.EQ_CODEC_PAIR
     assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == 0
-    p.codec = 3
+    p.codec = eq.EQ_CODEC_PAIR_G
+    assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == 0
+    p.codec = 4
     assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == eq.EQ_ERR_ARG

@@ -41,11 +41,14 @@ def test_eqsynth_bit_identical_on_cuda():
         assert torch.equal(a.view(torch.int16), b.cpu().view(torch.int16)), dist
 
 
-@pytest.fixture(scope="module", params=[eq.EQ_CODEC_PAIR, eq.EQ_CODEC_WORD, eq.EQ_CODEC_BYTE],
-                ids=["pair", "word", "byte"])
+@pytest.fixture(scope="module", params=[(eq.EQ_CODEC_PAIR_G, eq.EQ_CHUNK_INTERLEAVED),
+                                        (eq.EQ_CODEC_PAIR, eq.EQ_CHUNK_LAYER),
+                                        (eq.EQ_CODEC_WORD, eq.EQ_CHUNK_LAYER), (eq.EQ_CODEC_BYTE, eq.EQ_CHUNK_LAYER)],
+                ids=["pairg-il", "pair", "word", "byte"])
 def layer_set(request):
-    """The bench's layer set in its codec (pair, R15), the word codec (R14) and SPEC's byte
-    codec (R9)."""
+    """The bench's layer set in its encoding (R18 pair codec, R17 interleaved chunks), the
+    pair codec of R15 with layer chunks, the word codec (R14) and SPEC's byte codec (R9)."""
+    codec, mode = request.param
     dev = torch.device("cuda")
     blocks, kept = [], {}
     scratch = None
@@ -53,7 +56,7 @@ def layer_set(request):
         Ws = eqsynth.block_weights("llama-3-8b", lid, device=dev)
         if scratch is None:
             scratch = torch.empty(eq.encode_bounds(Ws, codec=eq.EQ_CODEC_BYTE)[2], dtype=torch.uint8, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=LAM, scratch=scratch, codec=request.param))
+        blocks.append(eq.quantize_encode(Ws, lam=LAM, scratch=scratch, codec=codec, chunk_mode=mode))
         if lid in (0, 15, 31):
             kept[lid] = [W.cpu() for W in Ws]          # the INPUT weights, for the oracle
         del Ws
@@ -68,7 +71,7 @@ def _host_block(b):
     off = b.chunk_off.cpu().numpy().astype(np.uint32)
     table = b.freq.cpu().numpy().view(np.uint16)
     pair = None
-    if b.codec == eq.EQ_CODEC_PAIR:
+    if b.codec in eq.PAIR_CODECS:
         pair = o.PairTable(table.view(np.uint8)[968:984].copy(), int(table[482]), table[256:481].copy(),
                            int(table[481]))
     return payload, off, table, pair, u16(b.scales)
@@ -90,7 +93,7 @@ def test_config3_every_symbol_matches_oracle_decode(layer_set):
         for (r, c), v in zip(b.shapes, vb):
             nk = (r * c + b.chunk_symbols - 1) // b.chunk_symbols
             ref = o.decode_dequant_layer_mt(payload, off[k0:k0 + nk + 1], b.chunk_symbols, r, c, scales[r0:r0 + r],
-                                            table[:256], threads, b.codec, pair)
+                                            table[:256], threads, b.codec, pair, b.chunk_mode)
             got = u16(v).reshape(r, c)
             assert np.array_equal(ref, got), (b.codec, r, c, int(np.count_nonzero(ref != got)))
             total += r * c
@@ -111,10 +114,10 @@ def test_config3_full_block_encode_matches_oracle(layer_set):
         for (r, _) in b.shapes:
             S.append(scales[r0:r0 + r])
             r0 += r
-        ref = o.quantize_encode(Ws, scales=S, cs=b.chunk_symbols, codec=b.codec)
+        ref = o.quantize_encode(Ws, scales=S, cs=b.chunk_symbols, codec=b.codec, chunk_mode=b.chunk_mode)
         want = np.zeros_like(table)
         want[:256] = ref.freq
-        if b.codec == eq.EQ_CODEC_PAIR:
+        if b.codec in eq.PAIR_CODECS:
             want[256:481] = ref.pair.pf
             want[481] = ref.pair.fesc
             want[482] = ref.pair.K
@@ -170,7 +173,7 @@ def test_config3_lossless_and_rate_properties(layer_set):
         assert coded <= 1.02 * b.n_params * H / 8                     # north_star 1.02×
         assert 8 * b.payload_bytes >= b.n_params * H * (1 - 1e-3)    # Shannon
         # re-encoding the decoded codes with the same table reproduces the payload exactly
-        again = eq.rans_encode(codes, b.shapes, b.freq, codec=b.codec)
+        again = eq.rans_encode(codes, b.shapes, b.freq, codec=b.codec, chunk_mode=b.chunk_mode)
         assert again.payload_bytes == b.payload_bytes
         assert torch.equal(again.payload[:again.payload_bytes], b.payload[:b.payload_bytes])
         n += b.n_params
@@ -193,7 +196,7 @@ def _decode_all_vs_oracle(blocks):
         for (r, c), v in zip(b.shapes, vb):
             nk = (r * c + b.chunk_symbols - 1) // b.chunk_symbols
             ref = o.decode_dequant_layer_mt(payload, off[k0:k0 + nk + 1], b.chunk_symbols, r, c, scales[r0:r0 + r],
-                                            table[:256], threads, b.codec, pair)
+                                            table[:256], threads, b.codec, pair, b.chunk_mode)
             assert np.array_equal(ref, u16(v).reshape(r, c)), (b.codec, r, c)
             total += r * c
             k0 += nk

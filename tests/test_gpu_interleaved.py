@@ -18,16 +18,17 @@ def _layers(shapes, seed):
     return [eqsynth.weights(r, c, seed=seed, layer=0, matrix=m) for m, (r, c) in enumerate(shapes)]
 
 
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
 @pytest.mark.parametrize("cs", [4096, 256, 32])
-def test_interleaved_encode_byte_identical_and_decode(cs):
+def test_interleaved_encode_byte_identical_and_decode(cs, pc):
     """Whole super-chunks plus ragged tails of plain chunks (24·704 = 16896 symbols: at cs 256,
     2 super-chunks of 8192 and a 512-symbol tail)."""
     shapes = [(64, 4096), (24, 704), (48, 1024)]
     layers = _layers(shapes, 21)
     S = [(o.absmax_scales(W).astype(np.int32) + 128 * 12).astype(np.uint16) for W in layers]
-    ref = o.quantize_encode(layers, scales=S, cs=cs, codec=o.CODEC_PAIR, chunk_mode=o.CHUNK_INTERLEAVED)
+    ref = o.quantize_encode(layers, scales=S, cs=cs, codec=pc, chunk_mode=o.CHUNK_INTERLEAVED)
     g = eq.quantize_encode([W.to(DEV) for W in layers], scales=to_bf16(np.concatenate(S)), chunk_symbols=cs,
-                           codec=eq.EQ_CODEC_PAIR, chunk_mode=IL)
+                           codec=pc, chunk_mode=IL)
     assert g.n_chunks == ref.n_chunks
     assert (g.freq.cpu().numpy().view(np.uint16) == table_u16(ref)).all()
     assert (g.chunk_off.cpu().numpy().astype(np.uint32) == ref.chunk_off).all()
@@ -41,14 +42,15 @@ def test_interleaved_encode_byte_identical_and_decode(cs):
         a += r * c
 
 
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
 @pytest.mark.parametrize("cs", [4096, 64, 32])
 @pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16])
-def test_interleaved_decode_oracle_streams(cs, out):
+def test_interleaved_decode_oracle_streams(cs, out, pc):
     """Streams written by the oracle's encoder (independent of the GPU one); shapes whose symbol
     counts end in partial super-chunks and in a tail shorter than one group."""
     layers = small_layers(seed=9, shapes=[(16, 4096), (3, 4112), (64, 64), (1, 16)])
     scales = [(o.absmax_scales(W).astype(np.int32) + 1600).astype(np.uint16) for W in layers]
-    blk = o.quantize_encode(layers, scales=scales, cs=cs, codec=o.CODEC_PAIR, chunk_mode=o.CHUNK_INTERLEAVED)
+    blk = o.quantize_encode(layers, scales=scales, cs=cs, codec=pc, chunk_mode=o.CHUNK_INTERLEAVED)
     views = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0]
     a = 0
     for (r, c), v, S in zip(blk.layer_shapes, views, blk.scales):
@@ -60,7 +62,8 @@ def test_interleaved_decode_oracle_streams(cs, out):
             assert (u16(v) == o.dequant(codes, S)).all()
 
 
-def test_interleaved_decode_many_blocks_one_launch_vs_layer_mode():
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
+def test_interleaved_decode_many_blocks_one_launch_vs_layer_mode(pc):
     """Three blocks in one launch: the interleaved streams decode to the same weights as the
     layer-chunked streams of the same codes (the layout is a permutation of chunk membership)."""
     blocks_il, blocks_l = [], []
@@ -69,8 +72,8 @@ def test_interleaved_decode_many_blocks_one_launch_vs_layer_mode():
         S = [(o.absmax_scales(W).astype(np.int32) + 128 * 13).astype(np.uint16) for W in layers]
         sc = to_bf16(np.concatenate(S))
         Ws = [W.to(DEV) for W in layers]
-        blocks_il.append(eq.quantize_encode(Ws, scales=sc, chunk_symbols=64, codec=eq.EQ_CODEC_PAIR, chunk_mode=IL))
-        blocks_l.append(eq.quantize_encode(Ws, scales=sc, chunk_symbols=64, codec=eq.EQ_CODEC_PAIR))
+        blocks_il.append(eq.quantize_encode(Ws, scales=sc, chunk_symbols=64, codec=pc, chunk_mode=IL))
+        blocks_l.append(eq.quantize_encode(Ws, scales=sc, chunk_symbols=64, codec=pc))
     a = eq.decode_dequant(blocks_il, eq.EQ_OUT_BF16)
     b = eq.decode_dequant(blocks_l, eq.EQ_OUT_BF16)
     for va, vb in zip(a, b):

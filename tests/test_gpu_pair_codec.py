@@ -14,14 +14,15 @@ pytestmark = pytest.mark.gpu
 PAIR = o.CODEC_PAIR
 
 
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
 @pytest.mark.parametrize("cs", [4096, 1000, 64, 7, 1])
 @pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16])
-def test_pair_decode_oracle_streams(cs, out):
+def test_pair_decode_oracle_streams(cs, out, pc):
     layers = small_layers()
     scales = [o.absmax_scales(W) for W in layers]
     scales[2] = (scales[2].astype(np.int32) + 1700).astype(np.uint16)
     scales[4] = (scales[4].astype(np.int32) + 2000).astype(np.uint16)
-    blk = o.quantize_encode(layers, scales=scales, cs=cs, codec=PAIR)
+    blk = o.quantize_encode(layers, scales=scales, cs=cs, codec=pc)
     views = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0]
     a = 0
     for (r, c), v, S in zip(blk.layer_shapes, views, blk.scales):
@@ -33,16 +34,17 @@ def test_pair_decode_oracle_streams(cs, out):
             assert (u16(v) == o.dequant(codes, S)).all()
 
 
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
 @pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16], ids=["fp8", "bf16"])
 @pytest.mark.parametrize("kind", ["uniform", "subset2", "single", "skewed", "subset40"])
-def test_pair_decode_extreme_streams(kind, out):
+def test_pair_decode_extreme_streams(kind, out, pc):
     """Escape-heavy (uniform bytes: 15 of 256 codes ranked), single-code and two-code tables.
     The single-code table's (0,0) pair has f > 2048, so it also runs the decoder's wide LUT
     entries (the narrow 2·id layout needs every kept pair at f ≤ 2048)."""
     s = eqsynth.random_codes_stream(64 * 4096, 3, kind)
     s = np.where((s & 0x7F) == 0x7F, s ^ 1, s).astype(np.uint8)       # no NaN codes (never produced, R1)
     S = (np.arange(64, dtype=np.uint16) * 37 + 0x3C00).astype(np.uint16)
-    blk = o.encode_codes([s.reshape(64, 4096)], [(64, 4096)], [S], 4096, codec=PAIR)
+    blk = o.encode_codes([s.reshape(64, 4096)], [(64, 4096)], [S], 4096, codec=pc)
     v = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0][0]
     if out == eq.EQ_OUT_FP8:
         assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == s).all()
@@ -97,16 +99,17 @@ def test_pair_table_kernel_vs_oracle():
         eq.check(err)
 
 
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
 @pytest.mark.parametrize("cs", [4096, 333, 1])
-def test_pair_quantize_encode_byte_identical(cs):
+def test_pair_quantize_encode_byte_identical(cs, pc):
     """Alg. 1 on the GPU with the pair codec, given the oracle's scales: the table buffer
     (single + pair tables, both built by device kernels) and the stream are the oracle's."""
     from test_gpu_parity import table_u16
     layers = small_layers(seed=5)
     S = [(o.absmax_scales(W).astype(np.int32) + 1500).astype(np.uint16) for W in layers]
     g = eq.quantize_encode([W.to(DEV) for W in layers], scales=to_bf16(np.concatenate(S)), chunk_symbols=cs,
-                           codec=eq.EQ_CODEC_PAIR)
-    ref = o.quantize_encode(layers, scales=S, cs=cs, codec=PAIR)
+                           codec=pc)
+    ref = o.quantize_encode(layers, scales=S, cs=cs, codec=pc)
     assert (g.freq.cpu().numpy().view(np.uint16) == table_u16(ref)).all()
     assert g.payload_bytes == len(ref.payload)
     assert g.payload[:g.payload_bytes].cpu().numpy().tobytes() == ref.payload
@@ -122,9 +125,10 @@ def test_pair_rate_at_two_bits_gpu():
     assert gp.payload_bytes + 4 * (gp.n_chunks + 1) <= 1.02 * W.numel() * H / 8
 
 
-def test_pair_host_buffer_e2e_decode():
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
+def test_pair_host_buffer_e2e_decode(pc):
     layers = small_layers(seed=8, shapes=[(64, 256), (32, 512)])
-    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=80.0, codec=eq.EQ_CODEC_PAIR)
+    g = eq.quantize_encode([W.to(DEV) for W in layers], lam=80.0, codec=pc)
     hb = eq.HostBlocks([g], eq.EQ_OUT_BF16)
     arena = hb.decode()
     dev = eq.Decoder([g], eq.EQ_OUT_BF16)
@@ -133,12 +137,13 @@ def test_pair_host_buffer_e2e_decode():
     assert torch.equal(arena[:dev.total], dev.arena[:dev.total].cpu())
 
 
-def test_pair_runaway_stream_is_reported():
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
+def test_pair_runaway_stream_is_reported(pc):
     """A chunk whose state is forced to 1 (every step then escapes or renormalises) runs past
     its end: reported as CORRUPT, never read beyond the payload slack (see memcheck runs)."""
     Ws = [eqsynth.weights(128, 4096, seed=12)]
     blk = o.quantize_encode(Ws, scales=[(o.absmax_scales(Ws[0]).astype(np.int32) + 1700).astype(np.uint16)],
-                            cs=2048, codec=PAIR)
+                            cs=2048, codec=pc)
     g = oracle_block_to_gpu(blk)
     a = int(blk.chunk_off[blk.n_chunks - 1])
     g.payload[a:a + 4] = torch.tensor([1, 0, 0, 0], dtype=torch.uint8, device=DEV)
@@ -149,15 +154,16 @@ def test_pair_runaway_stream_is_reported():
     assert ei.value.status == eq.EQ_ERR_CORRUPT
 
 
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
 @pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16], ids=["fp8", "bf16"])
-def test_pair_decode_many_tiny_chunks(out):
+def test_pair_decode_many_tiny_chunks(out, pc):
     """204,800 chunks of 16 symbols in one launch (800 CTAs: a second, thin round on 148 SMs at
     5 CTAs/SM; every chunk is one fast group): the decoded symbols equal the oracle's stream."""
     rows, cols, cs = 800, 4096, 16
     s = eqsynth.random_codes_stream(rows * cols, 5, "skewed")
     s = np.where((s & 0x7F) == 0x7F, s ^ 1, s).astype(np.uint8)
     S = (np.arange(rows, dtype=np.uint16) % 61 + 0x3B80).astype(np.uint16)
-    blk = o.encode_codes([s.reshape(rows, cols)], [(rows, cols)], [S], cs, codec=PAIR)
+    blk = o.encode_codes([s.reshape(rows, cols)], [(rows, cols)], [S], cs, codec=pc)
     assert blk.n_chunks == rows * cols // cs
     v = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0][0]
     if out == eq.EQ_OUT_FP8:
@@ -174,13 +180,14 @@ def test_gpu_pair_codec_reproduces_hand_derived_streams():
     import json, os
     from test_oracle_codec import _expand, hist_of
     g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rans_pair_worked.json")))
-    for case in g["cases"]:
+    cases = [(c, eq.EQ_CODEC_PAIR) for c in g["cases"]] + [(c, eq.EQ_CODEC_PAIR_G) for c in g["grouped_cases"]]
+    for case, codec in cases:                      # R15 streams, then R18's (grouped escapes)
         h = hist_of(_expand(case["counts"]))
         tab, err = eq.build_pair_table(torch.from_numpy(h.astype(np.int64)).to(DEV))
         eq.check(err)
         sym = np.array(case["symbols"], dtype=np.uint8)
         n = sym.size
-        blk = eq.rans_encode(torch.from_numpy(sym).to(DEV), [(1, n)], tab, chunk_symbols=4096, codec=eq.EQ_CODEC_PAIR)
+        blk = eq.rans_encode(torch.from_numpy(sym).to(DEV), [(1, n)], tab, chunk_symbols=4096, codec=codec)
         assert blk.payload[:blk.payload_bytes].cpu().numpy().tobytes().hex() == case["bytes_hex"], case["name"]
         v = eq.decode_dequant([blk], eq.EQ_OUT_FP8)[0][0]
         assert (v.view(torch.uint8).cpu().numpy().reshape(-1) == sym).all(), case["name"]

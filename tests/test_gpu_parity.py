@@ -29,7 +29,7 @@ def to_bf16(bits: np.ndarray) -> torch.Tensor:
 def table_u16(blk: o.OracleBlock) -> np.ndarray:
     """The block's table buffer in the device layout of include/entquant.h: the 256 single
     frequencies, plus for EQ_CODEC_PAIR the pair table, escape, K and the rank codes."""
-    if blk.codec != o.CODEC_PAIR:
+    if blk.codec not in o.PAIR_CODECS:
         return np.ascontiguousarray(blk.freq, dtype=np.uint16)
     t = np.zeros(512, dtype=np.uint16)
     t[:256] = blk.freq
