@@ -75,9 +75,10 @@ def parse():
                          "16-symbol groups of 32 consecutive chunks dealt round-robin, so a warp's 32 "
                          "lanes store 1 KB contiguously; pair codec only).  auto: interleaved for the "
                          "pair codec, layer for the others")
-    ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair", "pairg"],
-                    help="wire format: byte rANS (SPEC S:355, R9), 16-bit-word rANS (R14), or the word "
-                         "rANS over symbol pairs with escapes (R15, default: fastest, smallest)")
+    ap.add_argument("--codec", default="pairg", choices=["byte", "word", "pair", "pairg"],
+                    help="wire format: byte rANS (SPEC S:355, R9), 16-bit-word rANS (R14), the word "
+                         "rANS over symbol pairs with escapes (R15), or the same with each 16-symbol "
+                         "group's escaped codes after its pair steps (R18, default: fastest, smallest)")
     args = ap.parse_args()
     if args.chunk_mode == "auto":
         args.chunk_mode = "interleaved" if args.codec in ("pair", "pairg") else "layer"

@@ -253,8 +253,8 @@ eq_status eq_decode_dequant_host(const eq_block* blocks_host, uint32_t n_blocks,
                                  void* arena_host, uint64_t arena_bytes, void* workspace,
                                  uint64_t workspace_bytes, eq_stream_t stream);
 
-/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4; all three codecs — the word
- * and pair codecs run the warp-specialised kernel): Y_q = X_q · Ŵ_qᵀ for
+/* Alg. 2 l.3 fused with l.1-2 (§8(f) NEXT row 1, config 4; all four codecs — the word
+ * and pair codecs (R15, R18) run the warp-specialised kernel): Y_q = X_q · Ŵ_qᵀ for
  * n_jobs layers `layers[q]` of block `blk` in ONE launch, Ŵ = the layer's decoded +
  * dequantised bf16 weights (never written to memory): each chunk is decoded straight into
  * tcgen05 shared-memory tiles and multiplied on the 5th-gen tensor cores (bf16 × bf16 →

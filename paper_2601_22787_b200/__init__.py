@@ -28,7 +28,7 @@ EQ_CODEC_BYTE, EQ_CODEC_WORD, EQ_CODEC_PAIR, EQ_CODEC_PAIR_G = 0, 1, 2, 3
 PAIR_CODECS = (EQ_CODEC_PAIR, EQ_CODEC_PAIR_G)   # R15 and its group-ordered form R18: one table layout
 # The binding's default codec: the pair codec (R15), the fastest decoder and the lowest rate.
 # The C ABI's zero-initialised eq_params keep SPEC's byte codec (R9); pass codec= for it here.
-EQ_DEFAULT_CODEC = EQ_CODEC_PAIR
+EQ_DEFAULT_CODEC = EQ_CODEC_PAIR_G
 EQ_OUT_FP8, EQ_OUT_BF16 = 0, 1
 EQ_CHUNK_LAYER, EQ_CHUNK_ROW, EQ_CHUNK_INTERLEAVED = 0, 1, 2
 EQ_SCALES_SEARCH, EQ_SCALES_ABSMAX, EQ_SCALES_GIVEN = 0, 1, 2

@@ -20,15 +20,31 @@
 #pragma once
 #include "decode_core.cuh"
 
+
 namespace eq {
 
 constexpr int kPairOff = 256, kFescIdx = 481, kKIdx = 482, kRankIdx = 484;
 constexpr uint32_t kEscId = 225;                  // LUT id of the escape slots (codes-table word 225)
-constexpr uint32_t kEscCodes = 0xFFFFu;           // ... which holds this sentinel
+
+// The escape's codes-table word (R18): a code pair no kept pair can decode to — (c, c) for the
+// smallest code c that is not one of the block's K ≤ 15 ranked codes (a kept pair has ranked
+// codes only; every byte is a possible Int8 code, so no fixed sentinel would do).
+__device__ __forceinline__ uint32_t escape_codes(const uint16_t* freq) {
+    const uint32_t K = min((uint32_t)freq[kKIdx], 15u);
+    const uint8_t* rc = reinterpret_cast<const uint8_t*>(freq + kRankIdx);
+    uint32_t c = 0;
+    for (; c < 16; ++c) {
+        bool ranked = false;
+        for (uint32_t k = 0; k < K; ++k) ranked |= rc[k] == c;
+        if (!ranked) break;
+    }
+    return c | (c << 8);
+}
 constexpr int kPairLutWords = kM + 113;           // + the 225 × u16 codes table
 constexpr int kPairValWords = 226;                // + (bf16 output of R18) the bf16x2 value table
 constexpr uint32_t kValOff = 4 * kM + 4 * 113;    // its byte offset from the LUT base
 constexpr uint32_t kEscVals = 0xFFFFFFFFu;        // the escape's value word (bf16 NaN pair: never a grid value)
+
 
 constexpr uint32_t kPairSmemBytes = kPairLutWords * 4 + kM + 258 * 2;
 
@@ -66,10 +82,11 @@ __device__ __forceinline__ uint32_t grid_bf16(uint32_t code, bool i8) {
 
 // two bf16 products in one instruction, each the RNE of the exact product (subnormals kept):
 // s·v has at most 8 + 7 significant bits, so this is the bf16 RNE of P:142's s·Q — the same
-// single rounding as the f32 product followed by one RNE
+// single rounding as the f32 product followed by one RNE.  The +0 addend maps the product of
+// code 0x80 (−0) to +0 as the oracle's dequantiser does (R3); a nonzero product is unchanged.
 __device__ __forceinline__ uint32_t mul_bf16x2(uint32_t a, uint32_t b) {
     uint32_t d;
-    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(0u));
     return d;
 }
 
@@ -145,6 +162,8 @@ __device__ __forceinline__ uint32_t decode_pair_g(uint32_t& x, WordReader& r, co
         asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo2), "=r"(id4) : "r"(e), "r"(T.k2p10));
         x = mad_lo(e & 0x7FFu, xs, xs + (lo2 >> 21));                  // f·⌊x/M⌋ + slot − c
         renorm_w(x, r);
+        // (ptxas adds the table base with one IADD whatever the form: a 64-bit addend to the
+        // product costs a carry chain, a link-time constant address is not folded into the LDS)
         if (VALS) return lds_u32(T.lut_s + kValOff + id4);
         return lds_u16(T.lut_s + 4 * kM + (id4 >> 1));
     }
@@ -184,7 +203,9 @@ __device__ __forceinline__ void patch_escapes(uint32_t* q, uint32_t m, uint32_t&
     #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) {
         const uint32_t sh = 16 * (k & 1);
-        if (k < m && ((q[k >> 1] >> sh) & 0xFFFFu) == kEscCodes) {
+        // (the sentinel is read from the codes table here, off the fast path: no register
+        // held across the decode loop)
+        if (k < m && ((q[k >> 1] >> sh) & 0xFFFFu) == lds_u16(T.lut_s + 4 * kM + 2 * kEscId)) {
             ring_step_w(r, payload);               // up to 2 more words: keep the ring ahead
             const uint32_t a = decode_single_p(x, r, T);
             const uint32_t b = decode_single_p(x, r, T);
@@ -312,7 +333,7 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
     cesc = s_cesc;
     if (ALL || t < NT) {
         // escape slots: an ordinary entry (slot − c, f − 1) with id kEscId, whose codes-table
-        // word is the sentinel 0xFFFF (code 0xFF, E4M3 NaN, is never a symbol, R1).  R15 tests
+        // word is the sentinel escape_codes() and value word kEscVals.  R15 tests
         // for the escape before the lookup; R18 takes the step like any pair and patches later.
         const uint32_t idsh = narrow ? 1u : 0u, scsh = narrow ? 9u : 8u;
         lut_walk<226, NT>(lut, pcum, [&](uint32_t slot, int q) -> uint32_t {
@@ -343,7 +364,7 @@ __device__ __forceinline__ uint32_t pair_tables_build(const uint16_t* freq, uint
         uint16_t* ctab = reinterpret_cast<uint16_t*>(lut + kM);
         for (int q = t; q < 225; q += NT)
             ctab[pair_id((uint32_t)q / 15, (uint32_t)q % 15)] = (uint16_t)(rcb[q / 15] | (rcb[q % 15] << 8));
-        if (t == 0) ctab[kEscId] = kEscCodes;
+        if (t == 0) ctab[kEscId] = (uint16_t)escape_codes(freq);
         if (VALS) {
             uint32_t* vtab = lut + kValOff / 4;
             for (int q = t; q < 225; q += NT)

@@ -494,7 +494,8 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
     uint8_t* a_st = dsm;
     uint8_t* b_st = dsm + STAGES * kAStage;
     uint8_t* tabs = b_st + STAGES * P.b_stage_bytes;
-    constexpr uint32_t kTabBytes = CODEC == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4u;
+    constexpr bool kPairC = is_pair_codec(CODEC);
+    constexpr uint32_t kTabBytes = kPairC ? kPairSmemBytes : (kM + 260) * 4u;
     uint32_t* rings = reinterpret_cast<uint32_t*>(tabs + ((kTabBytes + 127u) & ~127u));
     uint64_t* bars = reinterpret_cast<uint64_t*>(rings + kDec * (kWRing / 4));     // full[S], empty[S]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES);
@@ -545,7 +546,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
     DecTable WT{};
     bool ok;
     uint32_t mode = 1;                             // pair codec: 2 = narrow LUT entries (2·id)
-    if constexpr (CODEC == EQ_CODEC_PAIR) {
+    if constexpr (kPairC) {
         uint32_t* lut = reinterpret_cast<uint32_t*>(tabs);
         uint8_t* lut1 = tabs + kPairLutWords * 4;
         uint16_t* cum = reinterpret_cast<uint16_t*>(lut1 + kM);
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
         // once per step (live chain, scale mode), stage index / phase by counters
         auto run = [&](auto narrow_c) {
             constexpr bool NARROW = decltype(narrow_c)::value;
-            static_assert(CODEC == EQ_CODEC_PAIR || !NARROW, "narrow entries are a pair-codec layout");
+            static_assert(kPairC || !NARROW, "narrow entries are a pair-codec layout");
             const uint32_t s16 = c.i8 ? 0u : (uint32_t)c.s16;
             uint32_t sidx = 0, use = 0;
             for (uint32_t st = 0; st < steps; ++st) {
@@ -685,7 +686,19 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                     #pragma unroll 1
                     for (uint32_t hs = 0; hs < 2; ++hs) {
                         uint32_t q[4];
-                        if constexpr (CODEC == EQ_CODEC_PAIR) {
+                        if constexpr (CODEC == EQ_CODEC_PAIR_G) {
+                            // R18: the half is one 16-symbol group — 8 pair steps without an
+                            // escape branch, then its escaped pairs' codes
+                            bool esc = false;
+                            #pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t p0 = decode_pair_g<NARROW>(c.x, c.r, PT, esc);
+                                const uint32_t p1 = decode_pair_g<NARROW>(c.x, c.r, PT, esc);
+                                q[u] = __byte_perm(p0, p1, 0x5410);
+                            }
+                            ring_step_w(c.r, P.payload);
+                            if (esc) patch_escapes(q, 8, c.x, c.r, PT, P.payload);
+                        } else if constexpr (CODEC == EQ_CODEC_PAIR) {
                             #pragma unroll
                             for (int u = 0; u < 2; ++u) {
                                 const uint32_t p0 = decode_pair<NARROW>(c.x, c.r, PT, P.payload);
@@ -728,6 +741,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                                      "r"(0u), "r"(0u), "r"(0u) : "memory");
                 }
 #else
+                static_assert(CODEC != EQ_CODEC_PAIR_G, "R18 groups are the K step's 16-symbol halves (EQ_QMM_HALF)");
                 uint4 v[kWsK / 8];
                 if (c.active && !c.runaway) {
                     uint32_t q[kWsK / 4];
@@ -775,7 +789,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                 if (++sidx == (uint32_t)STAGES) { sidx = 0; ++use; }
             }
         };
-        if constexpr (CODEC == EQ_CODEC_PAIR && EQ_QMM_NARROW) {
+        if constexpr (kPairC && EQ_QMM_NARROW) {
             if (mode == 2) run(std::true_type{});                 // CTA-uniform
             else run(std::false_type{});
         } else {
@@ -842,7 +856,7 @@ static eq_status qmm_validate(const eq_block* blk, uint32_t n_jobs, const uint32
                               QmmPlan* plan) {
     if (!blk || !layers || n_jobs < 1 || n_jobs > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if (!blk->payload || !blk->chunk_off || !blk->freq || !blk->scales || blk->format > EQ_FMT_INT8) return EQ_ERR_ARG;
-    if (blk->codec > EQ_CODEC_PAIR) return EQ_ERR_ARG;
+    if (blk->codec > EQ_CODEC_PAIR_G) return EQ_ERR_ARG;
     if (blk->n_layers < 1 || blk->n_layers > EQ_MAX_LAYERS) return EQ_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(blk->payload) & 15) != 0) return EQ_ERR_ARG;
     if (blk->payload_cap < blk->payload_bytes + EQ_PAYLOAD_SLACK) return EQ_ERR_BUFFER;
@@ -948,16 +962,18 @@ static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint3
     W.k2p12 = 1u << 12;
     W.kneg2p14 = 0u - (1u << 14);
     W.k4 = 4u;
-    const size_t tab = blk->codec == EQ_CODEC_PAIR ? kPairSmemBytes : (kM + 260) * 4;
+    const size_t tab = is_pair_codec(blk->codec) ? kPairSmemBytes : (kM + 260) * 4;
     auto smem_for = [&](int stages) {
         return (size_t)1024 + stages * kQmmNTile * kWsATile + stages * W.b_stage_bytes + ((tab + 127) & ~(size_t)127) +
                kQmmNTile * kWsDec * kWRing + 2 * stages * 8 + 16;
     };
-    const bool pair = blk->codec == EQ_CODEC_PAIR;
-    const void* fS = pair ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, kWsStages>
-                          : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, kWsStages>;
-    const void* f1 = pair ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, 1>
-                          : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, 1>;
+    const uint32_t codec = blk->codec;
+    const void* fS = codec == EQ_CODEC_PAIR_G ? (const void*)k_qmm_ws<EQ_CODEC_PAIR_G, kQmmNTile, kWsStages>
+                   : codec == EQ_CODEC_PAIR   ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, kWsStages>
+                                              : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, kWsStages>;
+    const void* f1 = codec == EQ_CODEC_PAIR_G ? (const void*)k_qmm_ws<EQ_CODEC_PAIR_G, kQmmNTile, 1>
+                   : codec == EQ_CODEC_PAIR   ? (const void*)k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, 1>
+                                              : (const void*)k_qmm_ws<EQ_CODEC_WORD, kQmmNTile, 1>;
     const int threads = 32 * (4 * kQmmNTile + 1);
     // resident CTAs per SM with kWsStages stages and with 1: one stage (the decoders then wait for
     // each step's MMAs: ~6 % slower per CTA) only when it turns two waves into one — e.g. a
@@ -987,7 +1003,10 @@ static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint3
     EQ_CUDA_TRY(ctas_per_sm(f1, smem_for(1), &c1));
     const bool one = (uint64_t)tiles > (uint64_t)cS * sms && (uint64_t)tiles <= (uint64_t)c1 * sms;
     const size_t smem = smem_for(one ? 1 : kWsStages);
-    if (pair) {
+    if (codec == EQ_CODEC_PAIR_G) {
+        if (one) k_qmm_ws<EQ_CODEC_PAIR_G, kQmmNTile, 1><<<tiles, threads, smem, st>>>(W);
+        else k_qmm_ws<EQ_CODEC_PAIR_G, kQmmNTile, kWsStages><<<tiles, threads, smem, st>>>(W);
+    } else if (codec == EQ_CODEC_PAIR) {
         if (one) k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, 1><<<tiles, threads, smem, st>>>(W);
         else k_qmm_ws<EQ_CODEC_PAIR, kQmmNTile, kWsStages><<<tiles, threads, smem, st>>>(W);
     } else {

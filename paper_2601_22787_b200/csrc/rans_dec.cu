@@ -558,8 +558,11 @@ k_decode_w(const __grid_constant__ DecParams P) {
 // ================================================================ EQ_CODEC_PAIR decoder (R15)
 // Same CTA ↔ block and lane ↔ chunk mapping and staging as k_decode_w; the pair tables and the
 // pair / single decode steps are in pair_core.cuh (shared with the fused GEMM).
+#ifndef EQ_PAIR_VALS
+#define EQ_PAIR_VALS 1              // R18 bf16: a bf16x2 value table (one HFMA2 per pair) instead of the codes
+#endif
 #ifndef EQ_PAIR_TOPID
-#define EQ_PAIR_TOPID 1             // R18 bf16: narrow entries with the id on top (decode_pair_g)
+#define EQ_PAIR_TOPID 1             // R18 bf16 values: narrow entries with the id on top (decode_pair_g)
 #endif
 // R18 (EQ_CODEC_PAIR_G) generic path: one group of len ≤ 16 symbols — its pair steps, the
 // escaped pairs' codes, its odd last symbol — stored one symbol at a time (ragged tails and
@@ -609,9 +612,10 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
         uint32_t ng = ng0;
         uint8_t* o = c.out + (uint64_t)c.i * (BF16 ? 2 : 1);
         uint32_t s16 = c.i8 ? 0u : (uint32_t)c.s16;
-        uint32_t s2 = (BF16 && GROUPED) ? c.sc[c.row] * 0x10001u : 0u;     // the row's bf16 scale, twice
+        constexpr bool VALS = BF16 && GROUPED && EQ_PAIR_VALS;
+        uint32_t s2 = VALS ? c.sc[c.row] * 0x10001u : 0u;     // the row's bf16 scale, twice
         while (ng != 0 && c.r.Q <= qlim) {
-            if (BF16 && GROUPED) {                 // R18 + bf16: value words, one bf16x2 product per pair
+            if (VALS) {                            // R18 + bf16: value words, one bf16x2 product per pair
                 uint32_t v[8];
                 bool esc = false;
                 #pragma unroll
@@ -693,7 +697,7 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
         }
         c.i += (ng0 - ng) * G;
         if (ng != 0) { c.runaway = true; return; }
-        if (BF16 && GROUPED && ng0 != 0 && tail) { // the tail's row scale (s2 tracked the rows)
+        if (VALS && ng0 != 0 && tail) {            // the tail's row scale (s2 tracked the rows)
             c.s = bf16_bits_to_float(c.sc[c.row]);
             s16 = c.i8 ? 0u : (uint32_t)scale_f16(c.s);
         }
@@ -702,7 +706,7 @@ __device__ __forceinline__ void chain_finish_p(ChainW& c, const uint8_t* payload
     }
     if (GROUPED) {                                 // generic / ragged tail, group by group (R18)
         while (c.i < c.n) {
-            group_generic_g<BF16, NARROW, BF16 && EQ_PAIR_TOPID>(c, payload, T, min(16u, c.n - c.i));
+            group_generic_g<BF16, NARROW, BF16 && EQ_PAIR_VALS && EQ_PAIR_TOPID>(c, payload, T, min(16u, c.n - c.i));
             if (c.r.Q > qlim) { c.runaway = true; return; }
         }
         return;
@@ -744,7 +748,8 @@ template <bool BF16, bool GROUPED>
 __global__ void __launch_bounds__(kPThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) uint8_t rings[];      // kPThreads × kWRing
-    __shared__ __align__(16) uint32_t lut[kPairLutWords + (BF16 && GROUPED ? kPairValWords : 0)];  // pair LUT + codes (+ values)
+    constexpr bool VALS = BF16 && GROUPED && EQ_PAIR_VALS;
+    __shared__ __align__(16) uint32_t lut[kPairLutWords + (VALS ? kPairValWords : 0)];  // pair LUT + codes (+ values)
     __shared__ __align__(16) uint8_t lut1[kM];             // (first the pair cum, see pair_tables_build)
     __shared__ uint16_t cum[258];
 
@@ -757,8 +762,7 @@ k_decode_p(const __grid_constant__ DecParams P) {
                         (uint32_t)__cvta_generic_to_shared(rings + t * kWRing), P.arena, P.err);
     stage_commit();
     uint32_t cesc;
-    const uint32_t mode = pair_tables_build<kPThreads, true, EQ_PAIR_NARROW, BF16 && GROUPED,
-                                            BF16 && GROUPED && EQ_PAIR_TOPID>(
+    const uint32_t mode = pair_tables_build<kPThreads, true, EQ_PAIR_NARROW, VALS, VALS && EQ_PAIR_TOPID>(
         B.freq, lut, lut1, cum, cesc, P.err, B.format == EQ_FMT_INT8);
     if (!mode) {
         stage_wait_all();

@@ -34,14 +34,14 @@ def main():
     import argparse
     ap = argparse.ArgumentParser()
     ap.add_argument("model", nargs="?", default="llama-3-8b")
-    ap.add_argument("--codec", default="pair", choices=["word", "pair"])
+    ap.add_argument("--codec", default="pair", choices=["word", "pair", "pairg"])
     ap.add_argument("--cs", type=int, default=4096)
     args = ap.parse_args()
     model = args.model
     nb = eqsynth.LLAMA[model]["layers"]
     dev = torch.device("cuda")
     lam = 230.2
-    codec = {"word": eq.EQ_CODEC_WORD, "pair": eq.EQ_CODEC_PAIR}[args.codec]
+    codec = {"word": eq.EQ_CODEC_WORD, "pair": eq.EQ_CODEC_PAIR, "pairg": eq.EQ_CODEC_PAIR_G}[args.codec]
     blocks, dense = [], []
     for lid in range(nb):
         Ws = eqsynth.block_weights(model, lid, device=dev)

@@ -33,9 +33,9 @@ def main():
     ap.add_argument("--cs", type=int, default=4096)
     ap.add_argument("--chunk-mode", default="row", choices=["row", "layer"])
     ap.add_argument("--profile", action="store_true", help="one grouped launch per batch (for ncu)")
-    ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair"])
+    ap.add_argument("--codec", default="pair", choices=["byte", "word", "pair", "pairg"])
     args = ap.parse_args()
-    codec = {"byte": eq.EQ_CODEC_BYTE, "word": eq.EQ_CODEC_WORD, "pair": eq.EQ_CODEC_PAIR}[args.codec]
+    codec = {"byte": eq.EQ_CODEC_BYTE, "word": eq.EQ_CODEC_WORD, "pair": eq.EQ_CODEC_PAIR, "pairg": eq.EQ_CODEC_PAIR_G}[args.codec]
     mode = {"row": eq.EQ_CHUNK_ROW, "layer": eq.EQ_CHUNK_LAYER}[args.chunk_mode]
     dev = torch.device("cuda")
     Ws = eqsynth.block_weights("llama-3-8b", 0, device=dev)

@@ -212,24 +212,25 @@ def _encode_matches_oracle(b, Ws):
     for (r, _) in b.shapes:
         S.append(scales[r0:r0 + r])
         r0 += r
-    ref = o.quantize_encode(Ws, scales=S, cs=b.chunk_symbols, codec=b.codec)
+    ref = o.quantize_encode(Ws, scales=S, cs=b.chunk_symbols, codec=b.codec, chunk_mode=b.chunk_mode)
     assert np.array_equal(off, np.asarray(ref.chunk_off, dtype=np.uint32))
     assert b.payload_bytes == len(ref.payload)
     assert b.payload[:b.payload_bytes].cpu().numpy().tobytes() == ref.payload
 
 
 def test_config2_llama_1b_every_symbol_and_sampled_encode():
-    """BASELINE config 2 (Llama-3.2-1B shapes, 16 blocks, 0.97 G parameters), the bench's pair
-    codec: λ calibrated for 2 bits on the GPU, Alg. 1 for every block, one decode launch; every
+    """BASELINE config 2 (Llama-3.2-1B shapes, 16 blocks, 0.97 G parameters), the bench's encoding
+    (R18 pair codec, R17 interleaved chunks): λ calibrated for 2 bits on the GPU, Alg. 1 for every block, one decode launch; every
     symbol against the oracle's decoder, block 7's encode against the oracle's."""
     dev = torch.device("cuda")
     calib = eqsynth.block_weights("llama-3.2-1b", 0, device=dev)
-    lam, _ = eq.calibrate_lambda(calib, 2.0, row_stride=16, codec=eq.EQ_CODEC_PAIR)
+    lam, _ = eq.calibrate_lambda(calib, 2.0, row_stride=16, codec=eq.EQ_CODEC_PAIR_G,
+                                 chunk_mode=eq.EQ_CHUNK_INTERLEAVED)
     del calib
     blocks, kept = [], None
     for lid in range(16):
         Ws = eqsynth.block_weights("llama-3.2-1b", lid, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=lam, codec=eq.EQ_CODEC_PAIR))
+        blocks.append(eq.quantize_encode(Ws, lam=lam, codec=eq.EQ_CODEC_PAIR_G, chunk_mode=eq.EQ_CHUNK_INTERLEAVED))
         if lid == 7:
             kept = [W.cpu() for W in Ws]
         del Ws
@@ -242,11 +243,11 @@ def test_config2_llama_1b_every_symbol_and_sampled_encode():
 
 def test_config5_llama_70b_block_every_symbol_and_encode():
     """BASELINE config 5 (Llama-3-70B shapes; the per-rank parity of §8(d) is on sampled
-    blocks): one whole 70B block (856 M parameters) with the bench's pair codec — every symbol
+    blocks): one whole 70B block (856 M parameters) in the bench's encoding — every symbol
     of its decode against the oracle's decoder, and its encode against the oracle's."""
     dev = torch.device("cuda")
     Ws = eqsynth.block_weights("llama-3-70b", 3, device=dev)
-    b = eq.quantize_encode(Ws, lam=LAM, codec=eq.EQ_CODEC_PAIR)
+    b = eq.quantize_encode(Ws, lam=LAM, codec=eq.EQ_CODEC_PAIR_G, chunk_mode=eq.EQ_CHUNK_INTERLEAVED)
     Wc = [W.cpu() for W in Ws]
     del Ws
     torch.cuda.empty_cache()

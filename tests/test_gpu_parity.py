@@ -313,10 +313,17 @@ def test_calibrate_lambda_full_block_within_005_bits():
         assert abs(g.effective_bits() - target) < 0.05, (target, g.effective_bits())
 
 
-def test_dequant_all_codes_all_scale_ranges():
+ENCODINGS = [(o.CODEC_BYTE, o.CHUNK_LAYER), (o.CODEC_PAIR, o.CHUNK_LAYER), (o.CODEC_PAIR_G, o.CHUNK_INTERLEAVED),
+             (o.CODEC_PAIR_G, o.CHUNK_LAYER)]
+ENC_IDS = ["byte", "pair", "pairg-il", "pairg"]
+
+
+@pytest.mark.parametrize("codec,mode", ENCODINGS, ids=ENC_IDS)
+def test_dequant_all_codes_all_scale_ranges(codec, mode):
     """Every finite E4M3 code × row scales across the bf16 range (f16-exact scales take the
-    FHFMA path, the rest the FMUL path; subnormal bf16 products included), decoded through
-    the C-ABI and compared with the oracle's exact dequantiser."""
+    FHFMA path, the rest the FMUL path; subnormal bf16 products included; the R18 bf16 path
+    multiplies bf16 value pairs by the bf16 scale), decoded through the C-ABI and compared with
+    the oracle's exact dequantiser."""
     codes = np.array([c for c in range(256) if (c & 0x7F) != 0x7F and c != 0x80], dtype=np.uint8)   # 253
     row = np.concatenate([codes, codes[:3]])                                                       # 256 cols
     rng = np.random.default_rng(11)
@@ -328,7 +335,7 @@ def test_dequant_all_codes_all_scale_ranges():
     ]).astype(np.uint16)
     M = s_bits.size
     C = np.tile(row, (M, 1))
-    blk = o.encode_codes([C], [(M, 256)], [s_bits], cs=512)
+    blk = o.encode_codes([C], [(M, 256)], [s_bits], cs=512, codec=codec, chunk_mode=mode)
     v = eq.decode_dequant([oracle_block_to_gpu(blk)], eq.EQ_OUT_BF16)[0][0]
     assert (u16(v) == o.dequant(C, s_bits)).all()
 
@@ -368,11 +375,13 @@ def test_int8_search_vs_oracle(lam):
     assert near <= 1
 
 
+@pytest.mark.parametrize("codec,mode", ENCODINGS, ids=ENC_IDS)
 @pytest.mark.parametrize("out", [eq.EQ_OUT_FP8, eq.EQ_OUT_BF16])
-def test_int8_decode_oracle_streams(out):
-    layers = small_layers(seed=21)
+def test_int8_decode_oracle_streams(out, codec, mode):
+    shapes = RAGGED if mode == o.CHUNK_LAYER else [(37, 64), (1, 16), (64, 64), (5, 4096), (16, 4096)]
+    layers = small_layers(seed=21, shapes=shapes)
     scales = [(o.absmax_scales(W, o.FMT_INT8).astype(np.int32) + 128 * 5).astype(np.uint16) for W in layers]
-    blk = o.quantize_encode(layers, scales=scales, cs=512, fmt=o.FMT_INT8)
+    blk = o.quantize_encode(layers, scales=scales, cs=512, fmt=o.FMT_INT8, codec=codec, chunk_mode=mode)
     views = eq.decode_dequant([oracle_block_to_gpu(blk)], out)[0]
     a = 0
     for (r, c), v, S in zip(blk.layer_shapes, views, blk.scales):

@@ -18,7 +18,7 @@ def to_gpu_block(blk):
     return oracle_block_to_gpu(blk)            # incl. the pair codec's 512-entry table buffer
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G])
 @pytest.mark.parametrize("cs,fmt", [(4096, 0), (2048, 0), (1024, 1), (256, 0)])
 @pytest.mark.parametrize("batch", [1, 8, 61])
 def test_qmatmul_matches_fp64_reference(cs, fmt, batch, codec):
@@ -39,7 +39,7 @@ def test_qmatmul_matches_fp64_reference(cs, fmt, batch, codec):
             assert (np.abs(y - ref) <= bound).all(), (layer, rep, float(np.max(np.abs(y - ref) / bound)))
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G])
 def test_qmatmul_shape_errors_and_corruption(codec):
     Ws = [eqsynth.weights(128, 4096, seed=3)]
     blk = o.quantize_encode(Ws, scales=[o.absmax_scales(Ws[0])], cs=4096, codec=codec)
@@ -56,7 +56,7 @@ def test_qmatmul_shape_errors_and_corruption(codec):
     assert ei.value.status == eq.EQ_ERR_CORRUPT
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G])
 @pytest.mark.parametrize("batch", [1, 24])
 def test_qmatmul_group_one_launch_deterministic(batch, codec):
     """All layers of a block in one grouped launch (mixed chunk counts per row: split-K
@@ -99,7 +99,7 @@ def test_qmatmul_workspace_contract():
     assert st == eq.EQ_ERR_BUFFER
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G])
 def test_qmatmul_runaway_stream_is_reported_not_overread(codec):
     """A chunk whose state is forced to 1 consumes a renormalisation unit at every symbol and
     runs far past its end: the fused kernel must stop reading it (no access beyond the

@@ -12,7 +12,7 @@ import paper_2601_22787_b200 as eq
 from test_gpu_parity import DEV, oracle_block_to_gpu, small_layers, table_u16, to_bf16, u16
 
 pytestmark = pytest.mark.gpu
-CODECS = [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR]
+CODECS = [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G]
 
 
 @pytest.mark.parametrize("codec", CODECS)
@@ -49,7 +49,7 @@ def test_rowchunk_encode_byte_identical(codec, cs):
         assert (u16(v) == r).all()
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G])
 @pytest.mark.parametrize("batch", [1, 64])
 def test_rowchunk_qmatmul_ragged_k(codec, batch):
     """Fused GEMM on a row-chunked layer whose K is not a multiple of the chunk length:
@@ -72,8 +72,9 @@ def test_rowchunk_qmatmul_ragged_k(codec, batch):
             assert (np.abs(y - ref) <= bound).all(), (cs, layer, float(np.max(np.abs(y - ref) / bound)))
 
 
+@pytest.mark.parametrize("pc", [o.CODEC_PAIR, o.CODEC_PAIR_G], ids=["r15", "r18"])
 @pytest.mark.parametrize("batch", [1, 64])
-def test_qmatmul_escape_heavy_pair_stream(batch):
+def test_qmatmul_escape_heavy_pair_stream(batch, pc):
     """Pair codec with escapes on most steps (uniform bytes: only 15 of the codes are ranked):
     the fused GEMM's escape singles — from the 4 KB symbol table at small batches, by a binary
     search over the cumulative frequencies when the table does not fit 3 CTAs/SM (batch 64) —
@@ -82,7 +83,7 @@ def test_qmatmul_escape_heavy_pair_stream(batch):
     s = eqsynth.random_codes_stream(rows * cols, 11, "uniform")
     s = np.where((s & 0x7F) == 0x7F, s ^ 1, s).astype(np.uint8)        # no NaN codes (never produced, R1)
     S = (np.arange(rows, dtype=np.uint16) % 97 + 0x3A00).astype(np.uint16)
-    blk = o.encode_codes([s.reshape(rows, cols)], [(rows, cols)], [S], 2048, codec=o.CODEC_PAIR,
+    blk = o.encode_codes([s.reshape(rows, cols)], [(rows, cols)], [S], 2048, codec=pc,
                          chunk_mode=o.CHUNK_ROW)
     g = oracle_block_to_gpu(blk)
     W64 = torch.from_numpy(o.dequant(s.reshape(rows, cols), S).view(np.int16)).view(torch.bfloat16).double().numpy()

@@ -163,7 +163,7 @@ def test_word_decode_max_chunk_full_rows():
         assert (u16(v) == r).all()
 
 
-@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR])
+@pytest.mark.parametrize("codec", [o.CODEC_BYTE, o.CODEC_WORD, o.CODEC_PAIR, o.CODEC_PAIR_G])
 def test_decode_under_random_corruption_matches_oracle_verdicts(codec):
     """Fuzz: random byte flips in the payload.  The GPU decoder never faults; every chunk the
     oracle rejects makes the launch report an error; when the oracle accepts every chunk of a
