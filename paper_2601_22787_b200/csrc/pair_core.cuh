@@ -180,13 +180,17 @@ __device__ __forceinline__ uint32_t decode_pair_g(uint32_t& x, WordReader& r, co
     return lds_u16(T.lut_s + 4 * kM + ((e & 0xFFu) << 1));
 }
 
+// escapes per group whose singles need no ring step (see patch_escapes)
+constexpr uint32_t kFreeEsc = (kWRing - 32 - 16) / 4;
+
 // R18 patch for the value words of a group (bf16 output): v[k] is pair position k's bf16x2
 __device__ __forceinline__ void patch_escapes_vals(uint32_t* v, uint32_t& x, WordReader& r, const PairTab& T,
                                                    const uint8_t* payload, bool i8) {
+    uint32_t n = 0;
     #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) {
         if (v[k] == kEscVals) {
-            ring_step_w(r, payload);
+            if (n++ >= kFreeEsc) ring_step_w(r, payload);     // as patch_escapes
             const uint32_t a = decode_single_p(x, r, T);
             const uint32_t b = decode_single_p(x, r, T);
             v[k] = grid_bf16(a, i8) | (grid_bf16(b, i8) << 16);
@@ -194,19 +198,25 @@ __device__ __forceinline__ void patch_escapes_vals(uint32_t* v, uint32_t& x, Wor
     }
 }
 
-// R18, after a group's pair steps: each escaped position (codes sentinel), in position order,
-// is replaced by its two codes (a, then b) decoded with the single table.  q[0..3] hold the
-// group's 8 pair positions, two per word (position k in the half k & 1 of q[k >> 1]); only
-// positions < m are pair positions of the group.
+// R18, after a group's pair steps (and the group's ring step): each escaped position (codes
+// sentinel), in position order, is replaced by its two codes (a, then b) decoded with the
+// single table.  q[0..3] hold the group's 8 pair positions, two per word (position k in the
+// half k & 1 of q[k >> 1]); only positions < m are pair positions of the group.
+// Staging: at a group's start more than 32 landed bytes lie ahead of the reader (the segment
+// issued at a boundary starts > read + kWRing − 32, decode_core.cuh), the 8 pair steps take at
+// most 16 of them, so the first kFreeEsc escapes' two words each need no new segment — and no
+// cp.async wait, which would stall on the segment just issued at the boundary; from the next
+// escape on, one ring step (stage + wait) per escape as before.
 __device__ __forceinline__ void patch_escapes(uint32_t* q, uint32_t m, uint32_t& x, WordReader& r, const PairTab& T,
                                               const uint8_t* payload) {
+    uint32_t n = 0;
     #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) {
         const uint32_t sh = 16 * (k & 1);
         // (the sentinel is read from the codes table here, off the fast path: no register
         // held across the decode loop)
         if (k < m && ((q[k >> 1] >> sh) & 0xFFFFu) == lds_u16(T.lut_s + 4 * kM + 2 * kEscId)) {
-            ring_step_w(r, payload);               // up to 2 more words: keep the ring ahead
+            if (n++ >= kFreeEsc) ring_step_w(r, payload);     // up to 2 more words: keep the ring ahead
             const uint32_t a = decode_single_p(x, r, T);
             const uint32_t b = decode_single_p(x, r, T);
             q[k >> 1] = (q[k >> 1] & ~(0xFFFFu << sh)) | ((a | (b << 8)) << sh);
