@@ -181,7 +181,10 @@ __device__ __forceinline__ uint32_t decode_pair_g(uint32_t& x, WordReader& r, co
 }
 
 // escapes per group whose singles need no ring step (see patch_escapes)
-constexpr uint32_t kFreeEsc = (kWRing - 32 - 16) / 4;
+#ifndef EQ_FREE_ESC
+#define EQ_FREE_ESC ((kWRing - 32 - 16) / 4)
+#endif
+constexpr uint32_t kFreeEsc = EQ_FREE_ESC;
 
 // R18 patch for the value words of a group (bf16 output): v[k] is pair position k's bf16x2
 __device__ __forceinline__ void patch_escapes_vals(uint32_t* v, uint32_t& x, WordReader& r, const PairTab& T,
