@@ -21,6 +21,7 @@
 #include "decode_core.cuh"
 
 
+
 namespace eq {
 
 constexpr int kPairOff = 256, kFescIdx = 481, kKIdx = 482, kRankIdx = 484;
@@ -41,17 +42,19 @@ __device__ __forceinline__ uint32_t escape_codes(const uint16_t* freq) {
     return c | (c << 8);
 }
 constexpr int kPairLutWords = kM + 113;           // + the 225 × u16 codes table
-constexpr int kPairValWords = 226;                // + (bf16 output of R18) the bf16x2 value table
-constexpr uint32_t kValOff = 4 * kM + 4 * 113;    // its byte offset from the LUT base
 constexpr uint32_t kEscVals = 0xFFFFFFFFu;        // the escape's value word (bf16 NaN pair: never a grid value)
 
 
 constexpr uint32_t kPairSmemBytes = kPairLutWords * 4 + kM + 258 * 2;
+// one contiguous table region: [pair LUT | codes | lut1 | cum | (R18 bf16) values], so every
+// table address is the LUT base plus a constant (one register across the decode loop)
+constexpr uint32_t kLut1Off = kPairLutWords * 4;  // byte offsets from the LUT base
+constexpr uint32_t kCumOff = kLut1Off + kM;
+constexpr int kPairValWords = 226;                // (bf16 output of R18) the bf16x2 value table
+constexpr uint32_t kValOff = kPairSmemBytes;
 
 struct PairTab {
     uint32_t lut_s;        // shared address of the pair LUT (the codes table follows at + 4·kM)
-    uint32_t lut1_s;       // shared address of the single table's symbol per slot
-    uint32_t cum_s;        // shared address of the single table's cum[257] (u16)
     uint32_t esc_lo;       // slot << 20 at and above which a pair step is the escape (0xFFFFFFFF: none)
     uint32_t fesc, cesc;   // escape frequency and cumulative start
     uint32_t k2p20, k2p12; // 2^20, 2^12 passed at run time (IMAD forms on the FMA pipe)
@@ -110,8 +113,8 @@ __device__ __forceinline__ uint32_t decode_single_p(uint32_t& x, WordReader& r, 
     uint32_t lo, xs;
     asm("{ .reg .u64 t; mul.wide.u32 t, %2, %3; mov.b64 {%0, %1}, t; }" : "=r"(lo), "=r"(xs) : "r"(x), "r"(T.k2p20));
     const uint32_t slot = lo >> 20;
-    const uint32_t s = lds_u8(T.lut1_s + slot);
-    const uint32_t cs = lds_u16(T.cum_s + 2 * s), ce = lds_u16(T.cum_s + 2 * s + 2);
+    const uint32_t s = lds_u8(T.lut_s + kLut1Off + slot);
+    const uint32_t cs = lds_u16(T.lut_s + kCumOff + 2 * s), ce = lds_u16(T.lut_s + kCumOff + 2 * s + 2);
     x = (ce - cs) * xs + slot - cs;
     renorm_w(x, r);
     return s;
@@ -392,8 +395,6 @@ __device__ __forceinline__ PairTab pair_tab(const uint16_t* freq, const uint32_t
                                             const uint16_t* cum, uint32_t cesc, uint32_t k2p20, uint32_t k2p12) {
     PairTab T;
     T.lut_s = (uint32_t)__cvta_generic_to_shared(lut);
-    T.lut1_s = (uint32_t)__cvta_generic_to_shared(lut1);
-    T.cum_s = (uint32_t)__cvta_generic_to_shared(cum);
     T.fesc = freq[kFescIdx];
     T.cesc = cesc;
     T.esc_lo = T.fesc ? (T.cesc << 20) : 0xFFFFFFFFu;

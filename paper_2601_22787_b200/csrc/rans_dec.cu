@@ -749,9 +749,12 @@ __global__ void __launch_bounds__(kPThreads, EQ_DECP_MIN_CTAS)
 k_decode_p(const __grid_constant__ DecParams P) {
     extern __shared__ __align__(128) uint8_t rings[];      // kPThreads × kWRing
     constexpr bool VALS = BF16 && GROUPED && EQ_PAIR_VALS;
-    __shared__ __align__(16) uint32_t lut[kPairLutWords + (VALS ? kPairValWords : 0)];  // pair LUT + codes (+ values)
-    __shared__ __align__(16) uint8_t lut1[kM];             // (first the pair cum, see pair_tables_build)
-    __shared__ uint16_t cum[258];
+    // the contiguous table region of pair_core.cuh: pair LUT + codes, lut1 (first the pair cum,
+    // see pair_tables_build), cum, and for R18 bf16 the value table
+    __shared__ __align__(16) uint8_t tabs[kPairSmemBytes + (VALS ? 4 * kPairValWords : 0)];
+    uint32_t* lut = reinterpret_cast<uint32_t*>(tabs);
+    uint8_t* lut1 = tabs + kLut1Off;
+    uint16_t* cum = reinterpret_cast<uint16_t*>(tabs + kCumOff);
 
     uint32_t bi = 0;
     while (bi + 1 < P.n_blocks && blockIdx.x >= P.b[bi + 1].cta0) ++bi;
