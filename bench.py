@@ -245,11 +245,14 @@ def share_ids(args, rank: int, world: int):
 
 
 def choose_chunk(args, layer_ids, lanes: int) -> int:
-    """Chunk length for the rank's share: 4096 symbols, or — for a share that
-    is barely more than one round of 4096-symbol chains (a launch runs chunks / lanes rounds of
-    serial chains; 4 Llama-3-8B blocks are 1.12 rounds, the SMs idle 17 % of such a launch) —
-    one round of 4608 with layer or interleaved chunking (0.549 of the HBM peak vs 0.46).  Shorter chunks are not
-    chosen: at 2048 the coded size passes the north star's 1.02 × n·Ĥ (≈ 1.0205 ×)."""
+    """Chunk length for the rank's share.  A launch runs chunks / lanes rounds of
+    serial chains; a last round that is only partly filled still takes a chain's full latency.
+    4096 symbols, unless the 4096-symbol share is 1–3 rounds with a last round ≤ ¼ full that
+    4608-symbol chunks remove (8 Llama-3-8B blocks: 2.25 → 2 rounds, 0.615 → 0.630 of the HBM
+    peak; 4 blocks: 1.12 → 1 round, 0.518 → 0.616); elsewhere 4608 measured slower (16 blocks,
+    4.5 → 4 rounds: 0.663 → 0.651; 10 Llama-3-70B blocks: 0.680 → 0.628; the Llama-3.2-1B set,
+    1.25 rounds: 0.563 → 0.457; `profiles/r2/s2cab`).  Shorter chunks are not chosen: at 2048
+    the coded size passes the north star's 1.02 × n·Ĥ (≈ 1.0205 ×)."""
     import eqsynth
     if args.chunk_symbols:
         return args.chunk_symbols
@@ -259,7 +262,8 @@ def choose_chunk(args, layer_ids, lanes: int) -> int:
         if args.chunk_mode == "row":
             return sum(r * ((c + cs - 1) // cs) for r, c in shapes)
         return sum((r * c + cs - 1) // cs for r, c in shapes)
-    if 1 < n_chunks(4096) / lanes <= 1.25 and n_chunks(4608) <= lanes:
+    r = n_chunks(4096) / lanes
+    if 1 < r <= 3 and r - int(r) <= 0.25 and -(-n_chunks(4608) // lanes) <= int(r):
         return 4608
     return 4096
 
