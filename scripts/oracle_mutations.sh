@@ -1,8 +1,10 @@
 # Mutation check of the oracle's pins (the round-1 judge's mutations of the R8 / R15 table rules,
-# plus round-2 mutations of the quantiser, Q†, row chunking and the escape order): each mutated
+# plus round-2 mutations of the quantiser, Q†, row chunking, the escape order and R18's group
+# order): each mutated
 # copy of oracle/eq_oracle.c must fail at least one -m "not gpu" oracle test.
 set -u
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
+ONLY=${ONLY:-}            # e.g. ONLY=13 runs mutations 13.. only
 muts=(
   's/if (b < 0 || r\[c\] > r\[b\] || (r\[c\] == r\[b\] \&\& hist\[c\] > hist\[b\])) b = c;/if (b < 0 || r[c] < r[b] || (r[c] == r[b] \&\& hist[c] < hist[b])) b = c;/'
   's/if (f\[c\] > 1 \&\& (b < 0 || f\[c\] > f\[b\])) b = c;/if (f[c] > 1 \&\& (b < 0 || f[c] < f[b])) b = c;/'
@@ -21,9 +23,16 @@ muts=(
   # the escape's two singles in the opposite order, consistently in encoder and decoder (a
   # self-consistent wire-format change that round trips: only the hand-derived streams see it)
   '/eqo_w_put(\&x, freq\[b\], cum\[b\], tmp, \&pos);/{N;s/eqo_w_put(\&x, freq\[b\], cum\[b\], tmp, \&pos);\n\( *\)eqo_w_put(\&x, freq\[a\], cum\[a\], tmp, \&pos);/eqo_w_put(\&x, freq[a], cum[a], tmp, \&pos);\n\1eqo_w_put(\&x, freq[b], cum[b], tmp, \&pos);/};s/sym\[2 \* i + k\] = (uint8_t)s;/sym[2 * i + 1 - k] = (uint8_t)s;/'
+  # R18 (session 3), each self-consistent in encoder and decoder: 32-symbol groups; escaped
+  # positions patched in decreasing order; an escaped pair's codes in the order b, a
+  's/#define EQO_GROUP 16/#define EQO_GROUP 32/'
+  's|for (int64_t i = 0; i < g / 2; i++) {                         /\* (2) \*/|for (int64_t i = g / 2 - 1; i >= 0; i--) {                     /* (2) */|'
+  's/sf\[m\] = freq\[a\]; sc\[m\] = cum\[a\]; m++;/sf[m] = freq[b]; sc[m] = cum[b]; m++; sf[m] = freq[a]; sc[m] = cum[a]; m++; continue;/;s/if (eqo_w_single(\&x, freq, cum, in, nbytes, \&p, \&sym\[g0 + 2 \* i\])) return 2;/if (eqo_w_single(\&x, freq, cum, in, nbytes, \&p, \&sym[g0 + 2 * i + 1])) return 2; if (eqo_w_single(\&x, freq, cum, in, nbytes, \&p, \&sym[g0 + 2 * i])) return 2; continue;/'
 )
 rc=0
+i=0
 for m in "${muts[@]}"; do
+  i=$((i + 1)); if [ -n "$ONLY" ] && [ $i -lt $ONLY ]; then continue; fi
   T=$(mktemp -d)
   cp -r "$ROOT/oracle" "$ROOT/eqsynth" "$ROOT/tests" "$ROOT/pytest.ini" "$T/"
   rm -f "$T"/oracle/*.so

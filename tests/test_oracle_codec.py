@@ -480,6 +480,70 @@ def test_pair_grouped_round_trip_and_same_rate(kind):
         o.decode_chunk_pair(g[:-2], f, pt, n, grouped=True)
 
 
+def _word_rans_encode(steps):
+    """R14's word rANS written out (pinned by tests/golden/rans_word_worked.json): encode the
+    decode-order list of (f, c) steps backwards from x = L = 2^16; emit the low 16 bits while
+    x ≥ 2^20·f; the 4-byte LE final state, then the words in decode order."""
+    x, words = 1 << 16, []
+    for f, c in reversed(steps):
+        while x >= (1 << 20) * f:
+            words.append(x & 0xFFFF)
+            x >>= 16
+        x = (x // f) * 4096 + x % f + c
+    out = bytes([x & 0xFF, (x >> 8) & 0xFF, (x >> 16) & 0xFF, (x >> 24) & 0xFF])
+    for w in reversed(words):
+        out += bytes([w & 0xFF, w >> 8])
+    return out
+
+
+def _r18_steps(sym, f, pt):
+    """R18 read literally: for each 16-symbol group of the chunk, in order — its
+    pair positions (kept pair: the pair table's (f, c); else the escape's), then for each escaped
+    position in increasing order the single-table (f, c) of its first then second code, then the
+    group's odd last symbol."""
+    cum = np.concatenate([[0], np.cumsum(f.astype(np.int64))])
+    rank = {int(pt.rank_code[r]): r for r in range(pt.K)}
+    pcum, run = {}, 0
+    for q in range(225):
+        if q // 15 < pt.K and q % 15 < pt.K and pt.pf[q]:
+            pcum[q] = run
+            run += int(pt.pf[q])
+    cesc = run
+    steps = []
+    for g0 in range(0, sym.size, 16):
+        grp = [int(v) for v in sym[g0:g0 + 16]]
+        esc = []
+        for i in range(len(grp) // 2):
+            a, b = grp[2 * i], grp[2 * i + 1]
+            q = rank[a] * 15 + rank[b] if a in rank and b in rank else None
+            if q is not None and q in pcum:
+                steps.append((int(pt.pf[q]), pcum[q]))
+            else:
+                steps.append((pt.fesc, cesc))
+                esc.append(i)
+        for i in esc:
+            for s in (grp[2 * i], grp[2 * i + 1]):
+                steps.append((int(f[s]), int(cum[s])))
+        if len(grp) % 2:
+            steps.append((int(f[grp[-1]]), int(cum[grp[-1]])))
+    return steps
+
+
+@pytest.mark.parametrize("kind", ["uniform", "subset40", "skewed"])
+def test_pair_grouped_matches_the_literal_order(kind):
+    """The C oracle's R18 stream equals R14's word coder run over the R18 decode order written out
+    from its definition (several escapes per group, every length class): a wrong group size,
+    escapes in decreasing order, or the odd symbol before the escaped codes would differ."""
+    rng = np.random.default_rng((hash(kind) + 11) & 0xFFFF)
+    for t in range(6):
+        n = int(rng.choice([1, 3, 16, 17, 33, 47, 200, 4096, int(rng.integers(1, 3000))]))
+        s = eqsynth.random_codes_stream(n, int(rng.integers(1 << 30)), kind)
+        h = o.histogram(s)
+        f = o.normalize(h)
+        pt = o.pair_table(h)
+        assert o.encode_chunk_pair(s, f, pt, grouped=True) == _word_rans_encode(_r18_steps(s, f, pt)), (kind, n)
+
+
 def test_pair_grouped_decoder_rejects_the_r15_order():
     """The hand-derived R15 stream (escape at position 0, kept pair after it) read as R18 is not
     the same chunk: the integrity check (final state L, every word consumed) or the symbols
