@@ -432,6 +432,9 @@ __global__ void __launch_bounds__(kQThreads, EQ_QMM_MIN_CTAS) k_qmatmul(const __
 #ifndef EQ_QMM_WS_MIN_CTAS
 #define EQ_QMM_WS_MIN_CTAS 3
 #endif
+#ifndef EQ_QMM_VALS
+#define EQ_QMM_VALS 1                          // R18: decode into bf16x2 values (one HFMA2 per pair)
+#endif
 #ifndef EQ_QMM_HALF
 #define EQ_QMM_HALF 1                          // decoder K step as a loop over two 16-symbol halves
 #endif
@@ -495,7 +498,8 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
     uint8_t* b_st = dsm + STAGES * kAStage;
     uint8_t* tabs = b_st + STAGES * P.b_stage_bytes;
     constexpr bool kPairC = is_pair_codec(CODEC);
-    constexpr uint32_t kTabBytes = kPairC ? kPairSmemBytes : (kM + 260) * 4u;
+    constexpr bool kVals = CODEC == EQ_CODEC_PAIR_G && EQ_QMM_VALS;    // R18: bf16x2 value table
+    constexpr uint32_t kTabBytes = kPairC ? kPairSmemBytes + (kVals ? 4u * kPairValWords : 0u) : (kM + 260) * 4u;
     uint32_t* rings = reinterpret_cast<uint32_t*>(tabs + ((kTabBytes + 127u) & ~127u));
     uint64_t* bars = reinterpret_cast<uint64_t*>(rings + kDec * (kWRing / 4));     // full[S], empty[S]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES);
@@ -520,7 +524,9 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
     c.s = 0.f;
     c.s16 = 0;
     const uint32_t ring = smem_u32(rings + t * (kWRing / 4));
+    uint32_t s2row = 0;
     if (t < kDec && grow < J.rows) {
+        s2row = (uint32_t)J.scales[grow] * 0x10001u;
         c.s = bf16_bits_to_float(J.scales[grow]);
         c.s16 = c.i8 ? 0 : scale_f16(c.s);
         const uint32_t chunk = J.chunk0 + grow * J.cpr + jcol;
@@ -551,7 +557,8 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
         uint8_t* lut1 = tabs + kPairLutWords * 4;
         uint16_t* cum = reinterpret_cast<uint16_t*>(lut1 + kM);
         uint32_t cesc = 0;
-        mode = pair_tables_build<kDec, false, EQ_QMM_NARROW>(P.freq, lut, lut1, cum, cesc, P.err);
+        mode = pair_tables_build<kDec, false, EQ_QMM_NARROW, kVals, kVals>(P.freq, lut, lut1, cum, cesc, P.err,
+                                                                          P.format == EQ_FMT_INT8);
         ok = mode != 0;
         __syncthreads();                           // table stores visible to every decoder lane
         if (ok) PT = pair_tab(P.freq, lut, lut1, cum, cesc, P.k2p20, P.k2p12);
@@ -674,6 +681,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
             constexpr bool NARROW = decltype(narrow_c)::value;
             static_assert(kPairC || !NARROW, "narrow entries are a pair-codec layout");
             const uint32_t s16 = c.i8 ? 0u : (uint32_t)c.s16;
+            [[maybe_unused]] const uint32_t s2 = kVals ? s2row : 0u;   // the row's bf16 scale, twice (R18 values)
             uint32_t sidx = 0, use = 0;
             for (uint32_t st = 0; st < steps; ++st) {
                 if (st >= (uint32_t)STAGES) mbar_wait(smem_u32(&bars[STAGES + sidx]), (use & 1) ^ 1);
@@ -682,11 +690,25 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                 // the step as a (not unrolled) loop over two halves of 16 symbols: half the code
                 // of the fully unrolled step (the decoder loop then fits the instruction cache)
                 if (c.active && !c.runaway) {
-                    const uint16_t h16 = (uint16_t)s16;
+                    [[maybe_unused]] const uint16_t h16 = (uint16_t)s16;
                     #pragma unroll 1
                     for (uint32_t hs = 0; hs < 2; ++hs) {
-                        uint32_t q[4];
-                        if constexpr (CODEC == EQ_CODEC_PAIR_G) {
+                        [[maybe_unused]] uint32_t q[4];
+                        if constexpr (kVals) {
+                            // R18 with values: the half's 8 pairs as bf16x2 words, one HFMA2 each
+                            uint32_t v[8];
+                            bool esc = false;
+                            #pragma unroll
+                            for (int u = 0; u < 8; ++u) v[u] = decode_pair_g<NARROW, true, NARROW>(c.x, c.r, PT, esc);
+                            ring_step_w(c.r, P.payload);
+                            if (esc) patch_escapes_vals(v, c.x, c.r, PT, P.payload, c.i8);
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + (((2 * hs) ^ sw) << 4)),
+                                         "r"(mul_bf16x2(v[0], s2)), "r"(mul_bf16x2(v[1], s2)), "r"(mul_bf16x2(v[2], s2)),
+                                         "r"(mul_bf16x2(v[3], s2)) : "memory");
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + (((2 * hs + 1) ^ sw) << 4)),
+                                         "r"(mul_bf16x2(v[4], s2)), "r"(mul_bf16x2(v[5], s2)), "r"(mul_bf16x2(v[6], s2)),
+                                         "r"(mul_bf16x2(v[7], s2)) : "memory");
+                        } else if constexpr (CODEC == EQ_CODEC_PAIR_G) {
                             // R18: the half is one 16-symbol group — 8 pair steps without an
                             // escape branch, then its escaped pairs' codes
                             bool esc = false;
@@ -717,6 +739,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                             q[3] = decode4_w(c, WT);
                             ring_step_w(c.r, P.payload);
                         }
+                        if constexpr (!kVals) {
                         uint4 v0, v1;
                         if (s16) {
                             v0 = make_uint4(dequant2_h(q[0], h16), dequant2_h(q[0] >> 16, h16), dequant2_h(q[1], h16),
@@ -731,6 +754,7 @@ __global__ void __launch_bounds__(32 * (4 * NTILE + 1), EQ_QMM_WS_MIN_CTAS) k_qm
                                      "r"(v0.x), "r"(v0.y), "r"(v0.z), "r"(v0.w) : "memory");
                         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(arow + (((2 * hs + 1) ^ sw) << 4)),
                                      "r"(v1.x), "r"(v1.y), "r"(v1.z), "r"(v1.w) : "memory");
+                        }
                     }
                     c.i += kWsK;
                     if (c.r.Q > qlim) c.runaway = true;           // overran its chunk: stop reading
@@ -962,7 +986,9 @@ static eq_status qmm_ws_launch(const eq_block* blk, uint32_t n_jobs, const uint3
     W.k2p12 = 1u << 12;
     W.kneg2p14 = 0u - (1u << 14);
     W.k4 = 4u;
-    const size_t tab = is_pair_codec(blk->codec) ? kPairSmemBytes : (kM + 260) * 4;
+    const size_t tab = is_pair_codec(blk->codec)
+                           ? kPairSmemBytes + (blk->codec == EQ_CODEC_PAIR_G && EQ_QMM_VALS ? 4 * kPairValWords : 0)
+                           : (kM + 260) * 4;
     auto smem_for = [&](int stages) {
         return (size_t)1024 + stages * kQmmNTile * kWsATile + stages * W.b_stage_bytes + ((tab + 127) & ~(size_t)127) +
                kQmmNTile * kWsDec * kWRing + 2 * stages * 8 + 16;
