@@ -47,7 +47,7 @@ def test_fused_gemm_forward_matches_dense_forward_on_oracle_weights():
     x0 = (torch.arange(8 * 256, device=dev, dtype=torch.float32).reshape(8, 256).cos() * 0.2).to(torch.bfloat16)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     ws = torch.empty(1 << 22, dtype=torch.uint8, device=dev)
-    for codec in (o.CODEC_PAIR, o.CODEC_WORD):
+    for codec in (o.CODEC_PAIR_G, o.CODEC_PAIR, o.CODEC_WORD):
         x_ref = x_fused = x0
         for lid in range(3):
             Ws = [eqsynth.weights(r, c, seed=9, layer=lid, matrix=m) for m, (r, c) in enumerate(shapes)]
