@@ -331,6 +331,20 @@ eq_status eq_calibrate_lambda(const eq_tensor* layers, uint32_t n_layers, const 
                               double* est_bits_out, void* scratch, uint64_t scratch_bytes,
                               eq_stream_t stream);
 
+/* Optional CRC verify mode (CRC-32 over the uncompressed block
+ * stream — the codes vec(W_q) of a block's layers in order).  CRC-32/IEEE: reflected polynomial
+ * 0xEDB88320, initial value and final XOR 0xFFFFFFFF ("123456789" → 0xCBF43926).
+ * data: device, n bytes (any alignment); crc: device, one uint32 (written, not read);
+ * scratch: device, ≥ eq_crc32_scratch_bytes(n) (4 bytes per 4 KB piece), caller-owned.
+ * Two launches (per-piece CRCs, then one CTA folds them with GF(2) zero-byte operators).
+ * EQ_ERR_ARG for NULL pointers, EQ_ERR_BUFFER for short scratch.  Asynchronous.
+ * After eq_quantize_encode returns, its scratch begins with the block's codes in layer order
+ * (Σ rows·cols bytes): the stream whose CRC a container records at encode time; after a
+ * decode to EQ_OUT_FP8 the same CRC over the decoded layers verifies the round trip. */
+uint64_t eq_crc32_scratch_bytes(uint64_t n);
+eq_status eq_crc32(const void* data, uint64_t n, uint32_t* crc, void* scratch, uint64_t scratch_bytes,
+                   eq_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

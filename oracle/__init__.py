@@ -358,6 +358,14 @@ def decode_chunk_pair(data: bytes, freq: np.ndarray, pt: PairTable, n: int, grou
     return out[:n]
 
 
+def crc32(data) -> int:
+    """CRC-32/IEEE of a byte string (the checksum of the uncompressed block
+    stream; reflected polynomial 0xEDB88320, init and final XOR 0xFFFFFFFF) — the library routine
+    (zlib) as the oracle's one step."""
+    import zlib
+    return zlib.crc32(bytes(np.ascontiguousarray(data, dtype=np.uint8).reshape(-1))) & 0xFFFFFFFF
+
+
 # ---------------------------------------------------------------- block (Alg. 1 / Alg. 2)
 @dataclass
 class OracleBlock:

@@ -51,6 +51,8 @@ EXPORTS = (
     "eq_lbfgs_scratch_bytes",
     "eq_lbfgs_scales",
     "eq_rd_eval",
+    "eq_crc32_scratch_bytes",
+    "eq_crc32",
 )
 
 
@@ -126,6 +128,8 @@ def lib() -> ctypes.CDLL:
             "eq_lbfgs_scratch_bytes": (u64, [P, u32, P]),
             "eq_lbfgs_scales": (st, [P, u32, u32, dbl, P, P, P, P, P, u64, P]),
             "eq_rd_eval": (st, [P, u32, dbl, P, P, P, P, u64, P]),
+            "eq_crc32_scratch_bytes": (u64, [u64]),
+            "eq_crc32": (st, [P, u64, P, P, u64, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -194,6 +198,7 @@ class Block:
     format: int = EQ_FMT_E4M3
     codec: int = EQ_CODEC_BYTE
     chunk_mode: int = EQ_CHUNK_LAYER
+    crc: int | None = None           # CRC-32 of the block's codes at encode time (verify mode)
 
     @property
     def n_chunks(self) -> int:
@@ -251,8 +256,9 @@ def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH
                     chunk_symbols: int = EQ_DEFAULT_CHUNK, oct_lo: int = -1, oct_hi: int = 20,
                     stream=None, scratch: torch.Tensor | None = None, shrink: bool = True,
                     format: int = EQ_FMT_E4M3, exclude=(), codec: int = EQ_DEFAULT_CODEC,
-                    chunk_mode: int = EQ_CHUNK_LAYER) -> Block:
+                    chunk_mode: int = EQ_CHUNK_LAYER, crc: bool = False) -> Block:
     """Alg. 1 for one block of bf16 CUDA matrices.  Synchronous (reads payload size).
+    ``crc``: also record the CRC-32 of the block's codes (the verify mode, ``verify_crc``).
     ``exclude``: layer indices kept at AbsMax scales (λ = 0); ``codec``: rANS
     renormalisation (EQ_CODEC_BYTE, R9 / EQ_CODEC_WORD, R14 / EQ_CODEC_PAIR, R15 / EQ_CODEC_PAIR_G, R18);
     ``chunk_mode``: EQ_CHUNK_LAYER, EQ_CHUNK_ROW (chunks also restart at row starts) or
@@ -282,11 +288,43 @@ def quantize_encode(layers, lam: float = 0.0, scale_mode: int = EQ_SCALES_SEARCH
     _ck(lib().eq_quantize_encode(ts, len(layers), ctypes.byref(p), ctypes.byref(b), scratch.data_ptr(), scratch.numel(),
                                  _stream(stream)), "eq_quantize_encode")
     nbytes = b.payload_bytes
+    crc_val = None
+    if crc:      # the codes stream sits at the start of the scratch (include/entquant.h, eq_crc32)
+        crc_val = crc32(scratch[:sum(W.numel() for W in layers)], stream)
     if shrink:   # keep only what the block needs (+ decoder read slack)
         keep = (nbytes + EQ_PAYLOAD_SLACK + 255) // 256 * 256
         payload = payload[:keep].clone()
     return Block(payload, nbytes, off, freq, scales, [tuple(W.shape) for W in layers], chunk_symbols,
-                 {"lambda": lam, "scale_mode": scale_mode, "exclude": tuple(exclude)}, format, codec, chunk_mode)
+                 {"lambda": lam, "scale_mode": scale_mode, "exclude": tuple(exclude)}, format, codec, chunk_mode,
+                 crc_val)
+
+
+def crc32(data: torch.Tensor, stream=None) -> int:
+    """CRC-32/IEEE of a CUDA byte tensor, computed on the GPU (eq_crc32).  Synchronous."""
+    _require_cuda(data)
+    data = data.contiguous().view(torch.uint8).reshape(-1)
+    n = data.numel()
+    scratch = torch.empty(max(1, lib().eq_crc32_scratch_bytes(n)), dtype=torch.uint8, device=data.device)
+    out = torch.empty(1, dtype=torch.int32, device=data.device)
+    _ck(lib().eq_crc32(data.data_ptr() if n else None, n, out.data_ptr(), scratch.data_ptr(), scratch.numel(),
+                       _stream(stream)), "eq_crc32")
+    return int(out.item()) & 0xFFFFFFFF
+
+
+def verify_crc(blocks, stream=None) -> list:
+    """The verify mode: decode the blocks to their codes (EQ_OUT_FP8),
+    CRC-32 each block's layers in order and compare with the CRC recorded at encode time.
+    Returns the per-block verdicts (True = match); raises EqError on a stream error."""
+    dec = Decoder(blocks, EQ_OUT_FP8)
+    dec(stream)
+    dec.check(stream)
+    ok = []
+    for b, vs in zip(blocks, dec.views()):
+        if b.crc is None:
+            raise ValueError("block encoded without crc=True")
+        codes = torch.cat([v.reshape(-1).view(torch.uint8) for v in vs])
+        ok.append(crc32(codes, stream) == b.crc)
+    return ok
 
 
 def arena_layout(blocks, out_dtype=EQ_OUT_BF16):

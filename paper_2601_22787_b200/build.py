@@ -9,7 +9,7 @@ import tempfile
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libentquant.so")
-SOURCES = ["rans_dec.cu", "quant.cu", "table.cu", "rans_enc.cu", "api.cu", "qmatmul.cu", "lbfgs.cu"]
+SOURCES = ["rans_dec.cu", "quant.cu", "table.cu", "rans_enc.cu", "api.cu", "qmatmul.cu", "lbfgs.cu", "crc.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-ftz=false", "-prec-div=true",
               "-prec-sqrt=true", "-fmad=false"]

@@ -116,3 +116,15 @@ def test_codec_parameter_validated(lib):
     assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == 0
     p.codec = 4
     assert lib.eq_encode_bounds(t, 1, ctypes.byref(p), None, None, None) == eq.EQ_ERR_ARG
+
+
+def test_crc32_host_side(lib):
+    """eq_crc32's host-side contract without a GPU: scratch size (4 bytes per 4 KB piece + 16),
+    argument errors before any launch."""
+    assert lib.eq_crc32_scratch_bytes(0) == 16
+    assert lib.eq_crc32_scratch_bytes(1) == 20
+    assert lib.eq_crc32_scratch_bytes(4096) == 20
+    assert lib.eq_crc32_scratch_bytes(4097) == 24
+    assert lib.eq_crc32(None, 10, None, None, 0, None) == eq.EQ_ERR_ARG
+    assert lib.eq_crc32(None, 10, ctypes.c_void_p(16), None, 0, None) == eq.EQ_ERR_ARG
+    assert lib.eq_crc32(ctypes.c_void_p(16), 8192, ctypes.c_void_p(16), ctypes.c_void_p(16), 8, None) == eq.EQ_ERR_BUFFER

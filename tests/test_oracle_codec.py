@@ -697,3 +697,23 @@ def test_interleaved_chunking_threaded_dequant_helper(codec):
     out = o.decode_dequant_layer_mt(payload, blk.chunk_off, 256, 40, 704, S, blk.freq, 3, codec, blk.pair,
                                     chunk_mode=o.CHUNK_INTERLEAVED)
     assert (out == o.decode_dequant(blk)[0]).all()
+
+
+# ------------------------------------------------------------------ CRC verify mode
+def test_crc32_check_values():
+    """CRC-32/IEEE's catalogued check value ("123456789" → 0xCBF43926) and the empty message;
+    a bit-by-bit long division with the reflected polynomial on short random strings."""
+    assert o.crc32(np.frombuffer(b"123456789", np.uint8)) == 0xCBF43926
+    assert o.crc32(np.zeros(0, np.uint8)) == 0
+
+    def bitwise(b):
+        c = 0xFFFFFFFF
+        for byte in b:
+            c ^= int(byte)
+            for _ in range(8):
+                c = (c >> 1) ^ (0xEDB88320 if c & 1 else 0)
+        return c ^ 0xFFFFFFFF
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 7, 64, 333):
+        b = rng.integers(0, 256, n, dtype=np.uint8)
+        assert o.crc32(b) == bitwise(b)
