@@ -4,6 +4,8 @@
 One step = one pass of the whole hot path over one batch: eq_decode_dequant of every
 chunk of the rank's share of the Llama-3-8B-shaped layer set (32 blocks × 7 linear
 layers, ~2.0 effective bits/param) into the per-device bf16 arena — §8(a) rows a7+a8.
+The streams use the default encoding: the pair codec with grouped escapes (R18)
+over interleaved 4096-symbol chunks (R17); ``--codec`` / ``--chunk-mode`` select the others.
 The encode side (rows a1-a6) runs once before timing to produce the streams (its time is
 reported as ``encode_s``).  Inputs are synthetic (eqsynth), resident in HBM; the 1.76 GB
 compressed input and 13.96 GB decoded output per step are both far larger than the 126 MB
