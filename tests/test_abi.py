@@ -128,3 +128,15 @@ def test_crc32_host_side(lib):
     assert lib.eq_crc32(None, 10, None, None, 0, None) == eq.EQ_ERR_ARG
     assert lib.eq_crc32(None, 10, ctypes.c_void_p(16), None, 0, None) == eq.EQ_ERR_ARG
     assert lib.eq_crc32(ctypes.c_void_p(16), 8192, ctypes.c_void_p(16), ctypes.c_void_p(16), 8, None) == eq.EQ_ERR_BUFFER
+
+
+def test_header_constants_match_the_binding():
+    """Every #define EQ_* integer constant of include/entquant.h that the binding also names has
+    the binding's value (the codecs, chunk modes, formats, output types, status codes...)."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "entquant.h")).read()
+    defs = {m.group(1): int(m.group(2), 0) for m in re.finditer(r"#define\s+(EQ_[A-Z0-9_]+)\s+\(?(0x[0-9A-Fa-f]+|\d+)u?\)?", hdr)}
+    shared = [k for k in defs if hasattr(eq, k)]
+    assert {"EQ_CODEC_PAIR_G", "EQ_CHUNK_INTERLEAVED", "EQ_OUT_BF16", "EQ_FMT_INT8"} <= set(shared)
+    for k in shared:
+        assert getattr(eq, k) == defs[k], k
