@@ -63,6 +63,10 @@ def parse():
     ap.add_argument("--chunk-symbols", type=int, default=0,
                     help="symbols per chunk (0: auto — 4096 unless the rank's share is too few chunks "
                          "for whole rounds of the decoder's lanes, DESIGN.md §7)")
+    ap.add_argument("--tail-blocks", type=int, default=-1,
+                    help="encode the share's last N blocks with --tail-cs symbols per chunk (-1: auto, "
+                         "bench.choose_tail; 0: none)")
+    ap.add_argument("--tail-cs", type=int, default=2048)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp8", action="store_true")
@@ -249,11 +253,11 @@ def share_ids(args, rank: int, world: int):
 def choose_chunk(args, layer_ids, lanes: int) -> int:
     """Chunk length for the rank's share.  A launch runs chunks / lanes rounds of
     serial chains; a last round that is only partly filled still takes a chain's full latency.
-    4096 symbols, unless the 4096-symbol share is 1–3 rounds with a last round ≤ ¼ full that
-    4608-symbol chunks remove (8 Llama-3-8B blocks: 2.25 → 2 rounds, 0.615 → 0.630 of the HBM
-    peak; 4 blocks: 1.12 → 1 round, 0.518 → 0.616); elsewhere 4608 measured slower (16 blocks,
-    4.5 → 4 rounds: 0.663 → 0.651; 10 Llama-3-70B blocks: 0.680 → 0.628; the Llama-3.2-1B set,
-    1.25 rounds: 0.563 → 0.457; `profiles/r2/s2cab`).  Shorter chunks are not chosen: at 2048
+    4096 symbols, unless the 4096-symbol share is at most 1.25 rounds that 4608-symbol chunks
+    fit in one (4 Llama-3-8B blocks: 1.12 → 1 round, 0.518 → 0.616 of the HBM peak); elsewhere
+    4608 measured slower than 4096 with 2048-symbol tail blocks (choose_tail) or than 4096 alone
+    (16 blocks: 0.651 vs 0.663; 10 Llama-3-70B blocks: 0.628 vs 0.680; the Llama-3.2-1B set:
+    0.457 vs 0.563; `profiles/r2/s2cab`, `s2tail2`).  Shorter chunks are not chosen: at 2048
     the coded size passes the north star's 1.02 × n·Ĥ (≈ 1.0205 ×)."""
     import eqsynth
     if args.chunk_symbols:
@@ -265,9 +269,33 @@ def choose_chunk(args, layer_ids, lanes: int) -> int:
             return sum(r * ((c + cs - 1) // cs) for r, c in shapes)
         return sum((r * c + cs - 1) // cs for r, c in shapes)
     r = n_chunks(4096) / lanes
-    if 1 < r <= 3 and r - int(r) <= 0.25 and -(-n_chunks(4608) // lanes) <= int(r):
+    if 1 < r <= 1.25 and n_chunks(4608) <= lanes:
         return 4608
     return 4096
+
+
+def choose_tail(args, layer_ids, lanes: int, cs: int) -> int:
+    """Blocks of the share encoded in 2048-symbol chunks at its end: when the
+    4096-symbol share ends in a partly filled round (fraction ≤ ½) that 4608 did not remove, the
+    last k = ⌈B − ⌊rounds⌋ · lanes / chunks per block⌉ blocks are coded in 2048-symbol chunks, so
+    the 4096-symbol chains fill whole rounds and the short chains fill the tail (`profiles/r2/
+    s2tail2`: the Llama-3.2-1B set 0.561 → 0.620 of the HBM peak with k = 4; 16 8B blocks 0.663 →
+    0.677, k = 2; 8 blocks 0.630 (4608) → 0.647, k = 1; 10 70B blocks 0.680 → 0.686, k = 1).  Each
+    such block codes at ≈ 1.019 × n·Ĥ, under the north star's 1.02."""
+    import math
+
+    import eqsynth
+    if args.tail_blocks >= 0:
+        return args.tail_blocks
+    if args.chunk_symbols or cs != 4096 or args.chunk_mode == "row":
+        return 0
+    shapes = list(eqsynth.block_shapes(args.model))
+    per_block = sum((r * c + cs - 1) // cs for r, c in shapes)
+    B = len(layer_ids)
+    r = B * per_block / lanes
+    if r <= 1 or r - math.floor(r) > 0.5:
+        return 0
+    return min(B, max(0, math.ceil(B - math.floor(r) * lanes / per_block)))
 
 
 def encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist=None):
@@ -286,13 +314,17 @@ def encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist=None):
         dist.broadcast(t, 0)
         lam = float(t.item())
     blocks, scratch = [], None
-    for lid in layer_ids:
+    n_tail = min(args.tail_blocks, len(layer_ids))
+    for i, lid in enumerate(layer_ids):
         Ws = eqsynth.block_weights(args.model, lid, device=dev)
+        # the share's last n_tail blocks in shorter chunks: the launch's last, partly filled
+        # round of chains is then made of shorter chains (an experiment, --tail-blocks)
+        cs_b = args.tail_cs if i >= len(layer_ids) - n_tail else cs
         if scratch is None:
-            _, _, sb = eq.encode_bounds(Ws, chunk_symbols=cs, codec=CODECS[args.codec],
-                                        chunk_mode=CHUNK_MODES[args.chunk_mode])
+            _, _, sb = eq.encode_bounds(Ws, chunk_symbols=min(cs, args.tail_cs) if n_tail else cs,
+                                        codec=CODECS[args.codec], chunk_mode=CHUNK_MODES[args.chunk_mode])
             scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
-        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch, chunk_symbols=cs, codec=CODECS[args.codec],
+        blocks.append(eq.quantize_encode(Ws, lam=lam, scratch=scratch, chunk_symbols=cs_b, codec=CODECS[args.codec],
                                          chunk_mode=CHUNK_MODES[args.chunk_mode]))
         del Ws
     del scratch
@@ -306,7 +338,8 @@ def workload_config(args, n_blocks, n_params, cs, world):
                     f"{n_blocks} blocks per rank, ~{args.target_bits} effective bits/param, chunk-parallel rANS "
                     f"decode + fused dequant to bf16",
         "model_shapes": args.model, "blocks_per_rank": n_blocks, "params_per_rank": n_params,
-        "chunk_symbols": cs, "chunk_mode": args.chunk_mode, "codec": args.codec, "target_bits": args.target_bits,
+        "chunk_symbols": cs, "tail_blocks_2048": max(0, args.tail_blocks), "chunk_mode": args.chunk_mode,
+        "codec": args.codec, "target_bits": args.target_bits,
         "l2": "inputs larger than L2 (compressed in + decoded out per step >> 126 MB); no flush",
         "parallelism": f"block-sharded x{world} ({args.scaling}, contiguous ranges)" if args.scaling == "strong"
                        else f"block-sharded x{world} (weak)",
@@ -358,7 +391,10 @@ def run_reference(args, rank, world):
     if args.blocks <= 0:
         args.blocks = eqsynth.LLAMA[args.model]["layers"]
     ids, (r, g) = share_ids(args, rank, world)
-    cs = choose_chunk(args, ids, max(1, eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, 0)))
+    lanes0 = max(1, eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, 0))
+    cs = choose_chunk(args, ids, lanes0)
+    # block 0 is a 2048-symbol tail block of our arm's share only when every block is one
+    args.tail_blocks = 1 if choose_tail(args, ids, lanes0, cs) >= len(ids) else 0
     n_params = len(ids) * sum(a * b for a, b in eqsynth.block_shapes(args.model))
     blocks, lam, est, enc_s = encode_share(args, eq, eqsynth, dev, [0], cs)
     blk = blocks[0]
@@ -425,6 +461,7 @@ def main():
     layer_ids, (sim_rank, sim_world) = share_ids(args, rank, world)
     lanes = max(1, eq.decode_lanes(CODECS[args.codec], eq.EQ_OUT_BF16, local))
     cs = choose_chunk(args, layer_ids, lanes)
+    args.tail_blocks = choose_tail(args, layer_ids, lanes, cs)
 
     # ---- encode side (once): λ calibration (global) then Alg. 1 per block
     blocks, lam, est, enc_s = encode_share(args, eq, eqsynth, dev, layer_ids, cs, dist if world > 1 else None)

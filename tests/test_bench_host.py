@@ -20,18 +20,30 @@ def _steps(args, blocks, cs):
     return -(-n // LANES) * cs
 
 
-def test_chunk_rule_removes_small_partial_rounds_only():
-    """4608-symbol chunks only where they remove a last 4096-symbol round that is ≤ ¼ full for a
-    share of 1–3 rounds (the measured cases of DESIGN.md §15); 4096 everywhere else; never below
-    4096 (the 1.02 × n·Ĥ rate bound)."""
-    for model, blocks, want in [("llama-3-8b", 32, 4096), ("llama-3-8b", 16, 4096), ("llama-3-8b", 8, 4608),
-                                ("llama-3-8b", 4, 4608), ("llama-3.2-1b", 16, 4096), ("llama-3-70b", 10, 4096),
-                                ("llama-3-8b", 1, 4096)]:
+def test_chunk_rule_and_tail_blocks():
+    """4608-symbol chunks only for a share of ≤ 1.25 rounds that they fit in one; otherwise 4096,
+    with the share's last k blocks in 2048-symbol chunks when its last round is ≤ ½ full —
+    k = ⌈B − ⌊rounds⌋ · lanes / chunks per block⌉ (the measured cases of DESIGN.md §15); the
+    32-block config-3 set (9.0 rounds) is plain 4096."""
+    for model, blocks, want_cs, want_k in [("llama-3-8b", 32, 4096, 0), ("llama-3-8b", 16, 4096, 2),
+                                           ("llama-3-8b", 8, 4096, 1), ("llama-3-8b", 4, 4608, 0),
+                                           ("llama-3.2-1b", 16, 4096, 4), ("llama-3-70b", 10, 4096, 1),
+                                           ("llama-3-8b", 1, 4096, 0)]:
         a = _args(model)
+        a.tail_blocks = -1
         cs = bench.choose_chunk(a, list(range(blocks)), LANES)
-        assert cs == want, (model, blocks, cs)
-        if cs == 4608:                             # a whole round fewer than 4096 needs
-            assert _steps(a, blocks, 4608) // 4608 < _steps(a, blocks, 4096) // 4096
+        k = bench.choose_tail(a, list(range(blocks)), LANES, cs)
+        assert (cs, k) == (want_cs, want_k), (model, blocks, cs, k)
+        if k:                                      # the 4096-symbol blocks fill whole rounds
+            import eqsynth
+            per = sum((r * c + 4095) // 4096 for r, c in eqsynth.block_shapes(model))
+            assert (blocks - k) * per <= int(blocks * per / LANES) * LANES
+    a = _args()
+    a.tail_blocks = 3                              # explicit
+    assert bench.choose_tail(a, list(range(16)), LANES, 4096) == 3
+    a = _args(mode="row")
+    a.tail_blocks = -1
+    assert bench.choose_tail(a, list(range(16)), LANES, 4096) == 0      # the fused GEMM's streams stay uniform
 
 
 def test_chunk_rule_respects_an_explicit_length():
