@@ -97,3 +97,20 @@ def test_interleaved_argument_validation():
                              codec=eq.EQ_CODEC_PAIR, chunk_mode=IL)
     with pytest.raises(eq.EqError):                            # the fused GEMM needs row-contiguous chunks
         eq.qmatmul(blk, 0, torch.zeros(1, 512, dtype=torch.bfloat16, device=DEV))
+
+
+def test_mixed_chunk_lengths_in_one_launch():
+    """The bench's tail blocks: blocks of different chunk lengths in ONE
+    eq_decode_dequant launch, each block's bf16 layers equal to the oracle's decode."""
+    shapes = [(64, 256), (32, 512), (16, 1024)]
+    gpu_blocks, refs = [], []
+    for b, cs in enumerate((64, 32, 64, 128)):
+        layers = _layers(shapes, 40 + b)
+        S = [(o.absmax_scales(W).astype(np.int32) + 128 * 11).astype(np.uint16) for W in layers]
+        refs.append(o.quantize_encode(layers, scales=S, cs=cs, codec=o.CODEC_PAIR_G, chunk_mode=o.CHUNK_INTERLEAVED))
+        gpu_blocks.append(eq.quantize_encode([W.to(DEV) for W in layers], scales=to_bf16(np.concatenate(S)),
+                                             chunk_symbols=cs, codec=eq.EQ_CODEC_PAIR_G, chunk_mode=IL))
+    views = eq.decode_dequant(gpu_blocks, eq.EQ_OUT_BF16)
+    for vb, ref in zip(views, refs):
+        for v, r in zip(vb, o.decode_dequant(ref)):
+            assert (u16(v) == r).all()
